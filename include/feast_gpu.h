@@ -1,0 +1,190 @@
+/*
+ * feast_gpu.h — C-ABI of libfeastgpu.so, the B200-native FEAST inner loop.
+ *
+ * Drop-in boundary for the reference's solver plugin + loop
+ * (reference: /root/reference/proj/include/feast/...):
+ *
+ *   feast_gpu_solve        replaces feast::feast_solve<double>            core.hpp:264-391
+ *   feast_gpu_prepare      replaces the ensure_factors() lambda           core.hpp:304-311
+ *                          (InnerSolver<T>::prepare(z) per node,          inner_solver.hpp:32-39)
+ *   feast_gpu_solve_shift  replaces ShiftSystem::solve_in_place           inner_solver.hpp:24-28
+ *   feast_gpu_contour_pass replaces accumulate_subspace_real              core.hpp:163-185
+ *   feast_gpu_rayleigh_ritz replaces rayleigh_ritz + trace_of_in_interval core.hpp:228-240,114-124
+ *   feast_gpu_reduced_gevp replaces linalg::reduced_gevp                  eigh.hpp:178-225
+ *   feast_gpu_residuals    replaces linalg::residual_norms                residual.hpp:29-68
+ *
+ * Conventions (same as the reference, dense.hpp:15-17, types.hpp:12):
+ *   - all arithmetic is IEEE fp64; dense blocks are column-major, (i,j) at i + j*ld;
+ *   - complex values are interleaved (re, im) pairs, byte-compatible with std::complex<double>;
+ *   - every pointer argument is a HOST pointer unless its name ends in _dev;
+ *   - return codes map 1:1 onto the reference exception classes (types.hpp:15-38):
+ *       FEAST_EINPUT     <-> feast::InputError          (CLI exit 4)
+ *       FEAST_ENUMERICAL <-> feast::NumericalError      (CLI exit 5)
+ *       FEAST_EBREAKDOWN <-> feast::SubspaceBreakdown   (a status, not a throw, out of feast_solve)
+ *     plus FEAST_ECUDA / FEAST_ENCCL for device / collective failures (NumericalError class).
+ *   - one host thread per context at a time (the InnerSolver threading contract of
+ *     inner_solver.hpp:30-31 is met by serialising on the context's stream).
+ */
+#ifndef FEAST_GPU_H_
+#define FEAST_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FEAST_GPU_ABI_VERSION 1
+
+typedef enum {
+  FEAST_OK = 0,
+  FEAST_EINPUT = 4,
+  FEAST_ENUMERICAL = 5,
+  FEAST_EBREAKDOWN = 6,
+  FEAST_ECUDA = 7,
+  FEAST_ENCCL = 8,
+  FEAST_EINTERNAL = 9
+} feast_code_t;
+
+/* Storage of one symmetric operator (operator.hpp:37-40 plus the block-tridiagonal
+ * layout the BASELINE configs 3 and 5 need). */
+typedef enum {
+  FEAST_STORAGE_DENSE = 0,    /* n*n column-major, exactly symmetric            */
+  FEAST_STORAGE_CSR = 1,      /* symmetric-complete CSR, int32 indices          */
+  FEAST_STORAGE_BLOCKTRI = 2  /* nblocks diagonal b*b blocks + (nblocks-1) lower
+                                 couplings C_l = M(l+1, l); M(l, l+1) = C_l^T   */
+} feast_storage_t;
+
+typedef struct {
+  int32_t kind;            /* feast_storage_t */
+  int32_t n;               /* dimension (BLOCKTRI: nblocks * bsize)           */
+  const double* dense;     /* DENSE: n*n                                      */
+  const int32_t* row_ptr;  /* CSR: n+1                                        */
+  const int32_t* col_idx;  /* CSR: nnz                                        */
+  const double* values;    /* CSR: nnz                                        */
+  int32_t nblocks;         /* BLOCKTRI                                        */
+  int32_t bsize;           /* BLOCKTRI                                        */
+  const double* diag;      /* BLOCKTRI: nblocks * b*b, block l at l*b*b       */
+  const double* lower;     /* BLOCKTRI: (nblocks-1) * b*b, C_l at l*b*b       */
+} feast_operator_t;
+
+/* Mirrors feast::FeastConfig (core.hpp:25-33). `threads` is accepted for API
+ * parity; on the GPU it has no effect on results (SPEC determinism rule). */
+typedef struct {
+  int32_t m0;
+  int32_t n_e;
+  double trace_tol;
+  int32_t max_loops;
+  uint64_t seed;
+  int32_t threads;
+  int32_t low_memory;
+} feast_config_t;
+
+/* Mirrors feast::FeastStatus (core.hpp:35-41), same order. */
+typedef enum {
+  FEAST_STATUS_CONVERGED = 0,
+  FEAST_STATUS_MAX_LOOPS = 1,
+  FEAST_STATUS_NO_EIGENVALUES = 2,
+  FEAST_STATUS_SATURATED = 3,
+  FEAST_STATUS_BREAKDOWN = 4
+} feast_run_status_t;
+
+/* Mirrors feast::FeastResult<double> (core.hpp:61-78). The caller allocates the
+ * arrays: eigenvalues/residuals/residual_absolute_only hold m0 entries,
+ * eigenvectors/subspace hold n*m0 doubles, trace_history/in_interval_counts hold
+ * max_loops+1 entries. Any array pointer may be NULL to skip that output. */
+typedef struct {
+  double* eigenvalues;
+  double* eigenvectors;
+  double* residuals;
+  int32_t* residual_absolute_only;
+  double* trace_history;
+  int32_t* in_interval_counts;
+  double* subspace;
+  /* scalar outputs */
+  int32_t m;               /* eigenpairs found inside the interval          */
+  int32_t subspace_cols;   /* columns of the last Ritz block (<= m0)        */
+  int32_t loops_used;
+  int32_t status;          /* feast_run_status_t                            */
+  double max_residual;
+  double factorize_s, solve_s, reduce_s, total_s; /* FeastTimings core.hpp:54-59 */
+} feast_result_t;
+
+/* ------------------------------------------------------------------------- */
+/* Context                                                                   */
+/* ------------------------------------------------------------------------- */
+typedef struct feast_gpu_ctx feast_gpu_ctx;
+
+int feast_gpu_abi_version(void);
+
+/* Creates a context on CUDA device `device`. `stream` may be NULL (the context
+ * creates its own) or an existing cudaStream_t the caller owns. */
+int feast_gpu_create(int device, void* stream, feast_gpu_ctx** out);
+void feast_gpu_destroy(feast_gpu_ctx* ctx);
+const char* feast_gpu_last_error(const feast_gpu_ctx* ctx);
+
+/* Multi-GPU: contour nodes are sharded over `nranks` ranks (contiguous blocks,
+ * ascending e); one NCCL allreduce(sum) of the N*M0 partial Q per pass.
+ * `nccl_unique_id` is the 128-byte ncclUniqueId rank 0 created
+ * (feast_gpu_nccl_unique_id) and broadcast out of band. */
+int feast_gpu_nccl_unique_id(void* id_out_128_bytes);
+int feast_gpu_set_comm(feast_gpu_ctx* ctx, const void* nccl_unique_id, int rank, int nranks);
+
+/* Uploads the pencil (A symmetric, B symmetric positive definite). CSR inputs
+ * whose pattern is block-tridiagonal are stored block-tridiagonal; other CSR
+ * inputs are densified (the reference's Dense policy, inner_solver.hpp:88-92). */
+int feast_gpu_set_pencil(feast_gpu_ctx* ctx, const feast_operator_t* a, const feast_operator_t* b);
+
+/* Contour on the upper half circle over [emin, emax] with n_e Gauss-Legendre
+ * nodes (quadrature.cpp:69-87), then factors every node this rank owns
+ * (ensure_factors, core.hpp:304-311). */
+int feast_gpu_prepare(feast_gpu_ctx* ctx, double emin, double emax, int n_e);
+
+/* Contour points actually used (host copies): z (2*n_e interleaved) and the
+ * quadrature coefficients c_e = 0.5 * w_e * r * e^{i theta_e} (2*n_e). */
+int feast_gpu_contour(const feast_gpu_ctx* ctx, double* z, double* coeff);
+
+/* ShiftSystem::solve_in_place for node e on the prepared factors:
+ * rhs (n*m complex, interleaved) <- (z_e B - A)^{-1} rhs   (mode 0 = Normal)
+ *                                   (z_e B - A)^{-H} rhs   (mode 1 = ConjTranspose) */
+int feast_gpu_solve_shift(feast_gpu_ctx* ctx, int e, double* rhs, int m, int mode);
+
+/* accumulate_subspace_real: Q = -sum_e Re(c_e (z_e B - A)^{-1} Y), Y and Q n*m real. */
+int feast_gpu_contour_pass(feast_gpu_ctx* ctx, const double* y, int m, double* q);
+
+/* rayleigh_ritz on Q (n*m real): Ritz values (ascending, m_out of them) and Ritz
+ * vectors X (n*m_out). truncated = spectral-truncation fallback was used. */
+int feast_gpu_rayleigh_ritz(feast_gpu_ctx* ctx, const double* q, int m, double* eigenvalues,
+                            double* x, int* m_out, int* truncated);
+
+/* reduced_gevp on host blocks a_q, b_q (m*m): eigenvalues (m_out, ascending) and
+ * phi (m*m_out), B_Q-orthonormal. Returns FEAST_EBREAKDOWN like SubspaceBreakdown. */
+int feast_gpu_reduced_gevp(feast_gpu_ctx* ctx, int m, const double* a_q, const double* b_q,
+                           double* eigenvalues, double* phi, int* m_out, int* truncated);
+
+/* residual_norms (residual.hpp:29-68) for m pairs on the uploaded pencil. */
+int feast_gpu_residuals(feast_gpu_ctx* ctx, int m, const double* lambdas, const double* x,
+                        double* residuals, int32_t* absolute_only, double* max_residual);
+
+/* The whole FEAST loop (core.hpp:264-391) with Q, Y, X and the factors resident
+ * on the device. initial_y (n*y_cols) may be NULL (seeded random_block). The
+ * pencil must have been set; the contour/factors are (re)built for [emin, emax]. */
+int feast_gpu_solve(feast_gpu_ctx* ctx, double emin, double emax, const feast_config_t* config,
+                    const double* initial_y, int y_cols, feast_result_t* result);
+
+/* Benchmark hook: runs `passes` loop bodies (contour pass + Rayleigh-Ritz + trace/count
+ * + Y = B X) on the device-resident state left by the last feast_gpu_solve or
+ * feast_gpu_bench_init, with no stopping rule; returns device milliseconds measured
+ * with CUDA events on the context stream, plus per-phase milliseconds
+ * (phase_ms[0] = contour solves, [1] = Q reduction/allreduce, [2] = Rayleigh-Ritz). */
+int feast_gpu_bench_init(feast_gpu_ctx* ctx, int m0, uint64_t seed);
+int feast_gpu_bench_passes(feast_gpu_ctx* ctx, int passes, double* total_ms, double* phase_ms);
+
+/* Number of kernel launches this context issued since creation (evidence counter). */
+int64_t feast_gpu_launch_count(const feast_gpu_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FEAST_GPU_H_ */
