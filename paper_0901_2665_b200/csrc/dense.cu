@@ -1,0 +1,298 @@
+// dense.cu — batched complex-fp64 LU with partial pivoting and the multi-RHS solve for
+// dense pencils (the reference's DenseShiftSystem: assemble_shifted_dense assemble.hpp:12-38,
+// DenseLU ctor lu.hpp:24-52, DenseLU::solve_in_place lu.hpp:56-95), all contour nodes of
+// this rank batched into every launch (blockIdx.z / blockIdx.x = node slot).
+//
+// Factor (right-looking, panel width nb = 64, LAPACK getrf structure):
+//   panel_kernel    unblocked partial-pivot LU of the n-k0 x nb panel (pivot rule of
+//                   lu.hpp:29-38: largest |.|, first index on ties; NumericalError on 0)
+//   laswp_kernel    the panel's row interchanges applied to the other columns
+//   diag_inv_kernel explicit inverses of the unit-lower L11 and upper U11 blocks
+//   zgemm           U12 = L11^{-1} A12 (in place) and A22 -= L21 U12  (DMMA tiles)
+// Solve (per pass, multi-RHS, blocked forward/backward substitution):
+//   R = P Y; for k: Z_k = L_kk^{-1} R_k; R_{>k} -= L_{>k,k} Z_k;
+//            for k desc: X_k = U_kk^{-1} R_k; R_{<k} -= U_{<k,k} X_k;  T = Re(c_e X)
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace feastgpu {
+
+cudaError_t zgemm_batched(int m, int n, int k, double2 alpha, const double2* a, int lda, int64_t sa,
+                          const double2* b, int ldb, int64_t sb, double2 beta, double2* c, int ldc,
+                          int64_t sc, int batch, cudaStream_t st);
+
+__global__ void assemble_kernel(int n, const double* __restrict__ a, const double* __restrict__ bm,
+                                const double2* __restrict__ z, double2* __restrict__ lu) {
+  const int s = blockIdx.y;
+  const double2 zz = z[s];
+  const int64_t nn = (int64_t)n * n;
+  double2* out = lu + s * nn;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < nn;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const double bv = bm[idx], av = a[idx];
+    out[idx] = make_double2(zz.x * bv - av, zz.y * bv);  // z*B - A (assemble.hpp:33-43)
+  }
+}
+
+// One CTA per node. Columns [k0, k0+kb), rows [k0, n).
+__global__ void __launch_bounds__(1024) panel_kernel(int n, int k0, int kb, double2* lu, int* ipiv,
+                                                     int* status) {
+  const int s = blockIdx.x;
+  double2* A = lu + (int64_t)s * n * n;
+  int* piv = ipiv + (int64_t)s * n;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ double rv[32];
+  __shared__ int ri[32];
+  __shared__ int p_s;
+  __shared__ double2 rowk[kDenseNb];
+  for (int j = 0; j < kb; ++j) {
+    const int col = k0 + j;
+    double best = -1.0;
+    int bi = n;
+    for (int i = col + tid; i < n; i += nt) {
+      const double v = cabs_(A[i + (int64_t)col * n]);
+      if (v > best) { best = v; bi = i; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    if (lane == 0) { rv[warp] = best; ri[warp] = bi; }
+    __syncthreads();
+    if (warp == 0) {
+      best = lane < (nt >> 5) ? rv[lane] : -1.0;
+      bi = lane < (nt >> 5) ? ri[lane] : n;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+      }
+      if (lane == 0) {
+        p_s = (best > 0.0) ? bi : -1;
+        if (!(best > 0.0)) atomicExch(status, 1);
+      }
+    }
+    __syncthreads();
+    const int p = p_s;
+    if (p < 0) return;  // singular: DenseLU throws NumericalError (lu.hpp:38)
+    if (tid == 0) piv[col] = p;
+    if (p != col && tid < kb) {
+      const int c = k0 + tid;
+      const double2 t0 = A[col + (int64_t)c * n];
+      A[col + (int64_t)c * n] = A[p + (int64_t)c * n];
+      A[p + (int64_t)c * n] = t0;
+    }
+    __syncthreads();
+    const double2 pv = A[col + (int64_t)col * n];
+    if (tid < kb) rowk[tid] = A[col + (int64_t)(k0 + tid) * n];
+    for (int i = col + 1 + tid; i < n; i += nt) A[i + (int64_t)col * n] = cdiv(A[i + (int64_t)col * n], pv);
+    __syncthreads();
+    for (int i = col + 1 + tid; i < n; i += nt) {
+      const double2 l = A[i + (int64_t)col * n];
+      for (int c = j + 1; c < kb; ++c) {
+        double2* e = A + i + (int64_t)(k0 + c) * n;
+        *e = csub(*e, cmul(l, rowk[c]));
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// row interchanges of panel [k0, k0+kb) on the columns outside it
+__global__ void laswp_kernel(int n, int k0, int kb, double2* lu, const int* ipiv) {
+  const int s = blockIdx.y;
+  double2* A = lu + (int64_t)s * n * n;
+  const int* piv = ipiv + (int64_t)s * n;
+  const int others = n - kb;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < others; c += gridDim.x * blockDim.x) {
+    const int col = c < k0 ? c : c + kb;
+    for (int r = k0; r < k0 + kb; ++r) {
+      const int p = piv[r];
+      if (p != r) {
+        const double2 t0 = A[r + (int64_t)col * n];
+        A[r + (int64_t)col * n] = A[p + (int64_t)col * n];
+        A[p + (int64_t)col * n] = t0;
+      }
+    }
+  }
+}
+
+// inverses of the diagonal block k: dinv[s][blk][0] = L11^{-1} (unit lower), [1] = U11^{-1}
+__global__ void __launch_bounds__(128) diag_inv_kernel(int n, int blk, int nblk, const double2* lu,
+                                                       double2* dinv) {
+  constexpr int NB = kDenseNb;
+  const int s = blockIdx.x;
+  const int k0 = blk * NB, kb = min(NB, n - k0);
+  const double2* A = lu + (int64_t)s * n * n + k0 + (int64_t)k0 * n;
+  double2* Li = dinv + ((int64_t)s * nblk + blk) * 2 * NB * NB;
+  double2* Ui = Li + NB * NB;
+  extern __shared__ double2 T[];  // NB x (NB+1)
+  for (int idx = threadIdx.x; idx < kb * kb; idx += blockDim.x) {
+    const int i = idx % kb, j = idx / kb;
+    T[i + j * (NB + 1)] = A[i + (int64_t)j * n];
+  }
+  __syncthreads();
+  const int j = threadIdx.x;
+  if (j < kb) {
+    // column j of L^{-1}: x_j = 1, x_i = -sum_{k=j}^{i-1} L_ik x_k
+    double2 x[NB];
+    for (int i = 0; i < kb; ++i) x[i] = make_double2(0.0, 0.0);
+    x[j] = make_double2(1.0, 0.0);
+    for (int i = j + 1; i < kb; ++i) {
+      double2 acc = make_double2(0.0, 0.0);
+      for (int k = j; k < i; ++k) acc = cadd(acc, cmul(T[i + k * (NB + 1)], x[k]));
+      x[i] = make_double2(-acc.x, -acc.y);
+    }
+    for (int i = 0; i < kb; ++i) Li[i + j * NB] = x[i];
+    // column j of U^{-1}: x_j = 1/U_jj, x_i = -(sum_{k=i+1}^{j} U_ik x_k) / U_ii
+    for (int i = 0; i < kb; ++i) x[i] = make_double2(0.0, 0.0);
+    x[j] = cdiv(make_double2(1.0, 0.0), T[j + j * (NB + 1)]);
+    for (int i = j - 1; i >= 0; --i) {
+      double2 acc = make_double2(0.0, 0.0);
+      for (int k = i + 1; k <= j; ++k) acc = cadd(acc, cmul(T[i + k * (NB + 1)], x[k]));
+      x[i] = cdiv(make_double2(-acc.x, -acc.y), T[i + i * (NB + 1)]);
+    }
+    for (int i = 0; i < kb; ++i) Ui[i + j * NB] = x[i];
+  }
+}
+
+__global__ void perm_kernel(int n, int nodes, const int* ipiv, int* perm) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nodes) return;
+  int* pm = perm + (int64_t)s * n;
+  const int* pv = ipiv + (int64_t)s * n;
+  for (int i = 0; i < n; ++i) pm[i] = i;
+  for (int k = 0; k < n; ++k) {
+    const int p = pv[k];
+    if (p != k) { const int t = pm[k]; pm[k] = pm[p]; pm[p] = t; }
+  }
+}
+
+cudaError_t dense_factor(const DenseFactorArgs& a, cudaStream_t st) {
+  const int n = a.n, nb = kDenseNb, nodes = a.nodes;
+  const int nblk = (n + nb - 1) / nb;
+  const int64_t nn = (int64_t)n * n;
+  {
+    dim3 grid((unsigned)std::min<int64_t>((nn + 255) / 256, 1024), nodes);
+    assemble_kernel<<<grid, 256, 0, st>>>(n, a.a, a.bm, a.z, a.lu);
+    ++g_launches;
+  }
+  const double2 one = make_double2(1.0, 0.0), mone = make_double2(-1.0, 0.0),
+                zero = make_double2(0.0, 0.0);
+  for (int blk = 0; blk < nblk; ++blk) {
+    const int k0 = blk * nb, kb = std::min(nb, n - k0);
+    panel_kernel<<<nodes, 1024, 0, st>>>(n, k0, kb, a.lu, a.ipiv, a.status);
+    ++g_launches;
+    if (n - kb > 0) {
+      dim3 grid((n - kb + 255) / 256, nodes);
+      laswp_kernel<<<grid, 256, 0, st>>>(n, k0, kb, a.lu, a.ipiv);
+      ++g_launches;
+    }
+    {
+      const int sm = (int)sizeof(double2) * nb * (nb + 1);
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(diag_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        attr = true;
+      }
+      diag_inv_kernel<<<nodes, 128, sm, st>>>(n, blk, nblk, a.lu, a.dinv);
+    }
+    ++g_launches;
+    const int rest = n - k0 - kb;
+    if (rest > 0) {
+      double2* a12 = a.lu + k0 + (int64_t)(k0 + kb) * n;
+      const double2* linv = a.dinv + (int64_t)blk * 2 * nb * nb;
+      zgemm_batched(kb, rest, kb, one, linv, nb, (int64_t)nblk * 2 * nb * nb, a12, n, nn, zero,
+                    a12, n, nn, nodes, st);
+      const double2* l21 = a.lu + (k0 + kb) + (int64_t)k0 * n;
+      double2* a22 = a.lu + (k0 + kb) + (int64_t)(k0 + kb) * n;
+      zgemm_batched(rest, rest, kb, mone, l21, n, nn, a12, n, nn, one, a22, n, nn, nodes, st);
+    }
+  }
+  perm_kernel<<<(nodes + 31) / 32, 32, 0, st>>>(n, nodes, a.ipiv, a.perm);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// R_s = P_s Y (real -> complex), or P_s W_s (complex, via scratch copy in t-as-double2)
+__global__ void permute_rhs_kernel(int n, int m, int ldv, const int* perm, const double* y,
+                                   const double2* src, double2* w) {
+  const int s = blockIdx.y;
+  const int* pm = perm + (int64_t)s * n;
+  double2* W = w + (int64_t)s * ldv * m;
+  const double2* S = src ? src + (int64_t)s * ldv * m : nullptr;
+  const int64_t total = (int64_t)n * m;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(idx % n);
+    const int64_t j = idx / n;
+    const int pi = pm[i];
+    W[i + j * ldv] = S ? S[pi + j * ldv] : make_double2(y[pi + j * ldv], 0.0);
+  }
+}
+
+__global__ void term_kernel(int n, int m, int ldv, const double2* coeff, const double2* w, double* t) {
+  const int s = blockIdx.y;
+  const double2 c = coeff[s];
+  const double2* W = w + (int64_t)s * ldv * m;
+  double* T = t + (int64_t)s * ldv * m;
+  const int64_t total = (int64_t)n * m;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(idx % n);
+    const int64_t j = idx / n;
+    const double2 x = W[i + j * ldv];
+    T[i + j * ldv] = c.x * x.x - c.y * x.y;  // Re(coeff * x) (core.hpp:179)
+  }
+}
+
+cudaError_t dense_solve(const DenseSolveArgs& a, cudaStream_t st) {
+  const int n = a.n, nb = kDenseNb, nodes = a.nodes, m = a.m;
+  const int nblk = (n + nb - 1) / nb;
+  const int64_t nn = (int64_t)n * n, sv = (int64_t)a.ldv * m, sd = (int64_t)nblk * 2 * nb * nb;
+  const int64_t total = (int64_t)n * m;
+  dim3 g1((unsigned)std::min<int64_t>((total + 255) / 256, 1024), nodes);
+  double2* tmp = nullptr;
+  if (a.complex_mode) {
+    // permute a copy: the t buffer is sized nodes*ldv*m doubles; complex copy needs 2x -> caller
+    // passes t sized for complex in complex mode
+    tmp = reinterpret_cast<double2*>(a.t);
+    cudaMemcpyAsync(tmp, a.w, sizeof(double2) * sv * nodes, cudaMemcpyDeviceToDevice, st);
+  }
+  permute_rhs_kernel<<<g1, 256, 0, st>>>(n, m, a.ldv, a.perm, a.y, tmp, a.w);
+  ++g_launches;
+  const double2 one = make_double2(1.0, 0.0), mone = make_double2(-1.0, 0.0),
+                zero = make_double2(0.0, 0.0);
+  for (int blk = 0; blk < nblk; ++blk) {
+    const int k0 = blk * nb, kb = std::min(nb, n - k0);
+    double2* rk = a.w + k0;
+    zgemm_batched(kb, m, kb, one, a.dinv + (int64_t)blk * 2 * nb * nb, nb, sd, rk, a.ldv, sv, zero,
+                  rk, a.ldv, sv, nodes, st);
+    const int rest = n - k0 - kb;
+    if (rest > 0)
+      zgemm_batched(rest, m, kb, mone, a.lu + (k0 + kb) + (int64_t)k0 * n, n, nn, rk, a.ldv, sv, one,
+                    a.w + k0 + kb, a.ldv, sv, nodes, st);
+  }
+  for (int blk = nblk - 1; blk >= 0; --blk) {
+    const int k0 = blk * nb, kb = std::min(nb, n - k0);
+    double2* rk = a.w + k0;
+    zgemm_batched(kb, m, kb, one, a.dinv + (int64_t)blk * 2 * nb * nb + nb * nb, nb, sd, rk, a.ldv,
+                  sv, zero, rk, a.ldv, sv, nodes, st);
+    if (k0 > 0)
+      zgemm_batched(k0, m, kb, mone, a.lu + (int64_t)k0 * n, n, nn, rk, a.ldv, sv, one, a.w, a.ldv,
+                    sv, nodes, st);
+  }
+  if (!a.complex_mode) {
+    term_kernel<<<g1, 256, 0, st>>>(n, m, a.ldv, a.coeff, a.w, a.t);
+    ++g_launches;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace feastgpu

@@ -1,0 +1,1103 @@
+// feast_gpu.cpp — host side of libfeastgpu: the C-ABI of include/feast_gpu.h.
+//
+// This is the C++ host driver the north star asks for. It keeps the reference solver's
+// API and status semantics (feast::feast_solve<double>, core.hpp:264-391) and drives the
+// sm_100a kernels: contour solves + fused quadrature epilogue (blocktri.cu / dense.cu),
+// the ordered reduction of Q and the NCCL allreduce across ranks, Rayleigh-Ritz with
+// the reduced eigensolve on device (gemm.cu, eig.cu), residuals (misc.cu).
+// Nothing here computes on the CPU except scalars: the contour constants (once per
+// solve), the start block (mt19937_64, as the reference), the trace/count/status logic.
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/feast_gpu.h"
+#include "kernels.h"
+
+using namespace feastgpu;
+
+namespace {
+
+// ----------------------------------------------------------------------------
+// error plumbing: C++ exceptions inside, integer codes at the C-ABI
+// ----------------------------------------------------------------------------
+struct Failure : std::runtime_error {
+  int code;
+  Failure(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void fail(int code, const std::string& m) { throw Failure(code, m); }
+
+#define CK(x)                                                                             \
+  do {                                                                                    \
+    cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess)                                                                \
+      fail(FEAST_ECUDA, std::string("CUDA: ") + cudaGetErrorString(e_) + " at " #x);      \
+  } while (0)
+
+// ----------------------------------------------------------------------------
+// NCCL, resolved at run time (no link-time dependency; torch's copy is reused if loaded)
+// ----------------------------------------------------------------------------
+struct NcclApi {
+  void* h = nullptr;
+  int (*getUniqueId)(void*) = nullptr;
+  int (*commInitRank)(void**, int, const void* /*by value 128B*/, int) = nullptr;
+  int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*commDestroy)(void*) = nullptr;
+  const char* (*getErrorString)(int) = nullptr;
+};
+struct NcclUid {
+  char internal[128];
+};
+typedef int (*nccl_init_fn)(void**, int, NcclUid, int);
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    api.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (api.h) {
+      api.getUniqueId = (int (*)(void*))dlsym(api.h, "ncclGetUniqueId");
+      api.allReduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
+          api.h, "ncclAllReduce");
+      api.commDestroy = (int (*)(void*))dlsym(api.h, "ncclCommDestroy");
+      api.getErrorString = (const char* (*)(int))dlsym(api.h, "ncclGetErrorString");
+    }
+  }
+  return api;
+}
+constexpr int kNcclFloat64 = 8, kNcclSum = 0;
+
+// ----------------------------------------------------------------------------
+// Gauss-Legendre + half-circle contour (restates quadrature.cpp:14-87): Newton on the
+// three-term Legendre recurrence in extended precision, positive half mirrored.
+// ----------------------------------------------------------------------------
+void legendre(int n, long double x, long double& p, long double& dp) {
+  long double a = 1.0L, b = x;
+  for (int k = 2; k <= n; ++k) {
+    const long double c = ((2.0L * k - 1.0L) * x * b - (k - 1.0L) * a) / k;
+    a = b;
+    b = c;
+  }
+  p = b;
+  dp = n * (x * b - a) / (x * x - 1.0L);
+}
+
+void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
+  if (n < 1 || n > 64) fail(FEAST_EINPUT, "gauss_legendre: point count out of supported range");
+  x.assign(n, 0.0);
+  w.assign(n, 0.0);
+  const long double pi = 3.14159265358979323846264338327950288L;
+  for (int i = 0; i < n / 2; ++i) {
+    long double r = std::cos(static_cast<double>(pi * (i + 0.75L) / (n + 0.5L)));
+    long double p = 0, dp = 1;
+    for (int it = 0; it < 100; ++it) {
+      legendre(n, r, p, dp);
+      const long double d = p / dp;
+      r -= d;
+      if (std::fabs(static_cast<double>(d)) <= 1e-15) {
+        legendre(n, r, p, dp);
+        r -= p / dp;
+        break;
+      }
+    }
+    legendre(n, r, p, dp);
+    const long double wt = 2.0L / ((1.0L - r * r) * dp * dp);
+    x[n - 1 - i] = static_cast<double>(r);
+    x[i] = -static_cast<double>(r);
+    w[n - 1 - i] = w[i] = static_cast<double>(wt);
+  }
+  if (n % 2) {
+    long double p, dp;
+    legendre(n, 0.0L, p, dp);
+    x[n / 2] = 0.0;
+    w[n / 2] = static_cast<double>(2.0L / (dp * dp));
+  }
+}
+
+// random_block<double> (core.hpp:84-106): mt19937_64, top 53 bits, column-major fill
+void random_block(int n, int m, uint64_t seed, double* out, int ld) {
+  std::mt19937_64 gen(seed);
+  for (int j = 0; j < m; ++j)
+    for (int i = 0; i < n; ++i)
+      out[i + (size_t)j * ld] = 2.0 * (static_cast<double>(gen() >> 11) * 0x1p-53) - 1.0;
+}
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t count) {
+    if (count <= n) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    if (count) {
+      CK(cudaMalloc(&p, sizeof(T) * count));
+      n = count;
+    }
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+}  // namespace
+
+struct feast_gpu_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  // multi-GPU
+  void* comm = nullptr;
+  int rank = 0, nranks = 1;
+  // pencil
+  bool have_pencil = false;
+  int n = 0, npad = 0;
+  bool blocktri = false;
+  int L = 0, b = 0;
+  DevBuf<double> A, Bm;            // dense n*n
+  DevBuf<double2> abdiag, ablow;  // block-tridiagonal (A, B) pairs
+  double norm_a1 = 0.0;
+  // contour
+  bool have_contour = false;
+  double emin = 0, emax = 0, radius = 0;
+  int ne = 0, e0 = 0, e1 = 0;
+  std::vector<double2> z, coeff;  // all nodes
+  DevBuf<double2> dz, dcoeff;     // owned nodes
+  // factors
+  bool factored = false;
+  DevBuf<double2> sinv, gfac, lu, dinv, scratch;
+  DevBuf<int> ipiv, perm, status;
+  // workspaces
+  int mcap = 0;
+  DevBuf<double> Y, Q, X, AQ, BQ, T, gw;
+  DevBuf<double2> W;
+  DevBuf<double> Aq, Bq, Cm, Lm, Phi, Ev, Vm, S, Tm;
+  DevBuf<int> keep;
+  EigWork* eig = nullptr;
+  int eig_cap = 0;
+  // bench state
+  int bench_m = 0;
+  cudaEvent_t ev[8] = {};
+
+  int owned() const { return e1 - e0; }
+};
+
+namespace {
+
+void ensure_eig(feast_gpu_ctx* c, int m) {
+  if (c->eig && c->eig_cap >= m) return;
+  if (c->eig) eig_destroy(c->eig);
+  c->eig = eig_create(std::max(m, 16));
+  c->eig_cap = std::max(m, 16);
+}
+
+void ensure_workspace(feast_gpu_ctx* c, int m) {
+  if (m <= c->mcap) return;
+  const size_t nv = (size_t)c->npad * m;
+  const int own = std::max(c->owned(), 1);
+  c->Y.ensure(nv);
+  c->Q.ensure(nv);
+  c->X.ensure(nv);
+  c->AQ.ensure(nv);
+  c->BQ.ensure(nv);
+  c->T.ensure(2 * nv * own);  // doubles; complex-mode dense shim reuses it as double2
+  c->W.ensure(nv * own);
+  const size_t mm = (size_t)m * m;
+  for (DevBuf<double>* d : {&c->Aq, &c->Bq, &c->Cm, &c->Lm, &c->Phi, &c->Vm, &c->S, &c->Tm})
+    d->ensure(mm);
+  c->Ev.ensure(m);
+  c->keep.ensure(m);
+  c->gw.ensure(std::max<size_t>(mm * 64, nv));
+  ensure_eig(c, m);
+  c->mcap = m;
+}
+
+void sync(feast_gpu_ctx* c) { CK(cudaStreamSynchronize(c->stream)); }
+
+// ------------------------------- pencil -------------------------------------
+void validate_dense_symmetric(const double* m, int n) {
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < j; ++i)
+      if (m[i + (size_t)j * n] != m[j + (size_t)i * n])
+        fail(FEAST_EINPUT, "SymmetricOperator: matrix is not symmetric");
+}
+
+int csr_bandwidth(const feast_operator_t* o) {
+  int bw = 0;
+  for (int i = 0; i < o->n; ++i)
+    for (int k = o->row_ptr[i]; k < o->row_ptr[i + 1]; ++k) bw = std::max(bw, std::abs(i - o->col_idx[k]));
+  return bw;
+}
+
+void validate_csr(const feast_operator_t* o) {
+  const int n = o->n;
+  if (o->row_ptr[0] != 0) fail(FEAST_EINPUT, "SymmetricOperator: bad row_ptr");
+  for (int i = 0; i < n; ++i) {
+    if (o->row_ptr[i + 1] < o->row_ptr[i]) fail(FEAST_EINPUT, "SymmetricOperator: bad row_ptr");
+    for (int k = o->row_ptr[i]; k < o->row_ptr[i + 1]; ++k) {
+      const int j = o->col_idx[k];
+      if (j < 0 || j >= n) fail(FEAST_EINPUT, "SymmetricOperator: triplet index out of range");
+      if (j <= i) continue;
+      // mirror (j, i) must exist with the same value (operator.hpp:237-261)
+      const int* b = o->col_idx + o->row_ptr[j];
+      const int* e = o->col_idx + o->row_ptr[j + 1];
+      const int* f = std::lower_bound(b, e, i);
+      if (f == e || *f != i) {
+        bool found = false;  // unsorted rows: linear scan
+        for (const int* q = b; q != e; ++q)
+          if (*q == i) {
+            found = true;
+            if (o->values[o->row_ptr[j] + (q - b)] != o->values[k])
+              fail(FEAST_EINPUT, "SymmetricOperator: mirror entries disagree");
+          }
+        if (!found) fail(FEAST_EINPUT, "SymmetricOperator: missing mirror entry");
+      } else if (o->values[o->row_ptr[j] + (f - b)] != o->values[k]) {
+        fail(FEAST_EINPUT, "SymmetricOperator: mirror entries disagree");
+      }
+    }
+  }
+}
+
+// smallest block size (multiple of 16; of 32 above 128) for which the CSR pattern is
+// block-tridiagonal
+bool csr_fits_blocktri(const feast_operator_t* o, int b) {
+  for (int i = 0; i < o->n; ++i)
+    for (int k = o->row_ptr[i]; k < o->row_ptr[i + 1]; ++k)
+      if (std::abs(i / b - o->col_idx[k] / b) > 1) return false;
+  return true;
+}
+int round_block(int b) {
+  if (b <= 16) return 16;
+  if (b <= 128) return (b + 15) / 16 * 16;
+  return (b + 31) / 32 * 32;
+}
+
+// dense view (host) of any operator
+std::vector<double> to_dense(const feast_operator_t* o) {
+  const int n = o->n;
+  std::vector<double> m((size_t)n * n, 0.0);
+  if (o->kind == FEAST_STORAGE_DENSE) {
+    std::memcpy(m.data(), o->dense, sizeof(double) * m.size());
+  } else if (o->kind == FEAST_STORAGE_CSR) {
+    for (int i = 0; i < n; ++i)
+      for (int k = o->row_ptr[i]; k < o->row_ptr[i + 1]; ++k) m[i + (size_t)o->col_idx[k] * n] += o->values[k];
+  } else {
+    const int b = o->bsize;
+    for (int l = 0; l < o->nblocks; ++l) {
+      for (int j = 0; j < b; ++j)
+        for (int i = 0; i < b; ++i) m[(l * b + i) + (size_t)(l * b + j) * n] = o->diag[(size_t)l * b * b + i + j * b];
+      if (l + 1 < o->nblocks)
+        for (int j = 0; j < b; ++j)
+          for (int i = 0; i < b; ++i) {
+            const double v = o->lower[(size_t)l * b * b + i + j * b];
+            m[((l + 1) * b + i) + (size_t)(l * b + j) * n] = v;
+            m[(l * b + j) + (size_t)((l + 1) * b + i) * n] = v;
+          }
+    }
+  }
+  return m;
+}
+
+// block-tridiagonal host view with block size b and L = ceil(n/b) blocks; padding rows
+// get A = 0, B = 1 (decoupled, never reached by a zero-padded right-hand side)
+void to_blocktri(const feast_operator_t* o, int b, int L, bool is_b, std::vector<double>& diag,
+                 std::vector<double>& low) {
+  const int n = o->n;
+  diag.assign((size_t)L * b * b, 0.0);
+  low.assign((size_t)(L > 1 ? L - 1 : 0) * b * b, 0.0);
+  if (is_b)
+    for (int r = n; r < L * b; ++r) diag[(size_t)(r / b) * b * b + (r % b) * (b + 1)] = 1.0;
+  if (o->kind == FEAST_STORAGE_BLOCKTRI && o->bsize == b) {
+    std::memcpy(diag.data(), o->diag, sizeof(double) * (size_t)o->nblocks * b * b);
+    if (o->nblocks > 1) std::memcpy(low.data(), o->lower, sizeof(double) * (size_t)(o->nblocks - 1) * b * b);
+    return;
+  }
+  auto put = [&](int i, int j, double v) {
+    const int li = i / b, lj = j / b, ii = i % b, jj = j % b;
+    if (li == lj) diag[(size_t)li * b * b + ii + (size_t)jj * b] += v;
+    else if (li == lj + 1) low[(size_t)lj * b * b + ii + (size_t)jj * b] += v;
+  };
+  if (o->kind == FEAST_STORAGE_CSR) {
+    for (int i = 0; i < n; ++i)
+      for (int k = o->row_ptr[i]; k < o->row_ptr[i + 1]; ++k) put(i, o->col_idx[k], o->values[k]);
+  } else {
+    fail(FEAST_EINPUT, "set_pencil: cannot re-block this operator");
+  }
+}
+
+double norm_one(const feast_operator_t* o) {  // operator.hpp:195-212
+  const int n = o->n;
+  std::vector<double> cs(n, 0.0);
+  if (o->kind == FEAST_STORAGE_DENSE) {
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i) cs[j] += std::fabs(o->dense[i + (size_t)j * n]);
+  } else if (o->kind == FEAST_STORAGE_CSR) {
+    for (int i = 0; i < n; ++i)
+      for (int k = o->row_ptr[i]; k < o->row_ptr[i + 1]; ++k) cs[i] += std::fabs(o->values[k]);
+  } else {
+    const int b = o->bsize;
+    for (int l = 0; l < o->nblocks; ++l) {
+      for (int j = 0; j < b; ++j)
+        for (int i = 0; i < b; ++i) cs[l * b + j] += std::fabs(o->diag[(size_t)l * b * b + i + j * b]);
+      if (l + 1 < o->nblocks)
+        for (int j = 0; j < b; ++j)
+          for (int i = 0; i < b; ++i) {
+            const double v = std::fabs(o->lower[(size_t)l * b * b + i + j * b]);
+            cs[l * b + j] += v;        // column l*b+j gets C_l entries
+            cs[(l + 1) * b + i] += v;  // column (l+1)*b+i gets C_l^T entries
+          }
+    }
+  }
+  double best = 0.0;
+  for (double v : cs) best = std::max(best, v);
+  return best;
+}
+
+void check_operator(const feast_operator_t* o) {
+  if (!o) fail(FEAST_EINPUT, "set_pencil: null operator");
+  if (o->n < 1) fail(FEAST_EINPUT, "feast_solve: empty operator");
+  switch (o->kind) {
+    case FEAST_STORAGE_DENSE:
+      if (!o->dense) fail(FEAST_EINPUT, "set_pencil: dense data missing");
+      validate_dense_symmetric(o->dense, o->n);
+      break;
+    case FEAST_STORAGE_CSR:
+      if (!o->row_ptr || !o->col_idx || !o->values) fail(FEAST_EINPUT, "set_pencil: CSR data missing");
+      validate_csr(o);
+      break;
+    case FEAST_STORAGE_BLOCKTRI: {
+      if (!o->diag || (o->nblocks > 1 && !o->lower) || o->bsize < 1 ||
+          (int64_t)o->nblocks * o->bsize != o->n)
+        fail(FEAST_EINPUT, "set_pencil: bad block-tridiagonal descriptor");
+      const int b = o->bsize;
+      for (int l = 0; l < o->nblocks; ++l)
+        for (int j = 0; j < b; ++j)
+          for (int i = 0; i < j; ++i)
+            if (o->diag[(size_t)l * b * b + i + j * b] != o->diag[(size_t)l * b * b + j + i * b])
+              fail(FEAST_EINPUT, "SymmetricOperator: matrix is not symmetric");
+      break;
+    }
+    default:
+      fail(FEAST_EINPUT, "set_pencil: unknown storage kind");
+  }
+}
+
+void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operator_t* b) {
+  check_operator(a);
+  check_operator(b);
+  if (a->n != b->n) fail(FEAST_EINPUT, "feast_solve: operator dimensions differ");
+  const int n = a->n;
+  // storage policy (the reference's Auto policy, inner_solver.hpp:84-92, with the banded
+  // factorisation replaced by block-tridiagonal block Thomas)
+  int bsz = 0;
+  const bool a_bt = a->kind == FEAST_STORAGE_BLOCKTRI, b_bt = b->kind == FEAST_STORAGE_BLOCKTRI;
+  const bool a_sp = a->kind == FEAST_STORAGE_CSR || a_bt, b_sp = b->kind == FEAST_STORAGE_CSR || b_bt;
+  if (a_sp && b_sp) {
+    if (a_bt && b_bt && a->bsize == b->bsize && a->bsize % 16 == 0 && (a->bsize <= 128 || a->bsize % 32 == 0)) {
+      bsz = a->bsize;
+    } else {
+      int bw = 0;
+      for (const feast_operator_t* o : {a, b}) {
+        if (o->kind == FEAST_STORAGE_CSR) bw = std::max(bw, csr_bandwidth(o));
+        else bw = std::max(bw, 2 * o->bsize - 1);
+      }
+      if ((3 * bw + 1) * 2 <= n) {
+        const int lo = round_block(std::max(1, (bw + 2) / 2)), hi = round_block(std::max(bw, 1));
+        for (int cand = lo; cand <= hi; cand += (cand < 128 ? 16 : 32)) {
+          bool ok = true;
+          for (const feast_operator_t* o : {a, b}) {
+            if (o->kind == FEAST_STORAGE_CSR) ok = ok && csr_fits_blocktri(o, cand);
+            else ok = ok && (o->bsize == cand);
+          }
+          if (ok) { bsz = cand; break; }
+        }
+        if (!bsz) bsz = hi;
+      }
+    }
+  }
+  c->have_pencil = false;
+  c->have_contour = false;
+  c->factored = false;
+  c->mcap = 0;
+  c->n = n;
+  c->norm_a1 = norm_one(a);
+  if (bsz) {
+    c->blocktri = true;
+    c->b = bsz;
+    c->L = (n + bsz - 1) / bsz;
+    c->npad = c->L * bsz;
+    std::vector<double> ad, al, bd, bl;
+    to_blocktri(a, bsz, c->L, false, ad, al);
+    to_blocktri(b, bsz, c->L, true, bd, bl);
+    std::vector<double2> pd(ad.size()), pl(al.size());
+    for (size_t i = 0; i < ad.size(); ++i) pd[i] = make_double2(ad[i], bd[i]);
+    for (size_t i = 0; i < al.size(); ++i) pl[i] = make_double2(al[i], bl[i]);
+    c->abdiag.ensure(pd.size());
+    c->ablow.ensure(std::max<size_t>(pl.size(), 1));
+    CK(cudaMemcpyAsync(c->abdiag.p, pd.data(), sizeof(double2) * pd.size(), cudaMemcpyHostToDevice, c->stream));
+    if (!pl.empty())
+      CK(cudaMemcpyAsync(c->ablow.p, pl.data(), sizeof(double2) * pl.size(), cudaMemcpyHostToDevice, c->stream));
+    c->A.release();
+    c->Bm.release();
+    sync(c);
+  } else {
+    c->blocktri = false;
+    c->b = 0;
+    c->L = 0;
+    c->npad = n;
+    c->A.ensure((size_t)n * n);
+    c->Bm.ensure((size_t)n * n);
+    if (a->kind == FEAST_STORAGE_DENSE) {
+      CK(cudaMemcpyAsync(c->A.p, a->dense, sizeof(double) * n * (size_t)n, cudaMemcpyHostToDevice, c->stream));
+    } else {
+      auto d = to_dense(a);
+      CK(cudaMemcpyAsync(c->A.p, d.data(), sizeof(double) * d.size(), cudaMemcpyHostToDevice, c->stream));
+      sync(c);
+    }
+    if (b->kind == FEAST_STORAGE_DENSE) {
+      CK(cudaMemcpyAsync(c->Bm.p, b->dense, sizeof(double) * n * (size_t)n, cudaMemcpyHostToDevice, c->stream));
+    } else {
+      auto d = to_dense(b);
+      CK(cudaMemcpyAsync(c->Bm.p, d.data(), sizeof(double) * d.size(), cudaMemcpyHostToDevice, c->stream));
+      sync(c);
+    }
+    sync(c);
+  }
+  c->have_pencil = true;
+}
+
+// ------------------------------- contour + factors ---------------------------
+void build_contour(feast_gpu_ctx* c, double emin, double emax, int ne) {
+  if (!(emin < emax)) fail(FEAST_EINPUT, "SearchInterval: lambda_min must be strictly below lambda_max");
+  const double scale = std::max({1.0, std::fabs(emin), std::fabs(emax)});
+  if (emax - emin < 1e-12 * scale) fail(FEAST_EINPUT, "build_contour: interval is degenerate at round-off scale");
+  std::vector<double> x, w;
+  gauss_legendre(ne, x, w);
+  c->emin = emin;
+  c->emax = emax;
+  c->ne = ne;
+  c->radius = 0.5 * (emax - emin);
+  const double mid = 0.5 * (emin + emax);
+  c->z.resize(ne);
+  c->coeff.resize(ne);
+  for (int e = 0; e < ne; ++e) {
+    const double th = -(M_PI / 2.0) * (x[e] - 1.0);
+    c->z[e] = make_double2(mid + c->radius * std::cos(th), c->radius * std::sin(th));
+    const double f = 0.5 * w[e] * c->radius;  // coeff = 0.5 w r e^{i theta} (core.hpp:174-175)
+    c->coeff[e] = make_double2(f * std::cos(th), f * std::sin(th));
+  }
+  // contiguous node blocks per rank, ascending e
+  c->e0 = (int)((int64_t)ne * c->rank / c->nranks);
+  c->e1 = (int)((int64_t)ne * (c->rank + 1) / c->nranks);
+  const int own = c->owned();
+  c->dz.ensure(std::max(own, 1));
+  c->dcoeff.ensure(std::max(own, 1));
+  if (own) {
+    CK(cudaMemcpyAsync(c->dz.p, c->z.data() + c->e0, sizeof(double2) * own, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->dcoeff.p, c->coeff.data() + c->e0, sizeof(double2) * own, cudaMemcpyHostToDevice, c->stream));
+  }
+  c->have_contour = true;
+  c->factored = false;
+  c->mcap = 0;  // per-node workspaces depend on the owned node count
+}
+
+void factor(feast_gpu_ctx* c) {
+  if (!c->have_pencil) fail(FEAST_EINPUT, "feast_gpu: pencil not set");
+  if (!c->have_contour) fail(FEAST_EINPUT, "feast_gpu: contour not prepared");
+  const int own = c->owned();
+  c->status.ensure(1);
+  CK(cudaMemsetAsync(c->status.p, 0, sizeof(int), c->stream));
+  if (own == 0) {
+    c->factored = true;
+    return;
+  }
+  if (c->blocktri) {
+    const size_t bb = (size_t)c->b * c->b;
+    c->sinv.ensure(own * c->L * bb);
+    c->gfac.ensure(std::max<size_t>(own * (c->L - 1) * bb, 1));
+    if (c->b > 64) c->scratch.ensure(own * (size_t)c->b * 2 * (c->b + 1));
+    BtFactorArgs a{c->L, c->b, own, c->abdiag.p, c->ablow.p, c->dz.p, c->sinv.p, c->gfac.p, c->scratch.p, c->status.p};
+    CK(bt_factor(a, c->stream));
+  } else {
+    const int n = c->n, nb = kDenseNb, nblk = (n + nb - 1) / nb;
+    c->lu.ensure((size_t)own * n * n);
+    c->ipiv.ensure((size_t)own * n);
+    c->perm.ensure((size_t)own * n);
+    c->dinv.ensure((size_t)own * nblk * 2 * nb * nb);
+    DenseFactorArgs a{n, own, c->A.p, c->Bm.p, c->dz.p, c->lu.p, c->ipiv.p, c->perm.p, c->dinv.p, c->status.p};
+    CK(dense_factor(a, c->stream));
+  }
+  int st = 0;
+  CK(cudaMemcpyAsync(&st, c->status.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  if (st) fail(FEAST_ENUMERICAL, c->blocktri ? "BlockThomas: block pivot is numerically singular"
+                                             : "DenseLU: matrix is numerically singular");
+  c->factored = true;
+}
+
+// ------------------------------- passes --------------------------------------
+// Q = -sum_e Re(c_e (z_e B - A)^{-1} Y) over ALL nodes (allreduce across ranks)
+void contour_pass(feast_gpu_ctx* c, int m) {
+  const int own = c->owned();
+  const size_t nv = (size_t)c->npad * m;
+  if (own > 0) {
+    if (c->blocktri) {
+      BtSweepArgs a{c->L, c->b, own, m, c->npad, c->ablow.p, c->dz.p, c->dcoeff.p, c->sinv.p,
+                    c->gfac.p, c->Y.p, c->T.p, c->W.p, 0};
+      CK(bt_sweep(a, c->stream));
+    } else {
+      DenseSolveArgs a{c->n, own, m, c->npad, c->lu.p, c->perm.p, c->dinv.p, c->dcoeff.p, c->Y.p, c->T.p, c->W.p, 0};
+      CK(dense_solve(a, c->stream));
+    }
+    CK(reduce_terms(c->T.p, own, (int64_t)nv, c->npad, m, c->npad, c->Q.p, c->stream));
+  } else {
+    CK(fill_zero(c->Q.p, nv, c->stream));
+  }
+  if (c->nranks > 1) {
+    NcclApi& api = nccl();
+    if (!api.allReduce) fail(FEAST_ENCCL, "NCCL not available");
+    const int r = api.allReduce(c->Q.p, c->Q.p, nv, kNcclFloat64, kNcclSum, c->comm, c->stream);
+    if (r != 0) fail(FEAST_ENCCL, std::string("ncclAllReduce: ") + (api.getErrorString ? api.getErrorString(r) : "?"));
+  }
+}
+
+void apply_op(feast_gpu_ctx* c, int which, const double* x, double* y, int m) {
+  if (c->blocktri) {
+    CK(bt_apply(c->L, c->b, c->abdiag.p, c->ablow.p, which, x, c->npad, y, c->npad, m, c->stream));
+  } else {
+    CK(dgemm('N', 'N', c->n, m, c->n, 1.0, which ? c->Bm.p : c->A.p, c->n, x, c->npad, 0.0, y, c->npad,
+             c->gw.p, c->gw.n, c->stream));
+  }
+}
+
+struct Reduced {
+  std::vector<double> evals;
+  int mo = 0;
+  bool truncated = false;
+};
+
+// reduced_gevp (eigh.hpp:178-225) on device blocks Aq, Bq (m x m); Phi (m x mo) -> c->Phi
+Reduced reduced_gevp(feast_gpu_ctx* c, int m) {
+  Reduced r;
+  const size_t mm = (size_t)m * m;
+  CK(cudaMemcpyAsync(c->Lm.p, c->Bq.p, sizeof(double) * mm, cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemsetAsync(c->status.p, 0, sizeof(int), c->stream));
+  CK(cholesky(m, c->Lm.p, 1e-13, c->status.p, c->stream));
+  int st = 0;
+  CK(cudaMemcpyAsync(&st, c->status.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  r.evals.resize(m);
+  if (!st) {
+    // C = L^-1 A L^-T  via two lower solves and transposes (eigh.hpp:192-196)
+    CK(cudaMemcpyAsync(c->Cm.p, c->Aq.p, sizeof(double) * mm, cudaMemcpyDeviceToDevice, c->stream));
+    CK(trsm_lower(m, c->Lm.p, c->Cm.p, m, m, c->stream));
+    CK(transpose(c->Cm.p, m, m, m, c->Tm.p, m, c->stream));
+    CK(trsm_lower(m, c->Lm.p, c->Tm.p, m, m, c->stream));
+    CK(transpose(c->Tm.p, m, m, m, c->Cm.p, m, c->stream));
+    CK(symmetrize(c->Cm.p, m, m, c->stream));
+    CK(sym_eig(c->eig, m, c->Cm.p, c->Ev.p, c->Phi.p, c->stream));
+    CK(trsm_lower_t(m, c->Lm.p, c->Phi.p, m, m, c->stream));  // Phi = L^-T W
+    CK(cudaMemcpyAsync(r.evals.data(), c->Ev.p, sizeof(double) * m, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    r.mo = m;
+    return r;
+  }
+  // spectral truncation fallback (eigh.hpp:204-224)
+  CK(cudaMemcpyAsync(c->Cm.p, c->Bq.p, sizeof(double) * mm, cudaMemcpyDeviceToDevice, c->stream));
+  CK(symmetrize(c->Cm.p, m, m, c->stream));
+  CK(sym_eig(c->eig, m, c->Cm.p, c->Ev.p, c->Vm.p, c->stream));
+  std::vector<double> d(m);
+  CK(cudaMemcpyAsync(d.data(), c->Ev.p, sizeof(double) * m, cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  const double dmax = d.back();
+  if (!(dmax > 0.0)) fail(FEAST_EBREAKDOWN, "reduced_gevp: projected mass matrix has no positive modes");
+  std::vector<int> keep;
+  for (int i = 0; i < m; ++i)
+    if (d[i] > 1e-14 * dmax) keep.push_back(i);
+  if (keep.empty()) fail(FEAST_EBREAKDOWN, "reduced_gevp: projected mass matrix has no usable modes");
+  const int k = (int)keep.size();
+  CK(cudaMemcpyAsync(c->keep.p, keep.data(), sizeof(int) * k, cudaMemcpyHostToDevice, c->stream));
+  CK(scale_columns(c->Vm.p, m, c->keep.p, c->Ev.p, k, c->S.p, c->stream));   // S = V_keep diag(d^-1/2)
+  CK(dgemm('N', 'N', m, k, m, 1.0, c->Aq.p, m, c->S.p, m, 0.0, c->Tm.p, m, c->gw.p, c->gw.n, c->stream));
+  CK(dgemm('T', 'N', k, k, m, 1.0, c->S.p, m, c->Tm.p, m, 0.0, c->Cm.p, k, c->gw.p, c->gw.n, c->stream));
+  CK(symmetrize(c->Cm.p, k, k, c->stream));
+  CK(sym_eig(c->eig, k, c->Cm.p, c->Ev.p, c->Vm.p, c->stream));
+  CK(dgemm('N', 'N', m, k, k, 1.0, c->S.p, m, c->Vm.p, k, 0.0, c->Phi.p, m, c->gw.p, c->gw.n, c->stream));
+  r.evals.resize(k);
+  CK(cudaMemcpyAsync(r.evals.data(), c->Ev.p, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  r.mo = k;
+  r.truncated = true;
+  return r;
+}
+
+// rayleigh_ritz (core.hpp:228-240): X = Q Phi, Ritz values ascending
+Reduced rayleigh_ritz(feast_gpu_ctx* c, int m) {
+  const int n = c->npad;
+  apply_op(c, 0, c->Q.p, c->AQ.p, m);
+  apply_op(c, 1, c->Q.p, c->BQ.p, m);
+  CK(dgemm('T', 'N', m, m, n, 1.0, c->Q.p, n, c->AQ.p, n, 0.0, c->Aq.p, m, c->gw.p, c->gw.n, c->stream));
+  CK(dgemm('T', 'N', m, m, n, 1.0, c->Q.p, n, c->BQ.p, n, 0.0, c->Bq.p, m, c->gw.p, c->gw.n, c->stream));
+  CK(symmetrize(c->Aq.p, m, m, c->stream));
+  CK(symmetrize(c->Bq.p, m, m, c->stream));
+  Reduced r = reduced_gevp(c, m);
+  CK(dgemm('N', 'N', n, r.mo, m, 1.0, c->Q.p, n, c->Phi.p, m, 0.0, c->X.p, n, c->gw.p, c->gw.n, c->stream));
+  return r;
+}
+
+void upload_block(feast_gpu_ctx* c, const double* host, int m, double* dev) {
+  // rows [0, n) from host (ld n), zero padding rows [n, npad)
+  if (c->npad != c->n) CK(fill_zero(dev, (size_t)c->npad * m, c->stream));
+  CK(cudaMemcpy2DAsync(dev, sizeof(double) * c->npad, host, sizeof(double) * c->n, sizeof(double) * c->n, m,
+                       cudaMemcpyHostToDevice, c->stream));
+}
+void download_block(feast_gpu_ctx* c, const double* dev, int m, double* host) {
+  CK(cudaMemcpy2DAsync(host, sizeof(double) * c->n, dev, sizeof(double) * c->npad, sizeof(double) * c->n, m,
+                       cudaMemcpyDeviceToHost, c->stream));
+}
+
+// residual_norms (residual.hpp:29-68) of the first m columns of X (device, ld npad)
+void residuals(feast_gpu_ctx* c, int m, const double* lam_host, const double* xdev, double* res,
+               int32_t* absonly, double* maxres) {
+  *maxres = 0.0;
+  if (m == 0) return;
+  DevBuf<double> lam, sums;
+  lam.ensure(m);
+  sums.ensure(3 * (size_t)m);
+  CK(cudaMemcpyAsync(lam.p, lam_host, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
+  apply_op(c, 0, xdev, c->AQ.p, m);
+  apply_op(c, 1, xdev, c->BQ.p, m);
+  CK(residual_sums(c->n, m, c->AQ.p, c->BQ.p, xdev, c->npad, lam.p, sums.p, c->stream));
+  std::vector<double> h(3 * (size_t)m);
+  CK(cudaMemcpyAsync(h.data(), sums.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  lam.release();
+  sums.release();
+  const double eps = 2.220446049250313e-16;
+  for (int j = 0; j < m; ++j) {
+    const double num = h[3 * j], den = h[3 * j + 1], xn = h[3 * j + 2];
+    const double floor = 4.0 * c->n * eps * c->norm_a1 * xn;
+    if (den <= std::max(1e-300, floor)) {
+      res[j] = num;
+      if (absonly) absonly[j] = 1;
+    } else {
+      res[j] = num / den;
+      if (absonly) absonly[j] = 0;
+    }
+    *maxres = std::max(*maxres, res[j]);
+  }
+}
+
+double secs(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// The FEAST loop (core.hpp:264-391), state resident on the device.
+void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_t* cfg,
+                 const double* initial_y, int y_cols, feast_result_t* out) {
+  const auto t_start = std::chrono::steady_clock::now();
+  if (!c->have_pencil) fail(FEAST_EINPUT, "feast_gpu: pencil not set");
+  if (!cfg || !out) fail(FEAST_EINPUT, "feast_gpu_solve: null argument");
+  const int n = c->n;
+  if (cfg->m0 < 1 || cfg->m0 > n) fail(FEAST_EINPUT, "feast_solve: m0 must be in [1, n]");
+  if (cfg->m0 > 1024) fail(FEAST_EINPUT, "feast_solve: m0 exceeds the supported reduced size");
+  if (cfg->max_loops < 1) fail(FEAST_EINPUT, "feast_solve: max_loops must be positive");
+  if (!(cfg->trace_tol > 0.0)) fail(FEAST_EINPUT, "feast_solve: trace_tol must be positive");
+  if (cfg->threads < 1) fail(FEAST_EINPUT, "feast_solve: threads must be positive");
+  if (initial_y && (y_cols < 1 || y_cols > cfg->m0)) fail(FEAST_EINPUT, "feast_solve: initial block shape mismatch");
+  if (!(emin < emax)) fail(FEAST_EINPUT, "SearchInterval: lambda_min must be strictly below lambda_max");
+
+  const bool same_contour = c->have_contour && c->emin == emin && c->emax == emax && c->ne == cfg->n_e;
+  if (!same_contour) build_contour(c, emin, emax, cfg->n_e);
+  const double effective_tol = cfg->trace_tol;  // direct solves: residual_target() == 0
+  ensure_workspace(c, cfg->m0);
+
+  *out = feast_result_t{out->eigenvalues, out->eigenvectors, out->residuals, out->residual_absolute_only,
+                        out->trace_history, out->in_interval_counts, out->subspace};
+  int m = initial_y ? y_cols : cfg->m0;
+  {
+    std::vector<double> y((size_t)n * m);
+    if (initial_y) std::memcpy(y.data(), initial_y, sizeof(double) * y.size());
+    else random_block(n, m, cfg->seed, y.data(), n);
+    upload_block(c, y.data(), m, c->Y.p);
+    sync(c);
+  }
+  if (!same_contour || !c->factored) c->factored = false;
+
+  double prev_trace = 0.0;
+  int prev_count = -1;
+  std::vector<double> history;
+  std::vector<int> counts;
+
+  auto finalize = [&](int status, const Reduced& rr, int pass) {
+    out->status = status;
+    out->loops_used = pass;
+    std::vector<int> keep;
+    for (int i = 0; i < rr.mo; ++i)
+      if (emin <= rr.evals[i] && rr.evals[i] <= emax) keep.push_back(i);
+    const int k = (int)keep.size();
+    out->m = k;
+    out->subspace_cols = rr.mo;
+    std::vector<double> lam(k);
+    for (int j = 0; j < k; ++j) lam[j] = rr.evals[keep[j]];
+    if (out->eigenvalues) std::memcpy(out->eigenvalues, lam.data(), sizeof(double) * k);
+    // eigenvectors = X[:, keep] -> Q buffer (free at this point)
+    if (k) {
+      CK(cudaMemcpyAsync(c->keep.p, keep.data(), sizeof(int) * k, cudaMemcpyHostToDevice, c->stream));
+      CK(gather_columns(c->X.p, c->npad, c->npad, c->keep.p, k, c->Q.p, c->npad, c->stream));
+    }
+    if (out->eigenvectors && k) download_block(c, c->Q.p, k, out->eigenvectors);
+    if (out->subspace) download_block(c, c->X.p, rr.mo, out->subspace);
+    std::vector<double> res(k);
+    std::vector<int32_t> ab(k);
+    residuals(c, k, lam.data(), c->Q.p, res.data(), ab.data(), &out->max_residual);
+    if (out->residuals && k) std::memcpy(out->residuals, res.data(), sizeof(double) * k);
+    if (out->residual_absolute_only && k) std::memcpy(out->residual_absolute_only, ab.data(), sizeof(int32_t) * k);
+    if (out->trace_history) std::memcpy(out->trace_history, history.data(), sizeof(double) * history.size());
+    if (out->in_interval_counts) std::memcpy(out->in_interval_counts, counts.data(), sizeof(int) * counts.size());
+    sync(c);
+    out->total_s = secs(t_start);
+  };
+
+  for (int pass = 0; pass <= cfg->max_loops; ++pass) {
+    if (cfg->low_memory) c->factored = false;
+    if (!c->factored) {
+      const auto t0 = std::chrono::steady_clock::now();
+      factor(c);
+      out->factorize_s += secs(t0);
+    }
+    const auto t_solve = std::chrono::steady_clock::now();
+    contour_pass(c, m);
+    sync(c);
+    out->solve_s += secs(t_solve);
+
+    const auto t_reduce = std::chrono::steady_clock::now();
+    Reduced rr;
+    try {
+      rr = rayleigh_ritz(c, m);
+      sync(c);
+    } catch (const Failure& f) {
+      if (f.code != FEAST_EBREAKDOWN) throw;
+      out->status = FEAST_STATUS_BREAKDOWN;
+      out->loops_used = pass;
+      out->reduce_s += secs(t_reduce);
+      if (out->trace_history) std::memcpy(out->trace_history, history.data(), sizeof(double) * history.size());
+      if (out->in_interval_counts) std::memcpy(out->in_interval_counts, counts.data(), sizeof(int) * counts.size());
+      out->total_s = secs(t_start);
+      return;
+    }
+    out->reduce_s += secs(t_reduce);
+
+    double tr = 0.0;
+    int cnt = 0;
+    for (int i = 0; i < rr.mo; ++i)
+      if (emin <= rr.evals[i] && rr.evals[i] <= emax) {
+        tr += rr.evals[i];
+        ++cnt;
+      }
+    history.push_back(tr);
+    counts.push_back(cnt);
+
+    if (cnt == cfg->m0) {
+      finalize(FEAST_STATUS_SATURATED, rr, pass);
+      return;
+    }
+    if (pass >= 1) {
+      if (cnt == 0 && prev_count == 0) {
+        finalize(FEAST_STATUS_NO_EIGENVALUES, rr, pass);
+        return;
+      }
+      const double denom = std::max(std::fabs(tr), emax - emin);
+      if (cnt == prev_count && std::fabs(tr - prev_trace) <= effective_tol * denom) {
+        finalize(FEAST_STATUS_CONVERGED, rr, pass);
+        return;
+      }
+    }
+    if (pass == cfg->max_loops) {
+      finalize(FEAST_STATUS_MAX_LOOPS, rr, pass);
+      return;
+    }
+    prev_trace = tr;
+    prev_count = cnt;
+    m = rr.mo;
+    apply_op(c, 1, c->X.p, c->Y.p, m);  // y = B X over all retained Ritz vectors (core.hpp:387)
+  }
+  fail(FEAST_EINTERNAL, "feast_solve: unreachable");
+}
+
+template <typename F>
+int guarded(feast_gpu_ctx* c, F&& f) {
+  try {
+    if (c) CK(cudaSetDevice(c->device));
+    f();
+    return FEAST_OK;
+  } catch (const Failure& e) {
+    if (c) c->err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    if (c) c->err = e.what();
+    return FEAST_EINTERNAL;
+  }
+}
+
+}  // namespace
+
+// =============================================================================
+// C-ABI
+// =============================================================================
+extern "C" {
+
+int feast_gpu_abi_version(void) { return FEAST_GPU_ABI_VERSION; }
+
+int feast_gpu_create(int device, void* stream, feast_gpu_ctx** out) {
+  if (!out) return FEAST_EINPUT;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return FEAST_ECUDA;
+  if (device < 0 || device >= ndev) return FEAST_EINPUT;
+  auto* c = new feast_gpu_ctx();
+  c->device = device;
+  const int rc = guarded(c, [&] {
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    for (auto& e : c->ev) CK(cudaEventCreate(&e));
+  });
+  if (rc) {
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return FEAST_OK;
+}
+
+void feast_gpu_destroy(feast_gpu_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (DevBuf<double>* d : {&c->A, &c->Bm, &c->Y, &c->Q, &c->X, &c->AQ, &c->BQ, &c->T, &c->gw, &c->Aq, &c->Bq,
+                            &c->Cm, &c->Lm, &c->Phi, &c->Ev, &c->Vm, &c->S, &c->Tm})
+    d->release();
+  for (DevBuf<double2>* d : {&c->abdiag, &c->ablow, &c->dz, &c->dcoeff, &c->sinv, &c->gfac, &c->lu, &c->dinv,
+                             &c->scratch, &c->W})
+    d->release();
+  for (DevBuf<int>* d : {&c->ipiv, &c->perm, &c->status, &c->keep}) d->release();
+  if (c->eig) eig_destroy(c->eig);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->comm && nccl().commDestroy) nccl().commDestroy(c->comm);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* feast_gpu_last_error(const feast_gpu_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int feast_gpu_nccl_unique_id(void* id_out) {
+  NcclApi& api = nccl();
+  if (!api.getUniqueId) return FEAST_ENCCL;
+  return api.getUniqueId(id_out) == 0 ? FEAST_OK : FEAST_ENCCL;
+}
+
+int feast_gpu_set_comm(feast_gpu_ctx* c, const void* uid, int rank, int nranks) {
+  return guarded(c, [&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) fail(FEAST_EINPUT, "set_comm: bad rank/nranks");
+    c->rank = rank;
+    c->nranks = nranks;
+    c->have_contour = false;
+    c->factored = false;
+    if (nranks > 1) {
+      NcclApi& api = nccl();
+      auto init = (nccl_init_fn)dlsym(api.h, "ncclCommInitRank");
+      if (!init) fail(FEAST_ENCCL, "NCCL not available");
+      NcclUid id;
+      std::memcpy(id.internal, uid, 128);
+      const int r = init(&c->comm, nranks, id, rank);
+      if (r != 0) fail(FEAST_ENCCL, "ncclCommInitRank failed");
+    }
+  });
+}
+
+int feast_gpu_set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operator_t* b) {
+  return guarded(c, [&] { set_pencil(c, a, b); });
+}
+
+int feast_gpu_prepare(feast_gpu_ctx* c, double emin, double emax, int n_e) {
+  return guarded(c, [&] {
+    if (!c->have_pencil) fail(FEAST_EINPUT, "feast_gpu: pencil not set");
+    build_contour(c, emin, emax, n_e);
+    factor(c);
+  });
+}
+
+int feast_gpu_contour(const feast_gpu_ctx* c, double* z, double* coeff) {
+  if (!c || !c->have_contour) return FEAST_EINPUT;
+  for (int e = 0; e < c->ne; ++e) {
+    if (z) { z[2 * e] = c->z[e].x; z[2 * e + 1] = c->z[e].y; }
+    if (coeff) { coeff[2 * e] = c->coeff[e].x; coeff[2 * e + 1] = c->coeff[e].y; }
+  }
+  return FEAST_OK;
+}
+
+int feast_gpu_solve_shift(feast_gpu_ctx* c, int e, double* rhs, int m, int mode) {
+  return guarded(c, [&] {
+    if (!c->factored) fail(FEAST_EINPUT, "feast_gpu: factors not prepared");
+    if (e < c->e0 || e >= c->e1) fail(FEAST_EINPUT, "solve_shift: node not owned by this rank");
+    if (m < 1) fail(FEAST_EINPUT, "solve_shift: no right-hand sides");
+    ensure_workspace(c, m);
+    const int s = e - c->e0;
+    const size_t nv = (size_t)c->npad * m;
+    double2* w = c->W.p + s * nv;
+    CK(cudaMemsetAsync(w, 0, sizeof(double2) * nv, c->stream));
+    CK(cudaMemcpy2DAsync(w, sizeof(double2) * c->npad, rhs, sizeof(double2) * c->n, sizeof(double2) * c->n, m,
+                         cudaMemcpyHostToDevice, c->stream));
+    // (zB - A)^H = conj(zB - A) for real symmetric A, B: solve at conj by conjugating in/out
+    if (mode) CK(conj_inplace(w, nv, c->stream));
+    if (c->blocktri) {
+      const size_t bb = (size_t)c->b * c->b;
+      BtSweepArgs a{c->L, c->b, 1, m, c->npad, c->ablow.p, c->dz.p + s, c->dcoeff.p + s,
+                    c->sinv.p + s * c->L * bb, c->gfac.p + s * (c->L - 1) * bb, nullptr, nullptr, w, 1};
+      CK(bt_sweep(a, c->stream));
+    } else {
+      const int n = c->n, nb = kDenseNb, nblk = (n + nb - 1) / nb;
+      DenseSolveArgs a{n, 1, m, c->npad, c->lu.p + (size_t)s * n * n, c->perm.p + (size_t)s * n,
+                       c->dinv.p + (size_t)s * nblk * 2 * nb * nb, c->dcoeff.p + s, nullptr, c->T.p, w, 1};
+      CK(dense_solve(a, c->stream));
+    }
+    if (mode) CK(conj_inplace(w, nv, c->stream));
+    CK(cudaMemcpy2DAsync(rhs, sizeof(double2) * c->n, w, sizeof(double2) * c->npad, sizeof(double2) * c->n, m,
+                         cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+  });
+}
+
+int feast_gpu_contour_pass(feast_gpu_ctx* c, const double* y, int m, double* q) {
+  return guarded(c, [&] {
+    if (!c->factored) fail(FEAST_EINPUT, "feast_gpu: factors not prepared");
+    ensure_workspace(c, m);
+    upload_block(c, y, m, c->Y.p);
+    contour_pass(c, m);
+    download_block(c, c->Q.p, m, q);
+    sync(c);
+  });
+}
+
+int feast_gpu_rayleigh_ritz(feast_gpu_ctx* c, const double* q, int m, double* eigenvalues, double* x, int* m_out,
+                            int* truncated) {
+  return guarded(c, [&] {
+    if (!c->have_pencil) fail(FEAST_EINPUT, "feast_gpu: pencil not set");
+    if (m < 1 || m > 1024) fail(FEAST_EINPUT, "rayleigh_ritz: bad block width");
+    ensure_workspace(c, m);
+    upload_block(c, q, m, c->Q.p);
+    Reduced r = rayleigh_ritz(c, m);
+    if (eigenvalues) std::memcpy(eigenvalues, r.evals.data(), sizeof(double) * r.mo);
+    if (x) download_block(c, c->X.p, r.mo, x);
+    sync(c);
+    if (m_out) *m_out = r.mo;
+    if (truncated) *truncated = r.truncated;
+  });
+}
+
+int feast_gpu_reduced_gevp(feast_gpu_ctx* c, int m, const double* a_q, const double* b_q, double* eigenvalues,
+                           double* phi, int* m_out, int* truncated) {
+  return guarded(c, [&] {
+    if (m < 1 || m > 1024) fail(FEAST_EINPUT, "reduced_gevp: blocks must be square with equal size");
+    if (c->mcap < m) {
+      const size_t mm = (size_t)m * m;
+      for (DevBuf<double>* d : {&c->Aq, &c->Bq, &c->Cm, &c->Lm, &c->Phi, &c->Vm, &c->S, &c->Tm}) d->ensure(mm);
+      c->Ev.ensure(m);
+      c->keep.ensure(m);
+      c->gw.ensure(mm * 64);
+      ensure_eig(c, m);
+    }
+    c->status.ensure(1);
+    CK(cudaMemcpyAsync(c->Aq.p, a_q, sizeof(double) * m * m, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->Bq.p, b_q, sizeof(double) * m * m, cudaMemcpyHostToDevice, c->stream));
+    Reduced r = reduced_gevp(c, m);
+    if (eigenvalues) std::memcpy(eigenvalues, r.evals.data(), sizeof(double) * r.mo);
+    if (phi) CK(cudaMemcpyAsync(phi, c->Phi.p, sizeof(double) * m * r.mo, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    if (m_out) *m_out = r.mo;
+    if (truncated) *truncated = r.truncated;
+  });
+}
+
+int feast_gpu_residuals(feast_gpu_ctx* c, int m, const double* lambdas, const double* x, double* res,
+                        int32_t* absonly, double* maxres) {
+  return guarded(c, [&] {
+    if (!c->have_pencil) fail(FEAST_EINPUT, "feast_gpu: pencil not set");
+    ensure_workspace(c, std::max(m, 1));
+    upload_block(c, x, m, c->X.p);
+    double mx = 0.0;
+    std::vector<double> r(m);
+    std::vector<int32_t> ab(m);
+    residuals(c, m, lambdas, c->X.p, r.data(), ab.data(), &mx);
+    if (res) std::memcpy(res, r.data(), sizeof(double) * m);
+    if (absonly) std::memcpy(absonly, ab.data(), sizeof(int32_t) * m);
+    if (maxres) *maxres = mx;
+  });
+}
+
+int feast_gpu_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_t* config,
+                    const double* initial_y, int y_cols, feast_result_t* result) {
+  return guarded(c, [&] { feast_solve(c, emin, emax, config, initial_y, y_cols, result); });
+}
+
+int feast_gpu_bench_init(feast_gpu_ctx* c, int m0, uint64_t seed) {
+  return guarded(c, [&] {
+    if (!c->factored) fail(FEAST_EINPUT, "feast_gpu: factors not prepared");
+    ensure_workspace(c, m0);
+    std::vector<double> y((size_t)c->n * m0);
+    random_block(c->n, m0, seed, y.data(), c->n);
+    upload_block(c, y.data(), m0, c->Y.p);
+    sync(c);
+    c->bench_m = m0;
+  });
+}
+
+int feast_gpu_bench_passes(feast_gpu_ctx* c, int passes, double* total_ms, double* phase_ms) {
+  return guarded(c, [&] {
+    if (!c->factored || c->bench_m < 1) fail(FEAST_EINPUT, "bench: call feast_gpu_bench_init first");
+    double ph[3] = {0, 0, 0};
+    float ms = 0;
+    CK(cudaEventRecord(c->ev[0], c->stream));
+    for (int p = 0; p < passes; ++p) {
+      CK(cudaEventRecord(c->ev[2], c->stream));
+      contour_pass(c, c->bench_m);
+      CK(cudaEventRecord(c->ev[3], c->stream));
+      Reduced r = rayleigh_ritz(c, c->bench_m);
+      apply_op(c, 1, c->X.p, c->Y.p, r.mo);
+      CK(cudaEventRecord(c->ev[4], c->stream));
+      CK(cudaEventSynchronize(c->ev[4]));
+      CK(cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]));
+      ph[0] += ms;
+      CK(cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]));
+      ph[2] += ms;
+      c->bench_m = r.mo;
+    }
+    CK(cudaEventRecord(c->ev[1], c->stream));
+    CK(cudaEventSynchronize(c->ev[1]));
+    CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+    if (total_ms) *total_ms = ms;
+    if (phase_ms) { phase_ms[0] = ph[0]; phase_ms[1] = ph[1]; phase_ms[2] = ph[2]; }
+  });
+}
+
+int64_t feast_gpu_launch_count(const feast_gpu_ctx*) { return g_launches; }
+
+}  // extern "C"

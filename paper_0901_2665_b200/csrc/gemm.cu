@@ -1,0 +1,379 @@
+// gemm.cu — FP64 DMMA GEMMs for sm_100a (mma.sync.m8n8k4.f64; tcgen05 has no f64 kind).
+//
+//  zgemm_batched : complex, column-major, C = alpha*A*B + beta*C, batched over contour
+//                  nodes (blockIdx.z). Used by the dense LU trailing update
+//                  (lu.hpp:44-50 restated blocked), the U12 = L11^{-1} A12 panel solve
+//                  and both blocked triangular sweeps of the multi-RHS solve (lu.hpp:56-95).
+//  dgemm         : real, C = alpha*op(A)*op(B) + beta*C with op in {N, T}; split-K with a
+//                  fixed-order reduction (deterministic) for the tall-skinny projections
+//                  Q^T (AQ), Q^T (BQ) of rayleigh_ritz (core.hpp:233-234, dense.hpp:76-90),
+//                  X = Q Phi (dense.hpp:59-73) and dense operator applies (operator.hpp:132).
+//
+// Tiles: 64x64 per CTA, 8 warps as 2 (m) x 4 (n), warp tile 32x16 = 4x2 DMMA 8x8 tiles,
+// 3-stage cp.async ring. Shared layouts are padded so fragment loads are conflict-free:
+// A as [k][m] (stride 64+2 complex / 64+4 real), B as [n][k] (stride BK+4).
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace feastgpu {
+
+FEAST_DEV void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+FEAST_DEV void cp_async8_zfill(void* smem, const void* gmem, bool valid) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  const int n = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+
+// ===========================================================================
+// complex
+// ===========================================================================
+namespace zg {
+constexpr int BM = 64, BN = 64, BK = 16, NS = 3;
+constexpr int SA = BM + 2;  // [k][m] double2
+constexpr int SB = BK + 4;  // [n][k] double2
+constexpr int STAGE = BK * SA + BN * SB;
+}  // namespace zg
+
+struct ZgemmArgs {
+  int m, n, k;
+  double2 alpha, beta;
+  const double2* a;
+  int lda;
+  int64_t sa;
+  const double2* b;
+  int ldb;
+  int64_t sb;
+  double2* c;
+  int ldc;
+  int64_t sc;
+};
+
+__global__ void __launch_bounds__(256, 2) zgemm_kernel(ZgemmArgs p) {
+  using namespace zg;
+  extern __shared__ __align__(16) double2 zsm[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const double2* A = p.a + blockIdx.z * p.sa;
+  const double2* B = p.b + blockIdx.z * p.sb;
+  double2* C = p.c + blockIdx.z * p.sc;
+  const int nk = (p.k + BK - 1) / BK;
+
+  auto load = [&](int kt) {
+    if (kt < nk) {
+      double2* As = zsm + (kt % NS) * STAGE;
+      double2* Bs = As + BK * SA;
+      const int k0 = kt * BK;
+      // A tile: BM x BK, element (m, k); 1024 entries, 4 per thread
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int e = tid + r * 256;
+        const int mm = e & (BM - 1), kk = e >> 6;
+        const bool v = (m0 + mm < p.m) && (k0 + kk < p.k);
+        const double2* src = v ? A + (m0 + mm) + (int64_t)(k0 + kk) * p.lda : A;
+        cp_async16_zfill(As + kk * SA + mm, src, v);
+      }
+      // B tile: BK x BN, element (k, n)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int e = tid + r * 256;
+        const int kk = e & (BK - 1), nn = e >> 4;
+        const bool v = (n0 + nn < p.n) && (k0 + kk < p.k);
+        const double2* src = v ? B + (k0 + kk) + (int64_t)(n0 + nn) * p.ldb : B;
+        cp_async16_zfill(Bs + nn * SB + kk, src, v);
+      }
+    }
+    cp_async_commit();
+  };
+
+  CAcc acc[4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j].zero();
+
+#pragma unroll
+  for (int s = 0; s < NS - 1; ++s) load(s);
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<NS - 2>();
+    __syncthreads();
+    load(kt + NS - 1);
+    const double2* As = zsm + (kt % NS) * STAGE;
+    const double2* Bs = As + BK * SA;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double2 af[4], bf[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = As[(kk + t4) * SA + wm * 32 + i * 8 + g];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bf[j] = Bs[(wn * 16 + j * 8 + g) * SB + kk + t4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) cmma(acc[i][j], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();  // B may alias C (in-place triangular apply): all reads done before writes
+
+  const bool beta0 = p.beta.x == 0.0 && p.beta.y == 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = m0 + wm * 32 + i * 8 + g;
+    if (row >= p.m) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = n0 + wn * 16 + j * 8 + 2 * t4 + h;
+        if (col >= p.n) continue;
+        const double2 v = make_double2(h ? acc[i][j].r1 : acc[i][j].r0, h ? acc[i][j].i1 : acc[i][j].i0);
+        double2* cp = C + row + (int64_t)col * p.ldc;
+        double2 out = cmul(p.alpha, v);
+        if (!beta0) out = cadd(out, cmul(p.beta, *cp));
+        *cp = out;
+      }
+    }
+  }
+}
+
+cudaError_t zgemm_batched(int m, int n, int k, double2 alpha, const double2* a, int lda, int64_t sa,
+                          const double2* b, int ldb, int64_t sb, double2 beta, double2* c, int ldc,
+                          int64_t sc, int batch, cudaStream_t st) {
+  if (m <= 0 || n <= 0 || batch <= 0) return cudaSuccess;
+  static bool attr = false;
+  const int smem = zg::NS * zg::STAGE * (int)sizeof(double2);
+  if (!attr) {
+    cudaFuncSetAttribute(zgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  ZgemmArgs p{m, n, k, alpha, beta, a, lda, sa, b, ldb, sb, c, ldc, sc};
+  dim3 grid((n + zg::BN - 1) / zg::BN, (m + zg::BM - 1) / zg::BM, batch);
+  zgemm_kernel<<<grid, 256, smem, st>>>(p);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// ===========================================================================
+// real
+// ===========================================================================
+namespace dg {
+constexpr int BM = 64, BN = 64, BK = 32, NS = 3;
+constexpr int SA = BM + 4;   // N-layout A: [k][m];   T-layout A: [m][k] with stride BK+4
+constexpr int SAT = BK + 4;
+constexpr int SB = BK + 4;   // N-layout B: [n][k];   T-layout B: [k][n] with stride BN+4
+constexpr int SBT = BN + 4;
+constexpr int A_ELEMS = BK * SA > BM * SAT ? BK * SA : BM * SAT;
+constexpr int B_ELEMS = BN * SB > BK * SBT ? BN * SB : BK * SBT;
+constexpr int STAGE = A_ELEMS + B_ELEMS;
+}  // namespace dg
+
+struct DgemmArgs {
+  int m, n, k;
+  int kslice;  // K per z-slice
+  const double* a;
+  int lda;
+  const double* b;
+  int ldb;
+  double* c;
+  int ldc;
+  int64_t sc;  // stride between z-slices of the output
+  double alpha, beta;
+};
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(256, 2) dgemm_kernel(DgemmArgs p) {
+  using namespace dg;
+  extern __shared__ __align__(16) double dsm[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int kbeg = blockIdx.z * p.kslice;
+  const int kend = min(p.k, kbeg + p.kslice);
+  const int nk = (kend - kbeg + BK - 1) / BK;
+  double* C = p.c + blockIdx.z * p.sc;
+
+  auto load = [&](int kt) {
+    if (kt < nk) {
+      double* As = dsm + (kt % NS) * STAGE;
+      double* Bs = As + A_ELEMS;
+      const int k0 = kbeg + kt * BK;
+      // A tile (BM x BK), 2048 doubles, 8 per thread
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int e = tid + r * 256;
+        if (!TA) {  // A(m, k) at a[m + k*lda] -> As[k][m]
+          const int mm = e & (BM - 1), kk = e >> 6;
+          const bool v = (m0 + mm < p.m) && (k0 + kk < kend);
+          const double* src = v ? p.a + (m0 + mm) + (int64_t)(k0 + kk) * p.lda : p.a;
+          cp_async8_zfill(As + kk * SA + mm, src, v);
+        } else {    // op(A)(m, k) = a[k + m*lda] -> As[m][k]
+          const int kk = e & (BK - 1), mm = e >> 5;
+          const bool v = (m0 + mm < p.m) && (k0 + kk < kend);
+          const double* src = v ? p.a + (k0 + kk) + (int64_t)(m0 + mm) * p.lda : p.a;
+          cp_async8_zfill(As + mm * SAT + kk, src, v);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int e = tid + r * 256;
+        if (!TB) {  // B(k, n) at b[k + n*ldb] -> Bs[n][k]
+          const int kk = e & (BK - 1), nn = e >> 5;
+          const bool v = (n0 + nn < p.n) && (k0 + kk < kend);
+          const double* src = v ? p.b + (k0 + kk) + (int64_t)(n0 + nn) * p.ldb : p.b;
+          cp_async8_zfill(Bs + nn * SB + kk, src, v);
+        } else {    // op(B)(k, n) = b[n + k*ldb] -> Bs[k][n]
+          const int nn = e & (BN - 1), kk = e >> 6;
+          const bool v = (n0 + nn < p.n) && (k0 + kk < kend);
+          const double* src = v ? p.b + (n0 + nn) + (int64_t)(k0 + kk) * p.ldb : p.b;
+          cp_async8_zfill(Bs + kk * SBT + nn, src, v);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+
+  double acc[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < NS - 1; ++s) load(s);
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<NS - 2>();
+    __syncthreads();
+    load(kt + NS - 1);
+    const double* As = dsm + (kt % NS) * STAGE;
+    const double* Bs = As + A_ELEMS;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[4], bf[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int mm = wm * 32 + i * 8 + g;
+        af[i] = TA ? As[mm * SAT + kk + t4] : As[(kk + t4) * SA + mm];
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int nn = wn * 16 + j * 8 + g;
+        bf[j] = TB ? Bs[(kk + t4) * SBT + nn] : Bs[nn * SB + kk + t4];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = m0 + wm * 32 + i * 8 + g;
+    if (row >= p.m) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = n0 + wn * 16 + j * 8 + 2 * t4 + h;
+        if (col >= p.n) continue;
+        double* cp = C + row + (int64_t)col * p.ldc;
+        const double v = p.alpha * acc[i][j][h];
+        *cp = p.beta == 0.0 ? v : v + p.beta * *cp;
+      }
+  }
+}
+
+__global__ void splitk_reduce_kernel(const double* __restrict__ w, int slices, int64_t slice, int m,
+                                     int n, double alpha, double beta, double* __restrict__ c,
+                                     int ldc) {
+  const int64_t total = (int64_t)m * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx % m, j = idx / m;
+    double s = 0.0;
+    for (int z = 0; z < slices; ++z) s += w[z * slice + i + j * m];
+    double* cp = c + i + j * ldc;
+    *cp = beta == 0.0 ? alpha * s : alpha * s + beta * *cp;
+  }
+}
+
+template <bool TA, bool TB>
+static void set_attr_once() {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(dgemm_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         dg::NS * dg::STAGE * (int)sizeof(double));
+    done = true;
+  }
+}
+
+cudaError_t dgemm(char ta, char tb, int m, int n, int k, double alpha, const double* A, int lda,
+                  const double* B, int ldb, double beta, double* C, int ldc, double* work,
+                  size_t work_elems, cudaStream_t st) {
+  if (m <= 0 || n <= 0) return cudaSuccess;
+  const bool TA = ta == 'T' || ta == 't', TB = tb == 'T' || tb == 't';
+  const int tiles = ((m + dg::BM - 1) / dg::BM) * ((n + dg::BN - 1) / dg::BN);
+  // split K until ~2 waves of CTAs, keeping >= 256 of K per slice
+  int slices = 1;
+  while (tiles * slices < 2 * 148 && k / (slices * 2) >= 256) slices *= 2;
+  if ((size_t)slices * m * n > work_elems) slices = 1;
+  int kslice = (k + slices - 1) / slices;
+  kslice = (kslice + dg::BK - 1) / dg::BK * dg::BK;
+  slices = (k + kslice - 1) / kslice;
+  if (slices < 1) slices = 1;
+  DgemmArgs p{m, n, k, kslice, A, lda, B, ldb, C, ldc, 0, alpha, beta};
+  if (slices > 1) {
+    p.c = work;
+    p.ldc = m;
+    p.sc = (int64_t)m * n;
+    p.alpha = 1.0;
+    p.beta = 0.0;
+  }
+  dim3 grid((n + dg::BN - 1) / dg::BN, (m + dg::BM - 1) / dg::BM, slices);
+  const int smem = dg::NS * dg::STAGE * (int)sizeof(double);
+  if (!TA && !TB) { set_attr_once<false, false>(); dgemm_kernel<false, false><<<grid, 256, smem, st>>>(p); }
+  if (TA && !TB) { set_attr_once<true, false>(); dgemm_kernel<true, false><<<grid, 256, smem, st>>>(p); }
+  if (!TA && TB) { set_attr_once<false, true>(); dgemm_kernel<false, true><<<grid, 256, smem, st>>>(p); }
+  if (TA && TB) { set_attr_once<true, true>(); dgemm_kernel<true, true><<<grid, 256, smem, st>>>(p); }
+  ++g_launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || slices == 1) return e;
+  const int64_t total = (int64_t)m * n;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(work, slices, (int64_t)m * n, m, n, alpha, beta, C, ldc);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+__global__ void symmetrize_kernel(double* c, int m, int ld) {
+  const int64_t total = (int64_t)m * m;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(idx % m), j = (int)(idx / m);
+    if (i < j) {
+      // hermitian_part (dense.hpp:127-134): (M(i,j) + M(j,i)) * 0.5 on both sides
+      const double v = (c[i + (int64_t)j * ld] + c[j + (int64_t)i * ld]) * 0.5;
+      c[i + (int64_t)j * ld] = v;
+      c[j + (int64_t)i * ld] = v;
+    }
+  }
+}
+
+cudaError_t symmetrize(double* c, int m, int ld, cudaStream_t st) {
+  const int64_t total = (int64_t)m * m;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+  symmetrize_kernel<<<blocks, 256, 0, st>>>(c, m, ld);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+}  // namespace feastgpu

@@ -1,0 +1,128 @@
+// kernels.h — host-side launchers for the sm_100a kernels of libfeastgpu.
+// Every launcher enqueues on `st` and returns cudaGetLastError() of its launch(es).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace feastgpu {
+
+struct cplx_t {
+  double re, im;
+};
+
+// Launch counter (evidence that the native path ran; read via feast_gpu_launch_count).
+extern int64_t g_launches;
+
+// ---------------- block-tridiagonal shifted solves (block Thomas) -------------
+// A/B in block-tridiagonal storage packed as double2 (x = A entry, y = B entry):
+//   abdiag: L blocks b*b col-major, ablow: (L-1) blocks, C_l = M(l+1, l).
+// For node slot s (0..nodes-1): shift z[s]; factors Sinv[s] (L*b*b), G[s] ((L-1)*b*b).
+struct BtFactorArgs {
+  int L, b, nodes;
+  const double2* abdiag;
+  const double2* ablow;
+  const double2* z;       // [nodes]
+  double2* sinv;          // nodes * L*b*b
+  double2* g;             // nodes * (L-1)*b*b (may alias unused if L == 1)
+  double2* scratch;       // nodes * b * 2b (used when b > 64)
+  int* status;            // set to 1 on a singular block pivot
+};
+cudaError_t bt_factor(const BtFactorArgs& a, cudaStream_t st);
+
+// Sweeps: for every node slot s and column j < m:
+//   real mode   : T_s = Re(coeff[s] * (z_s B - A)^{-1} Y)     (Y real, T real, ld = ldv)
+//   complex mode: W_s <- (z_s B - A)^{-1} W_s                 (complex in place, ld = ldv)
+struct BtSweepArgs {
+  int L, b, nodes, m, ldv;
+  const double2* ablow;
+  const double2* z;
+  const double2* coeff;
+  const double2* sinv;
+  const double2* g;
+  const double* y;        // real mode input (n*m, shared by nodes)
+  double* t;              // real mode output: nodes * ldv*m
+  double2* w;             // workspace / complex in-out: nodes * ldv*m
+  int complex_mode;
+};
+cudaError_t bt_sweep(const BtSweepArgs& a, cudaStream_t st);
+
+// Q = -sum_{s} T_s (ascending s), n rows (ld) x m
+cudaError_t reduce_terms(const double* t, int nodes, int64_t slice, int n, int m, int ld,
+                         double* q, cudaStream_t st);
+
+// block-tridiagonal real operator apply: Y = Op * X (ld n, m columns); uses .x of ab when
+// which == 0 (A) and .y when which == 1 (B)
+cudaError_t bt_apply(int L, int b, const double2* abdiag, const double2* ablow, int which,
+                     const double* x, int ldx, double* y, int ldy, int m, cudaStream_t st);
+
+// ---------------- dense shifted solves (batched complex LU) -------------------
+struct DenseFactorArgs {
+  int n, nodes;
+  const double* a;        // n*n real
+  const double* bm;       // n*n real
+  const double2* z;
+  double2* lu;            // nodes * n*n complex
+  int* ipiv;              // nodes * n
+  int* perm;              // nodes * n (row permutation applied to the RHS)
+  double2* dinv;          // nodes * (n/nb) * 2 * nb*nb : inverses of unit-L and U diagonal blocks
+  int* status;
+};
+cudaError_t dense_factor(const DenseFactorArgs& a, cudaStream_t st);
+constexpr int kDenseNb = 64;
+
+struct DenseSolveArgs {
+  int n, nodes, m, ldv;
+  const double2* lu;
+  const int* perm;
+  const double2* dinv;
+  const double2* coeff;
+  const double* y;
+  double* t;
+  double2* w;
+  int complex_mode;
+};
+cudaError_t dense_solve(const DenseSolveArgs& a, cudaStream_t st);
+
+// ---------------- real GEMM (DMMA) -------------------------------------------
+// C(m x n) = alpha * op(A) * op(B) + beta * C, column-major; op = 'N' or 'T'.
+// Split-K with a deterministic reduction when k is large relative to m*n.
+cudaError_t dgemm(char ta, char tb, int m, int n, int k, double alpha, const double* A, int lda,
+                  const double* B, int ldb, double beta, double* C, int ldc, double* work,
+                  size_t work_elems, cudaStream_t st);
+
+// C = (M + M^T)/2 in place (square m x m, ld)
+cudaError_t symmetrize(double* c, int m, int ld, cudaStream_t st);
+
+// ---------------- reduced generalized eigensolver ----------------------------
+struct EigWork;  // opaque, sized for mmax
+EigWork* eig_create(int mmax);
+void eig_destroy(EigWork* w);
+// Symmetric eigen-decomposition of W (m x m, ld m, overwritten): eigenvalues ascending
+// into `evals` (device), vectors into `v` (device, m x m), stable order.
+cudaError_t sym_eig(EigWork* w, int m, double* a, double* evals, double* v, cudaStream_t st);
+// Cholesky with relative pivot floor: L (lower, in place in `a`), status[0] = 1 on failure.
+cudaError_t cholesky(int m, double* a, double rel_tol, int* status, cudaStream_t st);
+// X <- L^{-1} X   (L lower m x m, X m x ncols)
+cudaError_t trsm_lower(int m, const double* l, double* x, int ldx, int ncols, cudaStream_t st);
+// X <- L^{-T} X
+cudaError_t trsm_lower_t(int m, const double* l, double* x, int ldx, int ncols, cudaStream_t st);
+// transpose copy: dst(n x m) = src(m x n)^T
+cudaError_t transpose(const double* src, int m, int n, int lds, double* dst, int ldd,
+                      cudaStream_t st);
+// S(:, j) = V(:, keep[j]) / sqrt(d[keep[j]])
+cudaError_t scale_columns(const double* v, int m, const int* keep, const double* d, int nk,
+                          double* s, cudaStream_t st);
+
+// ---------------- residuals ---------------------------------------------------
+// per column j: num = sum|AX - lam_j BX|, den = sum|AX|, xn = sum|X|  -> out[3*j + {0,1,2}]
+cudaError_t residual_sums(int n, int m, const double* ax, const double* bx, const double* x,
+                          int ld, const double* lam, double* out, cudaStream_t st);
+
+// misc
+cudaError_t fill_zero(double* p, size_t count, cudaStream_t st);
+cudaError_t gather_columns(const double* src, int ld, int n, const int* idx, int m, double* dst,
+                           int ldd, cudaStream_t st);
+cudaError_t conj_inplace(double2* p, size_t count, cudaStream_t st);
+
+}  // namespace feastgpu
