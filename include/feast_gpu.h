@@ -174,12 +174,15 @@ int feast_gpu_solve(feast_gpu_ctx* ctx, double emin, double emax, const feast_co
                     const double* initial_y, int y_cols, feast_result_t* result);
 
 /* Benchmark hook: runs `passes` loop bodies (contour pass + Rayleigh-Ritz + trace/count
- * + Y = B X) on the device-resident state left by the last feast_gpu_solve or
- * feast_gpu_bench_init, with no stopping rule; returns device milliseconds measured
- * with CUDA events on the context stream, plus per-phase milliseconds
- * (phase_ms[0] = contour solves, [1] = Q reduction/allreduce, [2] = Rayleigh-Ritz). */
+ * + Y = B X) on the device-resident state set up by feast_gpu_bench_init (after
+ * feast_gpu_prepare), with no stopping rule. Each pass is bracketed by CUDA events on the
+ * context stream; when flush_bytes > 0 a buffer of that size is overwritten between
+ * passes, outside the events, so every pass starts with a cold L2. Outputs: summed
+ * device milliseconds and phase_ms[4] = {contour-solve kernel(s), Q reduction +
+ * allreduce, Rayleigh-Ritz + Y = B X, dominant kernel alone}. */
 int feast_gpu_bench_init(feast_gpu_ctx* ctx, int m0, uint64_t seed);
-int feast_gpu_bench_passes(feast_gpu_ctx* ctx, int passes, double* total_ms, double* phase_ms);
+int feast_gpu_bench_passes(feast_gpu_ctx* ctx, int passes, size_t flush_bytes, double* total_ms,
+                           double* phase_ms);
 
 /* Number of kernel launches this context issued since creation (evidence counter). */
 int64_t feast_gpu_launch_count(const feast_gpu_ctx* ctx);

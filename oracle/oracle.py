@@ -59,6 +59,9 @@ def lib(kind="reference"):
     L.ref_feast_solve.argtypes = [_op, _op, C.c_double, C.c_double,
                                   C.POINTER(abi.FeastConfigT), _dp, C.c_int,
                                   C.POINTER(abi.FeastResultT)]
+    if hasattr(L, "ref_bench_passes"):
+        L.ref_bench_passes.argtypes = [_op, _op, C.c_double, C.c_double, C.c_int, C.c_int,
+                                       C.c_uint64, C.c_int, C.c_int, _dp]
     _cache[kind] = L
     return L
 
@@ -174,6 +177,18 @@ def reference_gevp(a, b, kind="reference"):
     ca, cb = a.to_c(), b.to_c()
     _check(L, L.ref_reference_gevp(C.byref(ca), C.byref(cb), abi.dptr(ev), abi.dptr(vec)))
     return ev, vec
+
+
+def bench_passes(problem, passes, threads=1, kind="reference"):
+    """Times the reference loop body (factor once, then `passes` passes of
+    accumulate + Rayleigh-Ritz + Y = B X). Returns dict(factorize_s, solve_s, reduce_s, count)."""
+    L = lib(kind)
+    p = problem
+    out = np.zeros(4)
+    ca, cb = p.a.to_c(), p.b.to_c()
+    _check(L, L.ref_bench_passes(C.byref(ca), C.byref(cb), p.emin, p.emax, p.m0, p.n_e, p.seed,
+                                 threads, passes, abi.dptr(out)))
+    return dict(factorize_s=out[0], solve_s=out[1], reduce_s=out[2], count=int(out[3]))
 
 
 def feast_solve(problem, threads=1, low_memory=False, initial_y=None, kind="reference",

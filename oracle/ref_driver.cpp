@@ -12,6 +12,7 @@
 // Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline / --impl reference)
 // may load the library built from this file.
 
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -252,6 +253,46 @@ int ref_residual_norms(const feast_operator_t* a, const feast_operator_t* b, int
       absonly[j] = rep.absolute_only[j] ? 1 : 0;
     }
     *maxres = rep.max_value;
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+
+// Pass-level timing of the reference's own loop body (core.hpp:304-311 factors, then per
+// pass accumulate_subspace_real + rayleigh_ritz + y = B X, core.hpp:340-387), with no
+// stopping rule. out[0] = factorize seconds, out[1] = summed solve seconds, out[2] = summed
+// reduce seconds, out[3] = in-interval count of the last pass.
+int ref_bench_passes(const feast_operator_t* a, const feast_operator_t* b, double emin, double emax,
+                     int m0, int ne, uint64_t seed, int threads, int passes, double* out) {
+  try {
+    using clk = std::chrono::steady_clock;
+    auto since = [](clk::time_point t0) {
+      return std::chrono::duration<double>(clk::now() - t0).count();
+    };
+    const auto ra = to_ref(a);
+    const auto rb = to_ref(b);
+    const feast::SearchInterval iv(emin, emax);
+    const auto contour = feast::quadrature::build_contour(iv, ne);
+    feast::DirectSolver<double> solver(ra, rb);
+    std::vector<std::unique_ptr<feast::ShiftSystem>> keep(ne);
+    std::vector<const feast::ShiftSystem*> sys(ne);
+    auto t0 = clk::now();
+    feast::detail::parallel_points(ne, threads, [&](int e) { keep[e] = solver.prepare(contour.points[e].z); });
+    for (int e = 0; e < ne; ++e) sys[e] = keep[e].get();
+    out[0] = since(t0);
+    out[1] = out[2] = 0.0;
+    DenseMatrix<double> y = feast::random_block<double>(ra.n(), m0, seed);
+    for (int p = 0; p < passes; ++p) {
+      t0 = clk::now();
+      const DenseMatrix<double> q = feast::accumulate_subspace_real(y, contour, sys, threads);
+      out[1] += since(t0);
+      t0 = clk::now();
+      const auto rr = feast::rayleigh_ritz(ra, rb, q);
+      out[2] += since(t0);
+      out[3] = feast::trace_of_in_interval(rr.eigenvalues, iv).count;
+      y = rb.apply(rr.x);
+    }
     return 0;
   } catch (const std::exception& e) {
     return code_of(e);

@@ -190,6 +190,7 @@ struct feast_gpu_ctx {
   int eig_cap = 0;
   // bench state
   int bench_m = 0;
+  bool timing = false;
   cudaEvent_t ev[8] = {};
 
   int owned() const { return e1 - e0; }
@@ -553,6 +554,7 @@ void factor(feast_gpu_ctx* c) {
 void contour_pass(feast_gpu_ctx* c, int m) {
   const int own = c->owned();
   const size_t nv = (size_t)c->npad * m;
+  if (c->timing) CK(cudaEventRecord(c->ev[2], c->stream));
   if (own > 0) {
     if (c->blocktri) {
       BtSweepArgs a{c->L, c->b, own, m, c->npad, c->ablow.p, c->dz.p, c->dcoeff.p, c->sinv.p,
@@ -562,8 +564,10 @@ void contour_pass(feast_gpu_ctx* c, int m) {
       DenseSolveArgs a{c->n, own, m, c->npad, c->lu.p, c->perm.p, c->dinv.p, c->dcoeff.p, c->Y.p, c->T.p, c->W.p, 0};
       CK(dense_solve(a, c->stream));
     }
+    if (c->timing) CK(cudaEventRecord(c->ev[3], c->stream));
     CK(reduce_terms(c->T.p, own, (int64_t)nv, c->npad, m, c->npad, c->Q.p, c->stream));
   } else {
+    if (c->timing) CK(cudaEventRecord(c->ev[3], c->stream));
     CK(fill_zero(c->Q.p, nv, c->stream));
   }
   if (c->nranks > 1) {
@@ -1070,31 +1074,40 @@ int feast_gpu_bench_init(feast_gpu_ctx* c, int m0, uint64_t seed) {
   });
 }
 
-int feast_gpu_bench_passes(feast_gpu_ctx* c, int passes, double* total_ms, double* phase_ms) {
+int feast_gpu_bench_passes(feast_gpu_ctx* c, int passes, size_t flush_bytes, double* total_ms,
+                           double* phase_ms) {
   return guarded(c, [&] {
     if (!c->factored || c->bench_m < 1) fail(FEAST_EINPUT, "bench: call feast_gpu_bench_init first");
-    double ph[3] = {0, 0, 0};
+    double ph[4] = {0, 0, 0, 0}, tot = 0.0;
     float ms = 0;
-    CK(cudaEventRecord(c->ev[0], c->stream));
+    DevBuf<char> flush;
+    if (flush_bytes) flush.ensure(flush_bytes);
+    c->timing = true;
     for (int p = 0; p < passes; ++p) {
-      CK(cudaEventRecord(c->ev[2], c->stream));
-      contour_pass(c, c->bench_m);
-      CK(cudaEventRecord(c->ev[3], c->stream));
+      if (flush_bytes) CK(cudaMemsetAsync(flush.p, p & 0xff, flush_bytes, c->stream));
+      CK(cudaEventRecord(c->ev[0], c->stream));
+      contour_pass(c, c->bench_m);  // records ev[2..5] around the solve and the reduction
+      CK(cudaEventRecord(c->ev[1], c->stream));
       Reduced r = rayleigh_ritz(c, c->bench_m);
       apply_op(c, 1, c->X.p, c->Y.p, r.mo);
-      CK(cudaEventRecord(c->ev[4], c->stream));
-      CK(cudaEventSynchronize(c->ev[4]));
+      CK(cudaEventRecord(c->ev[6], c->stream));
+      CK(cudaEventSynchronize(c->ev[6]));
+      CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[6]));
+      tot += ms;
       CK(cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]));
       ph[0] += ms;
-      CK(cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]));
+      ph[3] += ms;
+      CK(cudaEventElapsedTime(&ms, c->ev[3], c->ev[1]));
+      ph[1] += ms;
+      CK(cudaEventElapsedTime(&ms, c->ev[1], c->ev[6]));
       ph[2] += ms;
       c->bench_m = r.mo;
     }
-    CK(cudaEventRecord(c->ev[1], c->stream));
-    CK(cudaEventSynchronize(c->ev[1]));
-    CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
-    if (total_ms) *total_ms = ms;
-    if (phase_ms) { phase_ms[0] = ph[0]; phase_ms[1] = ph[1]; phase_ms[2] = ph[2]; }
+    c->timing = false;
+    flush.release();
+    if (total_ms) *total_ms = tot;
+    if (phase_ms)
+      for (int i = 0; i < 4; ++i) phase_ms[i] = ph[i];
   });
 }
 

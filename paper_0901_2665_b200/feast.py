@@ -86,7 +86,7 @@ def load_library(path: str = LIB_PATH):
     L.feast_gpu_solve.argtypes = [C.c_void_p, C.c_double, C.c_double, C.POINTER(abi.FeastConfigT),
                                   _dp, C.c_int, C.POINTER(abi.FeastResultT)]
     L.feast_gpu_bench_init.argtypes = [C.c_void_p, C.c_int, C.c_uint64]
-    L.feast_gpu_bench_passes.argtypes = [C.c_void_p, C.c_int, _dp, _dp]
+    L.feast_gpu_bench_passes.argtypes = [C.c_void_p, C.c_int, C.c_size_t, _dp, _dp]
     L.feast_gpu_launch_count.argtypes = [C.c_void_p]
     L.feast_gpu_launch_count.restype = C.c_int64
     _lib = L
@@ -302,7 +302,7 @@ class GpuContext:
         self._check(self.L.feast_gpu_solve(self.h, interval.lo, interval.hi, C.byref(cfg), abi.dptr(y0),
                                            0 if y0 is None else y0.shape[1], C.byref(r)))
         m, k, loops = r.m, r.subspace_cols, r.loops_used
-        nh = len([0 for _ in range(loops + 1)]) if r.status != 4 else loops
+        nh = loops if r.status == 4 else loops + 1  # breakdown returns before pushing (core.hpp:347-353)
         return FeastResult(
             eigenvalues=out["eigenvalues"][:m].copy(),
             eigenvectors=_cols(out["eigenvectors"], n, m),
@@ -320,10 +320,12 @@ class GpuContext:
     def bench_init(self, m0: int, seed: int = 42):
         self._check(self.L.feast_gpu_bench_init(self.h, m0, seed))
 
-    def bench_passes(self, passes: int):
+    def bench_passes(self, passes: int, flush_bytes: int = 0):
+        """Device ms over `passes` loop bodies (L2 flushed between passes when flush_bytes)
+        and phase ms {solve kernels, Q reduction+allreduce, Rayleigh-Ritz, dominant kernel}."""
         tot = C.c_double(0)
-        ph = np.zeros(3)
-        self._check(self.L.feast_gpu_bench_passes(self.h, passes, C.byref(tot), abi.dptr(ph)))
+        ph = np.zeros(4)
+        self._check(self.L.feast_gpu_bench_passes(self.h, passes, flush_bytes, C.byref(tot), abi.dptr(ph)))
         return tot.value, ph
 
     def launch_count(self) -> int:

@@ -1,0 +1,230 @@
+"""Parity of the CUDA path (through the C-ABI) with the CPU oracle on the same inputs.
+
+Tolerances (BASELINE.json north_star and the reference's own tests):
+  * in-interval eigenvalue count exact, same status as the oracle;
+  * eigenvalues within 1e-10 relative (reference criterion 1e-10*max(1,|lambda|),
+    acceptance.cpp:344-395, and also 1e-10 of the interval width for |lambda| << 1);
+  * max principal angle <= 1e-8, measured by sines (B-orthonormal bases);
+  * residual ||Ax - lambda Bx|| / (||A|| ||x||) <= 1e-10 and the reference's 1-norm ratio
+    (residual.hpp) <= 1e-9;
+  * shifted solves: relative error <= 1e-12 (test_linalg.cpp:138-190);
+  * contour accumulation: <= 1e-11 * max(1, max|Q_ref|) (test_core.cpp:94-109).
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.golden_problems import fixtures, load_fixture
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def F():
+    from paper_0901_2665_b200 import feast
+    feast.load_library()
+    return feast
+
+
+@pytest.fixture(scope="module")
+def ctx(F):
+    c = F.GpuContext(0)
+    yield c
+    c.close()
+
+
+def rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(1.0, float(np.max(np.abs(b)))))
+
+
+def sin_max_angle(x, xr, bmat):
+    """max principal angle between span(x) and span(xr), B-inner product, via sines:
+    sin = sigma_max((I - Xr Xr^T B) X) with B-orthonormal X, Xr."""
+    def borth(v):
+        g = v.T @ (bmat @ v)
+        w, u = np.linalg.eigh(0.5 * (g + g.T))
+        return v @ (u / np.sqrt(w))
+    x, xr = borth(x), borth(xr)
+    r = x - xr @ (xr.T @ (bmat @ x))
+    # B-norm of the residual block
+    g = r.T @ (bmat @ r)
+    return float(np.sqrt(max(np.max(np.linalg.eigvalsh(0.5 * (g + g.T))), 0.0)))
+
+
+FIX = fixtures()
+
+
+@pytest.mark.parametrize("path", FIX, ids=lambda p: p.split("/")[-1][:-4])
+def test_solve_shift_matches_reference(ctx, path):
+    prob, _ = load_fixture(path)
+    ctx.set_pencil(prob.a, prob.b)
+    ctx.prepare(prob.emin, prob.emax, prob.n_e)
+    z, _ = ctx.contour()
+    rng = np.random.default_rng(1)
+    rhs = rng.standard_normal((prob.n, 5)) + 1j * rng.standard_normal((prob.n, 5))
+    for e in (0, prob.n_e - 1):
+        for mode in (0, 1):
+            x = ctx.solve_shift(e, rhs, bool(mode))
+            xr = O.shift_solve(prob.a, prob.b, z[e], rhs, mode)
+            assert rel(x, xr) <= 1e-12, (e, mode, rel(x, xr))
+
+
+@pytest.mark.parametrize("path", FIX, ids=lambda p: p.split("/")[-1][:-4])
+def test_contour_pass_matches_accumulate(ctx, path):
+    prob, _ = load_fixture(path)
+    ctx.set_pencil(prob.a, prob.b)
+    ctx.prepare(prob.emin, prob.emax, prob.n_e)
+    y = O.random_block(prob.n, prob.m0, 42)
+    q = ctx.contour_pass(y)
+    qr = O.accumulate_real(prob.a, prob.b, prob.emin, prob.emax, prob.n_e, y)
+    assert np.max(np.abs(q - qr)) <= 1e-11 * max(1.0, np.max(np.abs(qr)))
+
+
+@pytest.mark.parametrize("path", FIX, ids=lambda p: p.split("/")[-1][:-4])
+def test_feast_solve_matches_reference_fixture(ctx, F, path):
+    prob, g = load_fixture(path)
+    ctx.set_pencil(prob.a, prob.b)
+    r = ctx.solve(F.SearchInterval(prob.emin, prob.emax),
+                  F.FeastConfig(m0=prob.m0, n_e=prob.n_e, trace_tol=prob.trace_tol,
+                                max_loops=prob.max_loops, seed=prob.seed))
+    assert r.status == str(g["status"])
+    m = int(g["m"])
+    assert len(r.eigenvalues) == m == prob.expected_count
+    ev_ref = g["eigenvalues"]
+    assert np.all(np.abs(r.eigenvalues - ev_ref) <= 1e-10 * np.maximum(1.0, np.abs(ev_ref)))
+    assert np.all(np.abs(r.eigenvalues - ev_ref) <= 1e-10 * (prob.emax - prob.emin))
+    assert r.max_residual <= 1e-9
+    bmat = prob.b.to_dense()
+    amat = prob.a.to_dense()
+    assert sin_max_angle(r.eigenvectors, g["eigenvectors"], bmat) <= 1e-8
+    an = np.linalg.norm(amat, 2)
+    for j in range(m):
+        x = r.eigenvectors[:, j]
+        res = np.linalg.norm(amat @ x - r.eigenvalues[j] * (bmat @ x)) / (an * np.linalg.norm(x))
+        assert res <= 1e-10
+    # B-orthonormal Ritz vectors (FeastResult contract, core.hpp:64)
+    gram = r.eigenvectors.T @ bmat @ r.eigenvectors
+    assert np.max(np.abs(gram - np.eye(m))) <= 1e-10
+    assert len(r.trace_history) == r.loops_used + 1
+    assert np.allclose(r.trace_history[-1], g["trace_history"][-1], rtol=1e-10)
+
+
+def test_reduced_gevp_matches_reference(ctx):
+    rng = np.random.default_rng(9)
+    for m in (1, 7, 40, 160, 192, 300):
+        a = rng.uniform(-1, 1, (m, m)); a = a + a.T
+        r = rng.uniform(-1, 1, (m, m)); b = r.T @ r / m + np.eye(m); b = 0.5 * (b + b.T)
+        ev, phi, tr = ctx.reduced_gevp(a, b)
+        evr, _, trr = O.reduced_gevp(a, b)
+        assert tr == trr and np.all(np.diff(ev) >= 0)
+        assert np.max(np.abs(ev - evr)) <= 1e-10 * max(1.0, np.max(np.abs(evr)))
+        assert np.max(np.abs(a @ phi - b @ phi * ev)) <= 1e-10 * max(1, m / 50)
+        assert np.max(np.abs(phi.T @ b @ phi - np.eye(m))) <= 1e-10 * max(1, m / 50)
+
+
+def test_reduced_gevp_truncation_path(ctx):
+    # B_Q rank deficient -> Cholesky floor fails -> spectral truncation (eigh.hpp:204-224)
+    rng = np.random.default_rng(4)
+    m = 40
+    a = rng.uniform(-1, 1, (m, m)); a = a + a.T
+    r = rng.uniform(-1, 1, (m, m)); r[:, :13] = 0.0
+    b = r.T @ r / m; b = 0.5 * (b + b.T)
+    ev, phi, tr = ctx.reduced_gevp(a, b)
+    evr, _, trr = O.reduced_gevp(a, b)
+    assert tr and trr and len(ev) == len(evr) == m - 13
+    assert np.max(np.abs(ev - evr)) <= 1e-9 * max(1.0, np.max(np.abs(evr)))
+
+
+def test_reduced_gevp_breakdown(ctx, F):
+    m = 6
+    with pytest.raises(F.SubspaceBreakdown):
+        ctx.reduced_gevp(np.eye(m), np.zeros((m, m)))
+
+
+def test_reduced_gevp_multiplicity(ctx):
+    # repeated eigenvalues (acceptance criterion 4's concern): Jacobi keeps them exact
+    rng = np.random.default_rng(5)
+    m = 48
+    q, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    lam = np.repeat(np.arange(12, dtype=float), 4)
+    a = (q * lam) @ q.T; a = 0.5 * (a + a.T)
+    ev, phi, tr = ctx.reduced_gevp(a, np.eye(m))
+    assert np.max(np.abs(ev - lam)) <= 1e-12 * m
+    assert np.max(np.abs(phi.T @ phi - np.eye(m))) <= 1e-12 * m
+
+
+def test_residuals_match_reference(ctx):
+    prob, g = load_fixture(FIX[0])
+    ctx.set_pencil(prob.a, prob.b)
+    res, ab, mx = ctx.residual_norms(g["eigenvalues"], g["eigenvectors"])
+    rr, rab, rmx = O.residual_norms(prob.a, prob.b, g["eigenvalues"], g["eigenvectors"])
+    assert np.array_equal(ab, rab)
+    assert np.allclose(res, rr, rtol=1e-6, atol=1e-16)
+
+
+def test_input_errors(ctx, F):
+    prob, _ = load_fixture(FIX[0])
+    ctx.set_pencil(prob.a, prob.b)
+    iv = F.SearchInterval(prob.emin, prob.emax)
+    for bad in (dict(m0=0), dict(m0=prob.n + 1), dict(m0=4, max_loops=0), dict(m0=4, trace_tol=0.0),
+                dict(m0=4, threads=0), dict(m0=4, n_e=65)):
+        with pytest.raises(F.InputError):
+            ctx.solve(iv, F.FeastConfig(**bad))
+    with pytest.raises(F.InputError):
+        F.SearchInterval(1.0, 1.0)
+    with pytest.raises(F.InputError):
+        ctx.solve(iv, F.FeastConfig(m0=4), initial_y=np.ones((prob.n, 5)))
+    from paper_0901_2665_b200.problems import Operator
+    asym = np.eye(4); asym[0, 1] = 1.0
+    with pytest.raises(F.InputError):
+        ctx.set_pencil(Operator.from_dense(asym), Operator.from_dense(np.eye(4)))
+
+
+def test_empty_interval_and_saturation(ctx, F):
+    prob, _ = load_fixture(FIX[0])
+    ctx.set_pencil(prob.a, prob.b)
+    ev = np.linalg.eigvalsh(np.linalg.solve(np.linalg.cholesky(prob.b.to_dense()),
+                                            np.linalg.solve(np.linalg.cholesky(prob.b.to_dense()),
+                                                            prob.a.to_dense()).T))
+    top = ev.max()
+    r = ctx.solve(F.SearchInterval(top + 10.0, top + 11.0), F.FeastConfig(m0=4))
+    ref = O.feast_solve(_with(prob, top + 10.0, top + 11.0, 4))
+    assert r.status == ref["status"] == "no-eigenvalues-in-interval" and len(r.eigenvalues) == 0
+    r = ctx.solve(F.SearchInterval(prob.emin, prob.emax), F.FeastConfig(m0=3))
+    ref = O.feast_solve(_with(prob, prob.emin, prob.emax, 3))
+    assert r.status == ref["status"] == "subspace-saturated"
+
+
+def _with(prob, lo, hi, m0):
+    import copy
+    p = copy.copy(prob)
+    p.emin, p.emax, p.m0 = lo, hi, m0
+    return p
+
+
+def test_determinism_and_low_memory(ctx, F):
+    prob, _ = load_fixture(FIX[-1])
+    ctx.set_pencil(prob.a, prob.b)
+    iv = F.SearchInterval(prob.emin, prob.emax)
+    cfg = F.FeastConfig(m0=prob.m0, n_e=prob.n_e, seed=prob.seed)
+    r1 = ctx.solve(iv, cfg)
+    r2 = ctx.solve(iv, cfg)
+    cfg.low_memory = True
+    cfg.threads = 4
+    r3 = ctx.solve(iv, cfg)
+    for r in (r2, r3):  # bit-identical across runs, threads and low_memory (test_core.cpp:341-376)
+        assert np.array_equal(r1.eigenvalues, r.eigenvalues)
+        assert np.array_equal(r1.eigenvectors, r.eigenvectors)
+        assert np.array_equal(r1.trace_history, r.trace_history)
+
+
+def test_warm_start_one_loop(ctx, F):
+    # test_core.cpp:378-395: restart from B * subspace converges in one loop
+    prob, _ = load_fixture(FIX[0])
+    ctx.set_pencil(prob.a, prob.b)
+    iv = F.SearchInterval(prob.emin, prob.emax)
+    r = ctx.solve(iv, F.FeastConfig(m0=prob.m0, seed=prob.seed))
+    y0 = prob.b.matmul(r.subspace)
+    r2 = ctx.solve(iv, F.FeastConfig(m0=prob.m0), initial_y=y0)
+    assert r2.status == "converged" and r2.loops_used <= 1
+    assert np.allclose(r2.eigenvalues, r.eigenvalues, rtol=1e-12, atol=1e-14)
