@@ -1,0 +1,17 @@
+"""Runs W+1 FEAST passes of a config through the C-ABI (for ncu launch lists)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_0901_2665_b200 import feast as F  # noqa: E402
+from paper_0901_2665_b200 import problems as P  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+passes = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+prob = {"cfg1": P.config1, "cfg2": P.config2, "cfg3": P.config3, "cfg4": P.config4}[cfg]()
+ctx = F.GpuContext(0)
+ctx.set_pencil(prob.a, prob.b)
+ctx.prepare(prob.emin, prob.emax, prob.n_e)
+ctx.bench_init(prob.m0, prob.seed)
+ms, ph = ctx.bench_passes(passes, 0)
+print(f"{cfg}: {passes} passes {ms:.3f} ms  phases {ph}")
