@@ -1,0 +1,273 @@
+// chol.cu — tiled Cholesky and triangular solves for the reduced problem (m <= 1024).
+//
+//   cholesky      lower Cholesky with the relative pivot floor of eigh.hpp:20-43
+//                 (kCholeskyRelTol = 1e-13 -> NotPositiveDefinite -> truncation fallback).
+//                 Blocked right-looking, 32x32 tiles, one cooperative kernel: per panel the
+//                 diagonal tile is factored in shared memory (and inverted for the solves),
+//                 the panel below is solved against it, then the trailing tiles are updated
+//                 by all CTAs — three grid barriers per 32-column panel.
+//   trsm_lower    X <- L^{-1} X      (solve_lower_in_place, eigh.hpp:46-58)
+//   trsm_lower_t  X <- L^{-T} X      (solve_lower_adjoint_in_place, eigh.hpp:61-73)
+//                 One CTA per 16-column tile of X; the tile stays in shared memory while the
+//                 CTA walks the block substitution chain, L tiles streamed from L2, diagonal
+//                 tiles applied through their precomputed inverses.
+
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace feastgpu {
+
+constexpr int TB = 32;  // tile
+constexpr int TL = TB + 1;
+
+struct CholArgs {
+  int m;
+  double* a;
+  double* dinv;  // nblk * TB*TB, inverse of each diagonal L tile (ld TB)
+  double rel_tol;
+  int* status;
+};
+
+__global__ void __launch_bounds__(256) chol_kernel(CholArgs p) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double T[TB * TL], U[TB * TL], Vt[TB * TL];
+  __shared__ double red[33];
+  __shared__ int bad;
+  const int m = p.m, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int nblk = (m + TB - 1) / TB;
+  double* A = p.a;
+
+  // max initial diagonal (every CTA computes the same value)
+  double md = 0.0;
+  for (int i = tid; i < m; i += nt) md = fmax(md, A[i + (int64_t)i * m]);
+  md = warp_max(md);
+  if (lane == 0) red[warp] = md;
+  __syncthreads();
+  if (tid == 0) {
+    double r = 0.0;
+    for (int w = 0; w < (nt >> 5); ++w) r = fmax(r, red[w]);
+    red[32] = r;
+    bad = 0;
+  }
+  __syncthreads();
+  const double floor_ = p.rel_tol * red[32];
+
+  for (int pn = 0; pn < nblk; ++pn) {
+    const int p0 = pn * TB, pb = min(TB, m - p0);
+    // ---- phase 1: diagonal tile (CTA 0, one warp) ----
+    if (blockIdx.x == 0) {
+      for (int idx = tid; idx < TB * TB; idx += nt) {
+        const int i = idx % TB, j = idx / TB;
+        T[i + j * TL] = (i < pb && j < pb) ? A[(p0 + i) + (int64_t)(p0 + j) * m] : (i == j ? 1.0 : 0.0);
+      }
+      __syncthreads();
+      if (warp == 0) {
+        // left-looking by columns; lane i owns row i
+        for (int j = 0; j < pb; ++j) {
+          double s = T[lane + j * TL];
+          for (int k = 0; k < j; ++k) s -= T[lane + k * TL] * T[j + k * TL];
+          const double d = __shfl_sync(0xffffffffu, s, j);
+          if (d <= 0.0 || d <= floor_) {
+            if (lane == 0) bad = 1;
+            break;
+          }
+          const double ljj = sqrt(d);
+          if (lane == j) T[j + j * TL] = ljj;
+          else if (lane > j) T[lane + j * TL] = s / ljj;
+          __syncwarp();
+        }
+        __syncwarp();
+        if (!bad) {
+          // column `lane` of L^{-1}
+          double x[TB];
+#pragma unroll
+          for (int i = 0; i < TB; ++i) x[i] = 0.0;
+          for (int i = 0; i < pb; ++i) {
+            double s = (i == lane) ? 1.0 : 0.0;
+            for (int k = lane; k < i; ++k) s -= T[i + k * TL] * x[k];
+            x[i] = (i >= lane) ? s / T[i + i * TL] : 0.0;
+          }
+          double* Di = p.dinv + (int64_t)pn * TB * TB;
+          for (int i = 0; i < TB; ++i) Di[i + lane * TB] = (lane < pb && i < pb) ? x[i] : (i == lane ? 1.0 : 0.0);
+        }
+      }
+      __syncthreads();
+      if (bad) {
+        if (tid == 0) p.status[0] = 1;
+      } else {
+        for (int idx = tid; idx < pb * pb; idx += nt) {
+          const int i = idx % pb, j = idx / pb;
+          A[(p0 + i) + (int64_t)(p0 + j) * m] = i >= j ? T[i + j * TL] : 0.0;
+        }
+      }
+    }
+    grid.sync();
+    if (p.status[0]) return;
+    // ---- phase 2: L_ip = A_ip * (L_pp^{-1})^T for row tiles below ----
+    const int below = nblk - pn - 1;
+    for (int task = blockIdx.x; task < below; task += gridDim.x) {
+      const int i0 = (pn + 1 + task) * TB, ib = min(TB, m - i0);
+      const double* Di = p.dinv + (int64_t)pn * TB * TB;
+      for (int idx = tid; idx < TB * TB; idx += nt) {
+        const int r = idx % TB, c = idx / TB;
+        U[r + c * TL] = (r < ib && c < pb) ? A[(i0 + r) + (int64_t)(p0 + c) * m] : 0.0;
+        Vt[r + c * TL] = Di[r + c * TB];
+      }
+      __syncthreads();
+      for (int idx = tid; idx < ib * pb; idx += nt) {
+        const int r = idx % ib, c = idx / ib;
+        double s = 0.0;
+        for (int k = 0; k < pb; ++k) s += U[r + k * TL] * Vt[c + k * TL];
+        A[(i0 + r) + (int64_t)(p0 + c) * m] = s;
+      }
+      __syncthreads();
+    }
+    grid.sync();
+    // ---- phase 3: A_ij -= L_ip L_jp^T, p < j <= i ----
+    const int ntask = below * (below + 1) / 2;
+    for (int task = blockIdx.x; task < ntask; task += gridDim.x) {
+      int ti = 0;
+      while ((ti + 1) * (ti + 2) / 2 <= task) ++ti;
+      const int tj = task - ti * (ti + 1) / 2;
+      const int i0 = (pn + 1 + ti) * TB, j0 = (pn + 1 + tj) * TB;
+      const int ib = min(TB, m - i0), jb = min(TB, m - j0);
+      for (int idx = tid; idx < TB * TB; idx += nt) {
+        const int r = idx % TB, c = idx / TB;
+        U[r + c * TL] = (r < ib && c < pb) ? A[(i0 + r) + (int64_t)(p0 + c) * m] : 0.0;
+        Vt[r + c * TL] = (r < jb && c < pb) ? A[(j0 + r) + (int64_t)(p0 + c) * m] : 0.0;
+      }
+      __syncthreads();
+      for (int idx = tid; idx < ib * jb; idx += nt) {
+        const int r = idx % ib, c = idx / ib;
+        double s = 0.0;
+        for (int k = 0; k < pb; ++k) s += U[r + k * TL] * Vt[c + k * TL];
+        A[(i0 + r) + (int64_t)(j0 + c) * m] -= s;
+      }
+      __syncthreads();
+    }
+    grid.sync();
+  }
+  // strict upper triangle -> 0 (cholesky() returns a lower factor)
+  for (int64_t idx = blockIdx.x * (int64_t)nt + tid; idx < (int64_t)m * m; idx += (int64_t)gridDim.x * nt) {
+    const int i = (int)(idx % m), j = (int)(idx / m);
+    if (i < j) A[idx] = 0.0;
+  }
+}
+
+cudaError_t cholesky(int m, double* a, double rel_tol, int* status, double* dinv, cudaStream_t st) {
+  if (m > 1024 || m < 1) return cudaErrorInvalidValue;
+  const int nblk = (m + TB - 1) / TB;
+  int grid = std::max(1, nblk * (nblk - 1) / 2);
+  int dev = 0, sms = 148, occ = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chol_kernel, 256, 0);
+  grid = std::min(grid, sms * std::max(occ, 1));
+  CholArgs p{m, a, dinv, rel_tol, status};
+  void* args[] = {&p};
+  cudaError_t e = cudaLaunchCooperativeKernel((void*)chol_kernel, grid, 256, args, 0, st);
+  ++g_launches;
+  return e;
+}
+
+// ---------------------------------------------------------------------------
+// triangular solves on 16-column tiles of X (resident in shared memory)
+// ---------------------------------------------------------------------------
+constexpr int XC = 16;
+
+template <bool TRANS>
+__global__ void __launch_bounds__(256) trsm_tile_kernel(int m, const double* __restrict__ l,
+                                                        const double* __restrict__ dinv, double* x,
+                                                        int ldx, int ncols) {
+  extern __shared__ double xs[];  // m x XC, column-major (ld m)
+  __shared__ double Lt[TB * TL];
+  __shared__ double acc_s[TB * XC];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int c0 = blockIdx.x * XC, nc = min(XC, ncols - c0);
+  const int nblk = (m + TB - 1) / TB;
+  for (int idx = tid; idx < m * XC; idx += nt) {
+    const int i = idx % m, c = idx / m;
+    xs[idx] = c < nc ? x[i + (int64_t)(c0 + c) * ldx] : 0.0;
+  }
+  __syncthreads();
+  // thread -> (row r, columns c, c+8) of a TB x XC tile
+  const int r = tid % TB, cA = tid / TB, cB = cA + 8;
+  for (int step = 0; step < nblk; ++step) {
+    const int bi = TRANS ? nblk - 1 - step : step;
+    const int i0 = bi * TB, ib = min(TB, m - i0);
+    double accA = (r < ib) ? xs[(i0 + r) + cA * m] : 0.0;
+    double accB = (r < ib) ? xs[(i0 + r) + cB * m] : 0.0;
+    const int jlo = TRANS ? bi + 1 : 0, jhi = TRANS ? nblk : bi;
+    for (int bj = jlo; bj < jhi; ++bj) {
+      const int j0 = bj * TB, jb = min(TB, m - j0);
+      // stage the L tile feeding this update: L_ij (lower) or L_ji^T (transposed)
+      for (int idx = tid; idx < TB * TB; idx += nt) {
+        const int rr = idx % TB, cc = idx / TB;
+        double v = 0.0;
+        if (!TRANS) { if (rr < ib && cc < jb) v = l[(i0 + rr) + (int64_t)(j0 + cc) * m]; }
+        else { if (cc < jb && rr < ib) v = l[(j0 + cc) + (int64_t)(i0 + rr) * m]; }
+        Lt[rr + cc * TL] = v;
+      }
+      __syncthreads();
+      double sA = 0.0, sB = 0.0;
+      for (int k = 0; k < jb; ++k) {
+        const double lv = Lt[r + k * TL];
+        sA += lv * xs[(j0 + k) + cA * m];
+        sB += lv * xs[(j0 + k) + cB * m];
+      }
+      accA -= sA;
+      accB -= sB;
+      __syncthreads();
+    }
+    // apply the inverse of the diagonal tile (transposed for L^{-T})
+    acc_s[r + cA * TB] = accA;
+    acc_s[r + cB * TB] = accB;
+    const double* Di = dinv + (int64_t)bi * TB * TB;
+    for (int idx = tid; idx < TB * TB; idx += nt) {
+      const int rr = idx % TB, cc = idx / TB;
+      Lt[rr + cc * TL] = TRANS ? Di[cc + rr * TB] : Di[rr + cc * TB];
+    }
+    __syncthreads();
+    if (r < ib) {
+      double sA = 0.0, sB = 0.0;
+      for (int k = 0; k < ib; ++k) {
+        sA += Lt[r + k * TL] * acc_s[k + cA * TB];
+        sB += Lt[r + k * TL] * acc_s[k + cB * TB];
+      }
+      xs[(i0 + r) + cA * m] = sA;
+      xs[(i0 + r) + cB * m] = sB;
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < m * XC; idx += nt) {
+    const int i = idx % m, c = idx / m;
+    if (c < nc) x[i + (int64_t)(c0 + c) * ldx] = xs[idx];
+  }
+}
+
+template <bool TRANS>
+static cudaError_t trsm_tiles(int m, const double* l, const double* dinv, double* x, int ldx, int ncols,
+                              cudaStream_t st) {
+  const size_t sm = sizeof(double) * (size_t)m * XC;
+  cudaFuncSetAttribute(trsm_tile_kernel<TRANS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  trsm_tile_kernel<TRANS><<<(ncols + XC - 1) / XC, 256, sm, st>>>(m, l, dinv, x, ldx, ncols);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t trsm_lower(int m, const double* l, const double* dinv, double* x, int ldx, int ncols,
+                       cudaStream_t st) {
+  return trsm_tiles<false>(m, l, dinv, x, ldx, ncols, st);
+}
+cudaError_t trsm_lower_t(int m, const double* l, const double* dinv, double* x, int ldx, int ncols,
+                         cudaStream_t st) {
+  return trsm_tiles<true>(m, l, dinv, x, ldx, ncols, st);
+}
+
+}  // namespace feastgpu

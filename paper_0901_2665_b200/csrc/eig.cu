@@ -1,9 +1,6 @@
 // eig.cu — the reduced generalized eigensolver on device (reduced_gevp, eigh.hpp:178-225).
 //
-//   cholesky      lower Cholesky with the relative pivot floor of eigh.hpp:20-43
-//                 (kCholeskyRelTol = 1e-13 -> NotPositiveDefinite -> truncation fallback)
-//   trsm_lower    X <- L^{-1} X      (solve_lower_in_place, eigh.hpp:46-58)
-//   trsm_lower_t  X <- L^{-T} X      (solve_lower_adjoint_in_place, eigh.hpp:61-73)
+//   (cholesky / trsm_lower / trsm_lower_t live in chol.cu)
 //   sym_eig       symmetric eigendecomposition, ascending, stable order (jacobi_eigh,
 //                 eigh.hpp:84-163). Same method class as the reference (cyclic Jacobi, so
 //                 multiplicities and tiny eigenvalues come out as accurately), re-shaped for
@@ -42,113 +39,6 @@ __device__ double block_sum(double v, double* red) {
   }
   __syncthreads();
   return red[32];
-}
-
-__global__ void __launch_bounds__(1024) cholesky_kernel(int m, double* a, double rel_tol, int* status) {
-  __shared__ double red[33];
-  __shared__ double rowj[1024];
-  double md = 0.0;
-  for (int i = threadIdx.x; i < m; i += blockDim.x) md = fmax(md, a[i + (int64_t)i * m]);
-  // block max
-  {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    md = warp_max(md);
-    if (lane == 0) red[warp] = md;
-    __syncthreads();
-    if (warp == 0) {
-      double r = lane < nw ? red[lane] : 0.0;
-      r = warp_max(r);
-      if (lane == 0) red[32] = r;
-    }
-    __syncthreads();
-    md = red[32];
-    __syncthreads();
-  }
-  const double floor = rel_tol * md;
-  for (int j = 0; j < m; ++j) {
-    // row j of L (k < j) into shared memory
-    for (int k = threadIdx.x; k < j; k += blockDim.x) rowj[k] = a[j + (int64_t)k * m];
-    __syncthreads();
-    double part = 0.0;
-    for (int k = threadIdx.x; k < j; k += blockDim.x) part += rowj[k] * rowj[k];
-    const double d = a[j + (int64_t)j * m] - block_sum(part, red);
-    if (d <= 0.0 || d <= floor) {
-      if (threadIdx.x == 0) status[0] = 1;
-      return;
-    }
-    const double ljj = sqrt(d);
-    for (int i = j + 1 + threadIdx.x; i < m; i += blockDim.x) {
-      double s = a[i + (int64_t)j * m];
-      for (int k = 0; k < j; ++k) s -= a[i + (int64_t)k * m] * rowj[k];
-      a[i + (int64_t)j * m] = s / ljj;
-    }
-    if (threadIdx.x == 0) a[j + (int64_t)j * m] = ljj;
-    __syncthreads();
-  }
-  // zero the strict upper triangle (cholesky() returns a lower factor)
-  for (int64_t idx = threadIdx.x; idx < (int64_t)m * m; idx += blockDim.x) {
-    const int i = (int)(idx % m), j = (int)(idx / m);
-    if (i < j) a[idx] = 0.0;
-  }
-}
-
-cudaError_t cholesky(int m, double* a, double rel_tol, int* status, cudaStream_t st) {
-  if (m > 1024) return cudaErrorInvalidValue;
-  cholesky_kernel<<<1, 1024, 0, st>>>(m, a, rel_tol, status);
-  ++g_launches;
-  return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------------------
-// triangular solves, one warp per right-hand side column (column cached in smem)
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) trsm_lower_kernel(int m, const double* __restrict__ l,
-                                                         double* x, int ldx, int ncols, int trans) {
-  extern __shared__ double col[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x * (blockDim.x >> 5) + warp;
-  if (c >= ncols) return;
-  double* b = col + warp * m;
-  double* xc = x + (int64_t)c * ldx;
-  for (int i = lane; i < m; i += 32) b[i] = xc[i];
-  __syncwarp();
-  if (!trans) {
-    for (int k = 0; k < m; ++k) {
-      const double bk = b[k] / l[k + (int64_t)k * m];
-      __syncwarp();
-      if (lane == 0) b[k] = bk;
-      for (int i = k + 1 + lane; i < m; i += 32) b[i] -= l[i + (int64_t)k * m] * bk;
-      __syncwarp();
-    }
-  } else {
-    for (int k = m - 1; k >= 0; --k) {
-      double s = 0.0;
-      for (int i = k + 1 + lane; i < m; i += 32) s += l[i + (int64_t)k * m] * b[i];
-      s = warp_sum(s);
-      const double v = (b[k] - s) / l[k + (int64_t)k * m];
-      __syncwarp();
-      if (lane == 0) b[k] = v;
-      __syncwarp();
-    }
-  }
-  for (int i = lane; i < m; i += 32) xc[i] = b[i];
-}
-
-static cudaError_t trsm_launch(int m, const double* l, double* x, int ldx, int ncols, int trans,
-                               cudaStream_t st) {
-  const int wpb = 8;
-  const size_t sm = sizeof(double) * m * wpb;
-  if (sm > 48 * 1024)
-    cudaFuncSetAttribute(trsm_lower_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  trsm_lower_kernel<<<(ncols + wpb - 1) / wpb, 32 * wpb, sm, st>>>(m, l, x, ldx, ncols, trans);
-  ++g_launches;
-  return cudaGetLastError();
-}
-cudaError_t trsm_lower(int m, const double* l, double* x, int ldx, int ncols, cudaStream_t st) {
-  return trsm_launch(m, l, x, ldx, ncols, 0, st);
-}
-cudaError_t trsm_lower_t(int m, const double* l, double* x, int ldx, int ncols, cudaStream_t st) {
-  return trsm_launch(m, l, x, ldx, ncols, 1, st);
 }
 
 __global__ void transpose_kernel(const double* __restrict__ src, int m, int n, int lds,
@@ -289,7 +179,7 @@ __global__ void __launch_bounds__(256) block_jacobi_kernel(JacobiArgs p) {
   for (int64_t idx = gtid; idx < (int64_t)mp * mp; idx += gstride) fro += p.w[idx] * p.w[idx];
   const double scale = fmax(sqrt(grid_sum(grid, fro, p.part, red)), DBL_MIN);
   const double tol_off = m * eps * scale;            // jacobi_eigh stopping rule (eigh.hpp:98)
-  const double tiny = eps * eps * scale;             // rotations below this are skipped
+  const double tiny = eps * scale / m;               // rotations below this are skipped
 
   double* S = jsm;                 // tb x ldt
   double* Jm = S + tb * ldt;       // tb x ldt
@@ -319,7 +209,9 @@ __global__ void __launch_bounds__(256) block_jacobi_kernel(JacobiArgs p) {
           Jm[u + v * ldt] = u == v ? 1.0 : 0.0;
         }
         __syncthreads();
-        for (int isw = 0; isw < 12; ++isw) {
+        // one or two inner sweeps per pair visit: block Jacobi converges without fully
+        // diagonalising each sub-problem, and every inner round costs two CTA barriers
+        for (int isw = 0; isw < 2; ++isw) {
           if (tid == 0) any_rot = 0;
           __syncthreads();
           for (int ir = 0; ir < tb - 1; ++ir) {
@@ -333,7 +225,9 @@ __global__ void __launch_bounds__(256) block_jacobi_kernel(JacobiArgs p) {
               const double aa = fabs(apq);
               const double app = S[pp + pp * ldt], aqq = S[qq + qq * ldt];
               double c = 1.0, sph = 0.0, phc = 1.0;
-              if (aa > tiny && aa > eps * 0.5 * (fabs(app) + fabs(aqq)) * 1e-3) {
+              // skip rotations below the global stopping floor (their squares sum to at
+              // most (eps*scale)^2 < tol_off^2) or at round-off relative to the diagonal
+              if (aa > tiny && aa > eps * 0.5 * (fabs(app) + fabs(aqq))) {
                 const double ph = apq > 0.0 ? 1.0 : -1.0;
                 const double tau = (aqq - app) / (2.0 * aa);
                 const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + hypot(1.0, tau));

@@ -178,13 +178,13 @@ struct feast_gpu_ctx {
   DevBuf<double2> dz, dcoeff;     // owned nodes
   // factors
   bool factored = false;
-  DevBuf<double2> sinv, gfac, lu, dinv, scratch;
+  DevBuf<double2> sinv, gfac, hfac, lu, dinv, scratch;
   DevBuf<int> ipiv, perm, status;
   // workspaces
   int mcap = 0;
   DevBuf<double> Y, Q, X, AQ, BQ, T, gw;
   DevBuf<double2> W;
-  DevBuf<double> Aq, Bq, Cm, Lm, Phi, Ev, Vm, S, Tm;
+  DevBuf<double> Aq, Bq, Cm, Lm, Phi, Ev, Vm, S, Tm, Dv;
   DevBuf<int> keep;
   EigWork* eig = nullptr;
   int eig_cap = 0;
@@ -451,8 +451,16 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
     CK(cudaMemcpyAsync(c->abdiag.p, pd.data(), sizeof(double2) * pd.size(), cudaMemcpyHostToDevice, c->stream));
     if (!pl.empty())
       CK(cudaMemcpyAsync(c->ablow.p, pl.data(), sizeof(double2) * pl.size(), cudaMemcpyHostToDevice, c->stream));
-    c->A.release();
-    c->Bm.release();
+    // plain real copies [diag blocks | lower blocks] for the operator applies (bt_apply)
+    const size_t nd = ad.size(), nl = al.size();
+    c->A.ensure(nd + nl);
+    c->Bm.ensure(nd + nl);
+    CK(cudaMemcpyAsync(c->A.p, ad.data(), sizeof(double) * nd, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->Bm.p, bd.data(), sizeof(double) * nd, cudaMemcpyHostToDevice, c->stream));
+    if (nl) {
+      CK(cudaMemcpyAsync(c->A.p + nd, al.data(), sizeof(double) * nl, cudaMemcpyHostToDevice, c->stream));
+      CK(cudaMemcpyAsync(c->Bm.p + nd, bl.data(), sizeof(double) * nl, cudaMemcpyHostToDevice, c->stream));
+    }
     sync(c);
   } else {
     c->blocktri = false;
@@ -529,8 +537,10 @@ void factor(feast_gpu_ctx* c) {
     const size_t bb = (size_t)c->b * c->b;
     c->sinv.ensure(own * c->L * bb);
     c->gfac.ensure(std::max<size_t>(own * (c->L - 1) * bb, 1));
+    c->hfac.ensure(std::max<size_t>(own * (c->L - 1) * bb, 1));
     if (c->b > 64) c->scratch.ensure(own * (size_t)c->b * 2 * (c->b + 1));
-    BtFactorArgs a{c->L, c->b, own, c->abdiag.p, c->ablow.p, c->dz.p, c->sinv.p, c->gfac.p, c->scratch.p, c->status.p};
+    BtFactorArgs a{c->L, c->b, own, c->abdiag.p, c->ablow.p, c->dz.p, c->sinv.p, c->gfac.p, c->hfac.p,
+                   c->scratch.p, c->status.p};
     CK(bt_factor(a, c->stream));
   } else {
     const int n = c->n, nb = kDenseNb, nblk = (n + nb - 1) / nb;
@@ -558,7 +568,7 @@ void contour_pass(feast_gpu_ctx* c, int m) {
   if (own > 0) {
     if (c->blocktri) {
       BtSweepArgs a{c->L, c->b, own, m, c->npad, c->ablow.p, c->dz.p, c->dcoeff.p, c->sinv.p,
-                    c->gfac.p, c->Y.p, c->T.p, c->W.p, 0};
+                    c->gfac.p, c->hfac.p, c->Y.p, c->T.p, c->W.p, 0};
       CK(bt_sweep(a, c->stream));
     } else {
       DenseSolveArgs a{c->n, own, m, c->npad, c->lu.p, c->perm.p, c->dinv.p, c->dcoeff.p, c->Y.p, c->T.p, c->W.p, 0};
@@ -580,7 +590,8 @@ void contour_pass(feast_gpu_ctx* c, int m) {
 
 void apply_op(feast_gpu_ctx* c, int which, const double* x, double* y, int m) {
   if (c->blocktri) {
-    CK(bt_apply(c->L, c->b, c->abdiag.p, c->ablow.p, which, x, c->npad, y, c->npad, m, c->stream));
+    const double* base = which ? c->Bm.p : c->A.p;
+    CK(bt_apply(c->L, c->b, base, base + (size_t)c->L * c->b * c->b, x, c->npad, y, c->npad, m, c->stream));
   } else {
     CK(dgemm('N', 'N', c->n, m, c->n, 1.0, which ? c->Bm.p : c->A.p, c->n, x, c->npad, 0.0, y, c->npad,
              c->gw.p, c->gw.n, c->stream));
@@ -599,7 +610,8 @@ Reduced reduced_gevp(feast_gpu_ctx* c, int m) {
   const size_t mm = (size_t)m * m;
   CK(cudaMemcpyAsync(c->Lm.p, c->Bq.p, sizeof(double) * mm, cudaMemcpyDeviceToDevice, c->stream));
   CK(cudaMemsetAsync(c->status.p, 0, sizeof(int), c->stream));
-  CK(cholesky(m, c->Lm.p, 1e-13, c->status.p, c->stream));
+  c->Dv.ensure((size_t)((m + 31) / 32) * 1024);
+  CK(cholesky(m, c->Lm.p, 1e-13, c->status.p, c->Dv.p, c->stream));
   int st = 0;
   CK(cudaMemcpyAsync(&st, c->status.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   sync(c);
@@ -607,13 +619,13 @@ Reduced reduced_gevp(feast_gpu_ctx* c, int m) {
   if (!st) {
     // C = L^-1 A L^-T  via two lower solves and transposes (eigh.hpp:192-196)
     CK(cudaMemcpyAsync(c->Cm.p, c->Aq.p, sizeof(double) * mm, cudaMemcpyDeviceToDevice, c->stream));
-    CK(trsm_lower(m, c->Lm.p, c->Cm.p, m, m, c->stream));
+    CK(trsm_lower(m, c->Lm.p, c->Dv.p, c->Cm.p, m, m, c->stream));
     CK(transpose(c->Cm.p, m, m, m, c->Tm.p, m, c->stream));
-    CK(trsm_lower(m, c->Lm.p, c->Tm.p, m, m, c->stream));
+    CK(trsm_lower(m, c->Lm.p, c->Dv.p, c->Tm.p, m, m, c->stream));
     CK(transpose(c->Tm.p, m, m, m, c->Cm.p, m, c->stream));
     CK(symmetrize(c->Cm.p, m, m, c->stream));
     CK(sym_eig(c->eig, m, c->Cm.p, c->Ev.p, c->Phi.p, c->stream));
-    CK(trsm_lower_t(m, c->Lm.p, c->Phi.p, m, m, c->stream));  // Phi = L^-T W
+    CK(trsm_lower_t(m, c->Lm.p, c->Dv.p, c->Phi.p, m, m, c->stream));  // Phi = L^-T W
     CK(cudaMemcpyAsync(r.evals.data(), c->Ev.p, sizeof(double) * m, cudaMemcpyDeviceToHost, c->stream));
     sync(c);
     r.mo = m;
@@ -896,9 +908,9 @@ void feast_gpu_destroy(feast_gpu_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (DevBuf<double>* d : {&c->A, &c->Bm, &c->Y, &c->Q, &c->X, &c->AQ, &c->BQ, &c->T, &c->gw, &c->Aq, &c->Bq,
-                            &c->Cm, &c->Lm, &c->Phi, &c->Ev, &c->Vm, &c->S, &c->Tm})
+                            &c->Cm, &c->Lm, &c->Phi, &c->Ev, &c->Vm, &c->S, &c->Tm, &c->Dv})
     d->release();
-  for (DevBuf<double2>* d : {&c->abdiag, &c->ablow, &c->dz, &c->dcoeff, &c->sinv, &c->gfac, &c->lu, &c->dinv,
+  for (DevBuf<double2>* d : {&c->abdiag, &c->ablow, &c->dz, &c->dcoeff, &c->sinv, &c->gfac, &c->hfac, &c->lu, &c->dinv,
                              &c->scratch, &c->W})
     d->release();
   for (DevBuf<int>* d : {&c->ipiv, &c->perm, &c->status, &c->keep}) d->release();
@@ -975,7 +987,8 @@ int feast_gpu_solve_shift(feast_gpu_ctx* c, int e, double* rhs, int m, int mode)
     if (c->blocktri) {
       const size_t bb = (size_t)c->b * c->b;
       BtSweepArgs a{c->L, c->b, 1, m, c->npad, c->ablow.p, c->dz.p + s, c->dcoeff.p + s,
-                    c->sinv.p + s * c->L * bb, c->gfac.p + s * (c->L - 1) * bb, nullptr, nullptr, w, 1};
+                    c->sinv.p + s * c->L * bb, c->gfac.p + s * (c->L - 1) * bb,
+                    c->hfac.p + s * (c->L - 1) * bb, nullptr, nullptr, w, 1};
       CK(bt_sweep(a, c->stream));
     } else {
       const int n = c->n, nb = kDenseNb, nblk = (n + nb - 1) / nb;

@@ -177,7 +177,7 @@ constexpr int STAGE = A_ELEMS + B_ELEMS;
 
 struct DgemmArgs {
   int m, n, k;
-  int kslice;  // K per z-slice
+  int kslice;  // K per z-slice (split-K mode)
   const double* a;
   int lda;
   const double* b;
@@ -186,6 +186,8 @@ struct DgemmArgs {
   int ldc;
   int64_t sc;  // stride between z-slices of the output
   double alpha, beta;
+  int batched;     // z indexes independent problems instead of K slices
+  int64_t sa, sb;  // batch strides of A and B
 };
 
 template <bool TA, bool TB>
@@ -195,10 +197,14 @@ __global__ void __launch_bounds__(256, 2) dgemm_kernel(DgemmArgs p) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
   const int wm = warp & 1, wn = warp >> 1;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int kbeg = blockIdx.z * p.kslice;
-  const int kend = min(p.k, kbeg + p.kslice);
+  const int kbeg = p.batched ? 0 : blockIdx.z * p.kslice;
+  const int kend = p.batched ? p.k : min(p.k, kbeg + p.kslice);
   const int nk = (kend - kbeg + BK - 1) / BK;
   double* C = p.c + blockIdx.z * p.sc;
+  if (p.batched) {
+    p.a += blockIdx.z * p.sa;
+    p.b += blockIdx.z * p.sb;
+  }
 
   auto load = [&](int kt) {
     if (kt < nk) {
@@ -330,7 +336,7 @@ cudaError_t dgemm(char ta, char tb, int m, int n, int k, double alpha, const dou
   kslice = (kslice + dg::BK - 1) / dg::BK * dg::BK;
   slices = (k + kslice - 1) / kslice;
   if (slices < 1) slices = 1;
-  DgemmArgs p{m, n, k, kslice, A, lda, B, ldb, C, ldc, 0, alpha, beta};
+  DgemmArgs p{m, n, k, kslice, A, lda, B, ldb, C, ldc, 0, alpha, beta, 0, 0, 0};
   if (slices > 1) {
     p.c = work;
     p.ldc = m;
@@ -352,6 +358,39 @@ cudaError_t dgemm(char ta, char tb, int m, int n, int k, double alpha, const dou
   splitk_reduce_kernel<<<blocks, 256, 0, st>>>(work, slices, (int64_t)m * n, m, n, alpha, beta, C, ldc);
   ++g_launches;
   return cudaGetLastError();
+}
+
+static cudaError_t dgemm_batched(bool TA, int m, int n, int k, double alpha, const double* A, int lda,
+                                 int64_t sa, const double* B, int ldb, int64_t sb, double beta, double* C,
+                                 int ldc, int64_t sc, int batch, cudaStream_t st) {
+  if (m <= 0 || n <= 0 || batch <= 0) return cudaSuccess;
+  DgemmArgs p{m, n, k, k, A, lda, B, ldb, C, ldc, sc, alpha, beta, 1, sa, sb};
+  const int smem = dg::NS * dg::STAGE * (int)sizeof(double);
+  for (int z0 = 0; z0 < batch; z0 += 65535) {
+    const int nz = std::min(batch - z0, 65535);
+    DgemmArgs q = p;
+    q.a += z0 * sa;
+    q.b += z0 * sb;
+    q.c += z0 * sc;
+    dim3 grid((n + dg::BN - 1) / dg::BN, (m + dg::BM - 1) / dg::BM, nz);
+    if (TA) { set_attr_once<true, false>(); dgemm_kernel<true, false><<<grid, 256, smem, st>>>(q); }
+    else { set_attr_once<false, false>(); dgemm_kernel<false, false><<<grid, 256, smem, st>>>(q); }
+    ++g_launches;
+  }
+  return cudaGetLastError();
+}
+
+// Y = Op X for a block-tridiagonal real operator (diag: L blocks b*b, low: L-1 couplings
+// C_l = Op(l+1, l), Op(l, l+1) = C_l^T), as three layer-batched DMMA GEMMs
+// (SymmetricOperator::apply, operator.hpp:132-158, on the block structure).
+cudaError_t bt_apply(int L, int b, const double* diag, const double* low, const double* x, int ldx,
+                     double* y, int ldy, int m, cudaStream_t st) {
+  const int64_t bb = (int64_t)b * b;
+  cudaError_t e = dgemm_batched(false, b, m, b, 1.0, diag, b, bb, x, ldx, b, 0.0, y, ldy, b, L, st);
+  if (e != cudaSuccess || L == 1) return e;
+  e = dgemm_batched(false, b, m, b, 1.0, low, b, bb, x, ldx, b, 1.0, y + b, ldy, b, L - 1, st);
+  if (e != cudaSuccess) return e;
+  return dgemm_batched(true, b, m, b, 1.0, low, b, bb, x + b, ldx, b, 1.0, y, ldy, b, L - 1, st);
 }
 
 __global__ void symmetrize_kernel(double* c, int m, int ld) {

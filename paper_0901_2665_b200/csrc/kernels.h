@@ -24,7 +24,8 @@ struct BtFactorArgs {
   const double2* ablow;
   const double2* z;       // [nodes]
   double2* sinv;          // nodes * L*b*b
-  double2* g;             // nodes * (L-1)*b*b (may alias unused if L == 1)
+  double2* g;             // nodes * (L-1)*b*b: G_l = S_l^{-1} C_l^T
+  double2* h;             // nodes * (L-1)*b*b: H_l = S_l^{-1} C_{l-1}, l >= 1
   double2* scratch;       // nodes * b * 2b (used when b > 64)
   int* status;            // set to 1 on a singular block pivot
 };
@@ -40,6 +41,7 @@ struct BtSweepArgs {
   const double2* coeff;
   const double2* sinv;
   const double2* g;
+  const double2* h;
   const double* y;        // real mode input (n*m, shared by nodes)
   double* t;              // real mode output: nodes * ldv*m
   double2* w;             // workspace / complex in-out: nodes * ldv*m
@@ -51,10 +53,9 @@ cudaError_t bt_sweep(const BtSweepArgs& a, cudaStream_t st);
 cudaError_t reduce_terms(const double* t, int nodes, int64_t slice, int n, int m, int ld,
                          double* q, cudaStream_t st);
 
-// block-tridiagonal real operator apply: Y = Op * X (ld n, m columns); uses .x of ab when
-// which == 0 (A) and .y when which == 1 (B)
-cudaError_t bt_apply(int L, int b, const double2* abdiag, const double2* ablow, int which,
-                     const double* x, int ldx, double* y, int ldy, int m, cudaStream_t st);
+// block-tridiagonal real operator apply: Y = Op * X (layer-batched DMMA GEMMs)
+cudaError_t bt_apply(int L, int b, const double* diag, const double* low, const double* x, int ldx,
+                     double* y, int ldy, int m, cudaStream_t st);
 
 // ---------------- dense shifted solves (batched complex LU) -------------------
 struct DenseFactorArgs {
@@ -101,12 +102,16 @@ void eig_destroy(EigWork* w);
 // Symmetric eigen-decomposition of W (m x m, ld m, overwritten): eigenvalues ascending
 // into `evals` (device), vectors into `v` (device, m x m), stable order.
 cudaError_t sym_eig(EigWork* w, int m, double* a, double* evals, double* v, cudaStream_t st);
-// Cholesky with relative pivot floor: L (lower, in place in `a`), status[0] = 1 on failure.
-cudaError_t cholesky(int m, double* a, double rel_tol, int* status, cudaStream_t st);
-// X <- L^{-1} X   (L lower m x m, X m x ncols)
-cudaError_t trsm_lower(int m, const double* l, double* x, int ldx, int ncols, cudaStream_t st);
+// Cholesky with relative pivot floor: L (lower, in place in `a`), status[0] = 1 on failure
+// (status must be zero on entry). dinv receives the inverses of the 32x32 diagonal tiles of
+// L (ceil(m/32) * 1024 doubles), consumed by the triangular solves.
+cudaError_t cholesky(int m, double* a, double rel_tol, int* status, double* dinv, cudaStream_t st);
+// X <- L^{-1} X   (L lower m x m from cholesky(), X m x ncols)
+cudaError_t trsm_lower(int m, const double* l, const double* dinv, double* x, int ldx, int ncols,
+                       cudaStream_t st);
 // X <- L^{-T} X
-cudaError_t trsm_lower_t(int m, const double* l, double* x, int ldx, int ncols, cudaStream_t st);
+cudaError_t trsm_lower_t(int m, const double* l, const double* dinv, double* x, int ldx, int ncols,
+                         cudaStream_t st);
 // transpose copy: dst(n x m) = src(m x n)^T
 cudaError_t transpose(const double* src, int m, int n, int lds, double* dst, int ldd,
                       cudaStream_t st);
