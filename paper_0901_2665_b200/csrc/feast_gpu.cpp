@@ -280,11 +280,13 @@ bool csr_fits_blocktri(const feast_operator_t* o, int b) {
       if (std::abs(i / b - o->col_idx[k] / b) > 1) return false;
   return true;
 }
+// block sizes the sweep kernels are specialised for (sweep.cu)
 int round_block(int b) {
-  if (b <= 16) return 16;
-  if (b <= 128) return (b + 15) / 16 * 16;
-  return (b + 31) / 32 * 32;
+  int r = 16;
+  while (r < b) r *= 2;
+  return r;
 }
+constexpr int kMaxBlock = 512;
 
 // dense view (host) of any operator
 std::vector<double> to_dense(const feast_operator_t* o) {
@@ -334,6 +336,21 @@ void to_blocktri(const feast_operator_t* o, int b, int L, bool is_b, std::vector
   if (o->kind == FEAST_STORAGE_CSR) {
     for (int i = 0; i < n; ++i)
       for (int k = o->row_ptr[i]; k < o->row_ptr[i + 1]; ++k) put(i, o->col_idx[k], o->values[k]);
+  } else if (o->kind == FEAST_STORAGE_BLOCKTRI) {  // re-block (lower triangle suffices)
+    const int bo = o->bsize;
+    for (int l = 0; l < o->nblocks; ++l) {
+      for (int j = 0; j < bo; ++j)
+        for (int i = 0; i < bo; ++i) {
+          const double v = o->diag[(size_t)l * bo * bo + i + (size_t)j * bo];
+          if (v != 0.0) put(l * bo + i, l * bo + j, v);
+        }
+      if (l + 1 < o->nblocks)
+        for (int j = 0; j < bo; ++j)
+          for (int i = 0; i < bo; ++i) {
+            const double v = o->lower[(size_t)l * bo * bo + i + (size_t)j * bo];
+            if (v != 0.0) put((l + 1) * bo + i, l * bo + j, v);
+          }
+    }
   } else {
     fail(FEAST_EINPUT, "set_pencil: cannot re-block this operator");
   }
@@ -407,7 +424,7 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
   const bool a_bt = a->kind == FEAST_STORAGE_BLOCKTRI, b_bt = b->kind == FEAST_STORAGE_BLOCKTRI;
   const bool a_sp = a->kind == FEAST_STORAGE_CSR || a_bt, b_sp = b->kind == FEAST_STORAGE_CSR || b_bt;
   if (a_sp && b_sp) {
-    if (a_bt && b_bt && a->bsize == b->bsize && a->bsize % 16 == 0 && (a->bsize <= 128 || a->bsize % 32 == 0)) {
+    if (a_bt && b_bt && a->bsize == b->bsize && round_block(a->bsize) == a->bsize && a->bsize <= kMaxBlock) {
       bsz = a->bsize;
     } else {
       int bw = 0;
@@ -416,16 +433,18 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
         else bw = std::max(bw, 2 * o->bsize - 1);
       }
       if ((3 * bw + 1) * 2 <= n) {
-        const int lo = round_block(std::max(1, (bw + 2) / 2)), hi = round_block(std::max(bw, 1));
-        for (int cand = lo; cand <= hi; cand += (cand < 128 ? 16 : 32)) {
+        // smallest supported block size whose block-tridiagonal pattern holds both operators
+        const int lo = round_block(std::max(1, (bw + 2) / 2));
+        const int hi = std::min(round_block(std::max(bw, 1)), kMaxBlock);
+        for (int cand = lo; cand <= hi && !bsz; cand *= 2) {
           bool ok = true;
           for (const feast_operator_t* o : {a, b}) {
             if (o->kind == FEAST_STORAGE_CSR) ok = ok && csr_fits_blocktri(o, cand);
-            else ok = ok && (o->bsize == cand);
+            else ok = ok && cand >= o->bsize && cand % o->bsize == 0;
           }
-          if (ok) { bsz = cand; break; }
+          if (ok) bsz = cand;
         }
-        if (!bsz) bsz = hi;
+        if (!bsz && round_block(std::max(bw, 1)) <= kMaxBlock) bsz = round_block(std::max(bw, 1));
       }
     }
   }
