@@ -67,7 +67,13 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
+
+    def wait_ready(self, timeout=5.0):
+        """nvidia-smi needs a moment before its first sample; start timing after it."""
+        t0 = time.monotonic()
+        while self.proc and not self.lines and time.monotonic() - t0 < timeout:
+            time.sleep(0.02)
 
     def __exit__(self, *a):
         if self.proc:
@@ -77,10 +83,14 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
-    def summary(self):
+    def summary(self, region=None):
+        """Samples taken during `region` (monotonic t0, t1), widened by one sampling period
+        on each side so short regions still get the samples that straddle them."""
         sm, smax, reasons = [], 0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for t, ln in self.lines:
+            if region and not (region[0] - 0.12 <= t <= region[1] + 0.12):
+                continue
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -201,7 +211,11 @@ def main():
         dist.barrier()
     l0 = ctx.launch_count()
     with ClockSampler(local) as clk:
+        clk.wait_ready()
+        t_region = time.monotonic()
         ms, ph = ctx.bench_passes(args.steps, flush)
+        t_region = (t_region, time.monotonic())
+        time.sleep(0.15)  # the sample straddling the end of the region
     launches = ctx.launch_count() - l0
     if dist:
         import torch
@@ -271,7 +285,7 @@ def main():
                      "hbm_frac": bytes_ / (k_ms * 1e-3) / 1e9 / peaks().get("hbm_gbs", 6650.0),
                      "avg_launch_ms": k_ms, "peak_source": "measured DMMA f64 (tools/microbench/fp64_peak.cu)"},
         "gpu_launches": launches,
-        "clocks": clk.summary(),
+        "clocks": clk.summary(t_region),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

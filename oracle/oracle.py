@@ -191,6 +191,41 @@ def bench_passes(problem, passes, threads=1, kind="reference"):
     return dict(factorize_s=out[0], solve_s=out[1], reduce_s=out[2], count=int(out[3]))
 
 
+SHIM = os.path.join(_HERE, "_ref", "libfeastref_gpu.so")
+
+
+def shim_feast_solve(problem, mode=0):
+    """mode 0: the REFERENCE's feast_solve with feast::gpu::GpuDirectSolver as its InnerSolver
+    (every shifted solve on the GPU through the C-ABI); mode 1: feast::gpu::feast_solve."""
+    if "shim" not in _cache:
+        L = C.CDLL(SHIM)
+        L.ref_last_error.restype = C.c_char_p
+        L.shim_feast_solve.argtypes = [_op, _op, C.c_double, C.c_double, C.POINTER(abi.FeastConfigT),
+                                       C.c_int, C.POINTER(abi.FeastResultT)]
+        _cache["shim"] = L
+    L = _cache["shim"]
+    p = problem
+    cfg = abi.FeastConfigT(m0=p.m0, n_e=p.n_e, trace_tol=p.trace_tol, max_loops=p.max_loops,
+                           seed=p.seed, threads=1, low_memory=0)
+    n = p.n
+    out = dict(eigenvalues=np.zeros(p.m0), eigenvectors=np.zeros((n, p.m0), order="F"),
+               residuals=np.zeros(p.m0), residual_absolute_only=np.zeros(p.m0, dtype=np.int32),
+               trace_history=np.zeros(p.max_loops + 1),
+               in_interval_counts=np.zeros(p.max_loops + 1, dtype=np.int32),
+               subspace=np.zeros((n, p.m0), order="F"))
+    r = abi.FeastResultT()
+    r.eigenvalues = abi.dptr(out["eigenvalues"])
+    r.eigenvectors = abi.dptr(out["eigenvectors"])
+    r.residuals = abi.dptr(out["residuals"])
+    r.residual_absolute_only = abi.iptr(out["residual_absolute_only"])
+    r.trace_history = abi.dptr(out["trace_history"])
+    r.in_interval_counts = abi.iptr(out["in_interval_counts"])
+    r.subspace = abi.dptr(out["subspace"])
+    ca, cb = p.a.to_c(), p.b.to_c()
+    _check(L, L.shim_feast_solve(C.byref(ca), C.byref(cb), p.emin, p.emax, C.byref(cfg), mode, C.byref(r)))
+    return unpack_result(out, r, n)
+
+
 def feast_solve(problem, threads=1, low_memory=False, initial_y=None, kind="reference",
                 m0=None, n_e=None, trace_tol=None, max_loops=None, seed=None):
     """Runs the CPU feast_solve (core.hpp:264) on a problems.Problem; returns a dict

@@ -30,7 +30,7 @@ using feast::linalg::SymmetricOperator;
 using feast::linalg::Triplet;
 using feast::linalg::TripletLayout;
 
-namespace {
+namespace refdrv {
 
 thread_local std::string g_err;
 
@@ -94,7 +94,8 @@ feast::FeastConfig to_ref(const feast_config_t* c) {
   return f;
 }
 
-}  // namespace
+}  // namespace refdrv
+using namespace refdrv;
 
 extern "C" {
 

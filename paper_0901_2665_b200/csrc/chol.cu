@@ -64,37 +64,53 @@ __global__ void __launch_bounds__(256) chol_kernel(CholArgs p) {
     if (blockIdx.x == 0) {
       for (int idx = tid; idx < TB * TB; idx += nt) {
         const int i = idx % TB, j = idx / TB;
-        T[i + j * TL] = (i < pb && j < pb) ? A[(p0 + i) + (int64_t)(p0 + j) * m] : (i == j ? 1.0 : 0.0);
+        if (i < pb && j < pb) cp_async8z(T + i + j * TL, A + (p0 + i) + (int64_t)(p0 + j) * m, true);
+        else T[i + j * TL] = i == j ? 1.0 : 0.0;
+      }
+      cp_async_wait_all();
+      __syncthreads();
+      // right-looking factor of the tile by all threads (pivot d = a_jj - sum_k l_jk^2
+      // after the updates; failure is uniform because every thread reads the same d)
+      for (int j = 0; j < pb; ++j) {
+        const double d = T[j + j * TL];
+        if (d <= 0.0 || d <= floor_) {
+          bad = 1;
+          break;
+        }
+        const double ljj = sqrt(d);
+        __syncthreads();
+        if (tid == 0) T[j + j * TL] = ljj;
+        for (int i = j + 1 + tid; i < pb; i += nt) T[i + j * TL] /= ljj;
+        __syncthreads();
+        const int r = pb - j - 1;
+        for (int idx = tid; idx < r * r; idx += nt) {
+          const int i = j + 1 + idx % r, k = j + 1 + idx / r;
+          if (k <= i) T[i + k * TL] -= T[i + j * TL] * T[k + j * TL];
+        }
+        __syncthreads();
       }
       __syncthreads();
-      if (warp == 0) {
-        // left-looking by columns; lane i owns row i
-        for (int j = 0; j < pb; ++j) {
-          double s = T[lane + j * TL];
-          for (int k = 0; k < j; ++k) s -= T[lane + k * TL] * T[j + k * TL];
-          const double d = __shfl_sync(0xffffffffu, s, j);
-          if (d <= 0.0 || d <= floor_) {
-            if (lane == 0) bad = 1;
-            break;
-          }
-          const double ljj = sqrt(d);
-          if (lane == j) T[j + j * TL] = ljj;
-          else if (lane > j) T[lane + j * TL] = s / ljj;
-          __syncwarp();
+      if (!bad) {
+        // L^{-1} of the tile: forward substitution on all identity columns at once
+        for (int idx = tid; idx < TB * TB; idx += nt) {
+          const int i = idx % TB, c = idx / TB;
+          U[i + c * TL] = i == c ? 1.0 : 0.0;
         }
-        __syncwarp();
-        if (!bad) {
-          // column `lane` of L^{-1}
-          double x[TB];
-#pragma unroll
-          for (int i = 0; i < TB; ++i) x[i] = 0.0;
-          for (int i = 0; i < pb; ++i) {
-            double s = (i == lane) ? 1.0 : 0.0;
-            for (int k = lane; k < i; ++k) s -= T[i + k * TL] * x[k];
-            x[i] = (i >= lane) ? s / T[i + i * TL] : 0.0;
+        __syncthreads();
+        for (int k = 0; k < pb; ++k) {
+          for (int c = tid; c <= k; c += nt) U[k + c * TL] /= T[k + k * TL];
+          __syncthreads();
+          const int r = pb - k - 1;
+          for (int idx = tid; idx < r * (k + 1); idx += nt) {
+            const int i = k + 1 + idx % r, c = idx / r;
+            U[i + c * TL] -= T[i + k * TL] * U[k + c * TL];
           }
-          double* Di = p.dinv + (int64_t)pn * TB * TB;
-          for (int i = 0; i < TB; ++i) Di[i + lane * TB] = (lane < pb && i < pb) ? x[i] : (i == lane ? 1.0 : 0.0);
+          __syncthreads();
+        }
+        double* Di = p.dinv + (int64_t)pn * TB * TB;
+        for (int idx = tid; idx < TB * TB; idx += nt) {
+          const int i = idx % TB, c = idx / TB;
+          Di[i + c * TB] = (i < pb && c < pb) ? U[i + c * TL] : (i == c ? 1.0 : 0.0);
         }
       }
       __syncthreads();
@@ -116,9 +132,11 @@ __global__ void __launch_bounds__(256) chol_kernel(CholArgs p) {
       const double* Di = p.dinv + (int64_t)pn * TB * TB;
       for (int idx = tid; idx < TB * TB; idx += nt) {
         const int r = idx % TB, c = idx / TB;
-        U[r + c * TL] = (r < ib && c < pb) ? A[(i0 + r) + (int64_t)(p0 + c) * m] : 0.0;
-        Vt[r + c * TL] = Di[r + c * TB];
+        const bool v = r < ib && c < pb;
+        cp_async8z(U + r + c * TL, v ? A + (i0 + r) + (int64_t)(p0 + c) * m : A, v);
+        cp_async8z(Vt + r + c * TL, Di + r + c * TB, true);
       }
+      cp_async_wait_all();
       __syncthreads();
       for (int idx = tid; idx < ib * pb; idx += nt) {
         const int r = idx % ib, c = idx / ib;
@@ -139,9 +157,11 @@ __global__ void __launch_bounds__(256) chol_kernel(CholArgs p) {
       const int ib = min(TB, m - i0), jb = min(TB, m - j0);
       for (int idx = tid; idx < TB * TB; idx += nt) {
         const int r = idx % TB, c = idx / TB;
-        U[r + c * TL] = (r < ib && c < pb) ? A[(i0 + r) + (int64_t)(p0 + c) * m] : 0.0;
-        Vt[r + c * TL] = (r < jb && c < pb) ? A[(j0 + r) + (int64_t)(p0 + c) * m] : 0.0;
+        const bool vu = r < ib && c < pb, vv = r < jb && c < pb;
+        cp_async8z(U + r + c * TL, vu ? A + (i0 + r) + (int64_t)(p0 + c) * m : A, vu);
+        cp_async8z(Vt + r + c * TL, vv ? A + (j0 + r) + (int64_t)(p0 + c) * m : A, vv);
       }
+      cp_async_wait_all();
       __syncthreads();
       for (int idx = tid; idx < ib * jb; idx += nt) {
         const int r = idx % ib, c = idx / ib;
@@ -204,17 +224,31 @@ __global__ void __launch_bounds__(256) trsm_tile_kernel(int m, const double* __r
     double accA = (r < ib) ? xs[(i0 + r) + cA * m] : 0.0;
     double accB = (r < ib) ? xs[(i0 + r) + cB * m] : 0.0;
     const int jlo = TRANS ? bi + 1 : 0, jhi = TRANS ? nblk : bi;
-    for (int bj = jlo; bj < jhi; ++bj) {
+    // the L tile feeding update bj: L_ij (lower) or L_ji^T (transposed); the next tile is
+    // loaded into registers while the current one is consumed (latency off the chain)
+    constexpr int PER = TB * TB / 256;
+    double nxt[PER];
+    auto fetch = [&](int bj) {
       const int j0 = bj * TB, jb = min(TB, m - j0);
-      // stage the L tile feeding this update: L_ij (lower) or L_ji^T (transposed)
-      for (int idx = tid; idx < TB * TB; idx += nt) {
-        const int rr = idx % TB, cc = idx / TB;
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int idx = tid + q * 256, rr = idx % TB, cc = idx / TB;
         double v = 0.0;
         if (!TRANS) { if (rr < ib && cc < jb) v = l[(i0 + rr) + (int64_t)(j0 + cc) * m]; }
         else { if (cc < jb && rr < ib) v = l[(j0 + cc) + (int64_t)(i0 + rr) * m]; }
-        Lt[rr + cc * TL] = v;
+        nxt[q] = v;
+      }
+    };
+    if (jlo < jhi) fetch(jlo);
+    for (int bj = jlo; bj < jhi; ++bj) {
+      const int j0 = bj * TB, jb = min(TB, m - j0);
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int idx = tid + q * 256;
+        Lt[(idx % TB) + (idx / TB) * TL] = nxt[q];
       }
       __syncthreads();
+      if (bj + 1 < jhi) fetch(bj + 1);
       double sA = 0.0, sB = 0.0;
       for (int k = 0; k < jb; ++k) {
         const double lv = Lt[r + k * TL];

@@ -74,7 +74,14 @@ FEAST_DEV void cp_async8(void* smem, const void* gmem) {
   const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
 }
+// 8-byte copy that writes 0.0 instead when !valid (src-size 0): tile fills issue every
+// element back to back instead of serialising one global latency per loop iteration
+FEAST_DEV void cp_async8z(double* smem, const double* gmem, bool valid) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 8 : 0));
+}
 FEAST_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+FEAST_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 template <int N>
 FEAST_DEV void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));

@@ -207,9 +207,10 @@ __global__ void __launch_bounds__(256) block_jacobi_kernel(JacobiArgs p) {
           const int u = idx % tb, v = idx / tb;
           const int gu = u < bs ? P * bs + u : Q * bs + u - bs;
           const int gv = v < bs ? P * bs + v : Q * bs + v - bs;
-          S0[u + v * ldt] = p.w[gu + (int64_t)gv * mp];
+          cp_async8z(S0 + u + v * ldt, p.w + gu + (int64_t)gv * mp, true);
           Jm[u + v * ldt] = u == v ? 1.0 : 0.0;
         }
+        cp_async_wait_all();
         __syncthreads();
         double* Sc = S0;
         double* Sn = S1;
@@ -282,13 +283,14 @@ __global__ void __launch_bounds__(256) block_jacobi_kernel(JacobiArgs p) {
           const int gv = v < bs ? Pb * bs + v : Qb * bs + v - bs;
           if (wt) {
             const int gu = u < bs ? Pa * bs + u : Qa * bs + u - bs;
-            X[u + v * ldt] = p.w[gu + (int64_t)gv * mp];
-            Ja[u + v * ldt] = JA[idx];
+            cp_async8z(X + u + v * ldt, p.w + gu + (int64_t)gv * mp, true);
+            cp_async8z(Ja + u + v * ldt, JA + idx, true);
           } else {
-            X[u + v * ldt] = p.v[(rc * tb + u) + (int64_t)gv * mp];
+            cp_async8z(X + u + v * ldt, p.v + (rc * tb + u) + (int64_t)gv * mp, true);
           }
-          Jb[u + v * ldt] = JB[idx];
+          cp_async8z(Jb + u + v * ldt, JB + idx, true);
         }
+        cp_async_wait_all();
         __syncthreads();
         // Y = X Jb; 2x2 register tile per thread
         for (int t = tid; t < (tb / 2) * (tb / 2); t += nt) {

@@ -332,6 +332,12 @@ class GpuContext:
         return int(self.L.feast_gpu_launch_count(self.h))
 
 
+def shard_nodes(n_e: int, rank: int, nranks: int):
+    """Contour nodes owned by `rank` (mirror of build_contour's split in feast_gpu.cpp):
+    contiguous blocks in ascending e, [floor(n_e*r/R), floor(n_e*(r+1)/R))."""
+    return range(n_e * rank // nranks, n_e * (rank + 1) // nranks)
+
+
 def feast_solve(a, b, interval: SearchInterval, config: FeastConfig, initial_y=None,
                 device: int = 0) -> FeastResult:
     """Drop-in for feast::feast_solve<double>(a, b, interval, config, nullptr, initial_y)."""

@@ -365,8 +365,17 @@ def config4(n: int = 8192, seed: int = 4, m0: int = 600, want: int = 400,
     bm = np.eye(n) + 0.1 * (h @ h.T) / n
     bm = 0.5 * (bm + bm.T)
     A, B = Operator.from_dense(a), Operator.from_dense(bm)
-    lo, hi = _cached_interval(f"cfg4_n{n}_s{seed}_k{want}",
-                              lambda: interval_with_count(A, B, want, start=0.0, span=0.1))
+
+    def dense_interval():
+        # all generalized eigenvalues once (LAPACK sygvd), then gap midpoints around `want`
+        # consecutive eigenvalues starting at the first one >= 0
+        import scipy.linalg as sl
+        ev = sl.eigh(a, bm, eigvals_only=True)
+        k0 = int(np.searchsorted(ev, 0.0))
+        lo_, hi_ = 0.5 * (ev[k0 - 1] + ev[k0]), 0.5 * (ev[k0 + want - 1] + ev[k0 + want])
+        return lo_, hi_, dict(lam_prev=float(ev[k0 - 1]), lam_first=float(ev[k0]),
+                              lam_last=float(ev[k0 + want - 1]), lam_next=float(ev[k0 + want]))
+    lo, hi = _cached_interval(f"cfg4_n{n}_s{seed}_k{want}", dense_interval)
     return Problem(f"cfg4_dense_n{n}", A, B, lo, hi, m0, n_e=8, seed=yseed,
                    expected_count=want)
 
