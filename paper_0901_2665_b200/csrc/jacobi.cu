@@ -43,6 +43,9 @@ static __device__ double block_sum(double v, double* red) {
   return red[32];
 }
 
+int tri_max_dim();
+cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws, int* iws, cudaStream_t st);
+
 struct EigWork {
   int mmax = 0;
   double* w = nullptr;     // mp x mp
@@ -50,6 +53,8 @@ struct EigWork {
   double* j = nullptr;     // npair * (2bs)^2
   double* part = nullptr;  // per-CTA partial sums
   unsigned long long* dbg = nullptr;
+  double* tws = nullptr;   // tridiagonal route (m <= tri_max_dim): 6m^2 + 3m
+  int* tiws = nullptr;     // m^2
   int grid = 0;
 };
 
@@ -71,6 +76,9 @@ EigWork* eig_create(int mmax) {
   cudaMalloc(&w->j, sizeof(double) * (mp / 32 + 2) * (4 * 32 * 32));
   cudaMalloc(&w->part, sizeof(double) * 1024);
   cudaMalloc(&w->dbg, sizeof(unsigned long long) * 8);
+  const size_t tm = (size_t)std::min(mmax, tri_max_dim());
+  cudaMalloc(&w->tws, sizeof(double) * (6 * tm * tm + 3 * tm));
+  cudaMalloc(&w->tiws, sizeof(int) * tm * tm);
   int dev = 0;
   cudaGetDevice(&dev);
   int sms = 148;
@@ -86,6 +94,8 @@ void eig_destroy(EigWork* w) {
   cudaFree(w->j);
   cudaFree(w->part);
   cudaFree(w->dbg);
+  cudaFree(w->tws);
+  cudaFree(w->tiws);
   delete w;
 }
 
@@ -372,6 +382,11 @@ __global__ void eig_sort_kernel(int m, int mp, const double* w, const double* v,
 
 cudaError_t sym_eig(EigWork* w, int m, double* a, double* evals, double* v, cudaStream_t st) {
   if (m < 1 || m > w->mmax) return cudaErrorInvalidValue;
+  // one-SM tridiagonal route while the packed matrix fits shared memory (FEAST_EIG=jacobi
+  // forces block Jacobi for comparison)
+  static const char* force = getenv("FEAST_EIG");
+  const bool jacobi_only = force && force[0] == 'j';
+  if (m <= tri_max_dim() && !jacobi_only) return tri_eig(m, a, evals, v, w->tws, w->tiws, st);
   static const bool debug = getenv("FEAST_EIG_DEBUG") != nullptr;
   const int bs = eig_bs(m), mp = eig_mp(m), tb = 2 * bs, ldt = tb + 1;
   JacobiArgs p{m, mp, bs, a, w->w, w->v, w->j, w->part, 60, debug ? w->dbg : nullptr};
