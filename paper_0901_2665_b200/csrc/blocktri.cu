@@ -155,7 +155,81 @@ __global__ void __launch_bounds__(256) bt_factor_kernel(BtFactorArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Large blocks (b >= 128): the same recursion, every dense b x b operation batched over the
+// nodes and run on the DMMA GEMM / batched-LU kernels (one layer at a time):
+//   S_l = M_l - C_{l-1} G_{l-1}  (zgemm) ;  LU(S_l) (zgetrf_batched) ;  S_l^{-1} = LU \ I ;
+//   H_l = S_l^{-1} C_{l-1} ;  G_l = S_l^{-1} C_l^T  (zgemm)
+// ---------------------------------------------------------------------------
+cudaError_t zgemm_batched(int m, int n, int k, double2 alpha, const double2* a, int lda, int64_t sa,
+                          const double2* b, int ldb, int64_t sb, double2 beta, double2* c, int ldc,
+                          int64_t sc, int batch, cudaStream_t st);
+cudaError_t zgetrf_batched(int n, int nodes, double2* lu, int64_t stride, int* ipiv, int* perm, double2* dinv,
+                           int* status, cudaStream_t st);
+cudaError_t zgetrs_batched(int n, int nodes, int m, const double2* lu, int64_t stride, const int* perm,
+                           const double2* dinv, double2* w, int ldv, double2* scratch, cudaStream_t st);
+
+// out_s = z_s * B - A for a block of (A, B) pairs (optionally transposed), or the identity
+__global__ void bt_make_kernel(int b, const double2* __restrict__ ab, const double2* __restrict__ z,
+                               double2* __restrict__ out, int mode) {
+  const int s = blockIdx.y;
+  const double2 zz = z[s];
+  double2* o = out + (size_t)s * b * b;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < b * b; idx += gridDim.x * blockDim.x) {
+    const int i = idx % b, j = idx / b;
+    if (mode == 2) {
+      o[idx] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+    } else {
+      const double2 e = ab[mode == 1 ? j + i * b : idx];
+      o[idx] = make_double2(zz.x * e.y - e.x, zz.y * e.y);
+    }
+  }
+}
+
+static cudaError_t bt_factor_big(const BtFactorArgs& a, cudaStream_t st) {
+  const int L = a.L, b = a.b, nodes = a.nodes;
+  const int64_t bb = (int64_t)b * b, lnode = (int64_t)L * bb, gnode = (int64_t)(L > 1 ? L - 1 : 0) * bb;
+  double2* S = a.work;                 // LU of S_l            (nodes x bb)
+  double2* Cp = S + nodes * bb;        // C_{l-1}, then C_l
+  double2* CT = Cp + nodes * bb;       // C_l^T
+  double2* X = CT + nodes * bb;        // S_l^{-1}
+  double2* scr = X + nodes * bb;       // zgetrs scratch
+  double2* dinv = scr + nodes * bb;    // diagonal-block inverses
+  int* ipiv = a.iwork;
+  int* perm = ipiv + nodes * b;
+  const double2 one = make_double2(1.0, 0.0), mone = make_double2(-1.0, 0.0), zero = make_double2(0.0, 0.0);
+  dim3 g((unsigned)std::min<int64_t>((bb + 255) / 256, 512), nodes);
+  for (int l = 0; l < L; ++l) {
+    bt_make_kernel<<<g, 256, 0, st>>>(b, a.abdiag + l * bb, a.z, S, 0);
+    ++g_launches;
+    if (l > 0)
+      zgemm_batched(b, b, b, mone, Cp, b, bb, a.g + (l - 1) * bb, b, gnode, one, S, b, bb, nodes, st);
+    zgetrf_batched(b, nodes, S, bb, ipiv, perm, dinv, a.status, st);
+    bt_make_kernel<<<g, 256, 0, st>>>(b, nullptr, a.z, X, 2);
+    ++g_launches;
+    zgetrs_batched(b, nodes, b, S, bb, perm, dinv, X, b, scr, st);
+    // S_l^{-1} out (node stride L*bb)
+    cudaMemcpy2DAsync(a.sinv + l * bb, sizeof(double2) * lnode, X, sizeof(double2) * bb, sizeof(double2) * bb,
+                      nodes, cudaMemcpyDeviceToDevice, st);
+    if (l > 0)
+      zgemm_batched(b, b, b, one, X, b, bb, Cp, b, bb, zero, a.h + (l - 1) * bb, b, gnode, nodes, st);
+    if (l + 1 < L) {
+      bt_make_kernel<<<g, 256, 0, st>>>(b, a.ablow + l * bb, a.z, Cp, 0);
+      bt_make_kernel<<<g, 256, 0, st>>>(b, a.ablow + l * bb, a.z, CT, 1);
+      g_launches += 2;
+      zgemm_batched(b, b, b, one, X, b, bb, CT, b, bb, zero, a.g + l * bb, b, gnode, nodes, st);
+    }
+  }
+  return cudaGetLastError();
+}
+
+size_t bt_factor_work_elems(int b, int nodes) {  // double2 elements of BtFactorArgs::work
+  const int nblk = (b + kDenseNb - 1) / kDenseNb;
+  return (size_t)nodes * (5 * (size_t)b * b + (size_t)nblk * 2 * kDenseNb * kDenseNb);
+}
+
 cudaError_t bt_factor(const BtFactorArgs& a, cudaStream_t st) {
+  if (a.b >= 128) return bt_factor_big(a, st);
   size_t sm = sizeof(double2) * (size_t)a.b;
   if (a.b <= 64) sm += sizeof(double2) * (size_t)a.b * 2 * (a.b + 1);
   if (sm > 48 * 1024)

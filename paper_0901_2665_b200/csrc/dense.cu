@@ -38,10 +38,10 @@ __global__ void assemble_kernel(int n, const double* __restrict__ a, const doubl
 }
 
 // One CTA per node. Columns [k0, k0+kb), rows [k0, n).
-__global__ void __launch_bounds__(1024) panel_kernel(int n, int k0, int kb, double2* lu, int* ipiv,
-                                                     int* status) {
+__global__ void __launch_bounds__(1024) panel_kernel(int n, int64_t stride, int k0, int kb, double2* lu,
+                                                     int* ipiv, int* status) {
   const int s = blockIdx.x;
-  double2* A = lu + (int64_t)s * n * n;
+  double2* A = lu + (int64_t)s * stride;
   int* piv = ipiv + (int64_t)s * n;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
   __shared__ double rv[32];
@@ -105,9 +105,9 @@ __global__ void __launch_bounds__(1024) panel_kernel(int n, int k0, int kb, doub
 }
 
 // row interchanges of panel [k0, k0+kb) on the columns outside it
-__global__ void laswp_kernel(int n, int k0, int kb, double2* lu, const int* ipiv) {
+__global__ void laswp_kernel(int n, int64_t stride, int k0, int kb, double2* lu, const int* ipiv) {
   const int s = blockIdx.y;
-  double2* A = lu + (int64_t)s * n * n;
+  double2* A = lu + (int64_t)s * stride;
   const int* piv = ipiv + (int64_t)s * n;
   const int others = n - kb;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < others; c += gridDim.x * blockDim.x) {
@@ -124,12 +124,12 @@ __global__ void laswp_kernel(int n, int k0, int kb, double2* lu, const int* ipiv
 }
 
 // inverses of the diagonal block k: dinv[s][blk][0] = L11^{-1} (unit lower), [1] = U11^{-1}
-__global__ void __launch_bounds__(128) diag_inv_kernel(int n, int blk, int nblk, const double2* lu,
-                                                       double2* dinv) {
+__global__ void __launch_bounds__(128) diag_inv_kernel(int n, int64_t stride, int blk, int nblk,
+                                                       const double2* lu, double2* dinv) {
   constexpr int NB = kDenseNb;
   const int s = blockIdx.x;
   const int k0 = blk * NB, kb = min(NB, n - k0);
-  const double2* A = lu + (int64_t)s * n * n + k0 + (int64_t)k0 * n;
+  const double2* A = lu + (int64_t)s * stride + k0 + (int64_t)k0 * n;
   double2* Li = dinv + ((int64_t)s * nblk + blk) * 2 * NB * NB;
   double2* Ui = Li + NB * NB;
   extern __shared__ double2 T[];  // NB x (NB+1)
@@ -174,24 +174,22 @@ __global__ void perm_kernel(int n, int nodes, const int* ipiv, int* perm) {
   }
 }
 
-cudaError_t dense_factor(const DenseFactorArgs& a, cudaStream_t st) {
-  const int n = a.n, nb = kDenseNb, nodes = a.nodes;
+// Batched right-looking LU with partial pivoting of `nodes` complex n x n matrices stored
+// `stride` apart (in place), plus the row permutation and the diagonal-block inverses the
+// blocked solves use. Shared by the dense path and the large-block block-Thomas factor.
+cudaError_t zgetrf_batched(int n, int nodes, double2* lu, int64_t stride, int* ipiv, int* perm, double2* dinv,
+                           int* status, cudaStream_t st) {
+  const int nb = kDenseNb;
   const int nblk = (n + nb - 1) / nb;
-  const int64_t nn = (int64_t)n * n;
-  {
-    dim3 grid((unsigned)std::min<int64_t>((nn + 255) / 256, 1024), nodes);
-    assemble_kernel<<<grid, 256, 0, st>>>(n, a.a, a.bm, a.z, a.lu);
-    ++g_launches;
-  }
   const double2 one = make_double2(1.0, 0.0), mone = make_double2(-1.0, 0.0),
                 zero = make_double2(0.0, 0.0);
   for (int blk = 0; blk < nblk; ++blk) {
     const int k0 = blk * nb, kb = std::min(nb, n - k0);
-    panel_kernel<<<nodes, 1024, 0, st>>>(n, k0, kb, a.lu, a.ipiv, a.status);
+    panel_kernel<<<nodes, 1024, 0, st>>>(n, stride, k0, kb, lu, ipiv, status);
     ++g_launches;
     if (n - kb > 0) {
       dim3 grid((n - kb + 255) / 256, nodes);
-      laswp_kernel<<<grid, 256, 0, st>>>(n, k0, kb, a.lu, a.ipiv);
+      laswp_kernel<<<grid, 256, 0, st>>>(n, stride, k0, kb, lu, ipiv);
       ++g_launches;
     }
     {
@@ -201,23 +199,32 @@ cudaError_t dense_factor(const DenseFactorArgs& a, cudaStream_t st) {
         cudaFuncSetAttribute(diag_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
         attr = true;
       }
-      diag_inv_kernel<<<nodes, 128, sm, st>>>(n, blk, nblk, a.lu, a.dinv);
+      diag_inv_kernel<<<nodes, 128, sm, st>>>(n, stride, blk, nblk, lu, dinv);
     }
     ++g_launches;
     const int rest = n - k0 - kb;
     if (rest > 0) {
-      double2* a12 = a.lu + k0 + (int64_t)(k0 + kb) * n;
-      const double2* linv = a.dinv + (int64_t)blk * 2 * nb * nb;
-      zgemm_batched(kb, rest, kb, one, linv, nb, (int64_t)nblk * 2 * nb * nb, a12, n, nn, zero,
-                    a12, n, nn, nodes, st);
-      const double2* l21 = a.lu + (k0 + kb) + (int64_t)k0 * n;
-      double2* a22 = a.lu + (k0 + kb) + (int64_t)(k0 + kb) * n;
-      zgemm_batched(rest, rest, kb, mone, l21, n, nn, a12, n, nn, one, a22, n, nn, nodes, st);
+      double2* a12 = lu + k0 + (int64_t)(k0 + kb) * n;
+      const double2* linv = dinv + (int64_t)blk * 2 * nb * nb;
+      zgemm_batched(kb, rest, kb, one, linv, nb, (int64_t)nblk * 2 * nb * nb, a12, n, stride, zero,
+                    a12, n, stride, nodes, st);
+      const double2* l21 = lu + (k0 + kb) + (int64_t)k0 * n;
+      double2* a22 = lu + (k0 + kb) + (int64_t)(k0 + kb) * n;
+      zgemm_batched(rest, rest, kb, mone, l21, n, stride, a12, n, stride, one, a22, n, stride, nodes, st);
     }
   }
-  perm_kernel<<<(nodes + 31) / 32, 32, 0, st>>>(n, nodes, a.ipiv, a.perm);
+  perm_kernel<<<(nodes + 31) / 32, 32, 0, st>>>(n, nodes, ipiv, perm);
   ++g_launches;
   return cudaGetLastError();
+}
+
+cudaError_t dense_factor(const DenseFactorArgs& a, cudaStream_t st) {
+  const int n = a.n, nodes = a.nodes;
+  const int64_t nn = (int64_t)n * n;
+  dim3 grid((unsigned)std::min<int64_t>((nn + 255) / 256, 1024), nodes);
+  assemble_kernel<<<grid, 256, 0, st>>>(n, a.a, a.bm, a.z, a.lu);
+  ++g_launches;
+  return zgetrf_batched(n, nodes, a.lu, nn, a.ipiv, a.perm, a.dinv, a.status, st);
 }
 
 // R_s = P_s Y (real -> complex), or P_s W_s (complex, via scratch copy in t-as-double2)
@@ -252,43 +259,57 @@ __global__ void term_kernel(int n, int m, int ldv, const double2* coeff, const d
   }
 }
 
-cudaError_t dense_solve(const DenseSolveArgs& a, cudaStream_t st) {
-  const int n = a.n, nb = kDenseNb, nodes = a.nodes, m = a.m;
-  const int nblk = (n + nb - 1) / nb;
-  const int64_t nn = (int64_t)n * n, sv = (int64_t)a.ldv * m, sd = (int64_t)nblk * 2 * nb * nb;
-  const int64_t total = (int64_t)n * m;
-  dim3 g1((unsigned)std::min<int64_t>((total + 255) / 256, 1024), nodes);
-  double2* tmp = nullptr;
-  if (a.complex_mode) {
-    // permute a copy: the t buffer is sized nodes*ldv*m doubles; complex copy needs 2x -> caller
-    // passes t sized for complex in complex mode
-    tmp = reinterpret_cast<double2*>(a.t);
-    cudaMemcpyAsync(tmp, a.w, sizeof(double2) * sv * nodes, cudaMemcpyDeviceToDevice, st);
-  }
-  permute_rhs_kernel<<<g1, 256, 0, st>>>(n, m, a.ldv, a.perm, a.y, tmp, a.w);
-  ++g_launches;
+// blocked forward/backward substitution on the factors of zgetrf_batched, in place on the
+// (already row-permuted) right-hand sides W (n x m per node, ld ldv, batch stride sv)
+static void zgetrs_core(int n, int nodes, int m, const double2* lu, int64_t stride, const double2* dinv,
+                        double2* w, int ldv, int64_t sv, cudaStream_t st) {
+  const int nb = kDenseNb, nblk = (n + nb - 1) / nb;
+  const int64_t sd = (int64_t)nblk * 2 * nb * nb;
   const double2 one = make_double2(1.0, 0.0), mone = make_double2(-1.0, 0.0),
                 zero = make_double2(0.0, 0.0);
   for (int blk = 0; blk < nblk; ++blk) {
     const int k0 = blk * nb, kb = std::min(nb, n - k0);
-    double2* rk = a.w + k0;
-    zgemm_batched(kb, m, kb, one, a.dinv + (int64_t)blk * 2 * nb * nb, nb, sd, rk, a.ldv, sv, zero,
-                  rk, a.ldv, sv, nodes, st);
+    double2* rk = w + k0;
+    zgemm_batched(kb, m, kb, one, dinv + (int64_t)blk * 2 * nb * nb, nb, sd, rk, ldv, sv, zero, rk, ldv, sv,
+                  nodes, st);
     const int rest = n - k0 - kb;
     if (rest > 0)
-      zgemm_batched(rest, m, kb, mone, a.lu + (k0 + kb) + (int64_t)k0 * n, n, nn, rk, a.ldv, sv, one,
-                    a.w + k0 + kb, a.ldv, sv, nodes, st);
+      zgemm_batched(rest, m, kb, mone, lu + (k0 + kb) + (int64_t)k0 * n, n, stride, rk, ldv, sv, one,
+                    w + k0 + kb, ldv, sv, nodes, st);
   }
   for (int blk = nblk - 1; blk >= 0; --blk) {
     const int k0 = blk * nb, kb = std::min(nb, n - k0);
-    double2* rk = a.w + k0;
-    zgemm_batched(kb, m, kb, one, a.dinv + (int64_t)blk * 2 * nb * nb + nb * nb, nb, sd, rk, a.ldv,
-                  sv, zero, rk, a.ldv, sv, nodes, st);
+    double2* rk = w + k0;
+    zgemm_batched(kb, m, kb, one, dinv + (int64_t)blk * 2 * nb * nb + nb * nb, nb, sd, rk, ldv, sv, zero, rk,
+                  ldv, sv, nodes, st);
     if (k0 > 0)
-      zgemm_batched(k0, m, kb, mone, a.lu + (int64_t)k0 * n, n, nn, rk, a.ldv, sv, one, a.w, a.ldv,
-                    sv, nodes, st);
+      zgemm_batched(k0, m, kb, mone, lu + (int64_t)k0 * n, n, stride, rk, ldv, sv, one, w, ldv, sv, nodes, st);
   }
-  if (!a.complex_mode) {
+}
+
+// W <- A^{-1} W for complex right-hand sides (scratch: nodes * ldv * m double2)
+cudaError_t zgetrs_batched(int n, int nodes, int m, const double2* lu, int64_t stride, const int* perm,
+                           const double2* dinv, double2* w, int ldv, double2* scratch, cudaStream_t st) {
+  const int64_t sv = (int64_t)ldv * m, total = (int64_t)n * m;
+  dim3 g1((unsigned)std::min<int64_t>((total + 255) / 256, 1024), nodes);
+  cudaMemcpyAsync(scratch, w, sizeof(double2) * sv * nodes, cudaMemcpyDeviceToDevice, st);
+  permute_rhs_kernel<<<g1, 256, 0, st>>>(n, m, ldv, perm, nullptr, scratch, w);
+  ++g_launches;
+  zgetrs_core(n, nodes, m, lu, stride, dinv, w, ldv, sv, st);
+  return cudaGetLastError();
+}
+
+cudaError_t dense_solve(const DenseSolveArgs& a, cudaStream_t st) {
+  const int n = a.n, nodes = a.nodes, m = a.m;
+  const int64_t nn = (int64_t)n * n, sv = (int64_t)a.ldv * m;
+  const int64_t total = (int64_t)n * m;
+  dim3 g1((unsigned)std::min<int64_t>((total + 255) / 256, 1024), nodes);
+  if (a.complex_mode)  // the t buffer is sized for a complex copy in complex mode
+    return zgetrs_batched(n, nodes, m, a.lu, nn, a.perm, a.dinv, a.w, a.ldv, reinterpret_cast<double2*>(a.t), st);
+  permute_rhs_kernel<<<g1, 256, 0, st>>>(n, m, a.ldv, a.perm, a.y, nullptr, a.w);
+  ++g_launches;
+  zgetrs_core(n, nodes, m, a.lu, nn, a.dinv, a.w, a.ldv, sv, st);
+  {
     term_kernel<<<g1, 256, 0, st>>>(n, m, a.ldv, a.coeff, a.w, a.t);
     ++g_launches;
   }

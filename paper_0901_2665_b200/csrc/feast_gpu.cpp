@@ -178,8 +178,8 @@ struct feast_gpu_ctx {
   DevBuf<double2> dz, dcoeff;     // owned nodes
   // factors
   bool factored = false;
-  DevBuf<double2> sinv, gfac, hfac, lu, dinv, scratch;
-  DevBuf<int> ipiv, perm, status;
+  DevBuf<double2> sinv, gfac, hfac, lu, dinv, scratch, fwork;
+  DevBuf<int> ipiv, perm, status, fiwork;
   // workspaces
   int mcap = 0;
   DevBuf<double> Y, Q, X, AQ, BQ, T, gw;
@@ -557,10 +557,16 @@ void factor(feast_gpu_ctx* c) {
     c->sinv.ensure(own * c->L * bb);
     c->gfac.ensure(std::max<size_t>(own * (c->L - 1) * bb, 1));
     c->hfac.ensure(std::max<size_t>(own * (c->L - 1) * bb, 1));
-    if (c->b > 64) c->scratch.ensure(own * (size_t)c->b * 2 * (c->b + 1));
+    if (c->b > 64 && c->b < 128) c->scratch.ensure(own * (size_t)c->b * 2 * (c->b + 1));
+    if (c->b >= 128) {
+      c->fwork.ensure(bt_factor_work_elems(c->b, own));
+      c->fiwork.ensure((size_t)own * 2 * c->b);
+    }
     BtFactorArgs a{c->L, c->b, own, c->abdiag.p, c->ablow.p, c->dz.p, c->sinv.p, c->gfac.p, c->hfac.p,
-                   c->scratch.p, c->status.p};
+                   c->scratch.p, c->status.p, c->fwork.p, c->fiwork.p};
     CK(bt_factor(a, c->stream));
+    c->fwork.release();  // factor workspaces are transient
+    c->fiwork.release();
   } else {
     const int n = c->n, nb = kDenseNb, nblk = (n + nb - 1) / nb;
     c->lu.ensure((size_t)own * n * n);

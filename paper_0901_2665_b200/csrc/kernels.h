@@ -26,10 +26,13 @@ struct BtFactorArgs {
   double2* sinv;          // nodes * L*b*b
   double2* g;             // nodes * (L-1)*b*b: G_l = S_l^{-1} C_l^T
   double2* h;             // nodes * (L-1)*b*b: H_l = S_l^{-1} C_{l-1}, l >= 1
-  double2* scratch;       // nodes * b * 2b (used when b > 64)
+  double2* scratch;       // nodes * b * 2b (single-CTA path, 64 < b < 128)
   int* status;            // set to 1 on a singular block pivot
+  double2* work;          // b >= 128: bt_factor_work_elems(b, nodes) double2
+  int* iwork;             // b >= 128: nodes * 2b
 };
 cudaError_t bt_factor(const BtFactorArgs& a, cudaStream_t st);
+size_t bt_factor_work_elems(int b, int nodes);
 
 // Sweeps: for every node slot s and column j < m:
 //   real mode   : T_s = Re(coeff[s] * (z_s B - A)^{-1} Y)     (Y real, T real, ld = ldv)

@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(NC * B / 64 / TPW * 32) bt_sweep_kernel(BtSwee
   // vector; big blocks (one step = many chunks, latency amortised): one slot loaded at the
   // step start, y_l read back by its own lane, and for B = 512 a single running buffer
   constexpr bool VPRE = B <= 128;
-  constexpr bool VDB = B <= 256;
+  constexpr bool VDB = B * NC <= 2048;
   constexpr int VS = VPRE ? NSTAGE : 1;               // vector slots
   constexpr int MT = B / 8;                           // m-tiles
   constexpr int NWARPS = (B / 8) * (NC / 8) / TPW;
@@ -296,7 +296,7 @@ template <int B, int NC, int TPW, int NSTAGE>
 static cudaError_t launch_sweep(const BtSweepArgs& a, cudaStream_t st) {
   using Sh = SweepShape<B>;
   constexpr int NWARPS = (B / 8) * (NC / 8) / TPW;
-  constexpr int nvec = (B <= 256 ? 2 : 1) + (B <= 128 ? NSTAGE : 1);
+  constexpr int nvec = (B * NC <= 2048 ? 2 : 1) + (B <= 128 ? NSTAGE : 1);
   const size_t sm = sizeof(double2) * ((size_t)nvec * NC * Sh::SV + (size_t)NSTAGE * Sh::KCMAX * Sh::SA);
   dim3 grid((a.m + NC - 1) / NC, a.nodes);
   cudaError_t e;
@@ -325,7 +325,7 @@ cudaError_t bt_sweep(const BtSweepArgs& a, cudaStream_t st) {
     case 32: return launch_sweep<32, 16, 1, 3>(a, st);    // 8 warps
     case 64: return launch_sweep<64, 16, 2, 3>(a, st);    // 8 warps
     case 128: return launch_sweep<128, 8, 2, 3>(a, st);   // 8 warps
-    case 256: return launch_sweep<256, 8, 4, 3>(a, st);   // 8 warps
+    case 256: return launch_sweep<256, 16, 8, 2>(a, st);  // 8 warps; 16 columns halve L2 bytes/flop
     case 512: return launch_sweep<512, 8, 8, 2>(a, st);   // 8 warps
   }
   return cudaErrorInvalidValue;
