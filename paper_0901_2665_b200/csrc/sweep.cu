@@ -18,26 +18,37 @@
 // shifts and the inner loops unroll; small blocks split every accumulator in two (even /
 // odd k) to halve the DMMA dependency chain.
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
+namespace cg = cooperative_groups;
+
 namespace feastgpu {
 
-// chunk widths: whole matrices while they fit 32 KB, else the largest power of two that does
-template <int B>
+// chunk widths: whole matrices while a chunk (the CTA's RB = B/P rows) fits 32 KB, else the
+// largest power of two that does
+template <int B, int P>
 struct SweepShape {
-  static constexpr int KCB = (B * B * 16 <= 32 * 1024) ? B : (32 * 1024) / (B * 16);
-  static constexpr int KCF = (2 * B * B * 16 <= 32 * 1024) ? 2 * B : KCB;
+  static constexpr int RB = B / P;
+  static constexpr int KCB = (B * RB * 16 <= 32 * 1024) ? B : (32 * 1024) / (RB * 16);
+  static constexpr int KCF = (2 * B * RB * 16 <= 32 * 1024) ? 2 * B : KCB;
   static constexpr int NCHF = 2 * B / KCF, NCHB = B / KCB;
   static constexpr int KCMAX = KCF > KCB ? KCF : KCB;
-  static constexpr int SA = B + 2;  // stage column stride (double2), conflict-free LDS.128
-  static constexpr int SV = B + 4;  // vector [col][k] stride (double2)
-  static constexpr int SY = B + 4;  // real vector stride (double), conflict-free LDS.64
+  static constexpr int SA = RB + 2;  // stage column stride (double2), conflict-free LDS.128
+  static constexpr int SV = B + 4;   // vector [col][k] stride (double2)
+  static constexpr int SY = B + 4;   // real vector stride (double), conflict-free LDS.64
 };
 
-template <int B, int NC, int TPW, int NSTAGE, bool CPLX_IN>
-__global__ void __launch_bounds__(NC * B / 64 / TPW * 32) bt_sweep_kernel(BtSweepArgs a) {
-  using Sh = SweepShape<B>;
+// P > 1: a thread-block cluster of P CTAs shares one column block; CTA rank p computes rows
+// [p*B/P, (p+1)*B/P) of every chain step and stores them into all P CTAs' running-vector
+// buffers through distributed shared memory, one cluster barrier per step (finer work units
+// for the 148 SMs, and enough CTAs when a GPU owns a single contour node).
+template <int B, int P, int NC, int TPW, int NSTAGE, bool CPLX_IN>
+__global__ void __launch_bounds__(NC * B / 64 / P / TPW * 32) bt_sweep_kernel(BtSweepArgs a) {
+  using Sh = SweepShape<B, P>;
+  constexpr int RB = Sh::RB;
   constexpr int KCF = Sh::KCF, KCB = Sh::KCB, NCHF = Sh::NCHF, NCHB = Sh::NCHB, KCMAX = Sh::KCMAX;
   constexpr int SA = Sh::SA, SV = Sh::SV, SY = Sh::SY;
   // small blocks: vectors prefetched through NSTAGE slots and a double-buffered running
@@ -46,13 +57,15 @@ __global__ void __launch_bounds__(NC * B / 64 / TPW * 32) bt_sweep_kernel(BtSwee
   constexpr bool VPRE = B <= 128;
   constexpr bool VDB = B * NC <= 2048;
   constexpr int VS = VPRE ? NSTAGE : 1;               // vector slots
-  constexpr int MT = B / 8;                           // m-tiles
-  constexpr int NWARPS = (B / 8) * (NC / 8) / TPW;
+  constexpr int MT = RB / 8;                          // local m-tiles
+  constexpr int NWARPS = MT * (NC / 8) / TPW;
   constexpr int NT = NWARPS * 32;
   constexpr bool SPLIT = TPW <= 2;                    // two accumulator sets
   constexpr size_t BB = (size_t)B * B;
   const int s = blockIdx.y;
-  const int c0 = blockIdx.x * NC;
+  const int prank = P > 1 ? (int)(blockIdx.x % P) : 0;
+  const int c0 = (blockIdx.x / P) * NC;
+  const int row0 = prank * RB;
   const int L = a.L, m = a.m, ldv = a.ldv;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
   extern __shared__ __align__(16) double2 smem[];
@@ -69,6 +82,8 @@ __global__ void __launch_bounds__(NC * B / 64 / TPW * 32) bt_sweep_kernel(BtSwee
   const int total = L * NCHF + (L - 1) * NCHB;
 
   for (int i = tid; i < (VDB ? 2 : 1) * NC * SV; i += NT) Vs0[i] = make_double2(0.0, 0.0);
+  // every CTA of the cluster has zeroed its buffers before anyone stores into them remotely
+  if (P > 1) cg::this_cluster().sync();
 
   // -------- producer: chunk q (+ the step's right-hand-side rows with its first chunk) --------
   auto issue = [&](int q) {
@@ -82,13 +97,13 @@ __global__ void __launch_bounds__(NC * B / 64 / TPW * 32) bt_sweep_kernel(BtSwee
         vseq = l;
         const int k0 = j * KCF;
 #pragma unroll
-        for (int e0 = 0; e0 < KCF * B; e0 += NT) {
+        for (int e0 = 0; e0 < KCF * RB; e0 += NT) {
           const int e = e0 + tid;
-          if (KCF * B % NT == 0 || e < KCF * B) {
-            const int k = e / B, i = e % B, kg = k0 + k;
+          if (KCF * RB % NT == 0 || e < KCF * RB) {
+            const int k = e / RB, i = e % RB, kg = k0 + k;
             const bool v = kg < B || l > 0;
-            const double2* src = kg < B ? sinv + (size_t)l * BB + (size_t)kg * B + i
-                                        : hm + (size_t)(l - 1) * BB + (size_t)(kg - B) * B + i;
+            const double2* src = kg < B ? sinv + (size_t)l * BB + (size_t)kg * B + row0 + i
+                                        : hm + (size_t)(l - 1) * BB + (size_t)(kg - B) * B + row0 + i;
             const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(dst + k * SA + i));
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(v ? src : sinv),
                          "r"(v ? 16 : 0));
@@ -99,11 +114,14 @@ __global__ void __launch_bounds__(NC * B / 64 / TPW * 32) bt_sweep_kernel(BtSwee
         l = L - 2 - q2 / NCHB;
         j = q2 - (q2 / NCHB) * NCHB;
         vseq = L + (L - 2 - l);
-        const double2* src = gm + (size_t)l * BB + (size_t)j * KCB * B;
+        const double2* src = gm + (size_t)l * BB + (size_t)j * KCB * B + row0;
 #pragma unroll
-        for (int e0 = 0; e0 < KCB * B; e0 += NT) {
+        for (int e0 = 0; e0 < KCB * RB; e0 += NT) {
           const int e = e0 + tid;
-          if (KCB * B % NT == 0 || e < KCB * B) cp_async16(dst + (e / B) * SA + e % B, src + e);
+          if (KCB * RB % NT == 0 || e < KCB * RB) {
+            const int k = e / RB, i = e % RB;
+            cp_async16(dst + k * SA + i, src + (size_t)k * B + i);
+          }
         }
       }
       if (VPRE && j == 0) {
@@ -146,13 +164,29 @@ __global__ void __launch_bounds__(NC * B / 64 / TPW * 32) bt_sweep_kernel(BtSwee
   };
 
   CAcc acc[TPW], acc2[SPLIT ? TPW : 1];
-  int arow[TPW], bcol[TPW];  // fragment offsets: A row 8*mt+g, B column 8*nt+g
+  // fragment offsets: A row 8*mt+g within this CTA's rows (arow), the same row within the
+  // layer (grow = row0 + arow), B column 8*nt+g
+  int arow[TPW], grow[TPW], bcol[TPW];
 #pragma unroll
   for (int j = 0; j < TPW; ++j) {
     const int tt = warp + NWARPS * j;
     arow[j] = 8 * (tt % MT) + g;
+    grow[j] = row0 + arow[j];
     bcol[j] = 8 * (tt / MT) + g;
   }
+  // this step's result rows go to every CTA of the cluster (DSMEM) or just here
+  auto put = [&](double2* Vout, int idx, double2 val) {
+    if (P == 1) {
+      Vout[idx] = val;
+    } else {
+      cg::cluster_group cl = cg::this_cluster();
+#pragma unroll
+      for (int q = 0; q < P; ++q) cl.map_shared_rank(Vout, q)[idx] = val;
+    }
+  };
+  auto step_barrier = [&]() {
+    if (P > 1) cg::this_cluster().sync();
+  };
   auto zero_acc = [&]() {
 #pragma unroll
     for (int j = 0; j < TPW; ++j) {
@@ -215,25 +249,29 @@ __global__ void __launch_bounds__(NC * B / 64 / TPW * 32) bt_sweep_kernel(BtSwee
       }
     }
     fold_acc();
-    if (!VDB) __syncthreads();  // single running buffer: every warp is done reading y_{l-1}
+    if (!VDB) {  // single running buffer: every warp (of every cluster CTA) is done with y_{l-1}
+      if (P > 1) step_barrier();
+      else __syncthreads();
+    }
 #pragma unroll
     for (int j = 0; j < TPW; ++j) {
       const int cl0 = bcol[j] - g + 2 * t4;
       const double2 y0 = make_double2(acc[j].r0, acc[j].i0);
       const double2 y1 = make_double2(acc[j].r1, acc[j].i1);
-      Vout[(cl0 + 0) * SV + arow[j]] = y0;
-      Vout[(cl0 + 1) * SV + arow[j]] = y1;
+      put(Vout, (cl0 + 0) * SV + grow[j], y0);
+      put(Vout, (cl0 + 1) * SV + grow[j], y1);
       if (l + 1 < L) {
-        const size_t row = (size_t)l * B + arow[j];
+        const size_t row = (size_t)l * B + grow[j];
         if (c0 + cl0 < m) W[row + (size_t)(c0 + cl0) * ldv] = y0;
         if (c0 + cl0 + 1 < m) W[row + (size_t)(c0 + cl0 + 1) * ldv] = y1;
       }
     }
+    step_barrier();
   }
 
   // ---------------- backward sweep ----------------
   auto epilogue = [&](int l, int j, double2 x0, double2 x1) {
-    const size_t row = (size_t)l * B + arow[j];
+    const size_t row = (size_t)l * B + grow[j];
     const int col = c0 + bcol[j] - g + 2 * t4;
     if (a.complex_mode) {
       if (col < m) W[row + (size_t)col * ldv] = x0;
@@ -268,11 +306,14 @@ __global__ void __launch_bounds__(NC * B / 64 / TPW * 32) bt_sweep_kernel(BtSwee
       }
     }
     fold_acc();
-    if (!VDB) __syncthreads();  // single running buffer: every warp is done reading x_{l+1}
+    if (!VDB) {  // single running buffer: every warp (of every cluster CTA) is done with x_{l+1}
+      if (P > 1) step_barrier();
+      else __syncthreads();
+    }
 #pragma unroll
     for (int j = 0; j < TPW; ++j) {
       const int cl0 = bcol[j] - g + 2 * t4;
-      const int r = arow[j];
+      const int r = grow[j];
       double2 y0, y1;
       if (VPRE) {
         y0 = Ys[(cl0 + 0) * SV + r];
@@ -284,35 +325,45 @@ __global__ void __launch_bounds__(NC * B / 64 / TPW * 32) bt_sweep_kernel(BtSwee
       }
       const double2 x0 = make_double2(y0.x - acc[j].r0, y0.y - acc[j].i0);
       const double2 x1 = make_double2(y1.x - acc[j].r1, y1.y - acc[j].i1);
-      Vout[(cl0 + 0) * SV + r] = x0;
-      Vout[(cl0 + 1) * SV + r] = x1;
+      put(Vout, (cl0 + 0) * SV + r, x0);
+      put(Vout, (cl0 + 1) * SV + r, x1);
       epilogue(l, j, x0, x1);
     }
+    step_barrier();
   }
   cp_async_wait<0>();
 }
 
-template <int B, int NC, int TPW, int NSTAGE>
+template <int B, int P, int NC, int TPW, int NSTAGE>
 static cudaError_t launch_sweep(const BtSweepArgs& a, cudaStream_t st) {
-  using Sh = SweepShape<B>;
-  constexpr int NWARPS = (B / 8) * (NC / 8) / TPW;
+  using Sh = SweepShape<B, P>;
+  constexpr int NWARPS = (B / 8 / P) * (NC / 8) / TPW;
   constexpr int nvec = (B * NC <= 2048 ? 2 : 1) + (B <= 128 ? NSTAGE : 1);
   const size_t sm = sizeof(double2) * ((size_t)nvec * NC * Sh::SV + (size_t)NSTAGE * Sh::KCMAX * Sh::SA);
-  dim3 grid((a.m + NC - 1) / NC, a.nodes);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((a.m + NC - 1) / NC * P), (unsigned)a.nodes);
+  cfg.blockDim = dim3(NWARPS * 32);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = P;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   cudaError_t e;
   if (a.complex_mode) {
-    auto kern = bt_sweep_kernel<B, NC, TPW, NSTAGE, true>;
+    auto kern = bt_sweep_kernel<B, P, NC, TPW, NSTAGE, true>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    kern<<<grid, NWARPS * 32, sm, st>>>(a);
+    if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, kern, a);
   } else {
-    auto kern = bt_sweep_kernel<B, NC, TPW, NSTAGE, false>;
+    auto kern = bt_sweep_kernel<B, P, NC, TPW, NSTAGE, false>;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    kern<<<grid, NWARPS * 32, sm, st>>>(a);
+    if (e == cudaSuccess) e = cudaLaunchKernelEx(&cfg, kern, a);
   }
   ++g_launches;
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 bool bt_block_supported(int b) {
@@ -321,12 +372,12 @@ bool bt_block_supported(int b) {
 
 cudaError_t bt_sweep(const BtSweepArgs& a, cudaStream_t st) {
   switch (a.b) {
-    case 16: return launch_sweep<16, 16, 1, 3>(a, st);    // 4 warps
-    case 32: return launch_sweep<32, 16, 1, 3>(a, st);    // 8 warps
-    case 64: return launch_sweep<64, 16, 2, 3>(a, st);    // 8 warps
-    case 128: return launch_sweep<128, 8, 2, 3>(a, st);   // 8 warps
-    case 256: return launch_sweep<256, 16, 8, 2>(a, st);  // 8 warps; 16 columns halve L2 bytes/flop
-    case 512: return launch_sweep<512, 8, 8, 2>(a, st);   // 8 warps
+    case 16: return launch_sweep<16, 1, 16, 1, 3>(a, st);    // 4 warps
+    case 32: return launch_sweep<32, 1, 16, 1, 3>(a, st);    // 8 warps
+    case 64: return launch_sweep<64, 1, 16, 2, 3>(a, st);    // 8 warps
+    case 128: return launch_sweep<128, 2, 8, 1, 3>(a, st);   // cluster of 2, 8 warps each
+    case 256: return launch_sweep<256, 4, 8, 1, 3>(a, st);   // cluster of 4, 8 warps each
+    case 512: return launch_sweep<512, 4, 8, 2, 2>(a, st);   // cluster of 4, 8 warps each
   }
   return cudaErrorInvalidValue;
 }
