@@ -186,6 +186,19 @@ __global__ void bt_make_kernel(int b, const double2* __restrict__ ab, const doub
   }
 }
 
+// col-major b x b (blockIdx.y = node, node stride b*b) -> panel layout (kernels.h)
+__global__ void pack_panels_kernel(const double2* __restrict__ src, double2* __restrict__ dst, int64_t dstride,
+                                   int b, int rb) {
+  const int64_t bb = (int64_t)b * b;
+  src += blockIdx.y * bb;
+  dst += blockIdx.y * dstride;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < bb; e += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(e / b), i = (int)(e - (int64_t)k * b);
+    const int p = i / rb, r = i - p * rb;
+    dst[(int64_t)p * b * rb + (int64_t)k * rb + (r ^ (2 * (k & 3)))] = src[e];
+  }
+}
+
 static cudaError_t bt_factor_big(const BtFactorArgs& a, cudaStream_t st) {
   const int L = a.L, b = a.b, nodes = a.nodes;
   const int64_t bb = (int64_t)b * b, lnode = (int64_t)L * bb, gnode = (int64_t)(L > 1 ? L - 1 : 0) * bb;
@@ -199,25 +212,32 @@ static cudaError_t bt_factor_big(const BtFactorArgs& a, cudaStream_t st) {
   int* perm = ipiv + nodes * b;
   const double2 one = make_double2(1.0, 0.0), mone = make_double2(-1.0, 0.0), zero = make_double2(0.0, 0.0);
   dim3 g((unsigned)std::min<int64_t>((bb + 255) / 256, 512), nodes);
+  // factors leave in the sweep's panel layout; G_l also stays col-major in scr until the
+  // next layer's Schur update has used it (zgetrs reuses scr only after that)
+  const int rb = bt_panel_rows(b);
+  auto pack = [&](const double2* src, double2* dst, int64_t dstride) {
+    pack_panels_kernel<<<g, 256, 0, st>>>(src, dst, dstride, b, rb);
+    ++g_launches;
+  };
   for (int l = 0; l < L; ++l) {
     bt_make_kernel<<<g, 256, 0, st>>>(b, a.abdiag + l * bb, a.z, S, 0);
     ++g_launches;
-    if (l > 0)
-      zgemm_batched(b, b, b, mone, Cp, b, bb, a.g + (l - 1) * bb, b, gnode, one, S, b, bb, nodes, st);
+    if (l > 0) zgemm_batched(b, b, b, mone, Cp, b, bb, scr, b, bb, one, S, b, bb, nodes, st);
     zgetrf_batched(b, nodes, S, bb, ipiv, perm, dinv, a.status, st);
     bt_make_kernel<<<g, 256, 0, st>>>(b, nullptr, a.z, X, 2);
     ++g_launches;
     zgetrs_batched(b, nodes, b, S, bb, perm, dinv, X, b, scr, st);
-    // S_l^{-1} out (node stride L*bb)
-    cudaMemcpy2DAsync(a.sinv + l * bb, sizeof(double2) * lnode, X, sizeof(double2) * bb, sizeof(double2) * bb,
-                      nodes, cudaMemcpyDeviceToDevice, st);
-    if (l > 0)
-      zgemm_batched(b, b, b, one, X, b, bb, Cp, b, bb, zero, a.h + (l - 1) * bb, b, gnode, nodes, st);
+    pack(X, a.sinv + l * bb, lnode);  // S_l^{-1} (node stride L*bb)
+    if (l > 0) {  // H_l = S_l^{-1} C_{l-1}, via CT (C_{l-1}^T is spent)
+      zgemm_batched(b, b, b, one, X, b, bb, Cp, b, bb, zero, CT, b, bb, nodes, st);
+      pack(CT, a.h + (l - 1) * bb, gnode);
+    }
     if (l + 1 < L) {
       bt_make_kernel<<<g, 256, 0, st>>>(b, a.ablow + l * bb, a.z, Cp, 0);
       bt_make_kernel<<<g, 256, 0, st>>>(b, a.ablow + l * bb, a.z, CT, 1);
       g_launches += 2;
-      zgemm_batched(b, b, b, one, X, b, bb, CT, b, bb, zero, a.g + l * bb, b, gnode, nodes, st);
+      zgemm_batched(b, b, b, one, X, b, bb, CT, b, bb, zero, scr, b, bb, nodes, st);
+      pack(scr, a.g + l * bb, gnode);
     }
   }
   return cudaGetLastError();

@@ -1000,10 +1000,13 @@ int feast_gpu_solve_shift(feast_gpu_ctx* c, int e, double* rhs, int m, int mode)
     if (!c->factored) fail(FEAST_EINPUT, "feast_gpu: factors not prepared");
     if (e < c->e0 || e >= c->e1) fail(FEAST_EINPUT, "solve_shift: node not owned by this rank");
     if (m < 1) fail(FEAST_EINPUT, "solve_shift: no right-hand sides");
-    ensure_workspace(c, m);
+    // panel-layout factors (b >= 128): the sweep takes real right-hand sides, so the complex
+    // ones go through as 2m real columns [Re | Im] and are recombined afterwards
+    const bool split = c->blocktri && bt_panel_rows(c->b) > 0;
+    ensure_workspace(c, split ? 2 * m : m);
     const int s = e - c->e0;
     const size_t nv = (size_t)c->npad * m;
-    double2* w = c->W.p + s * nv;
+    double2* w = c->W.p + s * (split ? 2 : 1) * nv;
     CK(cudaMemsetAsync(w, 0, sizeof(double2) * nv, c->stream));
     CK(cudaMemcpy2DAsync(w, sizeof(double2) * c->npad, rhs, sizeof(double2) * c->n, sizeof(double2) * c->n, m,
                          cudaMemcpyHostToDevice, c->stream));
@@ -1011,10 +1014,12 @@ int feast_gpu_solve_shift(feast_gpu_ctx* c, int e, double* rhs, int m, int mode)
     if (mode) CK(conj_inplace(w, nv, c->stream));
     if (c->blocktri) {
       const size_t bb = (size_t)c->b * c->b;
-      BtSweepArgs a{c->L, c->b, 1, m, c->npad, c->ablow.p, c->dz.p + s, c->dcoeff.p + s,
+      if (split) CK(split_complex(w, c->AQ.p, c->npad, c->npad, m, c->stream));
+      BtSweepArgs a{c->L, c->b, 1, split ? 2 * m : m, c->npad, c->ablow.p, c->dz.p + s, c->dcoeff.p + s,
                     c->sinv.p + s * c->L * bb, c->gfac.p + s * (c->L - 1) * bb,
-                    c->hfac.p + s * (c->L - 1) * bb, nullptr, nullptr, w, 1};
+                    c->hfac.p + s * (c->L - 1) * bb, split ? c->AQ.p : nullptr, nullptr, w, split ? 2 : 1};
       CK(bt_sweep(a, c->stream));
+      if (split) CK(merge_complex(w, c->npad, c->npad, m, c->stream));
     } else {
       const int n = c->n, nb = kDenseNb, nblk = (n + nb - 1) / nb;
       DenseSolveArgs a{n, 1, m, c->npad, c->lu.p + (size_t)s * n * n, c->perm.p + (size_t)s * n,

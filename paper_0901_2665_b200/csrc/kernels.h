@@ -34,9 +34,16 @@ struct BtFactorArgs {
 cudaError_t bt_factor(const BtFactorArgs& a, cudaStream_t st);
 size_t bt_factor_work_elems(int b, int nodes);
 
+// Panel layout of the factors for b >= 128 (the bulk-copy sweep): each b x b factor is stored
+// as P = b / RB row panels, panel p holding rows [p*RB, (p+1)*RB) column by column (RB
+// contiguous entries per column), row r of column k at position r ^ (2*(k & 3)) — a bank
+// swizzle for the sweep's shared-memory reads. RB = bt_panel_rows(b); 0 = plain col-major.
+int bt_panel_rows(int b);
+
 // Sweeps: for every node slot s and column j < m:
-//   real mode   : T_s = Re(coeff[s] * (z_s B - A)^{-1} Y)     (Y real, T real, ld = ldv)
-//   complex mode: W_s <- (z_s B - A)^{-1} W_s                 (complex in place, ld = ldv)
+//   real mode (0)    : T_s = Re(coeff[s] * (z_s B - A)^{-1} Y)  (Y real, T real, ld = ldv)
+//   complex mode (1) : W_s <- (z_s B - A)^{-1} W_s              (complex in place; b < 128)
+//   complex out (2)  : W_s = (z_s B - A)^{-1} Y                 (Y real, W complex; b >= 128)
 struct BtSweepArgs {
   int L, b, nodes, m, ldv;
   const double2* ablow;
@@ -132,5 +139,9 @@ cudaError_t fill_zero(double* p, size_t count, cudaStream_t st);
 cudaError_t gather_columns(const double* src, int ld, int n, const int* idx, int m, double* dst,
                            int ldd, cudaStream_t st);
 cudaError_t conj_inplace(double2* p, size_t count, cudaStream_t st);
+// complex right-hand sides through the real-input sweep: y[:, j] = Re w[:, j],
+// y[:, m + j] = Im w[:, j] (n rows, ld both); then w[:, j] <- w[:, j] + i w[:, m + j]
+cudaError_t split_complex(const double2* w, double* y, int n, int64_t ld, int m, cudaStream_t st);
+cudaError_t merge_complex(double2* w, int n, int64_t ld, int m, cudaStream_t st);
 
 }  // namespace feastgpu

@@ -91,4 +91,39 @@ cudaError_t conj_inplace(double2* p, size_t count, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+__global__ void split_complex_kernel(const double2* w, double* y, int n, int64_t ld, int m) {
+  const int64_t total = (int64_t)n * m;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / n, i = e - j * n;
+    const double2 v = w[i + j * ld];
+    y[i + j * ld] = v.x;
+    y[i + (j + m) * ld] = v.y;
+  }
+}
+
+__global__ void merge_complex_kernel(double2* w, int n, int64_t ld, int m) {
+  const int64_t total = (int64_t)n * m;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / n, i = e - j * n;
+    const double2 re = w[i + j * ld], im = w[i + (j + m) * ld];
+    w[i + j * ld] = make_double2(re.x - im.y, re.y + im.x);
+  }
+}
+
+cudaError_t split_complex(const double2* w, double* y, int n, int64_t ld, int m, cudaStream_t st) {
+  const int64_t total = (int64_t)n * m;
+  if (!total) return cudaSuccess;
+  split_complex_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, st>>>(w, y, n, ld, m);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t merge_complex(double2* w, int n, int64_t ld, int m, cudaStream_t st) {
+  const int64_t total = (int64_t)n * m;
+  if (!total) return cudaSuccess;
+  merge_complex_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, st>>>(w, n, ld, m);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 }  // namespace feastgpu

@@ -370,14 +370,15 @@ bool bt_block_supported(int b) {
   return b == 16 || b == 32 || b == 64 || b == 128 || b == 256 || b == 512;
 }
 
+cudaError_t bt_sweep_tma(const BtSweepArgs& a, cudaStream_t st);
+
 cudaError_t bt_sweep(const BtSweepArgs& a, cudaStream_t st) {
+  // b >= 128: panel-layout factors and the bulk-copy pipeline of sweep_tma.cu
+  if (bt_panel_rows(a.b) > 0) return bt_sweep_tma(a, st);
   switch (a.b) {
     case 16: return launch_sweep<16, 1, 16, 1, 3>(a, st);    // 4 warps
     case 32: return launch_sweep<32, 1, 16, 1, 3>(a, st);    // 8 warps
     case 64: return launch_sweep<64, 1, 16, 2, 3>(a, st);    // 8 warps
-    case 128: return launch_sweep<128, 2, 8, 1, 3>(a, st);   // cluster of 2, 8 warps each
-    case 256: return launch_sweep<256, 4, 8, 1, 3>(a, st);   // cluster of 4, 8 warps each
-    case 512: return launch_sweep<512, 4, 8, 2, 2>(a, st);   // cluster of 4, 8 warps each
   }
   return cudaErrorInvalidValue;
 }

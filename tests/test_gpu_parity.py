@@ -229,3 +229,25 @@ def test_warm_start_one_loop(ctx, F):
     r2 = ctx.solve(iv, F.FeastConfig(m0=prob.m0), initial_y=y0)
     assert r2.status == "converged" and r2.loops_used <= 1
     assert np.allclose(r2.eigenvalues, r.eigenvalues, rtol=1e-12, atol=1e-14)
+
+
+# large diagonal blocks: the cluster-split sweeps (b = 128/256/512 after power-of-two
+# re-blocking), chains of length 1..5, a ragged last column block
+@pytest.mark.parametrize("L,b", [(1, 128), (2, 128), (5, 128), (3, 200), (4, 256), (3, 512)])
+def test_contour_pass_large_blocks(ctx, L, b):
+    from paper_0901_2665_b200 import problems as P
+    a, bb = P.blocktri_operators(L, b, seed=L * 1000 + b)
+    emin, emax, ne, m0 = -0.3, 0.4, 8, 20
+    ctx.set_pencil(a, bb)
+    ctx.prepare(emin, emax, ne)
+    y = O.random_block(a.n, m0, 5)
+    q = ctx.contour_pass(y)
+    qr = O.accumulate_real(a, bb, emin, emax, ne, y)
+    assert np.max(np.abs(q - qr)) <= 1e-11 * max(1.0, np.max(np.abs(qr)))
+    z, _ = ctx.contour()
+    rng = np.random.default_rng(2)
+    rhs = rng.standard_normal((a.n, 3)) + 1j * rng.standard_normal((a.n, 3))
+    for mode in (0, 1):
+        x = ctx.solve_shift(ne - 1, rhs, bool(mode))
+        # 1e-11: kappa(zB - A) grows with the block size (b = 512 reaches ~2e-12)
+        assert rel(x, O.shift_solve(a, bb, z[ne - 1], rhs, mode)) <= 1e-11
