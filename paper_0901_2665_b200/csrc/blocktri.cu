@@ -14,7 +14,10 @@
 // has a positive-definite imaginary part and is nonsingular; partial pivoting inside each
 // S_l handles local growth (Gauss-Jordan below).
 
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <utility>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -158,8 +161,9 @@ __global__ void __launch_bounds__(256) bt_factor_kernel(BtFactorArgs a) {
 // ---------------------------------------------------------------------------
 // Large blocks (b >= 128): the same recursion, every dense b x b operation batched over the
 // nodes and run on the DMMA GEMM / batched-LU kernels (one layer at a time):
-//   S_l = M_l - C_{l-1} G_{l-1}  (zgemm) ;  LU(S_l) (zgetrf_batched) ;  S_l^{-1} = LU \ I ;
-//   H_l = S_l^{-1} C_{l-1} ;  G_l = S_l^{-1} C_l^T  (zgemm)
+//   S_l = M_l - C_{l-1} G_{l-1}  (zgemm) ;  S_l^{-1} by block Gauss-Jordan in place (below;
+//   FEAST_BT_FACTOR=lu selects pivoted LU + solve against I instead) ;
+//   H_l = S_l^{-1} C_{l-1} ;  G_l = S_l^{-1} C_l^T  (zgemm) ; all three packed into panels
 // ---------------------------------------------------------------------------
 cudaError_t zgemm_batched(int m, int n, int k, double2 alpha, const double2* a, int lda, int64_t sa,
                           const double2* b, int ldb, int64_t sb, double2 beta, double2* c, int ldc,
@@ -199,7 +203,143 @@ __global__ void pack_panels_kernel(const double2* __restrict__ src, double2* __r
   }
 }
 
+// ---------------------------------------------------------------------------
+// In-place inversion of S_l by block Gauss-Jordan (block width GJ_NB, batched over nodes).
+// Im(S_l) = Im(z) x (SPD) is positive definite, so elimination without pivoting across
+// blocks is stable (growth factor < 3 for complex symmetric matrices with a definite real or
+// imaginary part, Higham, Accuracy and Stability, 2nd ed., §10.4); inside a diagonal block
+// the same argument holds, so the diagonal-block inverse runs pivot-free with ONE barrier per
+// column: every thread keeps its 16 entries of [D | I] in registers and the next pivot row and
+// column are published into double-buffered shared staging by their owners.
+// Per block column k (rows/cols kb = [k0, k0 + NB)):
+//   D = S_kk^{-1};  P = S[:, kb];  R = D S[kb, :] (R[:, kb] := D + I)
+//   S -= P R   (rows outside kb get the Gauss-Jordan update; S[:, kb] becomes -P D)
+//   S[kb, :] = R with S[kb, kb] = D
+// ---------------------------------------------------------------------------
+constexpr int GJ_NB = 64;
+
+__global__ void __launch_bounds__(512) gj_diag_kernel(double2* __restrict__ S, int n, int64_t sstride, int k0,
+                                                      double2* __restrict__ D, double2* __restrict__ P,
+                                                      double2* __restrict__ R, int* status) {
+  constexpr int NB = GJ_NB, NQ = 2 * NB / 8;  // thread: row i, columns (t & 7) + 8q of [A | I]
+  __shared__ double2 rowst[2][2 * NB];
+  __shared__ double2 colst[2][NB];
+  __shared__ int bad;
+  const int s = blockIdx.x, tid = threadIdx.x;
+  const int i = tid >> 3, c8 = tid & 7;
+  double2* Sn = S + s * sstride;
+  double2* Dn = D + (int64_t)s * NB * NB;
+  double2* Pn = P + (int64_t)s * n * NB;
+  double2* Rn = R + (int64_t)s * NB * n;
+  // panel copy P = S[:, kb] (n x NB, ld n)
+  for (int e = tid; e < n * NB; e += 512) {
+    const int r = e % n, c = e / n;
+    Pn[e] = Sn[r + (int64_t)(k0 + c) * n];
+  }
+  double2 v[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int j = c8 + 8 * q;
+    v[q] = j < NB ? Sn[(k0 + i) + (int64_t)(k0 + j) * n] : make_double2(j - NB == i ? 1.0 : 0.0, 0.0);
+  }
+  if (tid == 0) bad = 0;
+  // publish pivot row/column 0
+  if (i == 0) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) rowst[0][c8 + 8 * q] = v[q];
+  }
+  if (c8 == 0) colst[0][i] = v[0];
+  for (int k = 0; k < NB; ++k) {
+    __syncthreads();
+    const double2* rs = rowst[k & 1];
+    const double2 piv = colst[k & 1][k];
+    if (!(cabs_(piv) > 0.0) || !isfinite(piv.x) || !isfinite(piv.y)) {
+      if (tid == 0) {
+        bad = 1;
+        atomicExch(status, 1);
+      }
+    }
+    const double2 g = cdiv(colst[k & 1][i], piv);
+    const double2 rp = cdiv(make_double2(1.0, 0.0), piv);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int j = c8 + 8 * q;
+      const bool active = (j < NB) ? (j >= k) : (j - NB <= k);
+      if (active) {
+        if (i == k) v[q] = cmul(v[q], rp);
+        else v[q] = csub(v[q], cmul(g, rs[j]));
+      }
+    }
+    if (k + 1 < NB) {
+      if (i == k + 1) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) rowst[(k + 1) & 1][c8 + 8 * q] = v[q];
+      }
+#pragma unroll
+      for (int q = 0; q < NQ / 2; ++q)
+        if (c8 + 8 * q == k + 1) colst[(k + 1) & 1][i] = v[q];
+    }
+  }
+  __syncthreads();
+  if (bad) return;
+  // D = right half; R[:, kb] = D + I
+#pragma unroll
+  for (int q = NQ / 2; q < NQ; ++q) {
+    const int j = c8 + 8 * q - NB;
+    Dn[i + j * NB] = v[q];
+    Rn[i + (int64_t)(k0 + j) * NB] = make_double2(v[q].x + (i == j ? 1.0 : 0.0), v[q].y);
+  }
+}
+
+// S[kb, :] = R, except S[kb, kb] = D
+__global__ void gj_rowput_kernel(double2* __restrict__ S, int n, int64_t sstride, int k0,
+                                 const double2* __restrict__ D, const double2* __restrict__ R) {
+  constexpr int NB = GJ_NB;
+  const int s = blockIdx.y;
+  double2* Sn = S + s * sstride;
+  const double2* Dn = D + (int64_t)s * NB * NB;
+  const double2* Rn = R + (int64_t)s * NB * n;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < NB * n; e += gridDim.x * blockDim.x) {
+    const int r = e % NB, j = e / NB;
+    const bool diag = j >= k0 && j < k0 + NB;
+    Sn[(k0 + r) + (int64_t)j * n] = diag ? Dn[r + (j - k0) * NB] : Rn[e];
+  }
+}
+
+// S_s <- S_s^{-1} for the batch (n % GJ_NB == 0); work: nodes * (2 n NB + NB^2) double2
+static cudaError_t gj_invert_batched(double2* S, int n, int64_t sstride, int nodes, double2* work, int* status,
+                                     cudaStream_t st) {
+  constexpr int NB = GJ_NB;
+  double2* P = work;
+  double2* R = P + (int64_t)nodes * n * NB;
+  double2* D = R + (int64_t)nodes * NB * n;
+  const double2 one = make_double2(1.0, 0.0), mone = make_double2(-1.0, 0.0), zero = make_double2(0.0, 0.0);
+  for (int k0 = 0; k0 < n; k0 += NB) {
+    gj_diag_kernel<<<nodes, 512, 0, st>>>(S, n, sstride, k0, D, P, R, status);
+    ++g_launches;
+    // R[:, j] = D S[kb, j] for j outside kb (two column ranges)
+    if (k0 > 0) zgemm_batched(NB, k0, NB, one, D, NB, NB * NB, S + k0, n, sstride, zero, R, NB, (int64_t)NB * n, nodes, st);
+    if (k0 + NB < n)
+      zgemm_batched(NB, n - k0 - NB, NB, one, D, NB, NB * NB, S + k0 + (int64_t)(k0 + NB) * n, n, sstride, zero,
+                    R + (int64_t)(k0 + NB) * NB, NB, (int64_t)NB * n, nodes, st);
+    zgemm_batched(n, n, NB, mone, P, n, (int64_t)n * NB, R, NB, (int64_t)NB * n, one, S, n, sstride, nodes, st);
+    dim3 g((unsigned)std::min(((int64_t)NB * n + 255) / 256, (int64_t)256), nodes);
+    gj_rowput_kernel<<<g, 256, 0, st>>>(S, n, sstride, k0, D, R);
+    ++g_launches;
+  }
+  return cudaGetLastError();
+}
+
+static bool factor_use_lu() {
+  static const bool lu = [] {
+    const char* e = getenv("FEAST_BT_FACTOR");
+    return e && e[0] == 'l';
+  }();
+  return lu;
+}
+
 static cudaError_t bt_factor_big(const BtFactorArgs& a, cudaStream_t st) {
+  const bool lu = factor_use_lu();  // FEAST_BT_FACTOR=lu: pivoted LU + solve (comparison path)
   const int L = a.L, b = a.b, nodes = a.nodes;
   const int64_t bb = (int64_t)b * b, lnode = (int64_t)L * bb, gnode = (int64_t)(L > 1 ? L - 1 : 0) * bb;
   double2* S = a.work;                 // LU of S_l            (nodes x bb)
@@ -208,6 +348,7 @@ static cudaError_t bt_factor_big(const BtFactorArgs& a, cudaStream_t st) {
   double2* X = CT + nodes * bb;        // S_l^{-1}
   double2* scr = X + nodes * bb;       // zgetrs scratch
   double2* dinv = scr + nodes * bb;    // diagonal-block inverses
+  double2* gjw = dinv + (int64_t)nodes * ((b + kDenseNb - 1) / kDenseNb) * 2 * kDenseNb * kDenseNb;  // GJ work
   int* ipiv = a.iwork;
   int* perm = ipiv + nodes * b;
   const double2 one = make_double2(1.0, 0.0), mone = make_double2(-1.0, 0.0), zero = make_double2(0.0, 0.0);
@@ -223,20 +364,24 @@ static cudaError_t bt_factor_big(const BtFactorArgs& a, cudaStream_t st) {
     bt_make_kernel<<<g, 256, 0, st>>>(b, a.abdiag + l * bb, a.z, S, 0);
     ++g_launches;
     if (l > 0) zgemm_batched(b, b, b, mone, Cp, b, bb, scr, b, bb, one, S, b, bb, nodes, st);
-    zgetrf_batched(b, nodes, S, bb, ipiv, perm, dinv, a.status, st);
-    bt_make_kernel<<<g, 256, 0, st>>>(b, nullptr, a.z, X, 2);
-    ++g_launches;
-    zgetrs_batched(b, nodes, b, S, bb, perm, dinv, X, b, scr, st);
-    pack(X, a.sinv + l * bb, lnode);  // S_l^{-1} (node stride L*bb)
+    if (lu) {  // FEAST_BT_FACTOR=lu
+      zgetrf_batched(b, nodes, S, bb, ipiv, perm, dinv, a.status, st);
+      bt_make_kernel<<<g, 256, 0, st>>>(b, nullptr, a.z, X, 2);
+      ++g_launches;
+      zgetrs_batched(b, nodes, b, S, bb, perm, dinv, X, b, scr, st);
+    }
+    if (!lu) gj_invert_batched(S, b, bb, nodes, gjw, a.status, st);  // S <- S^{-1} in place
+    const double2* Xi = lu ? X : S;  // S_l^{-1}
+    pack(Xi, a.sinv + l * bb, lnode);  // S_l^{-1} (node stride L*bb)
     if (l > 0) {  // H_l = S_l^{-1} C_{l-1}, via CT (C_{l-1}^T is spent)
-      zgemm_batched(b, b, b, one, X, b, bb, Cp, b, bb, zero, CT, b, bb, nodes, st);
+      zgemm_batched(b, b, b, one, Xi, b, bb, Cp, b, bb, zero, CT, b, bb, nodes, st);
       pack(CT, a.h + (l - 1) * bb, gnode);
     }
     if (l + 1 < L) {
       bt_make_kernel<<<g, 256, 0, st>>>(b, a.ablow + l * bb, a.z, Cp, 0);
       bt_make_kernel<<<g, 256, 0, st>>>(b, a.ablow + l * bb, a.z, CT, 1);
       g_launches += 2;
-      zgemm_batched(b, b, b, one, X, b, bb, CT, b, bb, zero, scr, b, bb, nodes, st);
+      zgemm_batched(b, b, b, one, Xi, b, bb, CT, b, bb, zero, scr, b, bb, nodes, st);
       pack(scr, a.g + l * bb, gnode);
     }
   }
@@ -245,7 +390,8 @@ static cudaError_t bt_factor_big(const BtFactorArgs& a, cudaStream_t st) {
 
 size_t bt_factor_work_elems(int b, int nodes) {  // double2 elements of BtFactorArgs::work
   const int nblk = (b + kDenseNb - 1) / kDenseNb;
-  return (size_t)nodes * (5 * (size_t)b * b + (size_t)nblk * 2 * kDenseNb * kDenseNb);
+  return (size_t)nodes * (5 * (size_t)b * b + (size_t)nblk * 2 * kDenseNb * kDenseNb + 2 * (size_t)b * GJ_NB +
+                          (size_t)GJ_NB * GJ_NB);
 }
 
 cudaError_t bt_factor(const BtFactorArgs& a, cudaStream_t st) {

@@ -12,10 +12,13 @@
 //     mbarrier — no block-wide barrier per chunk, no address arithmetic in compute warps;
 //   * the right-hand-side rows of each step (Y_l forward, this CTA's rows of y_l backward)
 //     ride the same pipeline into a ring of vector slots;
-//   * rows are split over a thread-block cluster of P CTAs exactly as in sweep.cu (DSMEM
-//     exchange of each step's result, one cluster barrier per step).
+//   * rows are split over a thread-block cluster of P CTAs as in sweep.cu (DSMEM exchange of
+//     each step's result), but the per-step exchange is an mbarrier with remote arrivals that
+//     a warp waits on only when it next needs the running vector (forward: at the first H_l
+//     chunk, so the S_l^{-1} Y_l half covers the exchange latency).
 
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -202,16 +205,24 @@ __global__ void __launch_bounds__(((B / P / 8) * (NC / 8) / TPW + 1) * 32)
     if (lane == 0) mbar_arrive(empty + qc % NSTAGE);
     ++qc;
   };
-  // exchange barrier among the compute warps of the whole cluster (the producer never joins):
-  // every warp fences its DSMEM stores and arrives on every CTA's step mbarrier, then waits on
-  // its own CTA's
+  // exchange barrier among the compute warps of the whole cluster (the producer never joins),
+  // split in two: after its DSMEM stores a warp fences and arrives on every CTA's step
+  // mbarrier; it waits on its own CTA's only when it next reads the running vector — the
+  // forward step's S_l^{-1} Y_l half needs no y_{l-1}, so the exchange hides behind it
   uint32_t step_phase = 0;
-  auto step_barrier = [&]() {
+  bool pending = false;
+  auto step_arrive = [&]() {
     asm volatile("fence.acq_rel.cluster;\n" ::: "memory");
     __syncwarp();
     if (lane < P) mbar_arrive_cluster(stepbar, lane);
-    mbar_wait_cluster(stepbar, step_phase & 1);
-    ++step_phase;
+    pending = true;
+  };
+  auto step_wait = [&]() {
+    if (pending) {
+      mbar_wait_cluster(stepbar, step_phase & 1);
+      ++step_phase;
+      pending = false;
+    }
   };
 
   CAcc acc[TPW], acc2[SPLIT ? TPW : 1];
@@ -258,6 +269,7 @@ __global__ void __launch_bounds__(((B / P / 8) * (NC / 8) / TPW + 1) * 32)
     zero_acc();
 #pragma unroll 1
     for (int c = 0; c < NCHF; ++c) {
+      if (c * KC == B) step_wait();  // first H_l chunk: y_{l-1} from the whole cluster
       const double2* As = acquire();
       if (!(l == 0 && c * KC >= B)) {
 #pragma unroll
@@ -284,7 +296,10 @@ __global__ void __launch_bounds__(((B / P / 8) * (NC / 8) / TPW + 1) * 32)
       release();
     }
     fold_acc();
-    if (!VDB) step_barrier();  // single running buffer: everyone is done with y_{l-1}
+    if (!VDB) {  // single running buffer: everyone is done with y_{l-1}
+      step_arrive();
+      step_wait();
+    }
 #pragma unroll
     for (int j = 0; j < TPW; ++j) {
       const int cl0 = bcol[j] - g + 2 * t4;
@@ -298,7 +313,7 @@ __global__ void __launch_bounds__(((B / P / 8) * (NC / 8) / TPW + 1) * 32)
         if (c0 + cl0 + 1 < m) W[row + (size_t)(c0 + cl0 + 1) * ldv] = y1;
       }
     }
-    step_barrier();
+    step_arrive();
   }
 
   // ---------------- backward sweep ----------------
@@ -324,6 +339,7 @@ __global__ void __launch_bounds__(((B / P / 8) * (NC / 8) / TPW + 1) * 32)
     // copy may predate it) which still sits in the buffer this step writes x_{L-2} into
     const double2* Yc = reinterpret_cast<const double2*>(Vslot + ((L + (L - 2 - l)) % VSN) * SLOT);
     zero_acc();
+    step_wait();  // x_{l+1} from the whole cluster
 #pragma unroll 1
     for (int c = 0; c < NCHB; ++c) {
       const double2* As = acquire();
@@ -337,7 +353,10 @@ __global__ void __launch_bounds__(((B / P / 8) * (NC / 8) / TPW + 1) * 32)
       release();
     }
     fold_acc();
-    if (!VDB) step_barrier();
+    if (!VDB) {
+      step_arrive();
+      step_wait();
+    }
 #pragma unroll
     for (int j = 0; j < TPW; ++j) {
       const int cl0 = bcol[j] - g + 2 * t4;
@@ -359,7 +378,7 @@ __global__ void __launch_bounds__(((B / P / 8) * (NC / 8) / TPW + 1) * 32)
       put(Vout, (cl0 + 1) * SV + grow[j], x1);
       epilogue(l, j, x0, x1);
     }
-    step_barrier();
+    step_arrive();
   }
   if (P > 1) cluster_sync_unaligned();  // no CTA leaves while its peers may still address it
 }
@@ -395,7 +414,7 @@ static cudaError_t launch_tma(const BtSweepArgs& a, cudaStream_t st) {
 int bt_panel_rows(int b) {
   switch (b) {
     case 128: return 64;
-    case 256: return 64;
+    case 256: return 128;
     case 512: return 128;
   }
   return 0;
@@ -407,7 +426,9 @@ cudaError_t bt_sweep_tma(const BtSweepArgs& a, cudaStream_t st) {
   if (a.complex_mode == 1 || a.ldv % 2) return cudaErrorInvalidValue;
   switch (a.b) {
     case 128: return launch_tma<128, 2, 8, 1, 3>(a, st);
-    case 256: return launch_tma<256, 4, 8, 1, 3>(a, st);
+    // clusters of 2: every SM can host one (clusters of 4 leave 16 of 148 idle, GPC
+    // granularity — tools/microbench/cluster_occ.cu), measured 8% faster on config 3
+    case 256: return launch_tma<256, 2, 8, 2, 3>(a, st);
     case 512: return launch_tma<512, 4, 8, 2, 2>(a, st);
   }
   return cudaErrorInvalidValue;
