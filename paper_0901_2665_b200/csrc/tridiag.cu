@@ -9,7 +9,7 @@
 //                       doubles, 148 KB at m = 192); one CTA of 1024 threads; reflectors out.
 //   tri_eigvals_kernel  one warp per eigenvalue: 32-way multisection of the Sturm count of
 //                       T - sigma I (dstebz) down to round-off; eigenvalue j is the j-th.
-//   tri_eigvecs_kernel  one warp per cluster (|lam_i - lam_j| <= 1e-3 ||T||, dstein):
+//   tri_eigvecs_kernel  one warp per cluster (|lam_i - lam_j| <= 1e-5 ||T||, cf. dstein):
 //                       inverse iteration with the partial-pivot tridiagonal LU (dgttrf /
 //                       dgtts2), modified Gram-Schmidt against earlier cluster members.
 //   tri_back_kernel     V = H_0 H_1 ... H_{m-3} Z, one warp per column.
@@ -318,7 +318,10 @@ __global__ void tri_eigvecs_kernel(TriArgs p) {
   if (cl >= m) return;
   double lo, hi, tnorm, pivmin;
   tri_bounds(m, p.d, p.e, lo, hi, tnorm, pivmin);
-  const double ortol = 1e-3 * tnorm, eps = DBL_EPSILON;
+  // reorthogonalisation threshold: dstein uses 1e-3 ||T||; inverse iteration leaves a
+  // non-orthogonality of O(eps ||T|| / gap), so 1e-5 ||T|| already bounds it by ~1e-11 while
+  // keeping FEAST's dense interior Ritz spectra from chaining into one long cluster
+  const double ortol = 1e-5 * tnorm, eps = DBL_EPSILON;
   if (cl > 0 && p.lam[cl] - p.lam[cl - 1] <= ortol) return;  // not the first of its cluster
   int cend = cl + 1;
   while (cend < m && p.lam[cend] - p.lam[cend - 1] <= ortol) ++cend;
