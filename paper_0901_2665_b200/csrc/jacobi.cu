@@ -382,7 +382,8 @@ __global__ void eig_sort_kernel(int m, int mp, const double* w, const double* v,
 
 cudaError_t sym_eig(EigWork* w, int m, double* a, double* evals, double* v, cudaStream_t st) {
   if (m < 1 || m > w->mmax) return cudaErrorInvalidValue;
-  // one-SM tridiagonal route while the packed matrix fits shared memory (FEAST_EIG=jacobi
+  // tridiagonal route up to m = 1024 (shared-memory reduction, preceded by an L2-resident
+  // stage for m > 236; FEAST_EIG=jacobi
   // forces block Jacobi for comparison)
   static const char* force = getenv("FEAST_EIG");
   const bool jacobi_only = force && force[0] == 'j';

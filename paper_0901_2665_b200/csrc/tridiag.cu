@@ -1,5 +1,5 @@
 // tridiag.cu — symmetric eigendecomposition for the reduced problem when it fits one SM
-// (m <= 240): the dense -> tridiagonal -> eigenpairs route of LAPACK's syevx, re-shaped for
+// (m <= 1024): the dense -> tridiagonal -> eigenpairs route of LAPACK's syevx, re-shaped for
 // one B200 CTA plus a grid of warps. Used by sym_eig (jacobi.cu) in place of block Jacobi for
 // those sizes; same contract as jacobi_eigh (eigh.hpp:84-163): eigenvalues ascending,
 // orthonormal eigenvectors, repeated eigenvalues allowed.
@@ -14,10 +14,17 @@
 //                       dgtts2), modified Gram-Schmidt against earlier cluster members.
 //   tri_back_kernel     V = H_0 H_1 ... H_{m-3} Z, one warp per column.
 
+#include <algorithm>
 #include <cfloat>
+#include <cstdio>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 #include "kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace feastgpu {
 
@@ -169,6 +176,398 @@ __global__ void __launch_bounds__(1024) tridiag_kernel(int m, const double* __re
     d[m - 1] = ps[pidx(m - 1, m - 1, m)];
     tau[m - 1] = 0.0;
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// 1b. Householder tridiagonalisation for m beyond one SM's shared memory: cooperative grid,
+//     packed lower triangle in global memory (L2-resident: 2.4 MB at m = 768). Trailing
+//     column j belongs to CTA j mod G (one warp per column, coalesced down the column).
+//     Per column, three grid barriers:
+//       (1) every CTA: v (from column k), its columns' dots p_j = A(j:, j).v(j:) and its
+//           per-warp axpy partials A(i, j) v_j -> part[c][i]        (fixed-order sums)
+//       (2) CTA c: p_i = t (dot_i + sum_c part[c][i]) for its row slice, and p.v partials
+//       (3) every CTA: w = p - (t/2)(p.v) v, rank-2 update of its columns; the owner of the
+//           next column leaves its norm
+//     Data written by other CTAs is read with ld.global.cg (L2), never through a stale L1.
+// ---------------------------------------------------------------------------
+struct TriCoopArgs {
+  int m;
+  const double* a;  // m x m input
+  double *d, *e, *hv, *tau;
+  double* gps;      // packed lower triangle, m(m+1)/2
+  double* part;     // G x m per-CTA axpy partials
+  double* pcol;     // m column dots
+  double* pvec;     // m: p = t A v
+  double* pvp;      // G: per-CTA p.v partials
+  double* xn2;      // 1: ||A(k+3:, k+1)||^2 for the next reflector
+};
+
+constexpr int TC_NT = 256, TC_NW = TC_NT / 32;
+
+__global__ void __launch_bounds__(TC_NT) tridiag_coop_kernel(TriCoopArgs p) {
+  cg::grid_group grid = cg::this_grid();
+  const int m = p.m, G = gridDim.x, c = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  extern __shared__ double csm[];
+  double* vsh = csm;          // m
+  double* wsh = vsh + m;      // m
+  double* qw = wsh + m;       // TC_NW x m per-warp axpy partials
+  __shared__ double red33[33];
+  __shared__ double bc;
+  double* gps = p.gps;
+  for (int64_t idx = c * (int64_t)TC_NT + tid; idx < (int64_t)m * m; idx += (int64_t)G * TC_NT) {
+    const int i = (int)(idx % m), j = (int)(idx / m);
+    if (i >= j) gps[pidx(i, j, m)] = p.a[idx];
+  }
+  grid.sync();
+  if (c == 0) {
+    double part = 0.0;
+    for (int i = 2 + tid; i < m; i += TC_NT) {
+      const double x = __ldcg(gps + pidx(i, 0, m));
+      part += x * x;
+    }
+    const double sm = tri_block_sum(part, red33);
+    if (tid == 0) *p.xn2 = sm;
+  }
+  grid.sync();
+
+  for (int k = 0; k + 2 < m; ++k) {
+    const int r = m - k - 1;
+    const double* colk = gps + pidx(k + 1, k, m);
+    const double xn2 = __ldcg(p.xn2);
+    const double alpha = __ldcg(colk);
+    double t = 0.0, beta = alpha, scal = 0.0;
+    if (xn2 > 0.0) {
+      beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+      t = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    for (int i = tid; i < r; i += TC_NT) {
+      const double vi = i == 0 ? 1.0 : (t != 0.0 ? __ldcg(colk + i) * scal : 0.0);
+      vsh[i] = vi;
+      if (c == 0) p.hv[(k + 1 + i) + (int64_t)k * m] = vi;
+    }
+    if (c == 0 && tid == 0) {
+      p.d[k] = __ldcg(gps + pidx(k, k, m));
+      p.e[k] = beta;
+      p.tau[k] = t;
+    }
+    for (int i = tid; i < TC_NW * r; i += TC_NT) qw[(i / r) * m + (i % r)] = 0.0;
+    __syncthreads();
+    // ---- (1) column dots and per-warp axpy partials ----
+    if (t != 0.0) {
+      for (int jj = warp; c + G * jj < r; jj += TC_NW) {
+        const int j = c + G * jj;
+        const double* colj = gps + pidx(k + 1 + j, k + 1 + j, m) - j;  // colj[i] = A22(i, j)
+        const double vj = vsh[j];
+        double ds = 0.0;
+        double* q = qw + warp * m;
+        for (int i0 = j + lane; i0 < r; i0 += 256) {  // 8 L2 loads in flight per lane
+          double x[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) x[u] = i0 + 32 * u < r ? __ldcg(colj + i0 + 32 * u) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int i = i0 + 32 * u;
+            if (i < r) {
+              if (i == j) {
+                ds += x[u] * vj;
+              } else {
+                ds += x[u] * vsh[i];
+                q[i] += x[u] * vj;
+              }
+            }
+          }
+        }
+        ds = warp_sum(ds);
+        if (lane == 0) p.pcol[j] = ds;
+      }
+    }
+    __syncthreads();
+    if (t != 0.0)
+      for (int i = tid; i < r; i += TC_NT) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int w = 0; w < TC_NW; ++w) sacc += qw[w * m + i];
+        p.part[(int64_t)c * m + i] = sacc;
+      }
+    grid.sync();  // (1)
+    // ---- (2) p = t A v on this CTA's row slice ----
+    if (t != 0.0) {
+      // rows [i0, i1) of this CTA (<= 8 when G >= r / 8); thread cc reads partial cc of all of
+      // them at once, then a fixed-order reduction over threads
+      const int sl = (r + G - 1) / G, i0 = c * sl, i1 = min(r, i0 + sl);
+      double pv = 0.0;
+      for (int b0 = i0; b0 < i1; b0 += 8) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          x[u] = 0.0;
+          for (int cc = tid; cc < G; cc += TC_NT)
+            if (b0 + u < i1) x[u] += __ldcg(p.part + (int64_t)cc * m + b0 + u);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          x[u] = warp_sum(x[u]);
+          if (lane == 0) qw[u * TC_NW + warp] = x[u];  // qw is free again here
+        }
+        __syncthreads();
+        if (tid < 8 && b0 + tid < i1) {
+          const int i = b0 + tid;
+          double pf = __ldcg(p.pcol + i);
+#pragma unroll
+          for (int w = 0; w < TC_NW; ++w) pf += qw[tid * TC_NW + w];
+          pf *= t;
+          p.pvec[i] = pf;
+          pv += pf * vsh[i];
+        }
+        __syncthreads();
+      }
+      pv = tri_block_sum(pv, red33);
+      if (tid == 0) p.pvp[c] = pv;
+    }
+    grid.sync();  // (2)
+    // ---- (3) w and the rank-2 update of this CTA's columns ----
+    if (t != 0.0) {
+      if (warp == 0) {
+        double s = 0.0;
+        for (int cc = lane; cc < G; cc += 32) s += __ldcg(p.pvp + cc);
+        s = warp_sum(s);
+        if (lane == 0) bc = s;
+      }
+      __syncthreads();
+      const double cf = -0.5 * t * bc;
+      for (int i = tid; i < r; i += TC_NT) wsh[i] = __ldcg(p.pvec + i) + cf * vsh[i];
+      __syncthreads();
+      for (int jj = warp; c + G * jj < r; jj += TC_NW) {
+        const int j = c + G * jj;
+        double* colj = gps + pidx(k + 1 + j, k + 1 + j, m) - j;
+        const double vj = vsh[j], wj = wsh[j];
+        double nrm = 0.0;
+        for (int i0 = j + lane; i0 < r; i0 += 256) {
+          double x[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) x[u] = i0 + 32 * u < r ? __ldcg(colj + i0 + 32 * u) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int i = i0 + 32 * u;
+            if (i < r) {
+              const double y = x[u] - (vsh[i] * wj + wsh[i] * vj);
+              __stcg(colj + i, y);
+              if (i >= 2) nrm += y * y;
+            }
+          }
+        }
+        if (j == 0) {
+          nrm = warp_sum(nrm);
+          if (lane == 0) *p.xn2 = nrm;
+        }
+      }
+    } else if (c == 0) {  // no reflection: the next column's norm directly
+      double part = 0.0;
+      const double* coln = gps + pidx(k + 1, k + 1, m);
+      for (int i = 2 + tid; i < r; i += TC_NT) {
+        const double x = __ldcg(coln + i);
+        part += x * x;
+      }
+      const double sm = tri_block_sum(part, red33);
+      if (tid == 0) *p.xn2 = sm;
+    }
+    grid.sync();  // (3)
+  }
+  if (c == 0 && tid == 0) {
+    if (m >= 2) {
+      p.d[m - 2] = __ldcg(gps + pidx(m - 2, m - 2, m));
+      p.e[m - 2] = __ldcg(gps + pidx(m - 1, m - 2, m));
+      p.tau[m - 2] = 0.0;
+    }
+    p.d[m - 1] = __ldcg(gps + pidx(m - 1, m - 1, m));
+    p.tau[m - 1] = 0.0;
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// 1c. Householder tridiagonalisation on a thread-block cluster of TCL_P CTAs: global column g
+//     lives (packed, rows g..m-1) in the shared memory of CTA g mod TCL_P, so all matrix
+//     traffic stays on-chip; only vectors cross CTAs, through distributed shared memory.
+//     Per column k (owner o = k mod P), three cluster barriers:
+//       (a) v and (t, beta) copied from the owner; each CTA: dots of its own columns
+//           (A(g:, g) . v) and its axpy partial q[i] = sum_{own g < i} A(i, g) v_g
+//       (b) CTA q: p_i = t (dot_i + sum_q' q_q'[i]) on its row slice, and p.v
+//       (c) every CTA: w = p - (t/2)(p.v) v and the rank-2 update of its own columns; the
+//           owner of column k+1 builds the next reflector into the other v buffer
+//     All sums run in a fixed order (deterministic).
+// ---------------------------------------------------------------------------
+constexpr int TCL_P = 16, TCL_NT = 512, TCL_NW = TCL_NT / 32;
+
+__host__ __device__ inline int tcl_ncols(int m, int q) { return q < m ? (m - q + TCL_P - 1) / TCL_P : 0; }
+// offset of the t-th own column (global g = q + t P, rows g..m-1) in CTA q's packed storage
+__host__ __device__ inline int tcl_off(int m, int q, int t) { return t * (m - q) - TCL_P * (t * (t - 1) / 2); }
+__host__ __device__ inline int tcl_local(int m, int q) { return tcl_off(m, q, tcl_ncols(m, q)); }
+
+__global__ void __launch_bounds__(TCL_NT) tridiag_cluster_kernel(int m, const double* __restrict__ a, double* d,
+                                                                 double* e, double* hv, double* tau) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int q = (int)cl.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  extern __shared__ double ksm[];
+  const int loc = tcl_local(m, 0);  // same layout size in every CTA (CTA 0 holds the most)
+  const int slmax = (m + TCL_P - 1) / TCL_P;
+  double* cols = ksm;               // own columns, packed
+  double* vb = cols + loc;          // 2 x m: reflector (trailing index), double-buffered by parity
+  double* ww = vb + 2 * m;          // m: w (trailing index)
+  double* pp = ww + m;              // m: p (trailing index), pushed by the slice owners
+  double* qall = pp + m;            // P x slmax: axpy partials of my row slice, pushed by every CTA
+  double* dall = qall + TCL_P * slmax;  // slmax: column dots of my row slice, pushed by the owners
+  __shared__ double scal_s[2];      // t per parity, pushed by the reflector's owner
+  __shared__ double pvall[TCL_P];   // p.v partials, pushed by every slice owner
+  __shared__ double xn2_s;          // owner of the next column: ||A(k+3:, k+1)||^2
+  __shared__ double red33[33];
+  const int ncol = tcl_ncols(m, q);
+  for (int t = 0; t < ncol; ++t) {  // own columns
+    const int g = q + t * TCL_P;
+    const int off = tcl_off(m, q, t);
+    for (int i = g + tid; i < m; i += TCL_NT) cols[off + (i - g)] = a[i + (int64_t)g * m];
+  }
+  __syncthreads();
+  // owner of column k (column k up to date locally): reflector into every CTA's v buffer
+  auto build = [&](int k, int par, bool fresh) {
+    const int t = (k - q) / TCL_P;
+    const double* ck = cols + tcl_off(m, q, t) - k;  // ck[i] = A(i, k), i >= k
+    const int r = m - k - 1;
+    double xn2;
+    if (fresh) {  // first column, or the previous step skipped its update (no norm left)
+      double part = 0.0;
+      for (int i = k + 2 + tid; i < m; i += TCL_NT) part += ck[i] * ck[i];
+      xn2 = tri_block_sum(part, red33);
+    } else {
+      xn2 = xn2_s;
+    }
+    const double alpha = ck[k + 1];
+    double tt = 0.0, beta = alpha, sc = 0.0;
+    if (xn2 > 0.0) {
+      beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+      tt = (beta - alpha) / beta;
+      sc = 1.0 / (alpha - beta);
+    }
+    for (int i = tid; i < r; i += TCL_NT) {
+      const double vi = i == 0 ? 1.0 : (tt != 0.0 ? ck[k + 1 + i] * sc : 0.0);
+      hv[(k + 1 + i) + (int64_t)k * m] = vi;
+#pragma unroll
+      for (int qq = 0; qq < TCL_P; ++qq) cl.map_shared_rank(vb + par * m, qq)[i] = vi;
+    }
+    if (tid < TCL_P) *cl.map_shared_rank(&scal_s[par], tid) = tt;
+    if (tid == 0) {
+      d[k] = ck[k];
+      e[k] = beta;
+      tau[k] = tt;
+    }
+  };
+  if (m > 2 && q == 0) build(0, 0, true);
+  cl.sync();
+
+  for (int k = 0; k + 2 < m; ++k) {
+    const int r = m - k - 1, par = k & 1, base = k + 1;  // trailing index = global - base
+    const double* v = vb + par * m;
+    const double tt = scal_s[par];
+    const int sl = (r + TCL_P - 1) / TCL_P;              // row slice of CTA qq: [qq sl, (qq+1) sl)
+    const int t0 = base > q ? (base - q + TCL_P - 1) / TCL_P : 0;  // first own column >= base
+    // ---- (a) dots of own columns and axpy partials, pushed to the slice owners ----
+    if (tt != 0.0) {
+      for (int t = t0 + warp; t < ncol; t += TCL_NW) {
+        const int g = q + t * TCL_P;
+        const double* cg_ = cols + tcl_off(m, q, t) - g;  // cg_[i] = A(i, g)
+        double s = 0.0;
+        for (int i = g + lane; i < m; i += 32) s += cg_[i] * v[i - base];
+        s = warp_sum(s);
+        if (lane == 0) {
+          const int ti = g - base, ow = ti / sl;
+          cl.map_shared_rank(dall, ow)[ti - ow * sl] = s;
+        }
+      }
+      for (int i = base + tid; i < m; i += TCL_NT) {
+        const int tend = min(ncol, (i - q + TCL_P - 1) / TCL_P);  // own g in [base, i)
+        double s0 = 0.0, s1 = 0.0;
+        int t = t0, off = tcl_off(m, q, t0), g = q + t0 * TCL_P;
+        for (; t + 1 < tend; t += 2) {
+          const int off1 = off + (m - g), g1 = g + TCL_P;
+          s0 += cols[off + (i - g)] * v[g - base];
+          s1 += cols[off1 + (i - g1)] * v[g1 - base];
+          off = off1 + (m - g1);
+          g = g1 + TCL_P;
+        }
+        if (t < tend) s0 += cols[off + (i - g)] * v[g - base];
+        const int ti = i - base, ow = ti / sl;
+        cl.map_shared_rank(qall, ow)[q * slmax + (ti - ow * sl)] = s0 + s1;
+      }
+    }
+    cl.sync();  // (a)
+    // ---- (b) p on my row slice, pushed to every CTA, with my p.v partial ----
+    if (tt != 0.0) {
+      const int i0 = q * sl, i1 = min(r, i0 + sl);
+      double pv = 0.0;
+      for (int ti = i0 + tid; ti < i1; ti += TCL_NT) {
+        const int li = ti - i0;
+        double pf = dall[li];
+#pragma unroll
+        for (int qq = 0; qq < TCL_P; ++qq) pf += qall[qq * slmax + li];
+        pf *= tt;
+        pv += pf * v[ti];
+#pragma unroll
+        for (int qq = 0; qq < TCL_P; ++qq) cl.map_shared_rank(pp, qq)[ti] = pf;
+      }
+      pv = tri_block_sum(pv, red33);
+      if (tid < TCL_P) cl.map_shared_rank(pvall, tid)[q] = pv;
+    }
+    cl.sync();  // (b)
+    // ---- (c) w, rank-2 update of own columns, next reflector ----
+    if (tt != 0.0) {
+      double pv = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < TCL_P; ++qq) pv += pvall[qq];
+      const double cf = -0.5 * tt * pv;
+      for (int ti = tid; ti < r; ti += TCL_NT) ww[ti] = pp[ti] + cf * v[ti];
+      __syncthreads();
+      for (int t = t0 + warp; t < ncol; t += TCL_NW) {
+        const int g = q + t * TCL_P;
+        double* cg_ = cols + tcl_off(m, q, t) - g;
+        const double vg = v[g - base], wg = ww[g - base];
+        double nrm = 0.0;
+        for (int i = g + lane; i < m; i += 32) {
+          const double y = cg_[i] - (v[i - base] * wg + ww[i - base] * vg);
+          cg_[i] = y;
+          if (i >= g + 2) nrm += y * y;
+        }
+        if (g == base) {  // the next reflector's column: its norm below the subdiagonal
+          nrm = warp_sum(nrm);
+          if (lane == 0) xn2_s = nrm;
+        }
+      }
+    }
+    __syncthreads();
+    if (k + 3 < m && q == base % TCL_P) build(base, par ^ 1, tt == 0.0);
+    cl.sync();  // (c)
+  }
+  if (m >= 2 && q == (m - 2) % TCL_P && tid == 0) {
+    const int t = (m - 2 - q) / TCL_P;
+    const double* ck = cols + tcl_off(m, q, t) - (m - 2);
+    d[m - 2] = ck[m - 2];
+    e[m - 2] = ck[m - 1];
+    tau[m - 2] = 0.0;
+  }
+  if (q == (m - 1) % TCL_P && tid == 0) {
+    const int t = (m - 1 - q) / TCL_P;
+    d[m - 1] = cols[tcl_off(m, q, t)];
+    tau[m - 1] = 0.0;
+  }
+}
+
+// largest m whose cluster layout fits the 227 KB opt-in shared memory
+static size_t tcl_smem(int m) {
+  const size_t slmax = (m + TCL_P - 1) / TCL_P;
+  return sizeof(double) * ((size_t)tcl_local(m, 0) + 4 * (size_t)m + (TCL_P + 1) * slmax);
 }
 
 // ---------------------------------------------------------------------------
@@ -389,24 +788,24 @@ __global__ void tri_eigvecs_kernel(TriArgs p) {
 // ---------------------------------------------------------------------------
 // 4. back-transformation V = H_0 ... H_{m-3} Z, one warp per column
 // ---------------------------------------------------------------------------
-// the column stays in registers (8 per lane: m <= 256); the next reflector is loaded while
-// the current one is applied, so the only serial latency is the warp reduction
+// the column stays in registers (NQ per lane: m <= 32 NQ); the next PD reflectors are loaded
+// while the current one is applied, so the only serial latency is the warp reduction
+template <int NQ, int PD>
 __global__ void tri_back_kernel(int m, const double* __restrict__ hv, const double* __restrict__ tau,
                                 const double* __restrict__ z, double* v) {
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (c >= m) return;
-  constexpr int PD = 4;  // reflectors in flight (one L2 latency ~ a few reflector steps)
-  double x[8], h[PD][8];
+  double x[NQ], h[PD][NQ];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
+  for (int q = 0; q < NQ; ++q) {
     const int i = lane + 32 * q;
     x[q] = i < m ? z[i + (int64_t)c * m] : 0.0;
   }
   auto load = [&](int k, double* dst) {
     const double* hk = hv + (int64_t)k * m;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < NQ; ++q) {
       const int i = lane + 32 * q;
       dst[q] = (k >= 0 && i > k && i < m) ? hk[i] : 0.0;
     }
@@ -421,24 +820,26 @@ __global__ void tri_back_kernel(int m, const double* __restrict__ hv, const doub
         const double t = tau[kk];
         double sum = 0.0;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) sum += h[s][q] * x[q];
+        for (int q = 0; q < NQ; ++q) sum += h[s][q] * x[q];
         sum = warp_sum(sum) * t;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) x[q] -= sum * h[s][q];
+        for (int q = 0; q < NQ; ++q) x[q] -= sum * h[s][q];
       }
       load(kk - PD, h[s]);  // refill this slot PD reflectors ahead
     }
   }
   double* vc = v + (int64_t)c * m;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
+  for (int q = 0; q < NQ; ++q) {
     const int i = lane + 32 * q;
     if (i < m) vc[i] = x[q];
   }
 }
 
-// packed m(m+1)/2 + v, w (2m) doubles <= 226 KB; 4 threads per trailing row (1024 threads)
-int tri_max_dim() { return 236; }
+// one-SM route while the packed matrix + v, w (2m) fit 226 KB of shared memory; the
+// cooperative grid route beyond (tws holds 6m^2 + 3m doubles for either)
+static int tri_smem_dim() { return 236; }
+int tri_max_dim() { return 1024; }
 
 // a (m x m, overwritten is allowed), eigenvalues ascending -> evals, vectors -> v (m x m)
 cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws, int* iws, cudaStream_t st) {
@@ -448,23 +849,81 @@ cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws
   double* tau = e + m;
   double* hv = tau + m;            // m*m
   double* z = hv + (size_t)m * m;  // m*m
-  double* lu = z + (size_t)m * m;  // 4*m*m
-  const size_t sm = sizeof(double) * ((size_t)m * (m + 1) / 2 + 2 * m);
+  double* gw = z + (size_t)m * m;  // 4*m*m: cooperative route scratch
   static bool attr = false;
   if (!attr) {
     // dynamic + static (the reduction scratch) must stay within the 227 KB opt-in limit
     cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
     attr = true;
   }
-  tridiag_kernel<<<1, 1024, sm, st>>>(m, a, d, e, hv, tau);
-  ++g_launches;
-  TriArgs p{m, d, e, evals, z, lu, iws};
+  // route: one SM for small m, the 16-CTA cluster while its layout fits (m <= ~840), the
+  // cooperative grid beyond; FEAST_TRI=s (one SM, m <= 236) / k (cluster) / c (cooperative)
+  static const char* route_env = getenv("FEAST_TRI");
+  const char rt = route_env ? route_env[0] : 0;
+  const bool fits_cluster = m > 2 && tcl_smem(m) <= 220 * 1024;
+  // (measured: the cluster overtakes the single SM above m ~ 128; 0.87 vs 0.92 ms at m = 192)
+  bool use_smem = m <= 128, use_cluster = !use_smem && fits_cluster;
+  if (!use_smem && !use_cluster && m <= tri_smem_dim()) use_smem = true;
+  if (rt == 's' && m <= tri_smem_dim()) use_smem = true, use_cluster = false;
+  if (rt == 'k' && fits_cluster) use_smem = false, use_cluster = true;
+  if (rt == 'c') use_smem = false, use_cluster = false;
+  if (use_cluster) {
+    const size_t ksm = tcl_smem(m);
+    cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ksm);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(TCL_P);
+    cfg.blockDim = dim3(TCL_NT);
+    cfg.dynamicSmemBytes = ksm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = TCL_P;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t err = cudaLaunchKernelEx(&cfg, tridiag_cluster_kernel, m, a, d, e, hv, tau);
+    ++g_launches;
+    if (err != cudaSuccess) return err;
+  } else if (use_smem) {
+    const size_t sm = sizeof(double) * ((size_t)m * (m + 1) / 2 + 2 * m);
+    tridiag_kernel<<<1, 1024, sm, st>>>(m, a, d, e, hv, tau);
+    ++g_launches;
+  } else {
+    static int grid = 0;
+    const size_t csm = sizeof(double) * (size_t)(2 + TC_NW) * 1024;  // sized for m <= 1024
+    if (!grid) {
+      cudaFuncSetAttribute(tridiag_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
+      int dev = 0, sms = 148, occ = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tridiag_coop_kernel, TC_NT, csm);
+      grid = sms * std::max(occ, 1);
+      grid = std::min(grid, sms);  // one CTA per SM: more CTAs only add barrier cost
+    }
+    TriCoopArgs p{m, a, d, e, hv, tau, gw, nullptr, nullptr, nullptr, nullptr, nullptr};
+    p.part = p.gps + (size_t)m * (m + 1) / 2;
+    p.pcol = p.part + (size_t)grid * m;
+    p.pvec = p.pcol + m;
+    p.pvp = p.pvec + m;
+    p.xn2 = p.pvp + grid;
+    void* args[] = {&p};
+    cudaError_t err = cudaLaunchCooperativeKernel((void*)tridiag_coop_kernel, grid, TC_NT, args, csm, st);
+    ++g_launches;
+    if (err != cudaSuccess) return err;
+  }
+  TriArgs p{m, d, e, evals, z, nullptr, iws};
   const int wpb = 4;
   tri_eigvals_kernel<<<(m + wpb - 1) / wpb, 32 * wpb, sizeof(double) * 2 * m, st>>>(p);
   ++g_launches;
-  tri_eigvecs_kernel<<<(m + wpb - 1) / wpb, 32 * wpb, sizeof(double) * 6 * m * wpb + 64, st>>>(p);
+  const size_t vsm = sizeof(double) * 6 * m * wpb + 64;
+  if (vsm > 48 * 1024) cudaFuncSetAttribute(tri_eigvecs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsm);
+  tri_eigvecs_kernel<<<(m + wpb - 1) / wpb, 32 * wpb, vsm, st>>>(p);
   ++g_launches;
-  tri_back_kernel<<<(m + 7) / 8, 256, 0, st>>>(m, hv, tau, z, v);
+  if (m <= 256) tri_back_kernel<8, 4><<<(m + 7) / 8, 256, 0, st>>>(m, hv, tau, z, v);
+  else if (m <= 512) tri_back_kernel<16, 4><<<(m + 3) / 4, 128, 0, st>>>(m, hv, tau, z, v);
+  else tri_back_kernel<32, 2><<<(m + 3) / 4, 128, 0, st>>>(m, hv, tau, z, v);
   ++g_launches;
   return cudaGetLastError();
 }
