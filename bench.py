@@ -260,6 +260,15 @@ def main():
     d2h = (8 * prob.n * (len(res.eigenvalues) + res.subspace.shape[1]) + 8 * prob.m0 * 3) / passes_e2e
 
     b_used = 16 if prob.a.kind != abi.STORAGE_DENSE else None
+    # DRAM traffic of the same kernel from the committed ncu --set full capture (profiles/)
+    traffic = None
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_traffic.json")) as f:
+            tr = json.load(f).get("bt_sweep_kernel<16,1,16,1,3,0>")
+        if b_used and tr and tr["config"].startswith(prob.name):
+            traffic = tr["dram_bytes_read_per_launch"] + tr["dram_bytes_write_per_launch"]
+    except (OSError, ValueError, KeyError):
+        traffic = None
     flops, bytes_ = sweep_flops(prob, b_used)
     k_ms = ph[3] / args.steps
     achieved = flops / (k_ms * 1e-3) / 1e12
@@ -280,7 +289,8 @@ def main():
                 "eigenpairs": len(res.eigenvalues), "seconds": e2e_s},
         "roofline": {"kernel": "bt_sweep_kernel" if b_used else "dense_solve (zgemm chain)",
                      "bound": "tensor", "achieved": achieved, "peak": PEAK_FP64_TFLOPS,
-                     "unit": "TFLOP/s", "frac": achieved / PEAK_FP64_TFLOPS, "traffic": None,
+                     "unit": "TFLOP/s", "frac": achieved / PEAK_FP64_TFLOPS, "traffic": traffic,
+                     "traffic_unit": "DRAM bytes per launch (ncu, profiles/r01_traffic.json)",
                      "algorithmic_flops_per_launch": flops, "algorithmic_bytes_per_launch": bytes_,
                      "hbm_frac": bytes_ / (k_ms * 1e-3) / 1e9 / peaks().get("hbm_gbs", 6650.0),
                      "avg_launch_ms": k_ms, "peak_source": "measured DMMA f64 (tools/microbench/fp64_peak.cu)"},
