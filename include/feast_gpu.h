@@ -141,6 +141,14 @@ int feast_gpu_set_pencil(feast_gpu_ctx* ctx, const feast_operator_t* a, const fe
  * (ensure_factors, core.hpp:304-311). */
 int feast_gpu_prepare(feast_gpu_ctx* ctx, double emin, double emax, int n_e);
 
+/* Memory plan for the factors (ensure_factors vs low_memory, core.hpp:302-311,335-336):
+ * nodes = 0 keeps every owned node's factors resident when they fit 80% of the free HBM
+ * and otherwise streams them in the largest batches that do; nodes > 0 forces batches of
+ * that many nodes. Streamed factors are recomputed every pass, batch by batch, and the
+ * quadrature sum continues in ascending e across batches (results are bit-identical to the
+ * resident plan). Takes effect at the next feast_gpu_prepare / feast_gpu_solve. */
+int feast_gpu_set_node_batch(feast_gpu_ctx* ctx, int nodes);
+
 /* Contour points actually used (host copies): z (2*n_e interleaved) and the
  * quadrature coefficients c_e = 0.5 * w_e * r * e^{i theta_e} (2*n_e). */
 int feast_gpu_contour(const feast_gpu_ctx* ctx, double* z, double* coeff);

@@ -409,23 +409,23 @@ cudaError_t bt_factor(const BtFactorArgs& a, cudaStream_t st) {
 // Q = -sum_s T_s, ascending s from zero (the ordered reduction of core.hpp:181-183)
 // ---------------------------------------------------------------------------
 __global__ void reduce_terms_kernel(const double* __restrict__ t, int nodes, int64_t slice, int n,
-                                    int m, int ld, double* __restrict__ q) {
+                                    int m, int ld, double* __restrict__ q, int accumulate) {
   const int64_t total = (int64_t)n * m;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = idx % n, j = idx / n;
     const int64_t off = i + j * ld;
-    double acc = 0.0;
+    double acc = accumulate ? q[off] : 0.0;  // node batches continue the same ascending sum
     for (int s = 0; s < nodes; ++s) acc -= t[s * slice + off];
     q[off] = acc;
   }
 }
 
 cudaError_t reduce_terms(const double* t, int nodes, int64_t slice, int n, int m, int ld, double* q,
-                         cudaStream_t st) {
+                         cudaStream_t st, int accumulate) {
   const int64_t total = (int64_t)n * m;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-  reduce_terms_kernel<<<blocks, 256, 0, st>>>(t, nodes, slice, n, m, ld, q);
+  reduce_terms_kernel<<<blocks, 256, 0, st>>>(t, nodes, slice, n, m, ld, q, accumulate);
   ++g_launches;
   return cudaGetLastError();
 }

@@ -176,8 +176,11 @@ struct feast_gpu_ctx {
   int ne = 0, e0 = 0, e1 = 0;
   std::vector<double2> z, coeff;  // all nodes
   DevBuf<double2> dz, dcoeff;     // owned nodes
-  // factors
+  // factors: all owned nodes resident (batch == 0 or batch >= owned), or streamed in node
+  // batches of `batch` (factors recomputed every pass: the memory plan for pencils whose
+  // factors exceed HBM, e.g. BASELINE config 5 at 1-2 GPUs); res0/rescnt = resident range
   bool factored = false;
+  int batch_req = 0, batch = 0, res0 = -1, rescnt = 0;
   DevBuf<double2> sinv, gfac, hfac, lu, dinv, scratch, fwork;
   DevBuf<int> ipiv, perm, status, fiwork;
   // workspaces
@@ -194,6 +197,8 @@ struct feast_gpu_ctx {
   cudaEvent_t ev[8] = {};
 
   int owned() const { return e1 - e0; }
+  bool streamed() const { return batch > 0 && batch < owned(); }
+  int wnodes() const { return streamed() ? batch : owned(); }  // node slots in the workspaces
 };
 
 namespace {
@@ -208,7 +213,7 @@ void ensure_eig(feast_gpu_ctx* c, int m) {
 void ensure_workspace(feast_gpu_ctx* c, int m) {
   if (m <= c->mcap) return;
   const size_t nv = (size_t)c->npad * m;
-  const int own = std::max(c->owned(), 1);
+  const int own = std::max(c->wnodes(), 1);
   c->Y.ensure(nv);
   c->Q.ensure(nv);
   c->X.ensure(nv);
@@ -434,8 +439,9 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
       }
       if ((3 * bw + 1) * 2 <= n) {
         // smallest supported block size whose block-tridiagonal pattern holds both operators
-        const int lo = round_block(std::max(1, (bw + 2) / 2));
-        const int hi = std::min(round_block(std::max(bw, 1)), kMaxBlock);
+        static const int min_block = getenv("FEAST_MIN_BLOCK") ? atoi(getenv("FEAST_MIN_BLOCK")) : 0;
+        const int lo = round_block(std::max(std::max(1, (bw + 2) / 2), min_block));
+        const int hi = std::min(std::max(round_block(std::max(bw, 1)), lo), kMaxBlock);
         for (int cand = lo; cand <= hi && !bsz; cand *= 2) {
           bool ok = true;
           for (const feast_operator_t* o : {a, b}) {
@@ -542,38 +548,56 @@ void build_contour(feast_gpu_ctx* c, double emin, double emax, int ne) {
   c->mcap = 0;  // per-node workspaces depend on the owned node count
 }
 
-void factor(feast_gpu_ctx* c) {
-  if (!c->have_pencil) fail(FEAST_EINPUT, "feast_gpu: pencil not set");
-  if (!c->have_contour) fail(FEAST_EINPUT, "feast_gpu: contour not prepared");
+size_t factor_bytes_per_node(const feast_gpu_ctx* c) {
+  if (c->blocktri) return sizeof(double2) * (size_t)(3 * c->L - 2) * c->b * c->b;
+  return sizeof(double2) * (size_t)c->n * c->n;
+}
+
+// node batch for this context: forced (feast_gpu_set_node_batch), else all owned nodes if
+// their factors fit 80% of the free HBM, else as many as do (at least one)
+void plan_batch(feast_gpu_ctx* c) {
   const int own = c->owned();
-  c->status.ensure(1);
-  CK(cudaMemsetAsync(c->status.p, 0, sizeof(int), c->stream));
-  if (own == 0) {
-    c->factored = true;
+  if (c->batch_req > 0) {
+    c->batch = std::min(c->batch_req, std::max(own, 1));
     return;
   }
+  size_t fr = 0, tot = 0;
+  CK(cudaMemGetInfo(&fr, &tot));
+  const size_t have = c->sinv.n * sizeof(double2) + c->lu.n * sizeof(double2);  // already ours
+  const size_t avail = (size_t)(0.8 * (double)(fr + have));
+  const size_t per = factor_bytes_per_node(c);
+  c->batch = (size_t)own * per <= avail ? own : (int)std::max<size_t>(1, avail / per);
+}
+
+// factors of owned nodes [s0, s0 + cnt) into factor slots 0..cnt-1
+void factor_range(feast_gpu_ctx* c, int s0, int cnt) {
+  c->status.ensure(1);
+  CK(cudaMemsetAsync(c->status.p, 0, sizeof(int), c->stream));
   if (c->blocktri) {
     const size_t bb = (size_t)c->b * c->b;
-    c->sinv.ensure(own * c->L * bb);
-    c->gfac.ensure(std::max<size_t>(own * (c->L - 1) * bb, 1));
-    c->hfac.ensure(std::max<size_t>(own * (c->L - 1) * bb, 1));
-    if (c->b > 64 && c->b < 128) c->scratch.ensure(own * (size_t)c->b * 2 * (c->b + 1));
+    const int slots = c->wnodes();
+    c->sinv.ensure(slots * c->L * bb);
+    c->gfac.ensure(std::max<size_t>(slots * (c->L - 1) * bb, 1));
+    c->hfac.ensure(std::max<size_t>(slots * (c->L - 1) * bb, 1));
+    if (c->b > 64 && c->b < 128) c->scratch.ensure(slots * (size_t)c->b * 2 * (c->b + 1));
     if (c->b >= 128) {
-      c->fwork.ensure(bt_factor_work_elems(c->b, own));
-      c->fiwork.ensure((size_t)own * 2 * c->b);
+      c->fwork.ensure(bt_factor_work_elems(c->b, cnt));
+      c->fiwork.ensure((size_t)cnt * 2 * c->b);
     }
-    BtFactorArgs a{c->L, c->b, own, c->abdiag.p, c->ablow.p, c->dz.p, c->sinv.p, c->gfac.p, c->hfac.p,
+    BtFactorArgs a{c->L, c->b, cnt, c->abdiag.p, c->ablow.p, c->dz.p + s0, c->sinv.p, c->gfac.p, c->hfac.p,
                    c->scratch.p, c->status.p, c->fwork.p, c->fiwork.p};
     CK(bt_factor(a, c->stream));
-    c->fwork.release();  // factor workspaces are transient
-    c->fiwork.release();
+    if (!c->streamed()) {  // factor workspaces are transient unless they are reused every pass
+      c->fwork.release();
+      c->fiwork.release();
+    }
   } else {
-    const int n = c->n, nb = kDenseNb, nblk = (n + nb - 1) / nb;
-    c->lu.ensure((size_t)own * n * n);
-    c->ipiv.ensure((size_t)own * n);
-    c->perm.ensure((size_t)own * n);
-    c->dinv.ensure((size_t)own * nblk * 2 * nb * nb);
-    DenseFactorArgs a{n, own, c->A.p, c->Bm.p, c->dz.p, c->lu.p, c->ipiv.p, c->perm.p, c->dinv.p, c->status.p};
+    const int n = c->n, nb = kDenseNb, nblk = (n + nb - 1) / nb, slots = c->wnodes();
+    c->lu.ensure((size_t)slots * n * n);
+    c->ipiv.ensure((size_t)slots * n);
+    c->perm.ensure((size_t)slots * n);
+    c->dinv.ensure((size_t)slots * nblk * 2 * nb * nb);
+    DenseFactorArgs a{n, cnt, c->A.p, c->Bm.p, c->dz.p + s0, c->lu.p, c->ipiv.p, c->perm.p, c->dinv.p, c->status.p};
     CK(dense_factor(a, c->stream));
   }
   int st = 0;
@@ -581,7 +605,34 @@ void factor(feast_gpu_ctx* c) {
   sync(c);
   if (st) fail(FEAST_ENUMERICAL, c->blocktri ? "BlockThomas: block pivot is numerically singular"
                                              : "DenseLU: matrix is numerically singular");
+  c->res0 = s0;
+  c->rescnt = cnt;
+}
+
+void factor(feast_gpu_ctx* c) {
+  if (!c->have_pencil) fail(FEAST_EINPUT, "feast_gpu: pencil not set");
+  if (!c->have_contour) fail(FEAST_EINPUT, "feast_gpu: contour not prepared");
+  const int own = c->owned();
+  c->status.ensure(1);
+  c->res0 = -1;
+  c->rescnt = 0;
+  if (own == 0) {
+    c->factored = true;
+    return;
+  }
+  const int prev = c->wnodes();
+  plan_batch(c);
+  if (c->wnodes() != prev) c->mcap = 0;  // per-node workspaces follow the node slots
+  factor_range(c, 0, c->wnodes());
   c->factored = true;
+}
+
+// make owned node s resident (streamed mode), returns its factor slot
+int resident_slot(feast_gpu_ctx* c, int s) {
+  if (s >= c->res0 && s < c->res0 + c->rescnt) return s - c->res0;
+  const int s0 = (s / c->wnodes()) * c->wnodes();
+  factor_range(c, s0, std::min(c->wnodes(), c->owned() - s0));
+  return s - s0;
 }
 
 // ------------------------------- passes --------------------------------------
@@ -591,16 +642,25 @@ void contour_pass(feast_gpu_ctx* c, int m) {
   const size_t nv = (size_t)c->npad * m;
   if (c->timing) CK(cudaEventRecord(c->ev[2], c->stream));
   if (own > 0) {
-    if (c->blocktri) {
-      BtSweepArgs a{c->L, c->b, own, m, c->npad, c->ablow.p, c->dz.p, c->dcoeff.p, c->sinv.p,
-                    c->gfac.p, c->hfac.p, c->Y.p, c->T.p, c->W.p, 0};
-      CK(bt_sweep(a, c->stream));
-    } else {
-      DenseSolveArgs a{c->n, own, m, c->npad, c->lu.p, c->perm.p, c->dinv.p, c->dcoeff.p, c->Y.p, c->T.p, c->W.p, 0};
-      CK(dense_solve(a, c->stream));
+    // node batches in ascending order (one batch = every owned node unless streamed); the
+    // reduction continues the same ascending-e sum across batches, so the result is
+    // bit-identical to the resident path
+    const int nbt = c->wnodes();
+    for (int s0 = 0; s0 < own; s0 += nbt) {
+      const int cnt = std::min(nbt, own - s0);
+      if (c->res0 != s0 || c->rescnt != cnt) factor_range(c, s0, cnt);
+      if (c->blocktri) {
+        BtSweepArgs a{c->L, c->b, cnt, m, c->npad, c->ablow.p, c->dz.p + s0, c->dcoeff.p + s0, c->sinv.p,
+                      c->gfac.p, c->hfac.p, c->Y.p, c->T.p, c->W.p, 0};
+        CK(bt_sweep(a, c->stream));
+      } else {
+        DenseSolveArgs a{c->n, cnt, m, c->npad, c->lu.p, c->perm.p, c->dinv.p, c->dcoeff.p + s0, c->Y.p, c->T.p,
+                         c->W.p, 0};
+        CK(dense_solve(a, c->stream));
+      }
+      if (c->timing && s0 + cnt >= own) CK(cudaEventRecord(c->ev[3], c->stream));
+      CK(reduce_terms(c->T.p, cnt, (int64_t)nv, c->npad, m, c->npad, c->Q.p, c->stream, s0 > 0));
     }
-    if (c->timing) CK(cudaEventRecord(c->ev[3], c->stream));
-    CK(reduce_terms(c->T.p, own, (int64_t)nv, c->npad, m, c->npad, c->Q.p, c->stream));
   } else {
     if (c->timing) CK(cudaEventRecord(c->ev[3], c->stream));
     CK(fill_zero(c->Q.p, nv, c->stream));
@@ -986,6 +1046,14 @@ int feast_gpu_prepare(feast_gpu_ctx* c, double emin, double emax, int n_e) {
   });
 }
 
+int feast_gpu_set_node_batch(feast_gpu_ctx* c, int nodes) {
+  return guarded(c, [&] {
+    if (nodes < 0) fail(FEAST_EINPUT, "set_node_batch: negative batch");
+    c->batch_req = nodes;
+    c->factored = false;  // re-plan at the next factorisation
+  });
+}
+
 int feast_gpu_contour(const feast_gpu_ctx* c, double* z, double* coeff) {
   if (!c || !c->have_contour) return FEAST_EINPUT;
   for (int e = 0; e < c->ne; ++e) {
@@ -1004,7 +1072,8 @@ int feast_gpu_solve_shift(feast_gpu_ctx* c, int e, double* rhs, int m, int mode)
     // ones go through as 2m real columns [Re | Im] and are recombined afterwards
     const bool split = c->blocktri && bt_panel_rows(c->b) > 0;
     ensure_workspace(c, split ? 2 * m : m);
-    const int s = e - c->e0;
+    const int sn = e - c->e0;                 // owned node index (shift, coefficient)
+    const int s = resident_slot(c, sn);       // its factor / workspace slot
     const size_t nv = (size_t)c->npad * m;
     double2* w = c->W.p + s * (split ? 2 : 1) * nv;
     CK(cudaMemsetAsync(w, 0, sizeof(double2) * nv, c->stream));
@@ -1015,7 +1084,7 @@ int feast_gpu_solve_shift(feast_gpu_ctx* c, int e, double* rhs, int m, int mode)
     if (c->blocktri) {
       const size_t bb = (size_t)c->b * c->b;
       if (split) CK(split_complex(w, c->AQ.p, c->npad, c->npad, m, c->stream));
-      BtSweepArgs a{c->L, c->b, 1, split ? 2 * m : m, c->npad, c->ablow.p, c->dz.p + s, c->dcoeff.p + s,
+      BtSweepArgs a{c->L, c->b, 1, split ? 2 * m : m, c->npad, c->ablow.p, c->dz.p + sn, c->dcoeff.p + sn,
                     c->sinv.p + s * c->L * bb, c->gfac.p + s * (c->L - 1) * bb,
                     c->hfac.p + s * (c->L - 1) * bb, split ? c->AQ.p : nullptr, nullptr, w, split ? 2 : 1};
       CK(bt_sweep(a, c->stream));
@@ -1023,7 +1092,7 @@ int feast_gpu_solve_shift(feast_gpu_ctx* c, int e, double* rhs, int m, int mode)
     } else {
       const int n = c->n, nb = kDenseNb, nblk = (n + nb - 1) / nb;
       DenseSolveArgs a{n, 1, m, c->npad, c->lu.p + (size_t)s * n * n, c->perm.p + (size_t)s * n,
-                       c->dinv.p + (size_t)s * nblk * 2 * nb * nb, c->dcoeff.p + s, nullptr, c->T.p, w, 1};
+                       c->dinv.p + (size_t)s * nblk * 2 * nb * nb, c->dcoeff.p + sn, nullptr, c->T.p, w, 1};
       CK(dense_solve(a, c->stream));
     }
     if (mode) CK(conj_inplace(w, nv, c->stream));

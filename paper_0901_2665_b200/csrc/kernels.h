@@ -59,9 +59,9 @@ struct BtSweepArgs {
 };
 cudaError_t bt_sweep(const BtSweepArgs& a, cudaStream_t st);
 
-// Q = -sum_{s} T_s (ascending s), n rows (ld) x m
+// Q = -sum_{s} T_s (ascending s), n rows (ld) x m; accumulate: Q -= sum (the next node batch)
 cudaError_t reduce_terms(const double* t, int nodes, int64_t slice, int n, int m, int ld,
-                         double* q, cudaStream_t st);
+                         double* q, cudaStream_t st, int accumulate = 0);
 
 // block-tridiagonal real operator apply: Y = Op * X (layer-batched DMMA GEMMs)
 cudaError_t bt_apply(int L, int b, const double* diag, const double* low, const double* x, int ldx,

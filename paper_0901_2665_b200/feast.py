@@ -78,6 +78,7 @@ def load_library(path: str = LIB_PATH):
     L.feast_gpu_set_pencil.argtypes = [C.c_void_p, _op, _op]
     L.feast_gpu_prepare.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_int]
     L.feast_gpu_contour.argtypes = [C.c_void_p, _dp, _dp]
+    L.feast_gpu_set_node_batch.argtypes = [C.c_void_p, C.c_int]
     L.feast_gpu_solve_shift.argtypes = [C.c_void_p, C.c_int, _dp, C.c_int, C.c_int]
     L.feast_gpu_contour_pass.argtypes = [C.c_void_p, _dp, C.c_int, _dp]
     L.feast_gpu_rayleigh_ritz.argtypes = [C.c_void_p, _dp, C.c_int, _dp, _dp, _ip, _ip]
@@ -99,6 +100,7 @@ EXPORTED_SYMBOLS = [
     "feast_gpu_contour", "feast_gpu_solve_shift", "feast_gpu_contour_pass",
     "feast_gpu_rayleigh_ritz", "feast_gpu_reduced_gevp", "feast_gpu_residuals", "feast_gpu_solve",
     "feast_gpu_bench_init", "feast_gpu_bench_passes", "feast_gpu_launch_count",
+    "feast_gpu_set_node_batch",
 ]
 
 
@@ -215,6 +217,10 @@ class GpuContext:
         self._ca, self._cb = a.to_c(), b.to_c()
         self._check(self.L.feast_gpu_set_pencil(self.h, C.byref(self._ca), C.byref(self._cb)))
         self.n = a.n
+
+    def set_node_batch(self, nodes: int):
+        """Factor memory plan: 0 = automatic (resident if they fit), k > 0 = stream k nodes."""
+        self._check(self.L.feast_gpu_set_node_batch(self.h, int(nodes)))
 
     def prepare(self, emin, emax, n_e=8):
         self._check(self.L.feast_gpu_prepare(self.h, emin, emax, n_e))

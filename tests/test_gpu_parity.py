@@ -251,3 +251,39 @@ def test_contour_pass_large_blocks(ctx, L, b):
         x = ctx.solve_shift(ne - 1, rhs, bool(mode))
         # 1e-11: kappa(zB - A) grows with the block size (b = 512 reaches ~2e-12)
         assert rel(x, O.shift_solve(a, bb, z[ne - 1], rhs, mode)) <= 1e-11
+
+
+# memory plan (feast_gpu_set_node_batch): streamed node batches refactor every pass and
+# continue the ascending-e quadrature sum, so results must be bit-identical to the resident plan
+@pytest.mark.parametrize("which", ["dense", "blocktri_small", "blocktri_panel"])
+def test_streamed_node_batches_bit_identical(F, which):
+    from paper_0901_2665_b200 import problems as P
+    if which == "dense":
+        prob, _ = load_fixture([p for p in FIX if "cfg1" in p][0])
+        a, b, lo, hi, m0 = prob.a, prob.b, prob.emin, prob.emax, prob.m0
+    elif which == "blocktri_small":
+        prob, _ = load_fixture([p for p in FIX if "bt_L16" in p][0])
+        a, b, lo, hi, m0 = prob.a, prob.b, prob.emin, prob.emax, prob.m0
+    else:
+        a, b = P.blocktri_operators(4, 128, seed=11)
+        lo, hi, m0 = -0.2, 0.2, 24
+    iv = F.SearchInterval(lo, hi)
+    cfg = F.FeastConfig(m0=m0, n_e=8, seed=42, max_loops=4)
+    out = []
+    for nb in (0, 3):
+        ctx = F.GpuContext(0)
+        ctx.set_node_batch(nb)
+        ctx.set_pencil(a, b)
+        out.append(ctx.solve(iv, cfg))
+        if nb:
+            ctx.prepare(lo, hi, 8)
+            z, _ = ctx.contour()
+            rhs = np.random.default_rng(3).standard_normal((a.n, 2)) + 0j
+            x = ctx.solve_shift(6, rhs.copy(), False)  # node 6 lives in the third batch
+            assert rel(x, O.shift_solve(a, b, z[6], rhs, 0)) <= 1e-11
+        ctx.close()
+    r0, r1 = out
+    assert r0.status == r1.status and r0.loops_used == r1.loops_used
+    assert np.array_equal(r0.eigenvalues, r1.eigenvalues)
+    assert np.array_equal(r0.eigenvectors, r1.eigenvectors)
+    assert np.array_equal(r0.trace_history, r1.trace_history)
