@@ -59,8 +59,21 @@ __global__ void __launch_bounds__(1024) tridiag_kernel(int m, const double* __re
   double* w = v + m;                  // m
   __shared__ double red[2][32];
   __shared__ double red33[33];
-  __shared__ double xn2s;
+  __shared__ double refl[3];  // next reflector's (t, beta, scal): one thread computes them
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  // Householder scalars of the column below row k+1 from alpha = A(k+1, k) and
+  // xn2 = ||A(k+2:, k)||^2 (sqrt + two divisions: one thread, not 1024)
+  auto reflector = [&](double alpha, double xn2) {
+    double t = 0.0, beta = alpha, scal = 0.0;
+    if (xn2 > 0.0) {
+      beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+      t = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    refl[0] = t;
+    refl[1] = beta;
+    refl[2] = scal;
+  };
   for (int idx = tid; idx < m * m; idx += nt) {  // all loads in flight at once
     const int i = idx % m, j = idx / m;
     if (i >= j) cp_async8z(ps + pidx(i, j, m), a + idx, true);
@@ -71,7 +84,7 @@ __global__ void __launch_bounds__(1024) tridiag_kernel(int m, const double* __re
     double part = 0.0;  // ||A(2:, 0)||^2 for the first reflector
     for (int i = 2 + tid; i < m; i += nt) part += ps[pidx(i, 0, m)] * ps[pidx(i, 0, m)];
     const double s = tri_block_sum(part, red33);
-    if (tid == 0) xn2s = s;
+    if (tid == 0 && m > 2) reflector(ps[pidx(1, 0, m)], s);
     __syncthreads();
   }
 
@@ -79,14 +92,7 @@ __global__ void __launch_bounds__(1024) tridiag_kernel(int m, const double* __re
   // next column's norm
   for (int k = 0; k + 2 < m; ++k) {
     const int r = m - k - 1;  // rows below the diagonal
-    const double xn2 = xn2s;
-    const double alpha = ps[pidx(k + 1, k, m)];
-    double t = 0.0, beta = alpha, scal = 0.0;
-    if (xn2 > 0.0) {
-      beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-      t = (beta - alpha) / beta;
-      scal = 1.0 / (alpha - beta);
-    }
+    const double t = refl[0], beta = refl[1], scal = refl[2];
     for (int i = tid; i < r; i += nt) {
       const double vi = i == 0 ? 1.0 : (t != 0.0 ? ps[pidx(k + 1 + i, k, m)] * scal : 0.0);
       v[i] = vi;
@@ -153,7 +159,8 @@ __global__ void __launch_bounds__(1024) tridiag_kernel(int m, const double* __re
             if (i >= 2) nrm += x * x;
           }
           nrm = warp_sum(nrm);
-          if (lane == 0) xn2s = nrm;
+          __syncwarp();
+          if (lane == 0 && k + 3 < m) reflector(col[1], nrm);  // A(k+2, k+1) is final here
         } else {
           for (int i = j + lane; i < r; i += 32) col[i] -= v[i] * wj + w[i] * vj;
         }
@@ -163,7 +170,7 @@ __global__ void __launch_bounds__(1024) tridiag_kernel(int m, const double* __re
       double part = 0.0;  // no reflection: the next column's norm directly
       for (int i = 2 + tid; i < r; i += nt) part += ps[pidx(k + 1 + i, k + 1, m)] * ps[pidx(k + 1 + i, k + 1, m)];
       const double s = tri_block_sum(part, red33);
-      if (tid == 0) xn2s = s;
+      if (tid == 0 && k + 3 < m) reflector(ps[pidx(k + 2, k + 1, m)], s);
       __syncthreads();
     }
   }
