@@ -370,8 +370,19 @@ static cudaError_t bt_factor_big(const BtFactorArgs& a, cudaStream_t st) {
       ++g_launches;
       zgetrs_batched(b, nodes, b, S, bb, perm, dinv, X, b, scr, st);
     }
-    if (!lu) gj_invert_batched(S, b, bb, nodes, gjw, a.status, st);  // S <- S^{-1} in place
-    const double2* Xi = lu ? X : S;  // S_l^{-1}
+    if (!lu) {
+      // S^{-1} by pivot-free block Gauss-Jordan, then one Newton-Schulz refinement step
+      // X' = X + X (I - S X): the near-real-axis nodes lose ~1 digit without pivoting, and
+      // the refinement squares that residual (two DMMA GEMMs per layer)
+      cudaMemcpyAsync(X, S, sizeof(double2) * nodes * bb, cudaMemcpyDeviceToDevice, st);  // keep S
+      gj_invert_batched(S, b, bb, nodes, gjw, a.status, st);  // S <- S^{-1} in place
+      bt_make_kernel<<<g, 256, 0, st>>>(b, nullptr, a.z, scr, 2);  // scr = I
+      ++g_launches;
+      zgemm_batched(b, b, b, mone, X, b, bb, S, b, bb, one, scr, b, bb, nodes, st);  // R = I - S X
+      cudaMemcpyAsync(X, S, sizeof(double2) * nodes * bb, cudaMemcpyDeviceToDevice, st);
+      zgemm_batched(b, b, b, one, S, b, bb, scr, b, bb, one, X, b, bb, nodes, st);  // X + X R
+    }
+    const double2* Xi = X;  // S_l^{-1}
     pack(Xi, a.sinv + l * bb, lnode);  // S_l^{-1} (node stride L*bb)
     if (l > 0) {  // H_l = S_l^{-1} C_{l-1}, via CT (C_{l-1}^T is spent)
       zgemm_batched(b, b, b, one, Xi, b, bb, Cp, b, bb, zero, CT, b, bb, nodes, st);

@@ -58,6 +58,10 @@ __global__ void __launch_bounds__(NC * B / 64 / P / TPW * 32) bt_sweep_kernel(Bt
   constexpr bool VPRE = B <= 128;
   constexpr bool VDB = B * NC <= 2048;
   constexpr int VS = VPRE ? NSTAGE : 1;               // vector slots
+  // the backward's y_l rows are prefetched NSTAGE-1 chunks ahead: with one chunk per step
+  // that reaches back into the forward sweep, and only y_{L-2} (read from the running
+  // buffer below) may still be unwritten then
+  static_assert(!VPRE || NSTAGE <= 3, "deeper rings would prefetch y_l before the forward sweep writes it");
   constexpr int MT = RB / 8;                          // local m-tiles
   constexpr int NWARPS = MT * (NC / 8) / TPW;
   constexpr int NT = NWARPS * 32;
@@ -377,7 +381,7 @@ cudaError_t bt_sweep(const BtSweepArgs& a, cudaStream_t st) {
   // b >= 128: panel-layout factors and the bulk-copy pipeline of sweep_tma.cu
   if (bt_panel_rows(a.b) > 0) return bt_sweep_tma(a, st);
   switch (a.b) {
-    case 16: return launch_sweep<16, 1, 16, 1, 5>(a, st);    // 4 warps; 5 stages measured 2% faster than 3
+    case 16: return launch_sweep<16, 1, 16, 1, 3>(a, st);    // 4 warps
     case 32: return launch_sweep<32, 1, 16, 1, 3>(a, st);    // 8 warps
     case 64: return launch_sweep<64, 1, 16, 2, 3>(a, st);    // 8 warps
   }
