@@ -719,7 +719,9 @@ Reduced reduced_gevp(feast_gpu_ctx* c, int m) {
   // spectral truncation fallback (eigh.hpp:204-224)
   CK(cudaMemcpyAsync(c->Cm.p, c->Bq.p, sizeof(double) * mm, cudaMemcpyDeviceToDevice, c->stream));
   CK(symmetrize(c->Cm.p, m, m, c->stream));
-  CK(sym_eig(c->eig, m, c->Cm.p, c->Ev.p, c->Vm.p, c->stream));
+  // mass-matrix modes at or below the 1e-14 truncation floor are discarded below, so their
+  // vectors are not computed (the near-null cluster of a filtered subspace is large)
+  CK(sym_eig(c->eig, m, c->Cm.p, c->Ev.p, c->Vm.p, c->stream, 1e-14));
   std::vector<double> d(m);
   CK(cudaMemcpyAsync(d.data(), c->Ev.p, sizeof(double) * m, cudaMemcpyDeviceToHost, c->stream));
   sync(c);

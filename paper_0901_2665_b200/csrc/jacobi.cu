@@ -44,7 +44,8 @@ static __device__ double block_sum(double v, double* red) {
 }
 
 int tri_max_dim();
-cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws, int* iws, cudaStream_t st);
+cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws, int* iws, cudaStream_t st,
+                    double vfloor);
 
 struct EigWork {
   int mmax = 0;
@@ -380,14 +381,14 @@ __global__ void eig_sort_kernel(int m, int mp, const double* w, const double* v,
   for (int r = threadIdx.x; r < m; r += blockDim.x) vout[r + (int64_t)rk * m] = v[r + (int64_t)i * mp];
 }
 
-cudaError_t sym_eig(EigWork* w, int m, double* a, double* evals, double* v, cudaStream_t st) {
+cudaError_t sym_eig(EigWork* w, int m, double* a, double* evals, double* v, cudaStream_t st, double vfloor) {
   if (m < 1 || m > w->mmax) return cudaErrorInvalidValue;
   // tridiagonal route up to m = 1024 (shared-memory reduction, preceded by an L2-resident
   // stage for m > 236; FEAST_EIG=jacobi
   // forces block Jacobi for comparison)
   static const char* force = getenv("FEAST_EIG");
   const bool jacobi_only = force && force[0] == 'j';
-  if (m <= tri_max_dim() && !jacobi_only) return tri_eig(m, a, evals, v, w->tws, w->tiws, st);
+  if (m <= tri_max_dim() && !jacobi_only) return tri_eig(m, a, evals, v, w->tws, w->tiws, st, vfloor);
   static const bool debug = getenv("FEAST_EIG_DEBUG") != nullptr;
   const int bs = eig_bs(m), mp = eig_mp(m), tb = 2 * bs, ldt = tb + 1;
   JacobiArgs p{m, mp, bs, a, w->w, w->v, w->j, w->part, 60, debug ? w->dbg : nullptr};

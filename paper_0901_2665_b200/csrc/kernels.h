@@ -110,8 +110,10 @@ struct EigWork;  // opaque, sized for mmax
 EigWork* eig_create(int mmax);
 void eig_destroy(EigWork* w);
 // Symmetric eigen-decomposition of W (m x m, ld m, overwritten): eigenvalues ascending
-// into `evals` (device), vectors into `v` (device, m x m), stable order.
-cudaError_t sym_eig(EigWork* w, int m, double* a, double* evals, double* v, cudaStream_t st);
+// into `evals` (device), vectors into `v` (device, m x m), stable order. vfloor > 0: the
+// tridiagonal route computes vectors only for evals > vfloor * max(evals) (others zero).
+cudaError_t sym_eig(EigWork* w, int m, double* a, double* evals, double* v, cudaStream_t st,
+                    double vfloor = 0.0);
 // Cholesky with relative pivot floor: L (lower, in place in `a`), status[0] = 1 on failure
 // (status must be zero on entry). dinv receives the inverses of the 32x32 diagonal tiles of
 // L (ceil(m/32) * 1024 doubles), consumed by the triangular solves.

@@ -611,6 +611,7 @@ struct TriArgs {
   double* z;    // m x m eigenvectors of T
   double* lu;   // 4*m per eigenpair (LU bands)
   int* piv;     // m per eigenpair
+  double vfloor;  // > 0: vectors only for lam > vfloor * lam_max (others zero)
 };
 
 __device__ void tri_bounds(int m, const double* d, const double* e, double& lo, double& hi, double& tnorm,
@@ -728,7 +729,24 @@ __global__ void tri_eigvecs_kernel(TriArgs p) {
   // non-orthogonality of O(eps ||T|| / gap), so 1e-5 ||T|| already bounds it by ~1e-11 while
   // keeping FEAST's dense interior Ritz spectra from chaining into one long cluster
   const double ortol = 1e-5 * tnorm, eps = DBL_EPSILON;
-  if (cl > 0 && p.lam[cl] - p.lam[cl - 1] <= ortol) return;  // not the first of its cluster
+  // vectors of the eigenvalues at or below the floor are not wanted (the truncation path of
+  // reduced_gevp discards them): the near-null cluster of a graded mass matrix never forms
+  int j0 = 0;
+  if (p.vfloor > 0.0) {
+    const double thr = p.vfloor * p.lam[m - 1];
+    int lo_ = 0, hi_ = m;  // first index with lam > thr (ascending)
+    while (lo_ < hi_) {
+      const int mid = (lo_ + hi_) >> 1;
+      if (p.lam[mid] > thr) hi_ = mid;
+      else lo_ = mid + 1;
+    }
+    j0 = lo_;
+  }
+  if (cl < j0) {
+    for (int i = lane; i < m; i += 32) p.z[i + (int64_t)cl * m] = 0.0;
+    return;
+  }
+  if (cl > j0 && p.lam[cl] - p.lam[cl - 1] <= ortol) return;  // not the first of its cluster
   int cend = cl + 1;
   while (cend < m && p.lam[cend] - p.lam[cend - 1] <= ortol) ++cend;
   // per-warp shared scratch: LU bands, pivots, the iterate (the O(m) recurrences run on
@@ -849,7 +867,8 @@ static int tri_smem_dim() { return 236; }
 int tri_max_dim() { return 1024; }
 
 // a (m x m, overwritten is allowed), eigenvalues ascending -> evals, vectors -> v (m x m)
-cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws, int* iws, cudaStream_t st) {
+cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws, int* iws, cudaStream_t st,
+                    double vfloor) {
   if (m < 1 || m > tri_max_dim()) return cudaErrorInvalidValue;
   double* d = ws;
   double* e = d + m;
@@ -920,7 +939,7 @@ cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws
     ++g_launches;
     if (err != cudaSuccess) return err;
   }
-  TriArgs p{m, d, e, evals, z, nullptr, iws};
+  TriArgs p{m, d, e, evals, z, nullptr, iws, vfloor};
   const int wpb = 4;
   tri_eigvals_kernel<<<(m + wpb - 1) / wpb, 32 * wpb, sizeof(double) * 2 * m, st>>>(p);
   ++g_launches;
