@@ -399,12 +399,13 @@ __global__ void __launch_bounds__(TC_NT) tridiag_coop_kernel(TriCoopArgs p) {
 // 1c. Householder tridiagonalisation on a thread-block cluster of TCL_P CTAs: global column g
 //     lives (packed, rows g..m-1) in the shared memory of CTA g mod TCL_P, so all matrix
 //     traffic stays on-chip; only vectors cross CTAs, through distributed shared memory.
-//     Per column k (owner o = k mod P), three cluster barriers:
-//       (a) v and (t, beta) copied from the owner; each CTA: dots of its own columns
-//           (A(g:, g) . v) and its axpy partial q[i] = sum_{own g < i} A(i, g) v_g
-//       (b) CTA q: p_i = t (dot_i + sum_q' q_q'[i]) on its row slice, and p.v
-//       (c) every CTA: w = p - (t/2)(p.v) v and the rank-2 update of its own columns; the
-//           owner of column k+1 builds the next reflector into the other v buffer
+//     Per column k, two cluster barriers:
+//       (a) each CTA: dots of its own columns (A(g:, g) . v) and its axpy partial
+//           q[i] = sum_{own g < i} A(i, g) v_g, both in its own shared memory
+//       (c) every CTA gathers all partials through DSMEM reads into the FULL p (same order in
+//           every CTA, so p, p.v and w agree bit for bit), w = p - (t/2)(p.v) v, the rank-2
+//           update of its own columns; the owner of column k+1 builds the next reflector
+//           and pushes it (and t) into every CTA's other v buffer
 //     All sums run in a fixed order (deterministic).
 // ---------------------------------------------------------------------------
 constexpr int TCL_P = 16, TCL_NT = 512, TCL_NW = TCL_NT / 32;
@@ -421,15 +422,12 @@ __global__ void __launch_bounds__(TCL_NT) tridiag_cluster_kernel(int m, const do
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   extern __shared__ double ksm[];
   const int loc = tcl_local(m, 0);  // same layout size in every CTA (CTA 0 holds the most)
-  const int slmax = (m + TCL_P - 1) / TCL_P;
   double* cols = ksm;               // own columns, packed
   double* vb = cols + loc;          // 2 x m: reflector (trailing index), double-buffered by parity
-  double* ww = vb + 2 * m;          // m: w (trailing index)
-  double* pp = ww + m;              // m: p (trailing index), pushed by the slice owners
-  double* qall = pp + m;            // P x slmax: axpy partials of my row slice, pushed by every CTA
-  double* dall = qall + TCL_P * slmax;  // slmax: column dots of my row slice, pushed by the owners
+  double* ww = vb + 2 * m;          // m: p, then w (trailing index), full in every CTA
+  double* qp = ww + m;              // m: my axpy partial (trailing row index), read by every CTA
+  double* dc = qp + m;              // m: dots of my own columns (trailing column index)
   __shared__ double scal_s[2];      // t per parity, pushed by the reflector's owner
-  __shared__ double pvall[TCL_P];   // p.v partials, pushed by every slice owner
   __shared__ double xn2_s;          // owner of the next column: ||A(k+3:, k+1)||^2
   __shared__ double red33[33];
   const int ncol = tcl_ncols(m, q);
@@ -479,7 +477,6 @@ __global__ void __launch_bounds__(TCL_NT) tridiag_cluster_kernel(int m, const do
     const int r = m - k - 1, par = k & 1, base = k + 1;  // trailing index = global - base
     const double* v = vb + par * m;
     const double tt = scal_s[par];
-    const int sl = (r + TCL_P - 1) / TCL_P;              // row slice of CTA qq: [qq sl, (qq+1) sl)
     const int t0 = base > q ? (base - q + TCL_P - 1) / TCL_P : 0;  // first own column >= base
     // ---- (a) dots of own columns and axpy partials, pushed to the slice owners ----
     if (tt != 0.0) {
@@ -489,10 +486,7 @@ __global__ void __launch_bounds__(TCL_NT) tridiag_cluster_kernel(int m, const do
         double s = 0.0;
         for (int i = g + lane; i < m; i += 32) s += cg_[i] * v[i - base];
         s = warp_sum(s);
-        if (lane == 0) {
-          const int ti = g - base, ow = ti / sl;
-          cl.map_shared_rank(dall, ow)[ti - ow * sl] = s;
-        }
+        if (lane == 0) dc[g - base] = s;
       }
       for (int i = base + tid; i < m; i += TCL_NT) {
         const int tend = min(ncol, (i - q + TCL_P - 1) / TCL_P);  // own g in [base, i)
@@ -506,36 +500,28 @@ __global__ void __launch_bounds__(TCL_NT) tridiag_cluster_kernel(int m, const do
           g = g1 + TCL_P;
         }
         if (t < tend) s0 += cols[off + (i - g)] * v[g - base];
-        const int ti = i - base, ow = ti / sl;
-        cl.map_shared_rank(qall, ow)[q * slmax + (ti - ow * sl)] = s0 + s1;
+        qp[i - base] = s0 + s1;
       }
     }
     cl.sync();  // (a)
-    // ---- (b) p on my row slice, pushed to every CTA, with my p.v partial ----
+    // ---- (b) every CTA gathers all partials (DSMEM reads) into the full p, then w ----
+    //      (each CTA sums in the same order, so p, p.v and w are identical in all of them)
     if (tt != 0.0) {
-      const int i0 = q * sl, i1 = min(r, i0 + sl);
       double pv = 0.0;
-      for (int ti = i0 + tid; ti < i1; ti += TCL_NT) {
-        const int li = ti - i0;
-        double pf = dall[li];
+      for (int ti = tid; ti < r; ti += TCL_NT) {
+        double x[TCL_P];
 #pragma unroll
-        for (int qq = 0; qq < TCL_P; ++qq) pf += qall[qq * slmax + li];
+        for (int qq = 0; qq < TCL_P; ++qq) x[qq] = *cl.map_shared_rank(qp + ti, qq);  // all in flight
+        double pf = *cl.map_shared_rank(dc + ti, (base + ti) % TCL_P);
+#pragma unroll
+        for (int qq = 0; qq < TCL_P; ++qq) pf += x[qq];
         pf *= tt;
+        ww[ti] = pf;
         pv += pf * v[ti];
-#pragma unroll
-        for (int qq = 0; qq < TCL_P; ++qq) cl.map_shared_rank(pp, qq)[ti] = pf;
       }
       pv = tri_block_sum(pv, red33);
-      if (tid < TCL_P) cl.map_shared_rank(pvall, tid)[q] = pv;
-    }
-    cl.sync();  // (b)
-    // ---- (c) w, rank-2 update of own columns, next reflector ----
-    if (tt != 0.0) {
-      double pv = 0.0;
-#pragma unroll
-      for (int qq = 0; qq < TCL_P; ++qq) pv += pvall[qq];
       const double cf = -0.5 * tt * pv;
-      for (int ti = tid; ti < r; ti += TCL_NT) ww[ti] = pp[ti] + cf * v[ti];
+      for (int ti = tid; ti < r; ti += TCL_NT) ww[ti] += cf * v[ti];
       __syncthreads();
       for (int t = t0 + warp; t < ncol; t += TCL_NW) {
         const int g = q + t * TCL_P;
@@ -572,10 +558,7 @@ __global__ void __launch_bounds__(TCL_NT) tridiag_cluster_kernel(int m, const do
 }
 
 // largest m whose cluster layout fits the 227 KB opt-in shared memory
-static size_t tcl_smem(int m) {
-  const size_t slmax = (m + TCL_P - 1) / TCL_P;
-  return sizeof(double) * ((size_t)tcl_local(m, 0) + 4 * (size_t)m + (TCL_P + 1) * slmax);
-}
+static size_t tcl_smem(int m) { return sizeof(double) * ((size_t)tcl_local(m, 0) + 5 * (size_t)m); }
 
 // ---------------------------------------------------------------------------
 // 2. eigenvalues: Sturm-count multisection
