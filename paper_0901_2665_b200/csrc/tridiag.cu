@@ -702,6 +702,11 @@ __device__ void gtts2(int m, const double* D, const double* DL, const double* DU
   for (int i = m - 3; i >= 0; --i) b[i] = (b[i] - DU[i] * b[i + 1] - DU2[i] * b[i + 2]) * D[i];
 }
 
+// inverse-iteration steps per vector: the Sturm eigenvalue is accurate to O(eps ||T||), so
+// the first solve already amplifies the wanted direction by ~1/eps; the second one (after the
+// in-cluster Gram-Schmidt) is the dstein "extra" step
+constexpr int kInvIters = 2;
+
 __global__ void tri_eigvecs_kernel(TriArgs p) {
   const int m = p.m, lane = threadIdx.x & 31;
   const int cl = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -757,7 +762,7 @@ __global__ void tri_eigvecs_kernel(TriArgs p) {
       zj[i] = 0.5 + (double)(h & 0xffff) / 65536.0;
     }
     __syncwarp();
-    for (int it = 0; it < 3; ++it) {
+    for (int it = 0; it < kInvIters; ++it) {
       if (lane == 0) gtts2(m, D, DL, DU, DU2, ipiv, zj);
       __syncwarp();
       for (int k = cl; k < j; ++k) {  // modified Gram-Schmidt within the cluster
