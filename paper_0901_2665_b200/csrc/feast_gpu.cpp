@@ -137,7 +137,7 @@ struct DevBuf {
   size_t n = 0;
   void ensure(size_t count) {
     if (count <= n) return;
-    if (p) cudaFree(p);
+    if (p && n) cudaFree(p);
     p = nullptr;
     n = 0;
     if (count) {
@@ -146,7 +146,7 @@ struct DevBuf {
     }
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p && n) cudaFree(p);  // n == 0: a non-owning view into another buffer
     p = nullptr;
     n = 0;
   }
@@ -210,6 +210,17 @@ void ensure_eig(feast_gpu_ctx* c, int m) {
   c->eig_cap = std::max(m, 16);
 }
 
+// reduced blocks: Aq and Bq adjacent (the m x 2m output of Q^T [AQ | BQ], ld m)
+void ensure_reduced(feast_gpu_ctx* c, int m) {
+  const size_t mm = (size_t)m * m;
+  c->Aq.ensure(2 * mm);
+  c->Bq.p = c->Aq.p + mm;
+  c->Bq.n = 0;
+  for (DevBuf<double>* d : {&c->Cm, &c->Lm, &c->Phi, &c->Vm, &c->S, &c->Tm}) d->ensure(mm);
+  c->Ev.ensure(m);
+  c->keep.ensure(m);
+}
+
 void ensure_workspace(feast_gpu_ctx* c, int m) {
   if (m <= c->mcap) return;
   const size_t nv = (size_t)c->npad * m;
@@ -217,15 +228,13 @@ void ensure_workspace(feast_gpu_ctx* c, int m) {
   c->Y.ensure(nv);
   c->Q.ensure(nv);
   c->X.ensure(nv);
-  c->AQ.ensure(nv);
-  c->BQ.ensure(nv);
+  c->AQ.ensure(2 * nv);  // [AQ | BQ] adjacent: one Q^T [AQ | BQ] GEMM forms both projections
+  c->BQ.p = c->AQ.p + nv;
+  c->BQ.n = 0;
   c->T.ensure(2 * nv * own);  // doubles; complex-mode dense shim reuses it as double2
   c->W.ensure(nv * own);
   const size_t mm = (size_t)m * m;
-  for (DevBuf<double>* d : {&c->Aq, &c->Bq, &c->Cm, &c->Lm, &c->Phi, &c->Vm, &c->S, &c->Tm})
-    d->ensure(mm);
-  c->Ev.ensure(m);
-  c->keep.ensure(m);
+  ensure_reduced(c, m);
   c->gw.ensure(std::max<size_t>(mm * 64, nv));
   ensure_eig(c, m);
   c->mcap = m;
@@ -752,8 +761,8 @@ Reduced rayleigh_ritz(feast_gpu_ctx* c, int m) {
   const int n = c->npad;
   apply_op(c, 0, c->Q.p, c->AQ.p, m);
   apply_op(c, 1, c->Q.p, c->BQ.p, m);
-  CK(dgemm('T', 'N', m, m, n, 1.0, c->Q.p, n, c->AQ.p, n, 0.0, c->Aq.p, m, c->gw.p, c->gw.n, c->stream));
-  CK(dgemm('T', 'N', m, m, n, 1.0, c->Q.p, n, c->BQ.p, n, 0.0, c->Bq.p, m, c->gw.p, c->gw.n, c->stream));
+  // [Aq | Bq] = Q^T [AQ | BQ] in one GEMM (adjacent buffers; same sums as two separate ones)
+  CK(dgemm('T', 'N', m, 2 * m, n, 1.0, c->Q.p, n, c->AQ.p, n, 0.0, c->Aq.p, m, c->gw.p, c->gw.n, c->stream));
   CK(symmetrize(c->Aq.p, m, m, c->stream));
   CK(symmetrize(c->Bq.p, m, m, c->stream));
   Reduced r = reduced_gevp(c, m);
@@ -1137,9 +1146,7 @@ int feast_gpu_reduced_gevp(feast_gpu_ctx* c, int m, const double* a_q, const dou
     if (m < 1 || m > 1024) fail(FEAST_EINPUT, "reduced_gevp: blocks must be square with equal size");
     if (c->mcap < m) {
       const size_t mm = (size_t)m * m;
-      for (DevBuf<double>* d : {&c->Aq, &c->Bq, &c->Cm, &c->Lm, &c->Phi, &c->Vm, &c->S, &c->Tm}) d->ensure(mm);
-      c->Ev.ensure(m);
-      c->keep.ensure(m);
+      ensure_reduced(c, m);
       c->gw.ensure(mm * 64);
       ensure_eig(c, m);
     }
