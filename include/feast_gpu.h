@@ -149,6 +149,12 @@ int feast_gpu_prepare(feast_gpu_ctx* ctx, double emin, double emax, int n_e);
  * resident plan). Takes effect at the next feast_gpu_prepare / feast_gpu_solve. */
 int feast_gpu_set_node_batch(feast_gpu_ctx* ctx, int nodes);
 
+/* Storage chosen for the pencil at feast_gpu_set_pencil: block size b and layer count L of the
+ * block-tridiagonal re-blocking (b = 0, L = 0 for the dense path), and twist = the meeting
+ * layer of the two-ended block-Thomas recursion used by the factors (-1: plain chain; valid
+ * after feast_gpu_prepare). Introspection for tests and benchmarks; any pointer may be NULL. */
+int feast_gpu_storage(const feast_gpu_ctx* ctx, int* b, int* layers, int* twist);
+
 /* Contour points actually used (host copies): z (2*n_e interleaved) and the
  * quadrature coefficients c_e = 0.5 * w_e * r * e^{i theta_e} (2*n_e). */
 int feast_gpu_contour(const feast_gpu_ctx* ctx, double* z, double* coeff);

@@ -19,143 +19,355 @@
 #include <cstdlib>
 #include <utility>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace feastgpu {
 
 int64_t g_launches = 0;
 
 // ---------------------------------------------------------------------------
-// Factor: one CTA per node walks the L-step chain. v0: any b; [S | I] lives in shared
-// memory for b <= 64 and in global scratch otherwise.
+// Small blocks (b = 16, 32, 64): one CTA per node and chain direction.
+//
+// Twisted recursion (kmid >= 0): a cluster of two CTAs per node eliminates from both ends.
+//   top    (rank 0), l = 0 .. kmid-1 : S_l = M_l - C_{l-1} G_{l-1}; G_l = S_l^{-1} C_l^T -> g[l],
+//                                      H_l = S_l^{-1} C_{l-1} -> h[l-1]
+//   bottom (rank 1), l = L-1 .. kmid+1: R_l = M_l - C_l^T G'_{l+1}; G'_l = R_l^{-1} C_{l-1} -> g[l-1],
+//                                      H'_l = R_l^{-1} C_l^T -> h[l]
+//   middle (rank 0, after a cluster barrier), l = kmid:
+//     T = M_k - C_{k-1} G_{k-1} - C_k^T G'_{k+1};  T^{-1} -> sinv[k], T^{-1} C_{k-1} -> h[k-1],
+//     T^{-1} C_k^T -> h[k]
+// so the dependency chain is ~L/2 layers long instead of L (and the sweep's 2L-1 steps become
+// ~L). Both directions are the same code: a layer's "in" coupling is the neighbour already
+// eliminated, its "out" coupling the one still ahead. kmid < 0: the plain top-down chain.
+//
+// Per layer: S = M - Cin Gprev (DMMA tiles, operands converted from the (A, B) pairs on the
+// fly), S^{-1} by Gauss-Jordan with partial pivoting (largest |.|^2, first index on ties)
+// in place — in one warp's registers for b <= 32 (lane j owns column j), in shared memory for
+// b = 64 — then H = S^{-1} Cin and G = S^{-1} Cout (DMMA). For b <= 32 the next layer's raw
+// blocks are prefetched with cp.async while this one is processed.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) bt_factor_kernel(BtFactorArgs a) {
-  const int s = blockIdx.x;
-  const int L = a.L, b = a.b, tid = threadIdx.x, nt = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const double2 z = a.z[s];
-  const int ld = b + 1;
-  extern __shared__ __align__(16) double2 fsm[];
-  double2* f = fsm;                                   // b
-  double2* aug = (b <= 64) ? fsm + b : a.scratch + (size_t)s * b * 2 * ld;
-  __shared__ int piv_s;
-  __shared__ int bad_s;
-  const size_t bb = (size_t)b * b;
-  double2* sinv = a.sinv + (size_t)s * L * bb;
-  double2* gm = a.g + (size_t)s * (L > 1 ? L - 1 : 0) * bb;
-  if (tid == 0) bad_s = 0;
+template <int B>
+struct FacShape {
+  static constexpr int NT = B == 16 ? 128 : 256;
+  static constexpr int LDS = B + 4;        // Sv / Gp column stride (double2)
+  static constexpr bool RAW_SMEM = B <= 32;
+  static constexpr size_t smem_bytes() {
+    return sizeof(double2) * (2 * (size_t)B * LDS + B + (RAW_SMEM ? 5 * (size_t)B * B : 0));
+  }
+};
 
-  for (int l = 0; l < L; ++l) {
-    // (a) S_l = M_l - C_{l-1} G_{l-1};  right half = I
-    const double2* ab = a.abdiag + (size_t)l * bb;
-    for (int idx = tid; idx < b * b; idx += nt) {
-      const int i = idx % b, j = idx / b;
-      const double2 e = ab[idx];
-      double2 v = make_double2(z.x * e.y - e.x, z.y * e.y);
-      if (l > 0) {
-        const double2* cl = a.ablow + (size_t)(l - 1) * bb;
-        const double2* gp = gm + (size_t)(l - 1) * bb;
-        double2 acc = make_double2(0.0, 0.0);
-        for (int k = 0; k < b; ++k) {
-          const double2 ce = cl[i + (size_t)k * b];
-          const double2 c = make_double2(z.x * ce.y - ce.x, z.y * ce.y);
-          acc = cadd(acc, cmul(c, gp[k + (size_t)j * b]));
-        }
-        v = csub(v, acc);
+FEAST_DEV double2 czb(double2 e, double2 z) { return make_double2(z.x * e.y - e.x, z.y * e.y); }
+
+// acc tiles of X(B x B) * Y(B x B) over the CTA's warps; out(i, j, v) per element
+template <int B, class FA, class FB, class FO>
+FEAST_DEV void cgemm_tiles(int warp, int nwarps, int lane, FA fa, FB fb, FO out) {
+  constexpr int MT = B / 8;
+  const int g = lane >> 2, t4 = lane & 3;
+  for (int tile = warp; tile < MT * MT; tile += nwarps) {
+    const int r0 = 8 * (tile % MT), c0 = 8 * (tile / MT);
+    CAcc acc, acc2;
+    acc.zero();
+    acc2.zero();
+#pragma unroll
+    for (int k = 0; k < B; k += 8) {
+      cmma(acc, fa(r0 + g, k + t4), fb(k + t4, c0 + g));
+      cmma(acc2, fa(r0 + g, k + 4 + t4), fb(k + 4 + t4, c0 + g));
+    }
+    out(r0 + g, c0 + 2 * t4, make_double2(acc.r0 + acc2.r0, acc.i0 + acc2.i0));
+    out(r0 + g, c0 + 2 * t4 + 1, make_double2(acc.r1 + acc2.r1, acc.i1 + acc2.i1));
+  }
+}
+
+// In-place Gauss-Jordan inverse of Sv (B x B, column stride lds) by one warp, rows spread over
+// the lanes (32 / B lanes per row, each owning B / (32 / B)... columns of it) and IMPLICIT
+// partial pivoting: the pivot of column k is the unused row with the largest |.|^2 (first
+// index on ties, a warp arg-max), it is never moved; at the end the row that pivoted column k
+// holds row k of (P S)^{-1}, and S^{-1}[i, p_t] = that row's element t. No row swaps, no
+// dynamically indexed registers, and the k loop stays rolled (small code).
+template <int B>
+FEAST_DEV void gj_rows(double2* Sv, int lds, int* pivs, int lane, int* status) {
+  constexpr int CS = 32 / B;     // lanes per row
+  constexpr int NCOL = B / CS;   // columns per lane
+  const int r = lane % B, j0 = (lane / B) * NCOL;
+  bool used = false, bad = false;
+  int mystep = 0;
+#pragma unroll 1
+  for (int k = 0; k < B; ++k) {
+    const double2 ak = Sv[r + k * lds];
+    double best = used ? -1.0 : ak.x * ak.x + ak.y * ak.y;
+    int p = r;
+#pragma unroll
+    for (int o = B / 2; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int op = __shfl_xor_sync(0xffffffffu, p, o);
+      if (ob > best || (ob == best && op < p)) {
+        best = ob;
+        p = op;
       }
-      aug[i + (size_t)j * ld] = v;
-      aug[i + (size_t)(b + j) * ld] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+    }
+    bad |= !(best > 0.0);
+    const bool isp = r == p;
+    used |= isp;
+    mystep = isp ? k : mystep;
+    if (lane == 0) pivs[k] = p;
+    // 1 / a_pk = conj(a_pk) / |a_pk|^2 (|a_pk|^2 = best, the pivot is O(1) here)
+    const double2 apk = Sv[p + k * lds];
+    const double rn = 1.0 / best;
+    const double2 inv = make_double2(apk.x * rn, -apk.y * rn);
+    double2 piv[NCOL];  // the pivot row (its owner lanes overwrite it below)
+#pragma unroll
+    for (int jj = 0; jj < NCOL; ++jj) piv[jj] = Sv[p + (j0 + jj) * lds];
+    __syncwarp();
+    const double2 mk = make_double2(-ak.x, -ak.y);
+#pragma unroll
+    for (int jj = 0; jj < NCOL; ++jj) {
+      const bool jk = j0 + jj == k;
+      const double2 pv = jk ? inv : cmul(piv[jj], inv);   // scaled pivot row
+      const double2 a0 = jk ? make_double2(0.0, 0.0) : Sv[r + (j0 + jj) * lds];
+      const double2 upd = make_double2(a0.x + mk.x * pv.x - mk.y * pv.y, a0.y + mk.x * pv.y + mk.y * pv.x);
+      Sv[r + (j0 + jj) * lds] = isp ? pv : upd;
+    }
+    __syncwarp();
+  }
+  double2 mine[NCOL];
+#pragma unroll
+  for (int jj = 0; jj < NCOL; ++jj) mine[jj] = Sv[r + (j0 + jj) * lds];
+  __syncwarp();
+#pragma unroll
+  for (int jj = 0; jj < NCOL; ++jj) Sv[mystep + pivs[j0 + jj] * lds] = mine[jj];
+  if (bad && lane == 0) atomicExch(status, 1);
+}
+
+// the same elimination by the whole CTA in shared memory (b = 64)
+template <int B, int NT>
+FEAST_DEV void gj_smem(double2* Sv, int lds, int* pivs, int* cpos, int* status) {
+  constexpr int PER = B * B / NT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double2 v[PER];
+  for (int k = 0; k < B; ++k) {
+    if (warp == 0) {
+      double best = -1.0;
+      int p = B;
+      for (int i = k + lane; i < B; i += 32) {
+        const double2 e = Sv[i + k * lds];
+        const double m = e.x * e.x + e.y * e.y;
+        if (m > best) {
+          best = m;
+          p = i;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int op = __shfl_xor_sync(0xffffffffu, p, o);
+        if (ob > best || (ob == best && op < p)) {
+          best = ob;
+          p = op;
+        }
+      }
+      if (lane == 0) {
+        pivs[k] = p;
+        if (!(best > 0.0)) atomicExch(status, 1);
+      }
     }
     __syncthreads();
-
-    // (b) Gauss-Jordan with partial pivoting (largest |.|, first index on ties,
-    //     the DenseLU / BandedLU rule of lu.hpp:29-38)
-    for (int k = 0; k < b; ++k) {
-      if (warp == 0) {
-        double best = -1.0;
-        int bi = b;
-        for (int i = k + lane; i < b; i += 32) {
-          const double v = cabs_(aug[i + (size_t)k * ld]);
-          if (v > best) { best = v; bi = i; }
-        }
+    const int p = pivs[k];
+    if (p != k)
+      for (int jj = tid; jj < B; jj += NT) {
+        const double2 t = Sv[k + jj * lds];
+        Sv[k + jj * lds] = Sv[p + jj * lds];
+        Sv[p + jj * lds] = t;
+      }
+    __syncthreads();
+    const double2 inv = cdiv(make_double2(1.0, 0.0), Sv[k + k * lds]);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-        }
-        if (lane == 0) {
-          piv_s = bi;
-          if (!(best > 0.0)) bad_s = 1;
-        }
-      }
-      __syncthreads();
-      if (bad_s) {
-        if (tid == 0) atomicExch(a.status, 1);
-        return;
-      }
-      const int p = piv_s;
-      if (p != k)
-        for (int j = k + tid; j < 2 * b; j += nt) {
-          const double2 t0 = aug[k + (size_t)j * ld];
-          aug[k + (size_t)j * ld] = aug[p + (size_t)j * ld];
-          aug[p + (size_t)j * ld] = t0;
-        }
-      __syncthreads();
-      const double2 pv = aug[k + (size_t)k * ld];
-      __syncthreads();
-      for (int j = k + 1 + tid; j < 2 * b; j += nt)
-        aug[k + (size_t)j * ld] = cdiv(aug[k + (size_t)j * ld], pv);
-      for (int i = tid; i < b; i += nt) f[i] = aug[i + (size_t)k * ld];
-      __syncthreads();
-      const int ncol = 2 * b - k - 1;
-      for (int idx = tid; idx < b * ncol; idx += nt) {
-        const int i = idx % b, j = k + 1 + idx / b;
-        if (i == k) continue;
-        aug[i + (size_t)j * ld] = csub(aug[i + (size_t)j * ld], cmul(f[i], aug[k + (size_t)j * ld]));
-      }
-      __syncthreads();
+    for (int e = 0; e < PER; ++e) {
+      const int idx = tid + e * NT, i = idx % B, jj = idx / B;
+      const double2 rk = cmul(jj == k ? make_double2(1.0, 0.0) : Sv[k + jj * lds], inv);
+      v[e] = i == k ? rk
+                    : csub(jj == k ? make_double2(0.0, 0.0) : Sv[i + jj * lds], cmul(Sv[i + k * lds], rk));
     }
-
-    // Sinv_l out
-    double2* si = sinv + (size_t)l * bb;
-    for (int idx = tid; idx < b * b; idx += nt) {
-      const int i = idx % b, j = idx / b;
-      si[idx] = aug[i + (size_t)(b + j) * ld];
-    }
-    // (c) G_l = S_l^{-1} C_l^T
-    if (l + 1 < L) {
-      const double2* cl = a.ablow + (size_t)l * bb;
-      double2* gp = gm + (size_t)l * bb;
-      for (int idx = tid; idx < b * b; idx += nt) {
-        const int i = idx % b, j = idx / b;
-        double2 acc = make_double2(0.0, 0.0);
-        for (int k = 0; k < b; ++k) {
-          const double2 ce = cl[j + (size_t)k * b];   // C_l(j, k)
-          const double2 c = make_double2(z.x * ce.y - ce.x, z.y * ce.y);
-          acc = cadd(acc, cmul(aug[i + (size_t)(b + k) * ld], c));
-        }
-        gp[idx] = acc;
-      }
-    }
-    // (d) H_l = S_l^{-1} C_{l-1}: folds the coupling into one GEMM per forward sweep step
-    if (l > 0) {
-      const double2* cl = a.ablow + (size_t)(l - 1) * bb;
-      double2* hp = a.h + ((size_t)s * (L - 1) + (l - 1)) * bb;
-      for (int idx = tid; idx < b * b; idx += nt) {
-        const int i = idx % b, j = idx / b;
-        double2 acc = make_double2(0.0, 0.0);
-        for (int k = 0; k < b; ++k) {
-          const double2 ce = cl[k + (size_t)j * b];   // C_{l-1}(k, j)
-          const double2 c = make_double2(z.x * ce.y - ce.x, z.y * ce.y);
-          acc = cadd(acc, cmul(aug[i + (size_t)(b + k) * ld], c));
-        }
-        hp[idx] = acc;
-      }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < PER; ++e) {
+      const int idx = tid + e * NT;
+      Sv[idx % B + (idx / B) * lds] = v[e];
     }
     __syncthreads();
   }
+  if (tid < B) {
+    int pos = tid;
+    for (int k = B - 1; k >= 0; --k) {
+      const int p = pivs[k];
+      if (pos == k) pos = p;
+      else if (pos == p) pos = k;
+    }
+    cpos[tid] = pos;
+  }
+#pragma unroll
+  for (int e = 0; e < PER; ++e) {
+    const int idx = tid + e * NT;
+    v[e] = Sv[idx % B + (idx / B) * lds];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < PER; ++e) {
+    const int idx = tid + e * NT;
+    Sv[idx % B + cpos[idx / B] * lds] = v[e];
+  }
+}
+
+template <int B>
+__global__ void __launch_bounds__(FacShape<B>::NT) bt_factor_small_kernel(BtFactorArgs a) {
+  using Sh = FacShape<B>;
+  constexpr int NT = Sh::NT, LDS = Sh::LDS, NW = NT / 32;
+  constexpr bool RAW = Sh::RAW_SMEM;
+  constexpr size_t BB = (size_t)B * B;
+  const bool tw = a.kmid >= 0;
+  const int node = tw ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int half = tw ? (int)(blockIdx.x & 1) : 0;
+  const int L = a.L, kmid = tw ? a.kmid : L - 1;
+  const int nsteps = half == 0 ? kmid + 1 : L - 1 - kmid;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double2 z = a.z[node];
+  extern __shared__ __align__(16) double2 fsm[];
+  double2* Sv = fsm;                  // B x LDS: S, then S^{-1}
+  double2* Gp = Sv + B * LDS;         // B x LDS: G of the previous layer (B operand of the S update)
+  double2* colbuf = Gp + B * LDS;     // B
+  double2* rawD = colbuf + B;         // RAW: 2 x BB (A, B) pairs of the diagonal block
+  double2* rawC = rawD + 2 * BB;      // RAW: 3 x BB (A, B) pairs of the out coupling
+  __shared__ int pivs[B], cpos[B];
+  double2* sinv = a.sinv + (size_t)node * L * BB;
+  double2* gm = a.g + (size_t)node * (L > 1 ? L - 1 : 0) * BB;
+  double2* hm = a.h + (size_t)node * (L > 1 ? L - 1 : 0) * BB;
+  // b <= 32: factors stored row-swizzled for the bulk-copy sweep (sweep_small.cu): row i of
+  // column j at j*B + (i ^ 2(j & 3)); b = 64: plain column-major (sweep.cu)
+  auto fidx = [&](int i, int j) { return RAW ? j * B + (i ^ ((j & 3) << 1)) : j * B + i; };
+
+  auto layer_of = [&](int r) { return half == 0 ? r : L - 1 - r; };
+  auto has_out = [&](int l) { return half == 0 ? l + 1 < L : true; };
+  auto prefetch = [&](int r) {
+    if (RAW && r < nsteps) {
+      const int l = layer_of(r);
+      const double2* d = a.abdiag + (size_t)l * BB;
+      double2* dd = rawD + (r & 1) * BB;
+      for (int e = tid; e < (int)BB; e += NT) cp_async16(dd + e, d + e);
+      if (has_out(l)) {
+        const double2* c = a.ablow + (size_t)(half == 0 ? l : l - 1) * BB;
+        double2* cd = rawC + (r % 3) * BB;
+        for (int e = tid; e < (int)BB; e += NT) cp_async16(cd + e, c + e);
+      }
+    }
+    cp_async_commit();
+  };
+
+  prefetch(0);
+  for (int r = 0; r < nsteps; ++r) {
+    const int l = layer_of(r);
+    prefetch(r + 1);
+    cp_async_wait<1>();
+    __syncthreads();
+    const double2* dsrc = RAW ? rawD + (r & 1) * BB : a.abdiag + (size_t)l * BB;
+    // raw (A, B) pairs of the in / out couplings (as stored: C_c = M(c+1, c), col-major)
+    const double2* cin = r == 0 ? nullptr
+                         : RAW ? rawC + ((r + 2) % 3) * BB
+                               : a.ablow + (size_t)(half == 0 ? l - 1 : l) * BB;
+    const double2* cout = !has_out(l) ? nullptr
+                          : RAW ? rawC + (r % 3) * BB
+                                : a.ablow + (size_t)(half == 0 ? l : l - 1) * BB;
+    // top: Cin = C_{l-1}, Cout = C_l^T ; bottom: Cin = C_l^T, Cout = C_{l-1}
+    auto Ci = [&](int i, int t) { return czb(half == 0 ? cin[i + t * B] : cin[t + i * B], z); };
+    auto Co = [&](int i, int t) { return czb(half == 0 ? cout[t + i * B] : cout[i + t * B], z); };
+    auto Gop = [&](int t, int j) { return Gp[t + j * LDS]; };
+    auto Sop = [&](int i, int t) { return Sv[i + t * LDS]; };
+
+    // (1) S = M_l - Cin G_prev   [- Cout G'_{k+1} at the middle layer]
+    if (r == 0) {
+      for (int e = tid; e < (int)BB; e += NT) Sv[e % B + (e / B) * LDS] = czb(dsrc[e], z);
+    } else {
+      cgemm_tiles<B>(warp, NW, lane, Ci, Gop,
+                     [&](int i, int j, double2 v) { Sv[i + j * LDS] = csub(czb(dsrc[i + j * B], z), v); });
+    }
+    const bool middle = tw && half == 0 && l == kmid;
+    if (middle) {
+      __syncthreads();                    // S complete, G_{k-1} no longer read
+      __threadfence();
+      cg::this_cluster().sync();          // the bottom CTA has stored G'_{k+1} = g[kmid]
+      for (int e = tid; e < (int)BB; e += NT)
+        Gp[e % B + (e / B) * LDS] = __ldcg(gm + (size_t)kmid * BB + fidx(e % B, e / B));
+      __syncthreads();
+      cgemm_tiles<B>(warp, NW, lane, Co, Gop,
+                     [&](int i, int j, double2 v) { Sv[i + j * LDS] = csub(Sv[i + j * LDS], v); });
+    }
+    __syncthreads();
+
+    // (2) S^{-1} in place
+    if constexpr (RAW) {
+      if (warp == 0) gj_rows<B>(Sv, LDS, pivs, lane, a.status);
+    } else {
+      gj_smem<B, NT>(Sv, LDS, pivs, cpos, a.status);
+    }
+    __syncthreads();
+
+    // (3) outputs: S^{-1}, H = S^{-1} Cin, G = S^{-1} Cout (kept for the next layer)
+    double2* so = sinv + (size_t)l * BB;
+    for (int e = tid; e < (int)BB; e += NT) so[fidx(e % B, e / B)] = Sv[e % B + (e / B) * LDS];
+    if (r > 0) {
+      double2* ho = hm + (size_t)(half == 0 ? l - 1 : l) * BB;
+      cgemm_tiles<B>(warp, NW, lane, Sop, [&](int t, int j) { return Ci(t, j); },
+                     [&](int i, int j, double2 v) { ho[fidx(i, j)] = v; });
+    }
+    if (cout) {
+      double2* go = middle ? hm + (size_t)kmid * BB : gm + (size_t)(half == 0 ? l : l - 1) * BB;
+      cgemm_tiles<B>(warp, NW, lane, Sop, [&](int t, int j) { return Co(t, j); },
+                     [&](int i, int j, double2 v) {
+                       go[fidx(i, j)] = v;
+                       Gp[i + j * LDS] = v;
+                     });
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+  if (tw && half == 1) {
+    __threadfence();
+    cg::this_cluster().sync();  // releases g[kmid] to the top CTA's middle layer
+  }
+}
+
+template <int B>
+static cudaError_t launch_factor_small(const BtFactorArgs& a, cudaStream_t st) {
+  using Sh = FacShape<B>;
+  const size_t sm = Sh::smem_bytes();
+  auto kern = bt_factor_small_kernel<B>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  const bool tw = a.kmid >= 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(a.nodes * (tw ? 2 : 1)));
+  cfg.blockDim = dim3(Sh::NT);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = tw ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, a);
+  ++g_launches;
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+int bt_twist_layer(int L, int b) {
+  const char* s = std::getenv("FEAST_BT_TWIST");  // read per call: tests flip it per context
+  const bool off = s && s[0] == '0';
+  return (!off && b <= 64 && L >= 4) ? L / 2 : -1;
 }
 
 // ---------------------------------------------------------------------------
@@ -406,14 +618,12 @@ size_t bt_factor_work_elems(int b, int nodes) {  // double2 elements of BtFactor
 }
 
 cudaError_t bt_factor(const BtFactorArgs& a, cudaStream_t st) {
-  if (a.b >= 128) return bt_factor_big(a, st);
-  size_t sm = sizeof(double2) * (size_t)a.b;
-  if (a.b <= 64) sm += sizeof(double2) * (size_t)a.b * 2 * (a.b + 1);
-  if (sm > 48 * 1024)
-    cudaFuncSetAttribute(bt_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  bt_factor_kernel<<<a.nodes, 256, sm, st>>>(a);
-  ++g_launches;
-  return cudaGetLastError();
+  switch (a.b) {
+    case 16: return launch_factor_small<16>(a, st);
+    case 32: return launch_factor_small<32>(a, st);
+    case 64: return launch_factor_small<64>(a, st);
+  }
+  return bt_factor_big(a, st);
 }
 
 // ---------------------------------------------------------------------------

@@ -14,6 +14,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <stdexcept>
@@ -182,6 +184,7 @@ struct feast_gpu_ctx {
   bool factored = false;
   int batch_req = 0, batch = 0, res0 = -1, rescnt = 0;
   DevBuf<double2> sinv, gfac, hfac, lu, dinv, scratch, fwork;
+  int kmid = -1;  // twisted block-Thomas meeting layer of the current factors (bt_twist_layer)
   DevBuf<int> ipiv, perm, status, fiwork;
   // workspaces
   int mcap = 0;
@@ -191,6 +194,10 @@ struct feast_gpu_ctx {
   DevBuf<int> keep;
   EigWork* eig = nullptr;
   int eig_cap = 0;
+  // host phase tracing (FEAST_TRACE=1: host wall clock per phase to stderr; =2: with a stream
+  // sync before each mark, so device work is attributed to the phase that enqueued it)
+  int trace = 0;
+  std::chrono::steady_clock::time_point tmark;
   // bench state
   int bench_m = 0;
   bool timing = false;
@@ -241,6 +248,16 @@ void ensure_workspace(feast_gpu_ctx* c, int m) {
 }
 
 void sync(feast_gpu_ctx* c) { CK(cudaStreamSynchronize(c->stream)); }
+
+void trace_mark(feast_gpu_ctx* c, const char* what) {
+  if (!c->trace) return;
+  if (c->trace >= 2) sync(c);
+  const auto now = std::chrono::steady_clock::now();
+  if (what)
+    std::fprintf(stderr, "[feast_gpu] %-34s %9.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - c->tmark).count());
+  c->tmark = now;
+}
 
 // ------------------------------- pencil -------------------------------------
 void validate_dense_symmetric(const double* m, int n) {
@@ -428,8 +445,10 @@ void check_operator(const feast_operator_t* o) {
 }
 
 void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operator_t* b) {
+  trace_mark(c, nullptr);
   check_operator(a);
   check_operator(b);
+  trace_mark(c, "set_pencil: validate operators");
   if (a->n != b->n) fail(FEAST_EINPUT, "feast_solve: operator dimensions differ");
   const int n = a->n;
   // storage policy (the reference's Auto policy, inner_solver.hpp:84-92, with the banded
@@ -480,6 +499,7 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
     std::vector<double2> pd(ad.size()), pl(al.size());
     for (size_t i = 0; i < ad.size(); ++i) pd[i] = make_double2(ad[i], bd[i]);
     for (size_t i = 0; i < al.size(); ++i) pl[i] = make_double2(al[i], bl[i]);
+    trace_mark(c, "set_pencil: storage choice + re-block");
     c->abdiag.ensure(pd.size());
     c->ablow.ensure(std::max<size_t>(pl.size(), 1));
     CK(cudaMemcpyAsync(c->abdiag.p, pd.data(), sizeof(double2) * pd.size(), cudaMemcpyHostToDevice, c->stream));
@@ -496,6 +516,7 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
       CK(cudaMemcpyAsync(c->Bm.p + nd, bl.data(), sizeof(double) * nl, cudaMemcpyHostToDevice, c->stream));
     }
     sync(c);
+    trace_mark(c, "set_pencil: alloc + H2D");
   } else {
     c->blocktri = false;
     c->b = 0;
@@ -588,13 +609,12 @@ void factor_range(feast_gpu_ctx* c, int s0, int cnt) {
     c->sinv.ensure(slots * c->L * bb);
     c->gfac.ensure(std::max<size_t>(slots * (c->L - 1) * bb, 1));
     c->hfac.ensure(std::max<size_t>(slots * (c->L - 1) * bb, 1));
-    if (c->b > 64 && c->b < 128) c->scratch.ensure(slots * (size_t)c->b * 2 * (c->b + 1));
     if (c->b >= 128) {
       c->fwork.ensure(bt_factor_work_elems(c->b, cnt));
       c->fiwork.ensure((size_t)cnt * 2 * c->b);
     }
     BtFactorArgs a{c->L, c->b, cnt, c->abdiag.p, c->ablow.p, c->dz.p + s0, c->sinv.p, c->gfac.p, c->hfac.p,
-                   c->scratch.p, c->status.p, c->fwork.p, c->fiwork.p};
+                   c->scratch.p, c->status.p, c->fwork.p, c->fiwork.p, c->kmid = bt_twist_layer(c->L, c->b)};
     CK(bt_factor(a, c->stream));
     if (!c->streamed()) {  // factor workspaces are transient unless they are reused every pass
       c->fwork.release();
@@ -660,7 +680,7 @@ void contour_pass(feast_gpu_ctx* c, int m) {
       if (c->res0 != s0 || c->rescnt != cnt) factor_range(c, s0, cnt);
       if (c->blocktri) {
         BtSweepArgs a{c->L, c->b, cnt, m, c->npad, c->ablow.p, c->dz.p + s0, c->dcoeff.p + s0, c->sinv.p,
-                      c->gfac.p, c->hfac.p, c->Y.p, c->T.p, c->W.p, 0};
+                      c->gfac.p, c->hfac.p, c->Y.p, c->T.p, c->W.p, 0, c->kmid};
         CK(bt_sweep(a, c->stream));
       } else {
         DenseSolveArgs a{c->n, cnt, m, c->npad, c->lu.p, c->perm.p, c->dinv.p, c->dcoeff.p + s0, c->Y.p, c->T.p,
@@ -821,6 +841,7 @@ double secs(std::chrono::steady_clock::time_point t0) {
 void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_t* cfg,
                  const double* initial_y, int y_cols, feast_result_t* out) {
   const auto t_start = std::chrono::steady_clock::now();
+  trace_mark(c, nullptr);
   if (!c->have_pencil) fail(FEAST_EINPUT, "feast_gpu: pencil not set");
   if (!cfg || !out) fail(FEAST_EINPUT, "feast_gpu_solve: null argument");
   const int n = c->n;
@@ -836,6 +857,7 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
   if (!same_contour) build_contour(c, emin, emax, cfg->n_e);
   const double effective_tol = cfg->trace_tol;  // direct solves: residual_target() == 0
   ensure_workspace(c, cfg->m0);
+  trace_mark(c, "solve: contour + workspaces");
 
   *out = feast_result_t{out->eigenvalues, out->eigenvectors, out->residuals, out->residual_absolute_only,
                         out->trace_history, out->in_interval_counts, out->subspace};
@@ -844,8 +866,10 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
     std::vector<double> y((size_t)n * m);
     if (initial_y) std::memcpy(y.data(), initial_y, sizeof(double) * y.size());
     else random_block(n, m, cfg->seed, y.data(), n);
+    trace_mark(c, "solve: initial block (host)");
     upload_block(c, y.data(), m, c->Y.p);
     sync(c);
+    trace_mark(c, "solve: initial block H2D");
   }
   if (!same_contour || !c->factored) c->factored = false;
 
@@ -871,8 +895,10 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
       CK(cudaMemcpyAsync(c->keep.p, keep.data(), sizeof(int) * k, cudaMemcpyHostToDevice, c->stream));
       CK(gather_columns(c->X.p, c->npad, c->npad, c->keep.p, k, c->Q.p, c->npad, c->stream));
     }
+    trace_mark(c, "finalize: gather");
     if (out->eigenvectors && k) download_block(c, c->Q.p, k, out->eigenvectors);
     if (out->subspace) download_block(c, c->X.p, rr.mo, out->subspace);
+    trace_mark(c, "finalize: D2H eigenvectors + subspace");
     std::vector<double> res(k);
     std::vector<int32_t> ab(k);
     residuals(c, k, lam.data(), c->Q.p, res.data(), ab.data(), &out->max_residual);
@@ -881,6 +907,7 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
     if (out->trace_history) std::memcpy(out->trace_history, history.data(), sizeof(double) * history.size());
     if (out->in_interval_counts) std::memcpy(out->in_interval_counts, counts.data(), sizeof(int) * counts.size());
     sync(c);
+    trace_mark(c, "finalize: residuals");
     out->total_s = secs(t_start);
   };
 
@@ -890,11 +917,13 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
       const auto t0 = std::chrono::steady_clock::now();
       factor(c);
       out->factorize_s += secs(t0);
+      trace_mark(c, "solve: factor");
     }
     const auto t_solve = std::chrono::steady_clock::now();
     contour_pass(c, m);
     sync(c);
     out->solve_s += secs(t_solve);
+    trace_mark(c, "solve: contour pass");
 
     const auto t_reduce = std::chrono::steady_clock::now();
     Reduced rr;
@@ -912,6 +941,7 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
       return;
     }
     out->reduce_s += secs(t_reduce);
+    trace_mark(c, "solve: rayleigh-ritz");
 
     double tr = 0.0;
     int cnt = 0;
@@ -982,6 +1012,7 @@ int feast_gpu_create(int device, void* stream, feast_gpu_ctx** out) {
   if (device < 0 || device >= ndev) return FEAST_EINPUT;
   auto* c = new feast_gpu_ctx();
   c->device = device;
+  if (const char* t = std::getenv("FEAST_TRACE")) c->trace = std::atoi(t);
   const int rc = guarded(c, [&] {
     if (stream) {
       c->stream = static_cast<cudaStream_t>(stream);
@@ -1065,6 +1096,14 @@ int feast_gpu_set_node_batch(feast_gpu_ctx* c, int nodes) {
   });
 }
 
+int feast_gpu_storage(const feast_gpu_ctx* c, int* b, int* layers, int* twist) {
+  if (!c || !c->have_pencil) return FEAST_EINPUT;
+  if (b) *b = c->blocktri ? c->b : 0;
+  if (layers) *layers = c->blocktri ? c->L : 0;
+  if (twist) *twist = c->blocktri ? c->kmid : -1;
+  return FEAST_OK;
+}
+
 int feast_gpu_contour(const feast_gpu_ctx* c, double* z, double* coeff) {
   if (!c || !c->have_contour) return FEAST_EINPUT;
   for (int e = 0; e < c->ne; ++e) {
@@ -1097,7 +1136,8 @@ int feast_gpu_solve_shift(feast_gpu_ctx* c, int e, double* rhs, int m, int mode)
       if (split) CK(split_complex(w, c->AQ.p, c->npad, c->npad, m, c->stream));
       BtSweepArgs a{c->L, c->b, 1, split ? 2 * m : m, c->npad, c->ablow.p, c->dz.p + sn, c->dcoeff.p + sn,
                     c->sinv.p + s * c->L * bb, c->gfac.p + s * (c->L - 1) * bb,
-                    c->hfac.p + s * (c->L - 1) * bb, split ? c->AQ.p : nullptr, nullptr, w, split ? 2 : 1};
+                    c->hfac.p + s * (c->L - 1) * bb, split ? c->AQ.p : nullptr, nullptr, w, split ? 2 : 1,
+                    c->kmid};
       CK(bt_sweep(a, c->stream));
       if (split) CK(merge_complex(w, c->npad, c->npad, m, c->stream));
     } else {

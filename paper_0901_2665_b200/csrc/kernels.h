@@ -26,12 +26,16 @@ struct BtFactorArgs {
   double2* sinv;          // nodes * L*b*b
   double2* g;             // nodes * (L-1)*b*b: G_l = S_l^{-1} C_l^T
   double2* h;             // nodes * (L-1)*b*b: H_l = S_l^{-1} C_{l-1}, l >= 1
-  double2* scratch;       // nodes * b * 2b (single-CTA path, 64 < b < 128)
+  double2* scratch;       // unused (kept for the launcher signature)
   int* status;            // set to 1 on a singular block pivot
   double2* work;          // b >= 128: bt_factor_work_elems(b, nodes) double2
   int* iwork;             // b >= 128: nodes * 2b
+  int kmid = -1;          // >= 0: twisted recursion meeting at layer kmid (bt_twist_layer)
 };
 cudaError_t bt_factor(const BtFactorArgs& a, cudaStream_t st);
+// Meeting layer of the twisted (two-ended) block-Thomas recursion for b <= 64 and L >= 4
+// (L / 2), else -1 (plain top-down chain). FEAST_BT_TWIST=0 disables it.
+int bt_twist_layer(int L, int b);
 size_t bt_factor_work_elems(int b, int nodes);
 
 // Panel layout of the factors for b >= 128 (the bulk-copy sweep): each b x b factor is stored
@@ -56,6 +60,7 @@ struct BtSweepArgs {
   double* t;              // real mode output: nodes * ldv*m
   double2* w;             // workspace / complex in-out: nodes * ldv*m
   int complex_mode;
+  int kmid = -1;          // the factors' twisted meeting layer (must match bt_factor's)
 };
 cudaError_t bt_sweep(const BtSweepArgs& a, cudaStream_t st);
 

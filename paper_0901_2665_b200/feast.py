@@ -78,6 +78,7 @@ def load_library(path: str = LIB_PATH):
     L.feast_gpu_set_pencil.argtypes = [C.c_void_p, _op, _op]
     L.feast_gpu_prepare.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_int]
     L.feast_gpu_contour.argtypes = [C.c_void_p, _dp, _dp]
+    L.feast_gpu_storage.argtypes = [C.c_void_p, _ip, _ip, _ip]
     L.feast_gpu_set_node_batch.argtypes = [C.c_void_p, C.c_int]
     L.feast_gpu_solve_shift.argtypes = [C.c_void_p, C.c_int, _dp, C.c_int, C.c_int]
     L.feast_gpu_contour_pass.argtypes = [C.c_void_p, _dp, C.c_int, _dp]
@@ -100,7 +101,7 @@ EXPORTED_SYMBOLS = [
     "feast_gpu_contour", "feast_gpu_solve_shift", "feast_gpu_contour_pass",
     "feast_gpu_rayleigh_ritz", "feast_gpu_reduced_gevp", "feast_gpu_residuals", "feast_gpu_solve",
     "feast_gpu_bench_init", "feast_gpu_bench_passes", "feast_gpu_launch_count",
-    "feast_gpu_set_node_batch",
+    "feast_gpu_set_node_batch", "feast_gpu_storage",
 ]
 
 
@@ -225,6 +226,13 @@ class GpuContext:
     def prepare(self, emin, emax, n_e=8):
         self._check(self.L.feast_gpu_prepare(self.h, emin, emax, n_e))
         self.n_e = n_e
+
+    def storage(self):
+        """(b, L, twist): block-tridiagonal block size and layer count (0, 0 when dense), and
+        the twisted block-Thomas meeting layer of the current factors (-1: plain chain)."""
+        b, lay, tw = C.c_int(0), C.c_int(0), C.c_int(-1)
+        self._check(self.L.feast_gpu_storage(self.h, C.pointer(b), C.pointer(lay), C.pointer(tw)))
+        return b.value, lay.value, tw.value
 
     def contour(self):
         z = np.zeros(2 * self.n_e)

@@ -287,3 +287,33 @@ def test_streamed_node_batches_bit_identical(F, which):
     assert np.array_equal(r0.eigenvalues, r1.eigenvalues)
     assert np.array_equal(r0.eigenvectors, r1.eigenvectors)
     assert np.array_equal(r0.trace_history, r1.trace_history)
+
+
+# small blocks (b <= 64): the twisted (two-ended) block-Thomas recursion and sweep, and the
+# plain top-down chain (FEAST_BT_TWIST=0), against the reference's pivoted BandedLU solves and
+# accumulate_subspace_real; L = 1..3 take the plain chain, L >= 4 meet at layer L // 2
+@pytest.mark.parametrize("twist", ["1", "0"])
+@pytest.mark.parametrize("L,b", [(1, 16), (2, 16), (3, 16), (4, 16), (5, 16), (9, 16), (33, 16),
+                                 (4, 32), (7, 32), (5, 64), (6, 64)])
+def test_contour_pass_small_blocks(F, monkeypatch, twist, L, b):
+    from paper_0901_2665_b200 import problems as P
+    monkeypatch.setenv("FEAST_BT_TWIST", twist)
+    a, bb = P.blocktri_operators(L, b, seed=L * 100 + b)
+    emin, emax, ne, m0 = -0.3, 0.4, 8, 20
+    c = F.GpuContext(0)
+    try:
+        c.set_pencil(a, bb)
+        c.prepare(emin, emax, ne)
+        assert c.storage() == (b, L, L // 2 if (twist == "1" and L >= 4) else -1)
+        y = O.random_block(a.n, m0, 5)
+        q = c.contour_pass(y)
+        qr = O.accumulate_real(a, bb, emin, emax, ne, y)
+        assert np.max(np.abs(q - qr)) <= 1e-11 * max(1.0, np.max(np.abs(qr)))
+        z, _ = c.contour()
+        rhs = np.random.default_rng(2).standard_normal((a.n, 3)) + 1j * np.random.default_rng(3).standard_normal((a.n, 3))
+        for e in (0, ne - 1):
+            for mode in (0, 1):
+                x = c.solve_shift(e, rhs, bool(mode))
+                assert rel(x, O.shift_solve(a, bb, z[e], rhs, mode)) <= 1e-12, (e, mode)
+    finally:
+        c.close()
