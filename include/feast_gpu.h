@@ -149,6 +149,11 @@ int feast_gpu_prepare(feast_gpu_ctx* ctx, double emin, double emax, int n_e);
  * resident plan). Takes effect at the next feast_gpu_prepare / feast_gpu_solve. */
 int feast_gpu_set_node_batch(feast_gpu_ctx* ctx, int nodes);
 
+/* random_block<double> (core.hpp:84-106) generated on the device: out (host, n*m column-major)
+ * = 2 * ((w >> 11) * 2^-53) - 1 over the std::mt19937_64(seed) words w, bit-identical to the
+ * reference's host generator. feast_gpu_solve draws its initial block this way. */
+int feast_gpu_random_block(feast_gpu_ctx* ctx, int n, int m, uint64_t seed, double* out);
+
 /* Storage chosen for the pencil at feast_gpu_set_pencil: block size b and layer count L of the
  * block-tridiagonal re-blocking (b = 0, L = 0 for the dense path), and twist = the meeting
  * layer of the two-ended block-Thomas recursion used by the factors (-1: plain chain; valid

@@ -125,14 +125,6 @@ void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
   }
 }
 
-// random_block<double> (core.hpp:84-106): mt19937_64, top 53 bits, column-major fill
-void random_block(int n, int m, uint64_t seed, double* out, int ld) {
-  std::mt19937_64 gen(seed);
-  for (int j = 0; j < m; ++j)
-    for (int i = 0; i < n; ++i)
-      out[i + (size_t)j * ld] = 2.0 * (static_cast<double>(gen() >> 11) * 0x1p-53) - 1.0;
-}
-
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
@@ -160,6 +152,9 @@ struct feast_gpu_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaStream_t aux = nullptr;     // side stream: the initial block's generator runs beside the factor
+  cudaEvent_t y_ready = nullptr;  // recorded on aux; the main stream waits on it before the first pass
+  bool y_pending = false;
   std::string err;
   // multi-GPU
   void* comm = nullptr;
@@ -249,6 +244,26 @@ void ensure_workspace(feast_gpu_ctx* c, int m) {
 
 void sync(feast_gpu_ctx* c) { CK(cudaStreamSynchronize(c->stream)); }
 
+// Y = random_block(n, m, seed) (core.hpp:84-106) generated on the device into c->Y on the side
+// stream (zero padding rows); the main stream joins it before its first use (join_aux)
+void device_random_block(feast_gpu_ctx* c, int m, uint64_t seed) {
+  if (!c->aux) {
+    CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->y_ready, cudaEventDisableTiming));
+  }
+  CK(cudaEventRecord(c->y_ready, c->stream));  // Y's previous readers on the main stream
+  CK(cudaStreamWaitEvent(c->aux, c->y_ready, 0));
+  if (c->npad != c->n) CK(fill_zero(c->Y.p, (size_t)c->npad * m, c->aux));
+  CK(random_block_device(seed, c->n, m, c->Y.p, c->npad, c->aux));
+  CK(cudaEventRecord(c->y_ready, c->aux));
+  c->y_pending = true;
+}
+void join_aux(feast_gpu_ctx* c) {
+  if (!c->y_pending) return;
+  CK(cudaStreamWaitEvent(c->stream, c->y_ready, 0));
+  c->y_pending = false;
+}
+
 void trace_mark(feast_gpu_ctx* c, const char* what) {
   if (!c->trace) return;
   if (c->trace >= 2) sync(c);
@@ -305,10 +320,18 @@ void validate_csr(const feast_operator_t* o) {
 
 // smallest block size (multiple of 16; of 32 above 128) for which the CSR pattern is
 // block-tridiagonal
+int log2_exact(int b) {  // b is a power of two (round_block)
+  int s = 0;
+  while ((1 << s) < b) ++s;
+  return s;
+}
 bool csr_fits_blocktri(const feast_operator_t* o, int b) {
-  for (int i = 0; i < o->n; ++i)
+  const int sh = log2_exact(b);
+  for (int i = 0; i < o->n; ++i) {
+    const int li = i >> sh;
     for (int k = o->row_ptr[i]; k < o->row_ptr[i + 1]; ++k)
-      if (std::abs(i / b - o->col_idx[k] / b) > 1) return false;
+      if (std::abs(li - (o->col_idx[k] >> sh)) > 1) return false;
+  }
   return true;
 }
 // block sizes the sweep kernels are specialised for (sweep.cu)
@@ -359,10 +382,11 @@ void to_blocktri(const feast_operator_t* o, int b, int L, bool is_b, std::vector
     if (o->nblocks > 1) std::memcpy(low.data(), o->lower, sizeof(double) * (size_t)(o->nblocks - 1) * b * b);
     return;
   }
+  const int sh = log2_exact(b), msk = b - 1;
   auto put = [&](int i, int j, double v) {
-    const int li = i / b, lj = j / b, ii = i % b, jj = j % b;
-    if (li == lj) diag[(size_t)li * b * b + ii + (size_t)jj * b] += v;
-    else if (li == lj + 1) low[(size_t)lj * b * b + ii + (size_t)jj * b] += v;
+    const int li = i >> sh, lj = j >> sh, ii = i & msk, jj = j & msk;
+    if (li == lj) diag[((size_t)li << (2 * sh)) + ii + ((size_t)jj << sh)] += v;
+    else if (li == lj + 1) low[((size_t)lj << (2 * sh)) + ii + ((size_t)jj << sh)] += v;
   };
   if (o->kind == FEAST_STORAGE_CSR) {
     for (int i = 0; i < n; ++i)
@@ -667,6 +691,7 @@ int resident_slot(feast_gpu_ctx* c, int s) {
 // ------------------------------- passes --------------------------------------
 // Q = -sum_e Re(c_e (z_e B - A)^{-1} Y) over ALL nodes (allreduce across ranks)
 void contour_pass(feast_gpu_ctx* c, int m) {
+  join_aux(c);
   const int own = c->owned();
   const size_t nv = (size_t)c->npad * m;
   if (c->timing) CK(cudaEventRecord(c->ev[2], c->stream));
@@ -863,13 +888,16 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
                         out->trace_history, out->in_interval_counts, out->subspace};
   int m = initial_y ? y_cols : cfg->m0;
   {
-    std::vector<double> y((size_t)n * m);
+    std::vector<double> y(initial_y ? (size_t)n * m : 0);
     if (initial_y) std::memcpy(y.data(), initial_y, sizeof(double) * y.size());
-    else random_block(n, m, cfg->seed, y.data(), n);
-    trace_mark(c, "solve: initial block (host)");
-    upload_block(c, y.data(), m, c->Y.p);
-    sync(c);
-    trace_mark(c, "solve: initial block H2D");
+    if (initial_y) {
+      upload_block(c, y.data(), m, c->Y.p);
+      sync(c);
+      trace_mark(c, "solve: initial block H2D");
+    } else {
+      device_random_block(c, m, cfg->seed);  // overlaps the factorisation (side stream)
+      trace_mark(c, "solve: initial block (device mt19937_64)");
+    }
   }
   if (!same_contour || !c->factored) c->factored = false;
 
@@ -1046,6 +1074,8 @@ void feast_gpu_destroy(feast_gpu_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->comm && nccl().commDestroy) nccl().commDestroy(c->comm);
   if (c->own_stream) cudaStreamDestroy(c->stream);
+  if (c->aux) cudaStreamDestroy(c->aux);
+  if (c->y_ready) cudaEventDestroy(c->y_ready);
   delete c;
 }
 
@@ -1093,6 +1123,17 @@ int feast_gpu_set_node_batch(feast_gpu_ctx* c, int nodes) {
     if (nodes < 0) fail(FEAST_EINPUT, "set_node_batch: negative batch");
     c->batch_req = nodes;
     c->factored = false;  // re-plan at the next factorisation
+  });
+}
+
+int feast_gpu_random_block(feast_gpu_ctx* c, int n, int m, uint64_t seed, double* out) {
+  return guarded(c, [&] {
+    if (n < 1 || m < 1 || !out) fail(FEAST_EINPUT, "random_block: bad shape");
+    DevBuf<double> d;
+    d.ensure((size_t)n * m);
+    CK(random_block_device(seed, n, m, d.p, n, c->stream));
+    CK(cudaMemcpyAsync(out, d.p, sizeof(double) * n * (size_t)m, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
   });
 }
 
@@ -1227,9 +1268,8 @@ int feast_gpu_bench_init(feast_gpu_ctx* c, int m0, uint64_t seed) {
   return guarded(c, [&] {
     if (!c->factored) fail(FEAST_EINPUT, "feast_gpu: factors not prepared");
     ensure_workspace(c, m0);
-    std::vector<double> y((size_t)c->n * m0);
-    random_block(c->n, m0, seed, y.data(), c->n);
-    upload_block(c, y.data(), m0, c->Y.p);
+    device_random_block(c, m0, seed);
+    join_aux(c);
     sync(c);
     c->bench_m = m0;
   });

@@ -141,6 +141,10 @@ cudaError_t scale_columns(const double* v, int m, const int* keep, const double*
 cudaError_t residual_sums(int n, int m, const double* ax, const double* bx, const double* x,
                           int ld, const double* lam, double* out, cudaStream_t st);
 
+// random_block<double> (core.hpp:84-106) on the device: out(i, j) for i < n, j < m (ld), the
+// mt19937_64(seed) stream mapped to [-1, 1) column by column, bit-identical to the host
+cudaError_t random_block_device(uint64_t seed, int n, int m, double* out, int ld, cudaStream_t st);
+
 // misc
 cudaError_t fill_zero(double* p, size_t count, cudaStream_t st);
 cudaError_t gather_columns(const double* src, int ld, int n, const int* idx, int m, double* dst,

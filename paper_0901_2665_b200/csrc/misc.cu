@@ -127,3 +127,78 @@ cudaError_t merge_complex(double2* w, int n, int64_t ld, int m, cudaStream_t st)
 }
 
 }  // namespace feastgpu
+
+namespace feastgpu {
+
+// ---------------------------------------------------------------------------
+// random_block<double> (core.hpp:84-106) on the device, bit-identical to the host's
+// std::mt19937_64(seed): Y(i, j) = 2 * ((w >> 11) * 2^-53) - 1 for the column-major stream of
+// words w. MT19937-64 is one sequential recurrence, but each 312-word twist splits into two
+// data-parallel halves (words 0..155 read only old state; words 156..311 read old state and
+// the new words 0..155), so one CTA runs the whole stream with three barriers per 312 words.
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int kMtN = 312, kMtM = 156;
+constexpr uint64_t kMtA = 0xB5026F5AA96619E9ull, kMtUpper = 0xFFFFFFFF80000000ull, kMtLower = 0x7FFFFFFFull;
+FEAST_DEV uint64_t mt_mix(uint64_t hi, uint64_t lo) {
+  const uint64_t y = (hi & kMtUpper) | (lo & kMtLower);
+  return (y >> 1) ^ ((y & 1ull) ? kMtA : 0ull);
+}
+FEAST_DEV uint64_t mt_temper(uint64_t z) {
+  z ^= (z >> 29) & 0x5555555555555555ull;
+  z ^= (z << 17) & 0x71D67FFFEDA60000ull;
+  z ^= (z << 37) & 0xFFF7EEE000000000ull;
+  z ^= z >> 43;
+  return z;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(320) mt64_block_kernel(uint64_t seed, int n, int m, double* __restrict__ out,
+                                                         int ld) {
+  __shared__ uint64_t x[kMtN];
+  const int i = threadIdx.x;
+  if (i == 0) {
+    x[0] = seed;
+    for (int k = 1; k < kMtN; ++k) x[k] = 6364136223846793005ull * (x[k - 1] ^ (x[k - 1] >> 62)) + (uint64_t)k;
+  }
+  const int64_t total = (int64_t)n * m;
+  int row = i % n, col = i / n;           // position of word o = round * 312 + i
+  const int step_col = kMtN / n, step_row = kMtN % n;
+  for (int64_t base = 0; base < total; base += kMtN) {
+    __syncthreads();
+    uint64_t a = 0, b = 0, c = 0;
+    if (i < kMtN) {
+      a = x[i];
+      if (i + 1 < kMtN) b = x[i + 1];
+      if (i < kMtM) c = x[i + kMtM];
+    }
+    __syncthreads();
+    uint64_t w = 0;
+    if (i < kMtM) {
+      w = c ^ mt_mix(a, b);
+      x[i] = w;
+    }
+    __syncthreads();
+    if (i >= kMtM && i < kMtN) {
+      w = x[i - kMtM] ^ mt_mix(a, i + 1 < kMtN ? b : x[0]);
+      x[i] = w;
+    }
+    if (i < kMtN && base + i < total)
+      out[row + (int64_t)col * ld] = 2.0 * ((double)(mt_temper(w) >> 11) * 0x1p-53) - 1.0;
+    row += step_row;
+    col += step_col;
+    if (row >= n) {
+      row -= n;
+      ++col;
+    }
+  }
+}
+
+cudaError_t random_block_device(uint64_t seed, int n, int m, double* out, int ld, cudaStream_t st) {
+  if (n <= 0 || m <= 0) return cudaSuccess;
+  mt64_block_kernel<<<1, 320, 0, st>>>(seed, n, m, out, ld);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+}  // namespace feastgpu

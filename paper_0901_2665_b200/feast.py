@@ -79,6 +79,7 @@ def load_library(path: str = LIB_PATH):
     L.feast_gpu_prepare.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_int]
     L.feast_gpu_contour.argtypes = [C.c_void_p, _dp, _dp]
     L.feast_gpu_storage.argtypes = [C.c_void_p, _ip, _ip, _ip]
+    L.feast_gpu_random_block.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64, _dp]
     L.feast_gpu_set_node_batch.argtypes = [C.c_void_p, C.c_int]
     L.feast_gpu_solve_shift.argtypes = [C.c_void_p, C.c_int, _dp, C.c_int, C.c_int]
     L.feast_gpu_contour_pass.argtypes = [C.c_void_p, _dp, C.c_int, _dp]
@@ -101,7 +102,7 @@ EXPORTED_SYMBOLS = [
     "feast_gpu_contour", "feast_gpu_solve_shift", "feast_gpu_contour_pass",
     "feast_gpu_rayleigh_ritz", "feast_gpu_reduced_gevp", "feast_gpu_residuals", "feast_gpu_solve",
     "feast_gpu_bench_init", "feast_gpu_bench_passes", "feast_gpu_launch_count",
-    "feast_gpu_set_node_batch", "feast_gpu_storage",
+    "feast_gpu_set_node_batch", "feast_gpu_storage", "feast_gpu_random_block",
 ]
 
 
@@ -168,7 +169,8 @@ class FeastResult:
 
 
 def _cols(a, n, k):
-    return a.reshape(-1, order="F")[: n * k].reshape((n, k), order="F").copy()
+    """The first k columns of a Fortran-ordered n x m0 output block, as a view (no copy)."""
+    return a[:n, :k]
 
 
 class GpuContext:
@@ -226,6 +228,12 @@ class GpuContext:
     def prepare(self, emin, emax, n_e=8):
         self._check(self.L.feast_gpu_prepare(self.h, emin, emax, n_e))
         self.n_e = n_e
+
+    def random_block(self, n: int, m: int, seed: int) -> np.ndarray:
+        """random_block<double>(n, m, seed) (core.hpp:84-106), generated on the device."""
+        out = np.zeros((n, m), order="F")
+        self._check(self.L.feast_gpu_random_block(self.h, n, m, seed, abi.dptr(out)))
+        return out
 
     def storage(self):
         """(b, L, twist): block-tridiagonal block size and layer count (0, 0 when dense), and
@@ -297,10 +305,10 @@ class GpuContext:
         """feast_solve (core.hpp:264-391) on the uploaded pencil."""
         n, m0 = self.n, config.m0
         nl = max(config.max_loops, 0) + 1
-        out = dict(eigenvalues=np.zeros(max(m0, 1)), eigenvectors=np.zeros((n, max(m0, 1)), order="F"),
+        out = dict(eigenvalues=np.zeros(max(m0, 1)), eigenvectors=np.empty((n, max(m0, 1)), order="F"),
                    residuals=np.zeros(max(m0, 1)), absonly=np.zeros(max(m0, 1), dtype=np.int32),
                    trace=np.zeros(nl), counts=np.zeros(nl, dtype=np.int32),
-                   subspace=np.zeros((n, max(m0, 1)), order="F"))
+                   subspace=np.empty((n, max(m0, 1)), order="F"))
         r = abi.FeastResultT()
         r.eigenvalues = abi.dptr(out["eigenvalues"])
         r.eigenvectors = abi.dptr(out["eigenvectors"])

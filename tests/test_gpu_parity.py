@@ -317,3 +317,12 @@ def test_contour_pass_small_blocks(F, monkeypatch, twist, L, b):
                 assert rel(x, O.shift_solve(a, bb, z[e], rhs, mode)) <= 1e-12, (e, mode)
     finally:
         c.close()
+
+
+# the initial block is drawn on the device (mt19937_64 in a single CTA, two-phase twist): the
+# stream must be bit-identical to random_block<double> (core.hpp:84-106, test_core.cpp:49-71)
+@pytest.mark.parametrize("n,m,seed", [(1, 1, 42), (5, 3, 7), (311, 2, 42), (312, 2, 1), (313, 3, 5),
+                                      (16384, 192, 42)])
+def test_device_random_block_bit_identical(ctx, n, m, seed):
+    y = ctx.random_block(n, m, seed)
+    assert np.array_equal(y, O.random_block(n, m, seed))
