@@ -57,6 +57,20 @@ FEAST_DEV void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* b
       : "memory");
 }
 
+// spin on mbarrier.test_wait (never suspends the thread; for latency-critical chains with
+// one warp per SMSP, where try_wait's suspend/wake-up would sit on the critical path)
+FEAST_DEV void mbar_spin(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "SPIN_%=:\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra SPIN_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // order this thread's generic-proxy global stores before later async-proxy (bulk copy) reads
 FEAST_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;\n" ::: "memory"); }
 
