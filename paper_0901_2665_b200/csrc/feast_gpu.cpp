@@ -11,6 +11,10 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
@@ -125,26 +129,51 @@ void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
   }
 }
 
+// Device buffers come from the device's stream-ordered memory pool on the calling context's
+// stream (set by guarded()): freed memory stays in the pool (release threshold = max, set at
+// feast_gpu_create), so a fresh context in the same process (a second solve, the bench's e2e
+// leg) reuses it without cudaMalloc/cudaFree round trips, and no free synchronises the device.
+thread_local cudaStream_t g_alloc_stream = nullptr;
+struct AllocStream {
+  cudaStream_t prev;
+  explicit AllocStream(cudaStream_t s) : prev(g_alloc_stream) { g_alloc_stream = s; }
+  ~AllocStream() { g_alloc_stream = prev; }
+};
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
   void ensure(size_t count) {
     if (count <= n) return;
-    if (p && n) cudaFree(p);
+    if (p && n) cudaFreeAsync(p, g_alloc_stream);
     p = nullptr;
     n = 0;
     if (count) {
-      CK(cudaMalloc(&p, sizeof(T) * count));
+      CK(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, g_alloc_stream));
       n = count;
     }
   }
   void release() {
-    if (p && n) cudaFree(p);  // n == 0: a non-owning view into another buffer
+    if (p && n) cudaFreeAsync(p, g_alloc_stream);  // n == 0: a non-owning view into another buffer
     p = nullptr;
     n = 0;
   }
 };
+
+// bytes the pool holds in reserve (freed by earlier contexts, reusable by this one)
+size_t pool_spare(int device) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return 0;
+  uint64_t reserved = 0, used = 0;
+  cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+  cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+  return reserved > used ? (size_t)(reserved - used) : 0;
+}
 
 }  // namespace
 
@@ -275,6 +304,36 @@ void trace_mark(feast_gpu_ctx* c, const char* what) {
 }
 
 // ------------------------------- pencil -------------------------------------
+// Host-side pencil preparation runs over row ranges on up to 8 threads (the C-ABI call is the
+// user's; its validation and re-blocking were ~11 ms of a 70 ms end-to-end solve at config 2).
+// fn(lo, hi) must only write state owned by rows [lo, hi); a Failure thrown by any range is
+// rethrown (the one from the lowest range, so the message is deterministic).
+template <typename F>
+void parallel_rows(int n, int align, F&& fn) {
+  const int hw = (int)std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  const int nt = n < 4096 ? 1 : hw;
+  if (nt == 1) {
+    fn(0, n);
+    return;
+  }
+  std::vector<int> cut(nt + 1);
+  for (int t = 0; t <= nt; ++t) cut[t] = std::min(n, (int)(((int64_t)n * t / nt + align - 1) / align * align));
+  cut[nt] = n;
+  std::vector<std::exception_ptr> errs(nt);
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      try {
+        if (cut[t] < cut[t + 1]) fn(cut[t], cut[t + 1]);
+      } catch (...) {
+        errs[t] = std::current_exception();
+      }
+    });
+  for (auto& x : th) x.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
 void validate_dense_symmetric(const double* m, int n) {
   for (int j = 0; j < n; ++j)
     for (int i = 0; i < j; ++i)
@@ -283,39 +342,48 @@ void validate_dense_symmetric(const double* m, int n) {
 }
 
 int csr_bandwidth(const feast_operator_t* o) {
-  int bw = 0;
-  for (int i = 0; i < o->n; ++i)
-    for (int k = o->row_ptr[i]; k < o->row_ptr[i + 1]; ++k) bw = std::max(bw, std::abs(i - o->col_idx[k]));
+  std::atomic<int> bw{0};
+  parallel_rows(o->n, 1, [&](int r0, int r1) {
+    int b = 0;
+    for (int i = r0; i < r1; ++i)
+      for (int k = o->row_ptr[i]; k < o->row_ptr[i + 1]; ++k) b = std::max(b, std::abs(i - o->col_idx[k]));
+    int cur = bw.load();
+    while (b > cur && !bw.compare_exchange_weak(cur, b)) {
+    }
+  });
   return bw;
 }
 
 void validate_csr(const feast_operator_t* o) {
   const int n = o->n;
   if (o->row_ptr[0] != 0) fail(FEAST_EINPUT, "SymmetricOperator: bad row_ptr");
-  for (int i = 0; i < n; ++i) {
+  for (int i = 0; i < n; ++i)
     if (o->row_ptr[i + 1] < o->row_ptr[i]) fail(FEAST_EINPUT, "SymmetricOperator: bad row_ptr");
-    for (int k = o->row_ptr[i]; k < o->row_ptr[i + 1]; ++k) {
-      const int j = o->col_idx[k];
-      if (j < 0 || j >= n) fail(FEAST_EINPUT, "SymmetricOperator: triplet index out of range");
-      if (j <= i) continue;
-      // mirror (j, i) must exist with the same value (operator.hpp:237-261)
-      const int* b = o->col_idx + o->row_ptr[j];
-      const int* e = o->col_idx + o->row_ptr[j + 1];
-      const int* f = std::lower_bound(b, e, i);
-      if (f == e || *f != i) {
-        bool found = false;  // unsorted rows: linear scan
-        for (const int* q = b; q != e; ++q)
-          if (*q == i) {
-            found = true;
-            if (o->values[o->row_ptr[j] + (q - b)] != o->values[k])
-              fail(FEAST_EINPUT, "SymmetricOperator: mirror entries disagree");
-          }
-        if (!found) fail(FEAST_EINPUT, "SymmetricOperator: missing mirror entry");
-      } else if (o->values[o->row_ptr[j] + (f - b)] != o->values[k]) {
-        fail(FEAST_EINPUT, "SymmetricOperator: mirror entries disagree");
+  parallel_rows(n, 1, [&](int r0, int r1) {
+    for (int i = r0; i < r1; ++i) {
+      for (int k = o->row_ptr[i]; k < o->row_ptr[i + 1]; ++k) {
+        const int j = o->col_idx[k];
+        if (j < 0 || j >= n) fail(FEAST_EINPUT, "SymmetricOperator: triplet index out of range");
+        if (j <= i) continue;
+        // mirror (j, i) must exist with the same value (operator.hpp:237-261)
+        const int* b = o->col_idx + o->row_ptr[j];
+        const int* e = o->col_idx + o->row_ptr[j + 1];
+        const int* f = std::lower_bound(b, e, i);
+        if (f == e || *f != i) {
+          bool found = false;  // unsorted rows: linear scan
+          for (const int* q = b; q != e; ++q)
+            if (*q == i) {
+              found = true;
+              if (o->values[o->row_ptr[j] + (q - b)] != o->values[k])
+                fail(FEAST_EINPUT, "SymmetricOperator: mirror entries disagree");
+            }
+          if (!found) fail(FEAST_EINPUT, "SymmetricOperator: missing mirror entry");
+        } else if (o->values[o->row_ptr[j] + (f - b)] != o->values[k]) {
+          fail(FEAST_EINPUT, "SymmetricOperator: mirror entries disagree");
+        }
       }
     }
-  }
+  });
 }
 
 // smallest block size (multiple of 16; of 32 above 128) for which the CSR pattern is
@@ -327,12 +395,18 @@ int log2_exact(int b) {  // b is a power of two (round_block)
 }
 bool csr_fits_blocktri(const feast_operator_t* o, int b) {
   const int sh = log2_exact(b);
-  for (int i = 0; i < o->n; ++i) {
-    const int li = i >> sh;
-    for (int k = o->row_ptr[i]; k < o->row_ptr[i + 1]; ++k)
-      if (std::abs(li - (o->col_idx[k] >> sh)) > 1) return false;
-  }
-  return true;
+  std::atomic<bool> ok{true};
+  parallel_rows(o->n, 1, [&](int r0, int r1) {
+    for (int i = r0; i < r1 && ok.load(std::memory_order_relaxed); ++i) {
+      const int li = i >> sh;
+      for (int k = o->row_ptr[i]; k < o->row_ptr[i + 1]; ++k)
+        if (std::abs(li - (o->col_idx[k] >> sh)) > 1) {
+          ok = false;
+          break;
+        }
+    }
+  });
+  return ok;
 }
 // block sizes the sweep kernels are specialised for (sweep.cu)
 int round_block(int b) {
@@ -388,9 +462,11 @@ void to_blocktri(const feast_operator_t* o, int b, int L, bool is_b, std::vector
     if (li == lj) diag[((size_t)li << (2 * sh)) + ii + ((size_t)jj << sh)] += v;
     else if (li == lj + 1) low[((size_t)lj << (2 * sh)) + ii + ((size_t)jj << sh)] += v;
   };
-  if (o->kind == FEAST_STORAGE_CSR) {
-    for (int i = 0; i < n; ++i)
-      for (int k = o->row_ptr[i]; k < o->row_ptr[i + 1]; ++k) put(i, o->col_idx[k], o->values[k]);
+  if (o->kind == FEAST_STORAGE_CSR) {  // row i writes only layer i/b's diagonal and lower blocks
+    parallel_rows(n, b, [&](int r0, int r1) {
+      for (int i = r0; i < r1; ++i)
+        for (int k = o->row_ptr[i]; k < o->row_ptr[i + 1]; ++k) put(i, o->col_idx[k], o->values[k]);
+    });
   } else if (o->kind == FEAST_STORAGE_BLOCKTRI) {  // re-block (lower triangle suffices)
     const int bo = o->bsize;
     for (int l = 0; l < o->nblocks; ++l) {
@@ -511,7 +587,9 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
   c->factored = false;
   c->mcap = 0;
   c->n = n;
+  trace_mark(c, "set_pencil: storage choice");
   c->norm_a1 = norm_one(a);
+  trace_mark(c, "set_pencil: norm_1(A)");
   if (bsz) {
     c->blocktri = true;
     c->b = bsz;
@@ -520,16 +598,9 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
     std::vector<double> ad, al, bd, bl;
     to_blocktri(a, bsz, c->L, false, ad, al);
     to_blocktri(b, bsz, c->L, true, bd, bl);
-    std::vector<double2> pd(ad.size()), pl(al.size());
-    for (size_t i = 0; i < ad.size(); ++i) pd[i] = make_double2(ad[i], bd[i]);
-    for (size_t i = 0; i < al.size(); ++i) pl[i] = make_double2(al[i], bl[i]);
-    trace_mark(c, "set_pencil: storage choice + re-block");
-    c->abdiag.ensure(pd.size());
-    c->ablow.ensure(std::max<size_t>(pl.size(), 1));
-    CK(cudaMemcpyAsync(c->abdiag.p, pd.data(), sizeof(double2) * pd.size(), cudaMemcpyHostToDevice, c->stream));
-    if (!pl.empty())
-      CK(cudaMemcpyAsync(c->ablow.p, pl.data(), sizeof(double2) * pl.size(), cudaMemcpyHostToDevice, c->stream));
-    // plain real copies [diag blocks | lower blocks] for the operator applies (bt_apply)
+    trace_mark(c, "set_pencil: re-block A, B");
+    // plain real copies [diag blocks | lower blocks] for the operator applies (bt_apply); the
+    // interleaved (A, B) pairs of the factorisation are packed from them on the device
     const size_t nd = ad.size(), nl = al.size();
     c->A.ensure(nd + nl);
     c->Bm.ensure(nd + nl);
@@ -539,6 +610,10 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
       CK(cudaMemcpyAsync(c->A.p + nd, al.data(), sizeof(double) * nl, cudaMemcpyHostToDevice, c->stream));
       CK(cudaMemcpyAsync(c->Bm.p + nd, bl.data(), sizeof(double) * nl, cudaMemcpyHostToDevice, c->stream));
     }
+    c->abdiag.ensure(nd);
+    c->ablow.ensure(std::max<size_t>(nl, 1));
+    CK(interleave_pairs(c->A.p, c->Bm.p, nd, c->abdiag.p, c->stream));
+    if (nl) CK(interleave_pairs(c->A.p + nd, c->Bm.p + nd, nl, c->ablow.p, c->stream));
     sync(c);
     trace_mark(c, "set_pencil: alloc + H2D");
   } else {
@@ -617,6 +692,7 @@ void plan_batch(feast_gpu_ctx* c) {
   }
   size_t fr = 0, tot = 0;
   CK(cudaMemGetInfo(&fr, &tot));
+  fr += pool_spare(c->device);
   const size_t have = c->sinv.n * sizeof(double2) + c->lu.n * sizeof(double2);  // already ours
   const size_t avail = (size_t)(0.8 * (double)(fr + have));
   const size_t per = factor_bytes_per_node(c);
@@ -821,7 +897,51 @@ void upload_block(feast_gpu_ctx* c, const double* host, int m, double* dev) {
   CK(cudaMemcpy2DAsync(dev, sizeof(double) * c->npad, host, sizeof(double) * c->n, sizeof(double) * c->n, m,
                        cudaMemcpyHostToDevice, c->stream));
 }
+// Process-wide pinned staging buffer for large result downloads: the DMA into page-locked
+// memory runs at link speed and the copy into the caller's pageable block is spread over host
+// threads (pageable cudaMemcpy measured 4 GB/s on the result blocks; pinning the caller's
+// memory per call with cudaHostRegister was slower still). Grown on demand, kept for reuse.
+struct PinnedStage {
+  std::mutex mu;
+  double* p = nullptr;
+  size_t n = 0;
+  double* get(size_t count) {
+    if (count > n) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      n = 0;
+      if (cudaMallocHost(reinterpret_cast<void**>(&p), sizeof(double) * count) != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+        return nullptr;
+      }
+      n = count;
+    }
+    return p;
+  }
+};
+PinnedStage& pinned_stage() {
+  static PinnedStage* s = new PinnedStage();  // never destroyed: may be used until exit
+  return *s;
+}
+
 void download_block(feast_gpu_ctx* c, const double* dev, int m, double* host) {
+  const size_t cnt = (size_t)c->n * m;
+  if (cnt * sizeof(double) >= (8u << 20)) {
+    PinnedStage& ps = pinned_stage();
+    std::lock_guard<std::mutex> lk(ps.mu);
+    if (double* st = ps.get(cnt)) {
+      CK(cudaMemcpy2DAsync(st, sizeof(double) * c->n, dev, sizeof(double) * c->npad, sizeof(double) * c->n, m,
+                           cudaMemcpyDeviceToHost, c->stream));
+      sync(c);
+      const size_t chunk = (cnt + 7) / 8;
+      std::vector<std::thread> th;
+      for (size_t off = 0; off < cnt; off += chunk)
+        th.emplace_back([=] { std::memcpy(host + off, st + off, sizeof(double) * std::min(chunk, cnt - off)); });
+      for (auto& t : th) t.join();
+      return;
+    }
+  }
   CK(cudaMemcpy2DAsync(host, sizeof(double) * c->n, dev, sizeof(double) * c->npad, sizeof(double) * c->n, m,
                        cudaMemcpyDeviceToHost, c->stream));
 }
@@ -924,6 +1044,8 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
       CK(gather_columns(c->X.p, c->npad, c->npad, c->keep.p, k, c->Q.p, c->npad, c->stream));
     }
     trace_mark(c, "finalize: gather");
+    // (pinning the caller's blocks with cudaHostRegister for these copies measured slower:
+    // 13.4 vs 10.2 ms for 41 MB at config 2, the registration costs more than it saves)
     if (out->eigenvectors && k) download_block(c, c->Q.p, k, out->eigenvectors);
     if (out->subspace) download_block(c, c->X.p, rr.mo, out->subspace);
     trace_mark(c, "finalize: D2H eigenvectors + subspace");
@@ -1010,6 +1132,7 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
 
 template <typename F>
 int guarded(feast_gpu_ctx* c, F&& f) {
+  AllocStream as(c ? c->stream : nullptr);
   try {
     if (c) CK(cudaSetDevice(c->device));
     f();
@@ -1040,6 +1163,13 @@ int feast_gpu_create(int device, void* stream, feast_gpu_ctx** out) {
   if (device < 0 || device >= ndev) return FEAST_EINPUT;
   auto* c = new feast_gpu_ctx();
   c->device = device;
+  {
+    cudaMemPool_t pool;
+    if (cudaSetDevice(device) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   if (const char* t = std::getenv("FEAST_TRACE")) c->trace = std::atoi(t);
   const int rc = guarded(c, [&] {
     if (stream) {
@@ -1061,14 +1191,17 @@ int feast_gpu_create(int device, void* stream, feast_gpu_ctx** out) {
 void feast_gpu_destroy(feast_gpu_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  if (c->aux) cudaStreamSynchronize(c->aux);
   cudaStreamSynchronize(c->stream);
+  AllocStream as(c->stream);
   for (DevBuf<double>* d : {&c->A, &c->Bm, &c->Y, &c->Q, &c->X, &c->AQ, &c->BQ, &c->T, &c->gw, &c->Aq, &c->Bq,
                             &c->Cm, &c->Lm, &c->Phi, &c->Ev, &c->Vm, &c->S, &c->Tm, &c->Dv})
     d->release();
   for (DevBuf<double2>* d : {&c->abdiag, &c->ablow, &c->dz, &c->dcoeff, &c->sinv, &c->gfac, &c->hfac, &c->lu, &c->dinv,
-                             &c->scratch, &c->W})
+                             &c->scratch, &c->W, &c->fwork})
     d->release();
-  for (DevBuf<int>* d : {&c->ipiv, &c->perm, &c->status, &c->keep}) d->release();
+  for (DevBuf<int>* d : {&c->ipiv, &c->perm, &c->status, &c->keep, &c->fiwork}) d->release();
+  cudaStreamSynchronize(c->stream);  // the frees above are stream-ordered
   if (c->eig) eig_destroy(c->eig);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);

@@ -145,6 +145,9 @@ cudaError_t residual_sums(int n, int m, const double* ax, const double* bx, cons
 // mt19937_64(seed) stream mapped to [-1, 1) column by column, bit-identical to the host
 cudaError_t random_block_device(uint64_t seed, int n, int m, double* out, int ld, cudaStream_t st);
 
+// out[i] = (a[i], b[i]): the interleaved (A, B) pairs of the block-tridiagonal factorisation
+cudaError_t interleave_pairs(const double* a, const double* b, size_t n, double2* out, cudaStream_t st);
+
 // misc
 cudaError_t fill_zero(double* p, size_t count, cudaStream_t st);
 cudaError_t gather_columns(const double* src, int ld, int n, const int* idx, int m, double* dst,

@@ -194,6 +194,19 @@ __global__ void __launch_bounds__(320) mt64_block_kernel(uint64_t seed, int n, i
   }
 }
 
+__global__ void interleave_pairs_kernel(const double* __restrict__ a, const double* __restrict__ b, size_t n,
+                                        double2* __restrict__ out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    out[i] = make_double2(a[i], b[i]);
+}
+
+cudaError_t interleave_pairs(const double* a, const double* b, size_t n, double2* out, cudaStream_t st) {
+  if (!n) return cudaSuccess;
+  interleave_pairs_kernel<<<(unsigned)std::min<size_t>((n + 255) / 256, 148 * 8), 256, 0, st>>>(a, b, n, out);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 cudaError_t random_block_device(uint64_t seed, int n, int m, double* out, int ld, cudaStream_t st) {
   if (n <= 0 || m <= 0) return cudaSuccess;
   mt64_block_kernel<<<1, 320, 0, st>>>(seed, n, m, out, ld);
