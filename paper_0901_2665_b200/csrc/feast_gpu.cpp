@@ -262,7 +262,10 @@ void ensure_workspace(feast_gpu_ctx* c, int m) {
   c->AQ.ensure(2 * nv);  // [AQ | BQ] adjacent: one Q^T [AQ | BQ] GEMM forms both projections
   c->BQ.p = c->AQ.p + nv;
   c->BQ.n = 0;
-  c->T.ensure(2 * nv * own);  // doubles; complex-mode dense shim reuses it as double2
+  // doubles; the dense path's complex-mode shim reuses it as double2 (2 nv per slot), the
+  // block-tridiagonal path needs the real terms only (nv per slot: 6.4 GB saved per node slot
+  // at config 5, the difference between one and two resident node slots on 180 GB)
+  c->T.ensure((c->blocktri ? 1 : 2) * nv * own);
   c->W.ensure(nv * own);
   const size_t mm = (size_t)m * m;
   ensure_reduced(c, m);
