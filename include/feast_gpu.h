@@ -172,6 +172,13 @@ int feast_gpu_solve_shift(feast_gpu_ctx* ctx, int e, double* rhs, int m, int mod
 /* accumulate_subspace_real: Q = -sum_e Re(c_e (z_e B - A)^{-1} Y), Y and Q n*m real. */
 int feast_gpu_contour_pass(feast_gpu_ctx* ctx, const double* y, int m, double* q);
 
+/* accumulate_subspace_hermitian (core.hpp:190-215): q (n*m complex) = -sum_e (w_e r / 4)
+ * (e^{i theta_e} G_e + e^{-i theta_e} G_e^H) y for a complex block y (n*m, interleaved), on the
+ * prepared factors, nodes summed in ascending e (+ allreduce across ranks). For the real
+ * symmetric pencils this path holds, G^H y = conj(G conj(y)): one complex solve of [Re y | Im y]
+ * per node gives both terms. */
+int feast_gpu_contour_pass_hermitian(feast_gpu_ctx* ctx, const double* y, int m, double* q);
+
 /* rayleigh_ritz on Q (n*m real): Ritz values (ascending, m_out of them) and Ritz
  * vectors X (n*m_out). truncated = spectral-truncation fallback was used. */
 int feast_gpu_rayleigh_ritz(feast_gpu_ctx* ctx, const double* q, int m, double* eigenvalues,

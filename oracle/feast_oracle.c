@@ -519,6 +519,9 @@ typedef struct {
   int n, m, threads, wid, banded, rc;
   double* terms;  /* ne * n*m */
   int prepare;
+  const double* yc; /* hermitian: complex block (interleaved n*m) */
+  double* tc;       /* hermitian: complex terms ne * 2n*m */
+  int herm;
 } work_t;
 
 static void* point_worker(void* arg) {
@@ -528,6 +531,28 @@ static void* point_worker(void* arg) {
     if (w->prepare) {
       int rc = shift_prepare(w->A, w->B, w->c->z[e], w->banded, &w->sys[e]);
       if (rc && !w->rc) w->rc = rc;
+      continue;
+    }
+    if (w->herm) {
+      /* accumulate_subspace_hermitian core.hpp:198-210: the Normal and the ConjTranspose solve
+         on the same factorisation, term = c1 s1 + c2 s2 with c1,2 = (w r / 4) e^{+-i theta} */
+      const size_t nm = (size_t)n * m;
+      cplx* s1 = malloc(sizeof(cplx) * nm);
+      cplx* s2 = malloc(sizeof(cplx) * nm);
+      for (size_t k = 0; k < nm; ++k) s1[k] = s2[k] = CMPLX(w->yc[2 * k], w->yc[2 * k + 1]);
+      shift_solve(&w->sys[e], s1, m, 0);
+      shift_solve(&w->sys[e], s2, m, 1);
+      const double pref = 0.25 * w->c->weight[e] * w->c->radius;
+      const cplx c1 = CMPLX(pref * cos(w->c->theta[e]), pref * sin(w->c->theta[e]));
+      const cplx c2 = CMPLX(pref * cos(w->c->theta[e]), -pref * sin(w->c->theta[e]));
+      double* term = w->tc + (size_t)e * 2 * nm;
+      for (size_t k = 0; k < nm; ++k) {
+        const cplx t = c1 * s1[k] + c2 * s2[k];
+        term[2 * k] = creal(t);
+        term[2 * k + 1] = cimag(t);
+      }
+      free(s1);
+      free(s2);
       continue;
     }
     /* accumulate_subspace_real core.hpp:170-180 */
@@ -582,6 +607,24 @@ static void accumulate(const op_t* A, const contour_t* c, shift_t* sys, const do
   for (int e = 0; e < c->ne; ++e)
     for (size_t k = 0; k < (size_t)n * m; ++k) q[k] -= p.terms[(size_t)e * n * m + k];
   free(p.terms);
+}
+
+/* accumulate_subspace_hermitian core.hpp:190-215 (ascending e reduction of the terms) */
+static void accumulate_herm(const op_t* A, const contour_t* c, shift_t* sys, const double* yc, int m, int threads,
+                            double* qc) {
+  const int n = A->n;
+  const size_t nm2 = 2 * (size_t)n * m;
+  work_t p = {0};
+  p.c = c; p.A = A; p.sys = sys; p.yc = yc; p.n = n; p.m = m; p.herm = 1;
+  p.tc = malloc(sizeof(double) * (size_t)c->ne * nm2);
+  run_points(&p, threads);
+  memset(qc, 0, sizeof(double) * nm2);
+  for (int e = 0; e < c->ne; ++e)
+    for (size_t k = 0; k < nm2; k += 2) {  /* complex subtraction, component-wise */
+      qc[k] -= p.tc[(size_t)e * nm2 + k];
+      qc[k + 1] -= p.tc[(size_t)e * nm2 + k + 1];
+    }
+  free(p.tc);
 }
 
 /* ---------------------------------------------------------------- reduced problem */
@@ -912,6 +955,25 @@ int ref_accumulate_real(const feast_operator_t* a, const feast_operator_t* b, do
   sys = calloc(ne, sizeof(shift_t));
   if ((rc = prepare_all(&A, &B, &c, threads, sys))) goto out;
   accumulate(&A, &c, sys, y, m, threads, q);
+out:
+  if (sys) { for (int e = 0; e < ne; ++e) shift_free(&sys[e]); free(sys); }
+  op_free(&A);
+  op_free(&B);
+  return rc;
+}
+
+int ref_accumulate_hermitian(const feast_operator_t* a, const feast_operator_t* b, double emin, double emax,
+                             int ne, const double* y, int m, double* q, int threads) {
+  op_t A, B;
+  contour_t c;
+  shift_t* sys = NULL;
+  int rc;
+  memset(&A, 0, sizeof A);
+  memset(&B, 0, sizeof B);
+  if ((rc = op_from(a, &A)) || (rc = op_from(b, &B)) || (rc = build_contour(emin, emax, ne, &c))) goto out;
+  sys = calloc(ne, sizeof(shift_t));
+  if ((rc = prepare_all(&A, &B, &c, threads, sys))) goto out;
+  accumulate_herm(&A, &c, sys, y, m, threads, q);
 out:
   if (sys) { for (int e = 0; e < ne; ++e) shift_free(&sys[e]); free(sys); }
   op_free(&A);

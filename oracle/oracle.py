@@ -49,6 +49,8 @@ def lib(kind="reference"):
     L.ref_random_block.argtypes = [C.c_int, C.c_int, C.c_uint64, _dp]
     L.ref_build_contour.argtypes = [C.c_double, C.c_double, C.c_int, _dp, _dp, _dp, _dp, _dp]
     L.ref_gauss_legendre.argtypes = [C.c_int, _dp, _dp]
+    L.ref_accumulate_hermitian.argtypes = [_op, _op, C.c_double, C.c_double, C.c_int, _dp, C.c_int, _dp,
+                                           C.c_int]
     L.ref_accumulate_real.argtypes = [_op, _op, C.c_double, C.c_double, C.c_int, _dp, C.c_int,
                                       _dp, C.c_int]
     L.ref_shift_solve.argtypes = [_op, _op, C.c_double, C.c_double, _dp, C.c_int, C.c_int]
@@ -116,6 +118,17 @@ def accumulate_real(a, b, emin, emax, ne, y, threads=1, kind="reference"):
     ca, cb = a.to_c(), b.to_c()
     _check(L, L.ref_accumulate_real(C.byref(ca), C.byref(cb), emin, emax, ne, abi.dptr(y),
                                     y.shape[1], abi.dptr(q), threads))
+    return q
+
+
+def accumulate_hermitian(a, b, emin, emax, ne, y, threads=1, kind="reference"):
+    """accumulate_subspace_hermitian (core.hpp:190-215): y, Q complex n x m."""
+    L = lib(kind)
+    y = np.asfortranarray(y, dtype=np.complex128)
+    q = np.zeros_like(y, order="F")
+    ca, cb = a.to_c(), b.to_c()
+    _check(L, L.ref_accumulate_hermitian(C.byref(ca), C.byref(cb), emin, emax, ne, y.ctypes.data_as(_dp),
+                                         y.shape[1], q.ctypes.data_as(_dp), threads))
     return q
 
 

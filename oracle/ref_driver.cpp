@@ -185,6 +185,30 @@ int ref_accumulate_real(const feast_operator_t* a, const feast_operator_t* b, do
   }
 }
 
+// accumulate_subspace_hermitian (core.hpp:190-215) with the default DirectSolver; y, q complex.
+int ref_accumulate_hermitian(const feast_operator_t* a, const feast_operator_t* b, double emin,
+                             double emax, int ne, const double* y, int m, double* q, int threads) {
+  try {
+    const auto ra = to_ref(a);
+    const auto rb = to_ref(b);
+    const auto contour = feast::quadrature::build_contour(feast::SearchInterval(emin, emax), ne);
+    feast::DirectSolver<double> solver(ra, rb);
+    std::vector<std::unique_ptr<feast::ShiftSystem>> keep(ne);
+    std::vector<const feast::ShiftSystem*> sys(ne);
+    for (int e = 0; e < ne; ++e) {
+      keep[e] = solver.prepare(contour.points[e].z);
+      sys[e] = keep[e].get();
+    }
+    DenseMatrix<cplx> yy(ra.n(), m);
+    std::memcpy(yy.data().data(), y, sizeof(cplx) * (size_t)ra.n() * m);
+    const auto qq = feast::accumulate_subspace_hermitian(yy, contour, sys, threads);
+    std::memcpy(q, qq.data().data(), sizeof(cplx) * (size_t)ra.n() * m);
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+
 // ShiftSystem::solve_in_place at shift z for the DirectSolver of (A, B).
 int ref_shift_solve(const feast_operator_t* a, const feast_operator_t* b, double zr, double zi,
                     double* rhs, int m, int mode) {

@@ -806,6 +806,51 @@ void contour_pass(feast_gpu_ctx* c, int m) {
   }
 }
 
+// accumulate_subspace_hermitian (core.hpp:190-215) for the real symmetric pencils this path
+// holds: (z B - A)^H = conj(z B - A), so the ConjTranspose solve is conj(G conj(Y)) and ONE
+// complex-mode solve of the 2m columns [Yr | Yi] per node gives both (hermitian_terms). Input
+// c->Y = [Yr | Yi] (npad x 2m real); output Q complex (npad x m) in c->AQ. Same node order,
+// node batches and allreduce as contour_pass.
+void contour_pass_hermitian(feast_gpu_ctx* c, int m) {
+  join_aux(c);
+  const int own = c->owned();
+  const int m2 = 2 * m;
+  double2* qc = reinterpret_cast<double2*>(c->AQ.p);
+  if (own > 0) {
+    const int nbt = c->wnodes();
+    for (int s0 = 0; s0 < own; s0 += nbt) {
+      const int cnt = std::min(nbt, own - s0);
+      if (c->res0 != s0 || c->rescnt != cnt) factor_range(c, s0, cnt);
+      if (c->blocktri && bt_panel_rows(c->b) > 0) {  // real input, complex output (mode 2)
+        BtSweepArgs a{c->L, c->b, cnt, m2, c->npad, c->ablow.p, c->dz.p + s0, c->dcoeff.p + s0, c->sinv.p,
+                      c->gfac.p, c->hfac.p, c->Y.p, nullptr, c->W.p, 2, c->kmid};
+        CK(bt_sweep(a, c->stream));
+      } else {
+        CK(real_to_complex_slots(c->Y.p, c->npad, m2, cnt, c->W.p, c->stream));
+        if (c->blocktri) {
+          BtSweepArgs a{c->L, c->b, cnt, m2, c->npad, c->ablow.p, c->dz.p + s0, c->dcoeff.p + s0, c->sinv.p,
+                        c->gfac.p, c->hfac.p, nullptr, nullptr, c->W.p, 1, c->kmid};
+          CK(bt_sweep(a, c->stream));
+        } else {
+          DenseSolveArgs a{c->n, cnt, m2, c->npad, c->lu.p, c->perm.p, c->dinv.p, c->dcoeff.p + s0, nullptr, c->T.p,
+                           c->W.p, 1};
+          CK(dense_solve(a, c->stream));
+        }
+      }
+      CK(hermitian_terms(c->W.p, cnt, c->npad, c->npad, m, c->dcoeff.p + s0, qc, s0 > 0, c->stream));
+    }
+  } else {
+    CK(fill_zero(c->AQ.p, 2 * (size_t)c->npad * m, c->stream));
+  }
+  if (c->nranks > 1) {
+    NcclApi& api = nccl();
+    if (!api.allReduce) fail(FEAST_ENCCL, "NCCL not available");
+    const int r = api.allReduce(c->AQ.p, c->AQ.p, 2 * (size_t)c->npad * m, kNcclFloat64, kNcclSum, c->comm,
+                                c->stream);
+    if (r != 0) fail(FEAST_ENCCL, std::string("ncclAllReduce: ") + (api.getErrorString ? api.getErrorString(r) : "?"));
+  }
+}
+
 void apply_op(feast_gpu_ctx* c, int which, const double* x, double* y, int m) {
   if (c->blocktri) {
     const double* base = which ? c->Bm.p : c->A.p;
@@ -1337,6 +1382,27 @@ int feast_gpu_contour_pass(feast_gpu_ctx* c, const double* y, int m, double* q) 
     upload_block(c, y, m, c->Y.p);
     contour_pass(c, m);
     download_block(c, c->Q.p, m, q);
+    sync(c);
+  });
+}
+
+int feast_gpu_contour_pass_hermitian(feast_gpu_ctx* c, const double* y, int m, double* q) {
+  return guarded(c, [&] {
+    if (!c->factored) fail(FEAST_EINPUT, "feast_gpu: factors not prepared");
+    if (m < 1) fail(FEAST_EINPUT, "contour_pass_hermitian: no columns");
+    ensure_workspace(c, 2 * m);
+    const int n = c->n;
+    std::vector<double> ri((size_t)n * 2 * m);  // [Re Y | Im Y]
+    for (int j = 0; j < m; ++j)
+      for (int i = 0; i < n; ++i) {
+        const size_t k = (size_t)i + (size_t)j * n;
+        ri[k] = y[2 * k];
+        ri[k + (size_t)n * m] = y[2 * k + 1];
+      }
+    upload_block(c, ri.data(), 2 * m, c->Y.p);
+    contour_pass_hermitian(c, m);
+    CK(cudaMemcpy2DAsync(q, sizeof(double2) * n, c->AQ.p, sizeof(double2) * c->npad, sizeof(double2) * n, m,
+                         cudaMemcpyDeviceToHost, c->stream));
     sync(c);
   });
 }

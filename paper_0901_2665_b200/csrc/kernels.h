@@ -148,6 +148,12 @@ cudaError_t random_block_device(uint64_t seed, int n, int m, double* out, int ld
 // out[i] = (a[i], b[i]): the interleaved (A, B) pairs of the block-tridiagonal factorisation
 cudaError_t interleave_pairs(const double* a, const double* b, size_t n, double2* out, cudaStream_t st);
 
+// accumulate_subspace_hermitian for real symmetric pencils (misc.cu): complex right-hand
+// sides [Yr | Yi] into every node slot, then Q -= sum_s c1 G Y + c2 G^H Y in ascending s
+cudaError_t real_to_complex_slots(const double* y, int64_t ld, int64_t m, int nodes, double2* w, cudaStream_t st);
+cudaError_t hermitian_terms(const double2* w, int nodes, int64_t ld, int n, int m, const double2* coeff,
+                            double2* q, int accumulate, cudaStream_t st);
+
 // misc
 cudaError_t fill_zero(double* p, size_t count, cudaStream_t st);
 cudaError_t gather_columns(const double* src, int ld, int n, const int* idx, int m, double* dst,

@@ -207,6 +207,65 @@ cudaError_t interleave_pairs(const double* a, const double* b, size_t n, double2
   return cudaGetLastError();
 }
 
+// W_s(i, j) = (Y(i, j), 0) for every node slot s < nodes, i < n (ld ld), j < m
+__global__ void real_to_complex_slots_kernel(const double* __restrict__ y, int64_t n, int64_t m, int64_t ld,
+                                             int nodes, double2* __restrict__ w) {
+  const int64_t per = ld * m;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < per * nodes;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = idx % per;
+    w[idx] = make_double2(y[k], 0.0);
+  }
+}
+
+cudaError_t real_to_complex_slots(const double* y, int64_t ld, int64_t m, int nodes, double2* w, cudaStream_t st) {
+  const int64_t total = ld * m * nodes;
+  if (!total) return cudaSuccess;
+  real_to_complex_slots_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st>>>(
+      y, ld, m, ld, nodes, w);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// accumulate_subspace_hermitian's reduction (core.hpp:198-214) for real symmetric pencils: node
+// slot s holds W_s = G_s [Yr | Yi] (ld x 2m complex). With W1 = W_s(:, j), W2 = W_s(:, m + j):
+//   s1 = G Y = W1 + i W2,  s2 = G^H Y = conj(G conj Y) = conj(W1) + i conj(W2)
+//   Q -= c1 s1 + c2 s2,    c1 = coeff_s / 2, c2 = conj(coeff_s) / 2   (coeff = w r e^{i theta} / 2)
+// summed over s in ascending order (accumulate: continue Q from an earlier node batch)
+__global__ void hermitian_terms_kernel(const double2* __restrict__ w, int nodes, int64_t ld, int n, int m,
+                                       const double2* __restrict__ coeff, double2* __restrict__ q,
+                                       int accumulate) {
+  const int64_t total = (int64_t)n * m;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx % n, j = idx / n;
+    double2 acc = accumulate ? q[i + j * ld] : make_double2(0.0, 0.0);
+    for (int s = 0; s < nodes; ++s) {
+      const double2* ws = w + (int64_t)s * ld * 2 * m;
+      const double2 w1 = ws[i + j * ld], w2 = ws[i + (j + m) * ld];
+      const double2 s1 = make_double2(w1.x - w2.y, w1.y + w2.x);   // W1 + i W2
+      const double2 s2 = make_double2(w1.x + w2.y, -w1.y + w2.x);  // conj(W1) + i conj(W2)
+      const double2 cf = coeff[s];
+      const double2 c1 = make_double2(0.5 * cf.x, 0.5 * cf.y), c2 = make_double2(0.5 * cf.x, -0.5 * cf.y);
+      const double2 t1 = cmul(c1, s1), t2 = cmul(c2, s2);
+      const double2 term = make_double2(t1.x + t2.x, t1.y + t2.y);
+      acc.x -= term.x;
+      acc.y -= term.y;
+    }
+    q[i + j * ld] = acc;
+  }
+}
+
+cudaError_t hermitian_terms(const double2* w, int nodes, int64_t ld, int n, int m, const double2* coeff,
+                            double2* q, int accumulate, cudaStream_t st) {
+  const int64_t total = (int64_t)n * m;
+  if (!total) return cudaSuccess;
+  hermitian_terms_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st>>>(
+      w, nodes, ld, n, m, coeff, q, accumulate);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 cudaError_t random_block_device(uint64_t seed, int n, int m, double* out, int ld, cudaStream_t st) {
   if (n <= 0 || m <= 0) return cudaSuccess;
   mt64_block_kernel<<<1, 320, 0, st>>>(seed, n, m, out, ld);

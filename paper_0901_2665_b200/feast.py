@@ -83,6 +83,7 @@ def load_library(path: str = LIB_PATH):
     L.feast_gpu_set_node_batch.argtypes = [C.c_void_p, C.c_int]
     L.feast_gpu_solve_shift.argtypes = [C.c_void_p, C.c_int, _dp, C.c_int, C.c_int]
     L.feast_gpu_contour_pass.argtypes = [C.c_void_p, _dp, C.c_int, _dp]
+    L.feast_gpu_contour_pass_hermitian.argtypes = [C.c_void_p, _dp, C.c_int, _dp]
     L.feast_gpu_rayleigh_ritz.argtypes = [C.c_void_p, _dp, C.c_int, _dp, _dp, _ip, _ip]
     L.feast_gpu_reduced_gevp.argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp, _dp, _ip, _ip]
     L.feast_gpu_residuals.argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp, _ip, _dp]
@@ -103,6 +104,7 @@ EXPORTED_SYMBOLS = [
     "feast_gpu_rayleigh_ritz", "feast_gpu_reduced_gevp", "feast_gpu_residuals", "feast_gpu_solve",
     "feast_gpu_bench_init", "feast_gpu_bench_passes", "feast_gpu_launch_count",
     "feast_gpu_set_node_batch", "feast_gpu_storage", "feast_gpu_random_block",
+    "feast_gpu_contour_pass_hermitian",
 ]
 
 
@@ -262,6 +264,14 @@ class GpuContext:
         y = np.asfortranarray(y, dtype=np.float64)
         q = np.zeros_like(y, order="F")
         self._check(self.L.feast_gpu_contour_pass(self.h, abi.dptr(y), y.shape[1], abi.dptr(q)))
+        return q
+
+    def contour_pass_hermitian(self, y: np.ndarray) -> np.ndarray:
+        """accumulate_subspace_hermitian (core.hpp:190-215): complex y -> complex Q."""
+        y = np.asfortranarray(y, dtype=np.complex128)
+        q = np.zeros_like(y, order="F")
+        self._check(self.L.feast_gpu_contour_pass_hermitian(self.h, y.ctypes.data_as(_dp), y.shape[1],
+                                                            q.ctypes.data_as(_dp)))
         return q
 
     def rayleigh_ritz(self, q: np.ndarray):

@@ -326,3 +326,45 @@ def test_contour_pass_small_blocks(F, monkeypatch, twist, L, b):
 def test_device_random_block_bit_identical(ctx, n, m, seed):
     y = ctx.random_block(n, m, seed)
     assert np.array_equal(y, O.random_block(n, m, seed))
+
+
+# accumulate_subspace_hermitian (core.hpp:190-215) on the device: Normal and ConjTranspose
+# solves combined per node, ascending e, against the reference itself; every storage route
+# (dense LU, small-block twisted sweep, large-block panel sweep) and the streamed node batches
+@pytest.mark.parametrize("case", ["small_dense_n60", "cfg1_n256", "bt_L16_b32", "cfg2_n2048", "panel_L3_b128",
+                                  "streamed_bt_L16_b32"])
+def test_contour_pass_hermitian_matches_reference(F, case):
+    from paper_0901_2665_b200 import problems as P
+    if case == "panel_L3_b128":
+        a, b = P.blocktri_operators(3, 128, seed=77)
+        emin, emax, ne, n = -0.3, 0.4, 8, 3 * 128
+    else:
+        prob, _ = load_fixture([p for p in FIX if case.replace("streamed_", "") in p][0])
+        a, b, emin, emax, ne, n = prob.a, prob.b, prob.emin, prob.emax, prob.n_e, prob.n
+    rng = np.random.default_rng(13)
+    y = rng.standard_normal((n, 6)) + 1j * rng.standard_normal((n, 6))
+    c = F.GpuContext(0)
+    try:
+        if case.startswith("streamed"):
+            c.set_node_batch(3)
+        c.set_pencil(a, b)
+        c.prepare(emin, emax, ne)
+        q = c.contour_pass_hermitian(y)
+    finally:
+        c.close()
+    qr = O.accumulate_hermitian(a, b, emin, emax, ne, y)
+    assert np.max(np.abs(q - qr)) <= 1e-11 * max(1.0, float(np.max(np.abs(qr))))
+
+
+def test_contour_pass_hermitian_equals_real_on_real_blocks(ctx):
+    # test_core.cpp:111-142 on the device: a real block through the Hermitian accumulation
+    # reproduces the real accumulation, imaginary part at round-off
+    prob, _ = load_fixture([p for p in FIX if "bt_L16_b32" in p][0])
+    ctx.set_pencil(prob.a, prob.b)
+    ctx.prepare(prob.emin, prob.emax, prob.n_e)
+    y = O.random_block(prob.n, 8, 4)
+    qh = ctx.contour_pass_hermitian(y + 0j)
+    qr = ctx.contour_pass(y)
+    scale = max(1.0, float(np.max(np.abs(qr))))
+    assert np.max(np.abs(qh.real - qr)) <= 1e-13 * scale
+    assert np.max(np.abs(qh.imag)) <= 1e-13 * scale

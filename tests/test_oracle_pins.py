@@ -117,6 +117,35 @@ def test_centered_singleton_accumulation(kind):
 
 
 @pytest.mark.parametrize("kind", KINDS)
+def test_hermitian_accumulation_matches_real(kind):
+    # test_core.cpp:111-142: on a real symmetric pencil the Hermitian accumulation of a real
+    # block equals the real accumulation (imaginary part ~0) to 1e-13
+    from tests.golden_problems import fixtures, load_fixture
+    prob, _ = load_fixture([p for p in fixtures() if "small_dense_n60" in p][0])
+    y = O.random_block(prob.n, 7, 3)
+    qr = O.accumulate_real(prob.a, prob.b, prob.emin, prob.emax, prob.n_e, y, kind=kind)
+    qh = O.accumulate_hermitian(prob.a, prob.b, prob.emin, prob.emax, prob.n_e, y + 0j, kind=kind)
+    scale = max(1.0, float(np.max(np.abs(qr))))
+    assert np.max(np.abs(qh.real - qr)) <= 1e-13 * scale
+    assert np.max(np.abs(qh.imag)) <= 1e-13 * scale
+
+
+def test_hermitian_accumulation_restatement_matches_reference():
+    # the C restatement's accumulate_subspace_hermitian against the compiled reference, on a
+    # complex block and both storage policies (dense LU, banded LU)
+    if not (O.available("reference") and O.available("port")):
+        pytest.skip("needs both checkers")
+    from tests.golden_problems import fixtures, load_fixture
+    rng = np.random.default_rng(9)
+    for name in ("small_dense_n60", "bt_L8_b48"):
+        prob, _ = load_fixture([p for p in fixtures() if name in p][0])
+        y = rng.standard_normal((prob.n, 5)) + 1j * rng.standard_normal((prob.n, 5))
+        q0 = O.accumulate_hermitian(prob.a, prob.b, prob.emin, prob.emax, prob.n_e, y, kind="reference")
+        q1 = O.accumulate_hermitian(prob.a, prob.b, prob.emin, prob.emax, prob.n_e, y, kind="port")
+        assert np.max(np.abs(q0 - q1)) <= 1e-12 * max(1.0, float(np.max(np.abs(q0)))), name
+
+
+@pytest.mark.parametrize("kind", KINDS)
 def test_reduced_gevp_properties(kind):
     # test_linalg.cpp:272-298
     rng = np.random.default_rng(3)
