@@ -119,6 +119,11 @@ void eig_destroy(EigWork* w);
 // tridiagonal route computes vectors only for evals > vfloor * max(evals) (others zero).
 cudaError_t sym_eig(EigWork* w, int m, double* a, double* evals, double* v, cudaStream_t st,
                     double vfloor = 0.0);
+// Householder tridiagonalisation of a symmetric m x m matrix (3 <= m <= tri_tiles_max_dim())
+// on one SM with the matrix in registers: d[m], e[m-1], tau[m], reflectors in hv (m x m)
+int tri_tiles_max_dim();
+cudaError_t tridiag_tiles(int m, const double* a, double* d, double* e, double* hv, double* tau,
+                          cudaStream_t st);
 // Cholesky with relative pivot floor: L (lower, in place in `a`), status[0] = 1 on failure
 // (status must be zero on entry). dinv receives the inverses of the 32x32 diagonal tiles of
 // L (ceil(m/32) * 1024 doubles), consumed by the triangular solves.

@@ -1093,7 +1093,13 @@ cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws
   // per column at m = 192, mostly the per-column dot reductions, and measured 1.0 ms against
   // the cluster kernel's 0.8 ms (profiles/r01_summary.md)
   const bool use_rows = m > 2 && m <= 32 * TR_SL && tr_rows_smem(m) <= 226 * 1024 && rt == 'r';
-  if (use_cluster && !use_rows) {
+  // default for 3 <= m <= 192: the register-tile kernel (tridiag_tiles.cu); the letters above
+  // select the older routes for comparison
+  const bool use_tiles = m > 2 && m <= tri_tiles_max_dim() && (rt == 0 || rt == 't');
+  if (use_tiles) {
+    cudaError_t err = tridiag_tiles(m, a, d, e, hv, tau, st);
+    if (err != cudaSuccess) return err;
+  } else if (use_cluster && !use_rows) {
     const size_t ksm = tcl_smem(m);
     cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ksm);

@@ -122,6 +122,28 @@ def test_reduced_gevp_matches_reference(ctx):
         assert np.max(np.abs(phi.T @ b @ phi - np.eye(m))) <= 1e-10 * max(1, m / 50)
 
 
+@pytest.mark.parametrize("m", [3, 4, 16, 17, 33, 100, 176, 191, 192])
+def test_tridiag_tiles_route(ctx, m):
+    """The register-tile tridiagonalisation (default for 3 <= m <= 192, tridiag_tiles.cu):
+    dense, already-tridiagonal (no reflection: tau = 0 columns), diagonal and graded inputs
+    against numpy's eigh (B = I isolates the symmetric eigensolve)."""
+    rng = np.random.default_rng(100 + m)
+    dense = rng.uniform(-1, 1, (m, m)); dense = dense + dense.T
+    tri = np.diag(rng.uniform(-1, 1, m)) + np.diag(rng.uniform(-1, 1, m - 1), 1)
+    tri = tri + np.triu(tri, 1).T
+    diag = np.diag(rng.uniform(-1, 1, m))
+    q, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    graded = (q * np.logspace(-12, 0, m)) @ q.T; graded = 0.5 * (graded + graded.T)
+    for a in (dense, tri, diag, graded):
+        ev, phi, _ = ctx.reduced_gevp(a, np.eye(m))
+        ref = np.linalg.eigvalsh(a)
+        scale = max(1.0, np.max(np.abs(ref)))
+        assert np.all(np.diff(ev) >= 0)
+        assert np.max(np.abs(ev - ref)) <= 1e-13 * m * scale
+        assert np.max(np.abs(a @ phi - phi * ev)) <= 1e-13 * m * scale
+        assert np.max(np.abs(phi.T @ phi - np.eye(m))) <= 1e-13 * m
+
+
 def test_reduced_gevp_truncation_path(ctx):
     # B_Q rank deficient -> Cholesky floor fails -> spectral truncation (eigh.hpp:204-224)
     rng = np.random.default_rng(4)

@@ -1,7 +1,7 @@
 """Full-size BASELINE config 5 on one GPU: L = 2048 layers of b = 512 (N = 1,048,576),
 seed 5, M0 = 768, Ne = 16, interval from tools/cfg5_interval.py (512 eigenvalues by inertia
 count). The factors (25.8 GB per node) of 16 nodes do not fit one B200, so the streamed memory
-plan runs with node batches of FEAST_CFG5_BATCH (default 2): each pass refactors every batch
+plan runs with node batches of FEAST_CFG5_BATCH (default 1: two slots with their W/T workspaces exceed 180 GB beside the pencil and the five N x M0 blocks): each pass refactors every batch
 (the reference's low_memory trade-off). Prints one JSON line with status, count vs the inertia
 count, residuals, timings."""
 import json
@@ -24,7 +24,7 @@ t = time.perf_counter()
 prob = P.config5()
 print(f"generated {prob.name} in {time.perf_counter() - t:.0f} s, interval [{prob.emin}, {prob.emax}]", flush=True)
 ctx = F.GpuContext(0)
-ctx.set_node_batch(int(os.environ.get("FEAST_CFG5_BATCH", "2")))
+ctx.set_node_batch(int(os.environ.get("FEAST_CFG5_BATCH", "1")))
 t = time.perf_counter()
 ctx.set_pencil(prob.a, prob.b)
 t_pencil = time.perf_counter() - t
@@ -38,5 +38,5 @@ out = dict(config=prob.name, n=prob.n, m0=prob.m0, n_e=prob.n_e, status=r.status
            expected=prob.expected_count, loops=r.loops_used, max_residual=r.max_residual,
            counts=[int(x) for x in r.in_interval_counts], trace_history=[float(x) for x in r.trace_history],
            timings=r.timings.__dict__, set_pencil_s=t_pencil, solve_wall_s=t_solve,
-           node_batch=int(os.environ.get("FEAST_CFG5_BATCH", "2")))
+           node_batch=int(os.environ.get("FEAST_CFG5_BATCH", "1")))
 print(json.dumps(out), flush=True)
