@@ -294,6 +294,9 @@ cudaError_t cholesky(int m, double* a, double rel_tol, int* status, double* dinv
   // one-CTA route: FEAST_CHOL=s only (measured 336 us against the cooperative kernel's 232 us
   // at m = 192: per-slot predicates and the serial column chain keep the SM at ~0.45 IPC)
   static const char* route = std::getenv("FEAST_CHOL");
+  // default for m <= 192: one CTA, 16 x 16 tiles in shared memory, DMMA tile products
+  // (chol_tiles.cu); FEAST_CHOL=c keeps the cooperative kernel below, s the packed one-CTA one
+  if ((!route || route[0] == 't') && m <= chol_tiles_max_dim()) return chol_tiles(m, a, rel_tol, status, dinv, st);
   if (route && route[0] == 's' && m <= 32 * CS_SL && chol_sm_bytes(m) <= 226 * 1024) {
     static bool attr = false;
     if (!attr) {
@@ -408,9 +411,125 @@ __global__ void __launch_bounds__(256) trsm_tile_kernel(int m, const double* __r
   }
 }
 
+// The same solves for m <= 192 with every lower 32 x 32 tile of L resident in shared memory
+// (21 tiles + the X tile: ~200 KB): the substitution chain never waits on L2, the diagonal-tile
+// inverse of the next step is fetched into registers while the current step runs, and each
+// tile product is split over four partial sums.
+constexpr int RS_MAXB = 6;  // 32-row blocks: m <= 192
+template <bool TRANS>
+__global__ void __launch_bounds__(256) trsm_res_kernel(int m, const double* __restrict__ l,
+                                                       const double* __restrict__ dinv, double* x, int ldx,
+                                                       int ncols) {
+  extern __shared__ double rsm[];
+  double* xs = rsm;                                 // m x XC, column-major (ld m)
+  double* Ls = xs + (size_t)m * XC;                 // lower tiles, id I(I+1)/2 + J, TB x TL col-major
+  double* Ds = Ls + (size_t)RS_MAXB * (RS_MAXB + 1) / 2 * TB * TL;  // current diagonal inverse
+  double* acc_s = Ds + TB * TL;                     // TB x XC
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int c0 = blockIdx.x * XC, nc = min(XC, ncols - c0);
+  const int nblk = (m + TB - 1) / TB;
+  // every staging copy in flight at once (cp.async, zero fill outside): the tiles are ~170 KB
+  for (int idx = tid; idx < m * XC; idx += nt) {
+    const int i = idx % m, c = idx / m;
+    cp_async8z(xs + idx, x + i + (int64_t)(c0 + min(c, nc - 1)) * ldx, c < nc);
+  }
+  for (int I = 0; I < nblk; ++I)
+    for (int J = 0; J <= I; ++J) {
+      double* T = Ls + (size_t)(I * (I + 1) / 2 + J) * TB * TL;
+      for (int idx = tid; idx < TB * TB; idx += nt) {
+        const int rr = idx % TB, cc = idx / TB, gi = I * TB + rr, gj = J * TB + cc;
+        const bool ok = gi < m && gj < m;
+        cp_async8z(T + rr + cc * TL, ok ? l + gi + (int64_t)gj * m : l, ok);
+      }
+    }
+  cp_async_wait_all();
+  const int r = tid % TB, cA = tid / TB, cB = cA + 8;
+  constexpr int PER = TB * TB / 256;
+  double dn[PER];
+  auto fetch_d = [&](int bi) {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) dn[q] = dinv[(int64_t)bi * TB * TB + tid + q * 256];
+  };
+  fetch_d(TRANS ? nblk - 1 : 0);
+  __syncthreads();
+  for (int step = 0; step < nblk; ++step) {
+    const int bi = TRANS ? nblk - 1 - step : step;
+    const int i0 = bi * TB, ib = min(TB, m - i0);
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {  // Di (transposed for L^{-T}) into shared memory
+      const int idx = tid + q * 256, rr = idx % TB, cc = idx / TB;
+      if (TRANS) Ds[cc + rr * TL] = dn[q];
+      else Ds[rr + cc * TL] = dn[q];
+    }
+    if (step + 1 < nblk) fetch_d(TRANS ? bi - 1 : bi + 1);
+    double a0 = (r < ib) ? xs[(i0 + r) + cA * m] : 0.0, a1 = 0.0;
+    double b0 = (r < ib) ? xs[(i0 + r) + cB * m] : 0.0, b1 = 0.0;
+    const int jlo = TRANS ? bi + 1 : 0, jhi = TRANS ? nblk : bi;
+    for (int bj = jlo; bj < jhi; ++bj) {
+      const int j0 = bj * TB, jb = min(TB, m - j0);
+      // !TRANS: L(bi, bj)[r][k]; TRANS: L(bj, bi)[k][r]
+      const double* T = Ls + (size_t)(TRANS ? bj * (bj + 1) / 2 + bi : bi * (bi + 1) / 2 + bj) * TB * TL;
+      const double* xa = xs + j0 + cA * m;
+      const double* xb = xs + j0 + cB * m;
+      int k = 0;
+      for (; k + 1 < jb; k += 2) {
+        const double l0 = TRANS ? T[k + r * TL] : T[r + k * TL];
+        const double l1 = TRANS ? T[k + 1 + r * TL] : T[r + (k + 1) * TL];
+        a0 = fma(-l0, xa[k], a0);
+        b0 = fma(-l0, xb[k], b0);
+        a1 = fma(-l1, xa[k + 1], a1);
+        b1 = fma(-l1, xb[k + 1], b1);
+      }
+      if (k < jb) {
+        const double l0 = TRANS ? T[k + r * TL] : T[r + k * TL];
+        a0 = fma(-l0, xa[k], a0);
+        b0 = fma(-l0, xb[k], b0);
+      }
+    }
+    acc_s[r + cA * TB] = a0 + a1;
+    acc_s[r + cB * TB] = b0 + b1;
+    __syncthreads();
+    if (r < ib) {
+      double sA = 0.0, sB = 0.0, tA = 0.0, tB = 0.0;
+      int k = 0;
+      for (; k + 1 < ib; k += 2) {
+        sA = fma(Ds[r + k * TL], acc_s[k + cA * TB], sA);
+        sB = fma(Ds[r + k * TL], acc_s[k + cB * TB], sB);
+        tA = fma(Ds[r + (k + 1) * TL], acc_s[k + 1 + cA * TB], tA);
+        tB = fma(Ds[r + (k + 1) * TL], acc_s[k + 1 + cB * TB], tB);
+      }
+      if (k < ib) {
+        sA = fma(Ds[r + k * TL], acc_s[k + cA * TB], sA);
+        sB = fma(Ds[r + k * TL], acc_s[k + cB * TB], sB);
+      }
+      xs[(i0 + r) + cA * m] = sA + tA;
+      xs[(i0 + r) + cB * m] = sB + tB;
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < m * XC; idx += nt) {
+    const int i = idx % m, c = idx / m;
+    if (c < nc) x[i + (int64_t)(c0 + c) * ldx] = xs[idx];
+  }
+}
+
 template <bool TRANS>
 static cudaError_t trsm_tiles(int m, const double* l, const double* dinv, double* x, int ldx, int ncols,
                               cudaStream_t st) {
+  static const char* route = std::getenv("FEAST_TRSM");
+  if (m <= RS_MAXB * TB && !(route && route[0] == 'g')) {  // FEAST_TRSM=g: L streamed from L2
+    const size_t rs = sizeof(double) * ((size_t)m * XC + (size_t)(RS_MAXB * (RS_MAXB + 1) / 2 + 1) * TB * TL +
+                                        TB * XC);
+    static bool rattr = false;
+    if (!rattr) {
+      cudaFuncSetAttribute(trsm_res_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      cudaFuncSetAttribute(trsm_res_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      rattr = true;
+    }
+    trsm_res_kernel<TRANS><<<(ncols + XC - 1) / XC, 256, rs, st>>>(m, l, dinv, x, ldx, ncols);
+    ++g_launches;
+    return cudaGetLastError();
+  }
   const size_t sm = sizeof(double) * (size_t)m * XC;
   cudaFuncSetAttribute(trsm_tile_kernel<TRANS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   trsm_tile_kernel<TRANS><<<(ncols + XC - 1) / XC, 256, sm, st>>>(m, l, dinv, x, ldx, ncols);

@@ -208,6 +208,7 @@ struct feast_gpu_ctx {
   bool factored = false;
   int batch_req = 0, batch = 0, res0 = -1, rescnt = 0;
   DevBuf<double2> sinv, gfac, hfac, lu, dinv, scratch, fwork;
+  DevBuf<double> Aband, Bband;  // band-row copies of A, B for the applies (b <= 32; band_apply.cu)
   int kmid = -1;  // twisted block-Thomas meeting layer of the current factors (bt_twist_layer)
   DevBuf<int> ipiv, perm, status, fiwork;
   // workspaces
@@ -252,8 +253,13 @@ void ensure_reduced(feast_gpu_ctx* c, int m) {
   c->keep.ensure(m);
 }
 
+void plan_batch(feast_gpu_ctx* c, int m);
+
 void ensure_workspace(feast_gpu_ctx* c, int m) {
   if (m <= c->mcap) return;
+  // the node batch decides how many W/T slots there are: plan it for this m first (a plan made
+  // for the owned nodes before the workspaces existed would size W/T for every node)
+  if (c->have_pencil) plan_batch(c, m);
   const size_t nv = (size_t)c->npad * m;
   const int own = std::max(c->wnodes(), 1);
   c->Y.ensure(nv);
@@ -617,6 +623,16 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
     c->ablow.ensure(std::max<size_t>(nl, 1));
     CK(interleave_pairs(c->A.p, c->Bm.p, nd, c->abdiag.p, c->stream));
     if (nl) CK(interleave_pairs(c->A.p + nd, c->Bm.p + nd, nl, c->ablow.p, c->stream));
+    if (bsz <= 32) {
+      const size_t nb3 = (size_t)c->L * bsz * 3 * bsz;
+      c->Aband.ensure(nb3);
+      c->Bband.ensure(nb3);
+      CK(band_rows(c->L, bsz, c->A.p, c->A.p + nd, c->Aband.p, c->stream));
+      CK(band_rows(c->L, bsz, c->Bm.p, c->Bm.p + nd, c->Bband.p, c->stream));
+    } else {
+      c->Aband.release();
+      c->Bband.release();
+    }
     sync(c);
     trace_mark(c, "set_pencil: alloc + H2D");
   } else {
@@ -685,9 +701,11 @@ size_t factor_bytes_per_node(const feast_gpu_ctx* c) {
   return sizeof(double2) * (size_t)c->n * c->n;
 }
 
-// node batch for this context: forced (feast_gpu_set_node_batch), else all owned nodes if
-// their factors fit 80% of the free HBM, else as many as do (at least one)
-void plan_batch(feast_gpu_ctx* c) {
+// node batch for this context: forced (feast_gpu_set_node_batch), else all owned nodes if their
+// factors plus their per-slot solve workspaces (W complex, T real; sized for m right-hand sides)
+// fit 80% of the HBM left after the m-column vector blocks, else as many as do (at least one).
+// Planned before the workspaces are sized (ensure_workspace) and again at each factorisation.
+void plan_batch(feast_gpu_ctx* c, int m) {
   const int own = c->owned();
   if (c->batch_req > 0) {
     c->batch = std::min(c->batch_req, std::max(own, 1));
@@ -696,9 +714,13 @@ void plan_batch(feast_gpu_ctx* c) {
   size_t fr = 0, tot = 0;
   CK(cudaMemGetInfo(&fr, &tot));
   fr += pool_spare(c->device);
-  const size_t have = c->sinv.n * sizeof(double2) + c->lu.n * sizeof(double2);  // already ours
-  const size_t avail = (size_t)(0.8 * (double)(fr + have));
-  const size_t per = factor_bytes_per_node(c);
+  const size_t have = sizeof(double2) * (c->sinv.n + c->gfac.n + c->hfac.n + c->lu.n + c->W.n) +
+                      sizeof(double) * (c->T.n + c->Y.n + c->Q.n + c->X.n + c->AQ.n + c->gw.n);  // already ours
+  const size_t nv = (size_t)c->npad * m, mm = (size_t)m * m;
+  const size_t fixed = m > 0 ? sizeof(double) * (5 * nv + std::max<size_t>(mm * 64, nv)) : 0;  // Y Q X AQ|BQ gw
+  const size_t per = factor_bytes_per_node(c) + (m > 0 ? sizeof(double2) * nv + sizeof(double) * nv * (c->blocktri ? 1 : 2) : 0);
+  const double budget = 0.8 * (double)(fr + have) - (double)fixed;
+  const size_t avail = budget > 0.0 ? (size_t)budget : 0;
   c->batch = (size_t)own * per <= avail ? own : (int)std::max<size_t>(1, avail / per);
 }
 
@@ -753,8 +775,12 @@ void factor(feast_gpu_ctx* c) {
     return;
   }
   const int prev = c->wnodes();
-  plan_batch(c);
-  if (c->wnodes() != prev) c->mcap = 0;  // per-node workspaces follow the node slots
+  plan_batch(c, c->mcap);
+  if (c->wnodes() != prev) {  // per-node workspaces follow the node slots
+    const int m = c->mcap;
+    c->mcap = 0;
+    if (m > 0) ensure_workspace(c, m);
+  }
   factor_range(c, 0, c->wnodes());
   c->factored = true;
 }
@@ -852,13 +878,26 @@ void contour_pass_hermitian(feast_gpu_ctx* c, int m) {
 }
 
 void apply_op(feast_gpu_ctx* c, int which, const double* x, double* y, int m) {
-  if (c->blocktri) {
+  if (c->blocktri && c->b <= 32) {
+    CK(band_apply(c->L, c->b, which ? c->Bband.p : c->Aband.p, nullptr, x, c->npad, y, nullptr, c->npad, m,
+                  c->stream));
+  } else if (c->blocktri) {
     const double* base = which ? c->Bm.p : c->A.p;
     CK(bt_apply(c->L, c->b, base, base + (size_t)c->L * c->b * c->b, x, c->npad, y, c->npad, m, c->stream));
   } else {
     CK(dgemm('N', 'N', c->n, m, c->n, 1.0, which ? c->Bm.p : c->A.p, c->n, x, c->npad, 0.0, y, c->npad,
              c->gw.p, c->gw.n, c->stream));
   }
+}
+
+// A x and B x (one pass over x for small blocks)
+void apply_both(feast_gpu_ctx* c, const double* x, double* ya, double* yb, int m) {
+  if (c->blocktri && c->b <= 32) {
+    CK(band_apply(c->L, c->b, c->Aband.p, c->Bband.p, x, c->npad, ya, yb, c->npad, m, c->stream));
+    return;
+  }
+  apply_op(c, 0, x, ya, m);
+  apply_op(c, 1, x, yb, m);
 }
 
 struct Reduced {
@@ -928,12 +967,21 @@ Reduced reduced_gevp(feast_gpu_ctx* c, int m) {
 // rayleigh_ritz (core.hpp:228-240): X = Q Phi, Ritz values ascending
 Reduced rayleigh_ritz(feast_gpu_ctx* c, int m) {
   const int n = c->npad;
-  apply_op(c, 0, c->Q.p, c->AQ.p, m);
-  apply_op(c, 1, c->Q.p, c->BQ.p, m);
+  // the one-GEMM projection needs BQ right after AQ and Bq right after Aq AT THIS m: the
+  // buffers are sized for mcap columns, and m shrinks after a truncated pass (core.hpp:387)
+  c->BQ.p = c->AQ.p + (size_t)n * m;
+  c->Bq.p = c->Aq.p + (size_t)m * m;
+  apply_both(c, c->Q.p, c->AQ.p, c->BQ.p, m);
   // [Aq | Bq] = Q^T [AQ | BQ] in one GEMM (adjacent buffers; same sums as two separate ones)
-  CK(dgemm('T', 'N', m, 2 * m, n, 1.0, c->Q.p, n, c->AQ.p, n, 0.0, c->Aq.p, m, c->gw.p, c->gw.n, c->stream));
-  CK(symmetrize(c->Aq.p, m, m, c->stream));
-  CK(symmetrize(c->Bq.p, m, m, c->stream));
+  if (m % 64 == 0) {  // symmetric halves: upper tiles only (2/3 of the flops at m = 192)
+    CK(dgemm_tn_sym2(m, n, c->Q.p, n, c->AQ.p, n, c->Aq.p, c->gw.p, c->gw.n, c->stream));
+    CK(symmetrize_tiles(c->Aq.p, m, m, c->stream));
+    CK(symmetrize_tiles(c->Bq.p, m, m, c->stream));
+  } else {
+    CK(dgemm('T', 'N', m, 2 * m, n, 1.0, c->Q.p, n, c->AQ.p, n, 0.0, c->Aq.p, m, c->gw.p, c->gw.n, c->stream));
+    CK(symmetrize(c->Aq.p, m, m, c->stream));
+    CK(symmetrize(c->Bq.p, m, m, c->stream));
+  }
   Reduced r = reduced_gevp(c, m);
   CK(dgemm('N', 'N', n, r.mo, m, 1.0, c->Q.p, n, c->Phi.p, m, 0.0, c->X.p, n, c->gw.p, c->gw.n, c->stream));
   return r;
@@ -1003,8 +1051,7 @@ void residuals(feast_gpu_ctx* c, int m, const double* lam_host, const double* xd
   lam.ensure(m);
   sums.ensure(3 * (size_t)m);
   CK(cudaMemcpyAsync(lam.p, lam_host, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
-  apply_op(c, 0, xdev, c->AQ.p, m);
-  apply_op(c, 1, xdev, c->BQ.p, m);
+  apply_both(c, xdev, c->AQ.p, c->BQ.p, m);
   CK(residual_sums(c->n, m, c->AQ.p, c->BQ.p, xdev, c->npad, lam.p, sums.p, c->stream));
   std::vector<double> h(3 * (size_t)m);
   CK(cudaMemcpyAsync(h.data(), sums.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, c->stream));
@@ -1243,8 +1290,8 @@ void feast_gpu_destroy(feast_gpu_ctx* c) {
   cudaStreamSynchronize(c->stream);
   AllocStream as(c->stream);
   for (DevBuf<double>* d : {&c->A, &c->Bm, &c->Y, &c->Q, &c->X, &c->AQ, &c->BQ, &c->T, &c->gw, &c->Aq, &c->Bq,
-                            &c->Cm, &c->Lm, &c->Phi, &c->Ev, &c->Vm, &c->S, &c->Tm, &c->Dv})
-    d->release();
+                            &c->Cm, &c->Lm, &c->Phi, &c->Ev, &c->Vm, &c->S, &c->Tm, &c->Dv, &c->Aband, &c->Bband})
+    d->release();  // every buffer, before the stream goes (the destructor would free on a dead stream)
   for (DevBuf<double2>* d : {&c->abdiag, &c->ablow, &c->dz, &c->dcoeff, &c->sinv, &c->gfac, &c->hfac, &c->lu, &c->dinv,
                              &c->scratch, &c->W, &c->fwork})
     d->release();

@@ -188,6 +188,7 @@ struct DgemmArgs {
   double alpha, beta;
   int batched;     // z indexes independent problems instead of K slices
   int64_t sa, sb;  // batch strides of A and B
+  int symhalf = 0;  // > 0: C = [S1 | S2] of symmetric symhalf x symhalf halves: lower tiles skipped
 };
 
 template <bool TA, bool TB>
@@ -197,6 +198,7 @@ __global__ void __launch_bounds__(256, 2) dgemm_kernel(DgemmArgs p) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
   const int wm = warp & 1, wn = warp >> 1;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (p.symhalf && m0 / BM > (n0 % p.symhalf) / BN) return;  // mirrored by symmetrize_tiles
   const int kbeg = p.batched ? 0 : blockIdx.z * p.kslice;
   const int kend = p.batched ? p.k : min(p.k, kbeg + p.kslice);
   const int nk = (kend - kbeg + BK - 1) / BK;
@@ -322,9 +324,27 @@ static void set_attr_once() {
   }
 }
 
+static cudaError_t dgemm_impl(char ta, char tb, int m, int n, int k, double alpha, const double* A, int lda,
+                              const double* B, int ldb, double beta, double* C, int ldc, double* work,
+                              size_t work_elems, cudaStream_t st, int symhalf);
+
 cudaError_t dgemm(char ta, char tb, int m, int n, int k, double alpha, const double* A, int lda,
                   const double* B, int ldb, double beta, double* C, int ldc, double* work,
                   size_t work_elems, cudaStream_t st) {
+  return dgemm_impl(ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, work, work_elems, st, 0);
+}
+
+// [S1 | S2] = Q^T [AQ | BQ] for symmetric S1, S2 (m x m each, m a multiple of the 64-wide
+// tile): the strictly-lower tiles of each half are not computed; symmetrize_tiles fills them
+cudaError_t dgemm_tn_sym2(int m, int k, const double* Q, int ldq, const double* AB, int ldab, double* C,
+                          double* work, size_t work_elems, cudaStream_t st) {
+  if (m % dg::BM != 0 || m % dg::BN != 0) return cudaErrorInvalidValue;
+  return dgemm_impl('T', 'N', m, 2 * m, k, 1.0, Q, ldq, AB, ldab, 0.0, C, m, work, work_elems, st, m);
+}
+
+static cudaError_t dgemm_impl(char ta, char tb, int m, int n, int k, double alpha, const double* A, int lda,
+                              const double* B, int ldb, double beta, double* C, int ldc, double* work,
+                              size_t work_elems, cudaStream_t st, int symhalf) {
   if (m <= 0 || n <= 0) return cudaSuccess;
   const bool TA = ta == 'T' || ta == 't', TB = tb == 'T' || tb == 't';
   const int tiles = ((m + dg::BM - 1) / dg::BM) * ((n + dg::BN - 1) / dg::BN);
@@ -336,7 +356,7 @@ cudaError_t dgemm(char ta, char tb, int m, int n, int k, double alpha, const dou
   kslice = (kslice + dg::BK - 1) / dg::BK * dg::BK;
   slices = (k + kslice - 1) / kslice;
   if (slices < 1) slices = 1;
-  DgemmArgs p{m, n, k, kslice, A, lda, B, ldb, C, ldc, 0, alpha, beta, 0, 0, 0};
+  DgemmArgs p{m, n, k, kslice, A, lda, B, ldb, C, ldc, 0, alpha, beta, 0, 0, 0, symhalf};
   if (slices > 1) {
     p.c = work;
     p.ldc = m;
@@ -488,6 +508,30 @@ __global__ void symmetrize_kernel(double* c, int m, int ld) {
       c[j + (int64_t)i * ld] = v;
     }
   }
+}
+
+// hermitian_part (dense.hpp:127-134) of a matrix whose strictly-lower 64-wide tiles were not
+// computed (dgemm_tn_sym2): inside a diagonal tile average the pair, elsewhere mirror the upper
+__global__ void symmetrize_tiles_kernel(double* c, int m, int ld, int tile) {
+  const int64_t total = (int64_t)m * m;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(idx % m), j = (int)(idx / m);
+    if (i < j) {
+      const double u = c[i + (int64_t)j * ld];
+      const double v = (i / tile == j / tile) ? (u + c[j + (int64_t)i * ld]) * 0.5 : u;
+      c[i + (int64_t)j * ld] = v;
+      c[j + (int64_t)i * ld] = v;
+    }
+  }
+}
+
+cudaError_t symmetrize_tiles(double* c, int m, int ld, cudaStream_t st) {
+  const int64_t total = (int64_t)m * m;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+  symmetrize_tiles_kernel<<<blocks, 256, 0, st>>>(c, m, ld, dg::BM);
+  ++g_launches;
+  return cudaGetLastError();
 }
 
 cudaError_t symmetrize(double* c, int m, int ld, cudaStream_t st) {

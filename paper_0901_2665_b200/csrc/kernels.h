@@ -107,8 +107,19 @@ cudaError_t dgemm(char ta, char tb, int m, int n, int k, double alpha, const dou
                   const double* B, int ldb, double beta, double* C, int ldc, double* work,
                   size_t work_elems, cudaStream_t st);
 
+// [S1 | S2] = Q^T [AQ | BQ] (m x 2m, ld m) with S1, S2 symmetric and m a multiple of 64: only
+// the upper tiles of each half are computed; follow with symmetrize_tiles on each half
+cudaError_t dgemm_tn_sym2(int m, int k, const double* Q, int ldq, const double* AB, int ldab, double* C,
+                          double* work, size_t work_elems, cudaStream_t st);
+cudaError_t symmetrize_tiles(double* c, int m, int ld, cudaStream_t st);
 // C = (M + M^T)/2 in place (square m x m, ld)
 cudaError_t symmetrize(double* c, int m, int ld, cudaStream_t st);
+
+// band-row copy of a block-tridiagonal operator (b = 16, 32): row l b + i = [C_{l-1} | D_l | C_l^T](i, :)
+cudaError_t band_rows(int L, int b, const double* diag, const double* low, double* ab, cudaStream_t st);
+// y1 = A x, and y2 = B x in the same pass when ab2 != nullptr (band rows from band_rows)
+cudaError_t band_apply(int L, int b, const double* ab1, const double* ab2, const double* x, int ldx, double* y1,
+                       double* y2, int ldy, int m, cudaStream_t st);
 
 // ---------------- reduced generalized eigensolver ----------------------------
 struct EigWork;  // opaque, sized for mmax
@@ -124,6 +135,13 @@ cudaError_t sym_eig(EigWork* w, int m, double* a, double* evals, double* v, cuda
 int tri_tiles_max_dim();
 cudaError_t tridiag_tiles(int m, const double* a, double* d, double* e, double* hv, double* tau,
                           cudaStream_t st);
+// V = H_0 ... H_{m-3} Z with block reflectors (tri_back.cu); tw: tri_back_wy_ws(m) doubles
+size_t tri_back_wy_ws(int m);
+cudaError_t tri_back_wy(int m, const double* hv, const double* tau, const double* z, double* v, double* tw,
+                        cudaStream_t st);
+// one-CTA tiled Cholesky (chol_tiles.cu) for m <= chol_tiles_max_dim(): same contract as cholesky()
+int chol_tiles_max_dim();
+cudaError_t chol_tiles(int m, double* a, double rel_tol, int* status, double* dinv, cudaStream_t st);
 // Cholesky with relative pivot floor: L (lower, in place in `a`), status[0] = 1 on failure
 // (status must be zero on entry). dinv receives the inverses of the 32x32 diagonal tiles of
 // L (ceil(m/32) * 1024 doubles), consumed by the triangular solves.

@@ -794,6 +794,37 @@ __device__ __forceinline__ int sturm(int m, const double* d, const double* e2, d
   return cnt;
 }
 
+// reciprocal to ~2^-46 relative (one Newton step on the hardware approximation): the Sturm
+// counts only need the sign of each pivot, and a relative error of 1e-14 in q_i is a relative
+// perturbation of the same order in e_{i-1}^2, i.e. eigenvalue shifts of O(1e-14 ||T||)
+__device__ __forceinline__ double fast_rcp1(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return fma(r, fma(-x, r, 1.0), r);
+}
+
+// four Sturm counts at once (independent chains interleaved: the division latency of one
+// chain hides behind the other three)
+__device__ __forceinline__ void sturm4(int m, const double* d, const double* e2, const double (&sg)[4], double pivmin,
+                                       int (&cnt)[4]) {
+  double q[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    q[u] = d[0] - sg[u];
+    if (fabs(q[u]) < pivmin) q[u] = -pivmin;
+    cnt[u] = q[u] < 0.0;
+  }
+  for (int i = 1; i < m; ++i) {
+    const double di = d[i], ei = e2[i - 1];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      q[u] = (di - sg[u]) - ei * fast_rcp1(q[u]);
+      if (fabs(q[u]) < pivmin) q[u] = -pivmin;
+      cnt[u] += q[u] < 0.0;
+    }
+  }
+}
+
 struct TriArgs {
   int m;
   const double* d;
@@ -826,26 +857,37 @@ __global__ void tri_eigvals_kernel(TriArgs p) {
   extern __shared__ double sm[];
   double* d = sm;
   double* e2 = d + p.m;
+  double* e = e2 + p.m;
   const int m = p.m;
   for (int i = threadIdx.x; i < m; i += blockDim.x) {
     d[i] = p.d[i];
-    if (i + 1 < m) e2[i] = p.e[i] * p.e[i];
+    if (i + 1 < m) {
+      e[i] = p.e[i];
+      e2[i] = p.e[i] * p.e[i];
+    }
   }
   __syncthreads();
   double lo, hi, tnorm, pivmin;
-  tri_bounds(m, p.d, p.e, lo, hi, tnorm, pivmin);
+  tri_bounds(m, d, e, lo, hi, tnorm, pivmin);  // from shared memory: one pass, no L2 round trips
   const int lane = threadIdx.x & 31;
   const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (j >= m) return;
-  double a = lo, b = hi;  // invariant: count(a) <= j < count(b)
-  for (int it = 0; it < 24; ++it) {
+  // 128-point multisection per step (4 Sturm chains per lane): points a + w (P + 1) / 129,
+  // P = 4 lane + u, computed identically on every lane; invariant count(a) <= j < count(b)
+  double a = lo, b = hi;
+  for (int it = 0; it < 16; ++it) {
     const double width = b - a;
     if (width <= 2.0 * DBL_EPSILON * fmax(fabs(a), fabs(b)) + 2.0 * pivmin) break;
-    const double s = a + width * (double)(lane + 1) / 33.0;
-    const int c = sturm(m, d, e2, s, pivmin);
-    const int nb = __popc(__ballot_sync(0xffffffffu, c <= j));  // lanes left of lam_j (monotone)
-    const double na = nb > 0 ? __shfl_sync(0xffffffffu, s, (nb > 0 ? nb : 1) - 1) : a;
-    const double nbb = nb < 32 ? __shfl_sync(0xffffffffu, s, nb < 32 ? nb : 31) : b;
+    double sg[4];
+    int c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) sg[u] = a + width * (double)(4 * lane + u + 1) / 129.0;
+    sturm4(m, d, e2, sg, pivmin, c);
+    int nb = 0;  // points left of lam_j (counts are monotone in the point index)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) nb += __popc(__ballot_sync(0xffffffffu, c[u] <= j));
+    const double na = nb > 0 ? a + width * (double)nb / 129.0 : a;
+    const double nbb = nb < 128 ? a + width * (double)(nb + 1) / 129.0 : b;
     a = na;
     b = nbb;
   }
@@ -918,9 +960,19 @@ constexpr int kInvIters = 2;
 __global__ void tri_eigvecs_kernel(TriArgs p) {
   const int m = p.m, lane = threadIdx.x & 31;
   const int cl = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // d, e in shared memory: the O(m) recurrences below run on one lane, where every L2 load
+  // would be a serial round trip
+  extern __shared__ double wsm[];
+  double* sd = wsm;
+  double* se = sd + m;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    sd[i] = p.d[i];
+    se[i] = i + 1 < m ? p.e[i] : 0.0;
+  }
+  __syncthreads();
   if (cl >= m) return;
   double lo, hi, tnorm, pivmin;
-  tri_bounds(m, p.d, p.e, lo, hi, tnorm, pivmin);
+  tri_bounds(m, sd, se, lo, hi, tnorm, pivmin);
   // reorthogonalisation threshold: dstein uses 1e-3 ||T||; inverse iteration leaves a
   // non-orthogonality of O(eps ||T|| / gap), so 1e-5 ||T|| already bounds it by ~1e-11 while
   // keeping FEAST's dense interior Ritz spectra from chaining into one long cluster
@@ -947,8 +999,7 @@ __global__ void tri_eigvecs_kernel(TriArgs p) {
   while (cend < m && p.lam[cend] - p.lam[cend - 1] <= ortol) ++cend;
   // per-warp shared scratch: LU bands, pivots, the iterate (the O(m) recurrences run on
   // lane 0 against shared memory, not L2)
-  extern __shared__ double wsm[];
-  double* D = wsm + (threadIdx.x >> 5) * 6 * m;
+  double* D = wsm + 2 * m + (threadIdx.x >> 5) * 6 * m;
   double* DL = D + m;
   double* DU = DL + m;
   double* DU2 = DU + m;
@@ -960,7 +1011,7 @@ __global__ void tri_eigvecs_kernel(TriArgs p) {
     const double sep = 10.0 * eps * fmax(tnorm, 1e-300);
     if (j > cl && lam - prev < sep) lam = prev + sep;  // separate coincident shifts (dstein)
     prev = lam;
-    if (lane == 0) gttrf(m, p.d, p.e, lam, D, DL, DU, DU2, ipiv, eps * tnorm);
+    if (lane == 0) gttrf(m, sd, se, lam, D, DL, DU, DU2, ipiv, eps * tnorm);
     double* zj = zs;
     for (int i = lane; i < m; i += 32) {  // deterministic pseudo-random start
       uint32_t h = (uint32_t)i * 2654435761u ^ ((uint32_t)j * 40503u + 12345u);
@@ -1156,16 +1207,27 @@ cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws
   }
   TriArgs p{m, d, e, evals, z, nullptr, iws, vfloor};
   const int wpb = 4;
-  tri_eigvals_kernel<<<(m + wpb - 1) / wpb, 32 * wpb, sizeof(double) * 2 * m, st>>>(p);
+  tri_eigvals_kernel<<<(m + wpb - 1) / wpb, 32 * wpb, sizeof(double) * 3 * m, st>>>(p);
   ++g_launches;
-  const size_t vsm = sizeof(double) * 6 * m * wpb + 64;
+  const size_t vsm = sizeof(double) * (6 * m * wpb + 2 * m) + 64;
   if (vsm > 48 * 1024) cudaFuncSetAttribute(tri_eigvecs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsm);
   tri_eigvecs_kernel<<<(m + wpb - 1) / wpb, 32 * wpb, vsm, st>>>(p);
   ++g_launches;
-  if (m <= 256) tri_back_kernel<8, 4><<<(m + 7) / 8, 256, 0, st>>>(m, hv, tau, z, v);
-  else if (m <= 512) tri_back_kernel<16, 4><<<(m + 3) / 4, 128, 0, st>>>(m, hv, tau, z, v);
-  else tri_back_kernel<32, 2><<<(m + 3) / 4, 128, 0, st>>>(m, hv, tau, z, v);
-  ++g_launches;
+  // blocked (WY) back-transformation above m = 384 (tri_back.cu; its T factors live in the
+  // cooperative route's scratch gw, free by now); below, one warp per column measured faster
+  // (m = 192: 83 us against 40 + 56 us, the WY products being shared-memory bound as written).
+  // FEAST_TRI_BACK=w / b forces one or the other.
+  static const char* back_env = getenv("FEAST_TRI_BACK");
+  const bool wy = back_env ? (back_env[0] == 'b' && m >= 64) : m > 384;
+  if (wy) {
+    cudaError_t err = tri_back_wy(m, hv, tau, z, v, gw, st);
+    if (err != cudaSuccess) return err;
+  } else {
+    if (m <= 256) tri_back_kernel<8, 4><<<(m + 7) / 8, 256, 0, st>>>(m, hv, tau, z, v);
+    else if (m <= 512) tri_back_kernel<16, 4><<<(m + 3) / 4, 128, 0, st>>>(m, hv, tau, z, v);
+    else tri_back_kernel<32, 2><<<(m + 3) / 4, 128, 0, st>>>(m, hv, tau, z, v);
+    ++g_launches;
+  }
   return cudaGetLastError();
 }
 

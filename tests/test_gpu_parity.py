@@ -144,6 +144,50 @@ def test_tridiag_tiles_route(ctx, m):
         assert np.max(np.abs(phi.T @ phi - np.eye(m))) <= 1e-13 * m
 
 
+@pytest.mark.parametrize("m", [2, 3, 17, 33, 100, 191, 192])
+def test_reduced_gevp_graded_mass(ctx, m):
+    """The tiled Cholesky (default for m <= 192, chol_tiles.cu) on graded mass matrices
+    (condition 1e8, the FEAST steady state) and odd sizes, against scipy's generalized eigh."""
+    import scipy.linalg as sl
+    rng = np.random.default_rng(200 + m)
+    a = rng.uniform(-1, 1, (m, m)); a = a + a.T
+    q, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    b = (q * np.logspace(-8, 0, m)) @ q.T; b = 0.5 * (b + b.T)
+    ev, phi, tr = ctx.reduced_gevp(a, b)
+    ref = sl.eigh(a, b, eigvals_only=True)
+    assert not tr
+    # cond(B) = 1e8: eigenvalues up to ~1e8 carry relative errors up to ~eps * cond(B) in any
+    # backward-stable solver (scipy's included); the residual below is the sharp check
+    assert np.max(np.abs(ev - ref) / np.maximum(1.0, np.abs(ref))) <= 1e-7
+    assert np.max(np.abs(a @ phi - b @ phi * ev)) <= 1e-9 * max(1.0, np.max(np.abs(ref)))
+    # B-orthonormality error ~ eps * m * max|phi|^2 (phi ~ 1/sqrt(lambda_min(B)) = 1e4)
+    assert np.max(np.abs(phi.T @ b @ phi - np.eye(m))) <= 1e-10 + 1e-15 * m * np.max(np.abs(phi)) ** 2
+
+
+@pytest.mark.parametrize("n,m0,want", [(300, 100, 8), (400, 160, 12)])
+def test_solve_with_shrinking_subspace(F, n, m0, want):
+    """m0 far above the count: the filtered block's B_Q goes numerically singular, the
+    truncation path keeps mo < m0 columns and the next pass runs on Y = B X[:, :mo]
+    (core.hpp:387). Regression: the one-GEMM projection once read BQ / Bq at their m0-column
+    offsets after the subspace shrank (config 5 drifted to no-eigenvalues-in-interval)."""
+    from paper_0901_2665_b200 import problems as P
+    prob = P.small_dense(n=n, seed=3, want=want, m0=m0)
+    ctx = F.GpuContext(0)
+    ctx.set_pencil(prob.a, prob.b)
+    r = ctx.solve(F.SearchInterval(prob.emin, prob.emax),
+                  F.FeastConfig(m0=m0, n_e=prob.n_e, trace_tol=prob.trace_tol, max_loops=prob.max_loops,
+                                seed=prob.seed))
+    ctx.close()
+    ref = O.feast_solve(prob)
+    assert r.subspace.shape[1] < m0  # the truncation path ran
+    assert r.status == ref["status"] == "converged"
+    assert len(r.eigenvalues) == ref["m"] == want
+    assert np.max(np.abs(r.eigenvalues - ref["eigenvalues"]) / np.maximum(1.0, np.abs(ref["eigenvalues"]))) <= 1e-10
+    # the reference's 1-norm ratio: the truncated reduced problem (S = V d^-1/2 over modes down
+    # to 1e-14 of the largest) limits both solvers alike
+    assert r.max_residual <= max(1e-9, 10.0 * ref["max_residual"]), (r.max_residual, ref["max_residual"])
+
+
 def test_reduced_gevp_truncation_path(ctx):
     # B_Q rank deficient -> Cholesky floor fails -> spectral truncation (eigh.hpp:204-224)
     rng = np.random.default_rng(4)
