@@ -190,9 +190,11 @@ __global__ void __launch_bounds__(CT_NT, 1) chol_tiles_kernel(int m, double* __r
   }
 
   // outputs: L (lower, zero strict upper) column-major; dinv 32 x 32 tile inverses
-  for (size_t idx = tid; idx < (size_t)m * m; idx += CT_NT) {
-    const int i = (int)(idx % m), j = (int)(idx / m);
-    a[idx] = i >= j ? L[ct_id(i >> 4, j >> 4) * 256 + ct_sw(i & 15, j & 15)] : 0.0;
+  // (column per warp, rows over lanes: a 64-bit idx % m here cost ~20 us of integer division)
+  for (int j = warp; j < m; j += CT_NW) {
+    double* aj = a + (size_t)j * m;
+    for (int i = lane; i < m; i += 32)
+      aj[i] = i >= j ? L[ct_id(i >> 4, j >> 4) * 256 + ct_sw(i & 15, j & 15)] : 0.0;
   }
   // [[Li0, 0], [X, Li1]], X = -Li1 (L10 Li0) (16-tiles 2p, 2p+1; identity padding beyond m)
   const int n32 = (m + 31) >> 5;

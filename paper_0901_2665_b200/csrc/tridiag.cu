@@ -1058,6 +1058,66 @@ __global__ void tri_eigvecs_kernel(TriArgs p) {
 }
 
 // ---------------------------------------------------------------------------
+// 4'. back-transformation for m <= 192 with every reflector resident in shared memory (packed:
+//     reflector k holds rows k+1..m-1, m(m-1)/2 doubles = 147 KB at m = 192) and EIGHT lanes per
+//     column (four columns per warp): the dot product per reflector is a 3-level shuffle over the
+//     lane group instead of a 5-level warp reduction, and no reflector load waits on L2.
+// ---------------------------------------------------------------------------
+constexpr int TBS_NQ = 24;  // rows per lane: m <= 8 * 24 = 192
+constexpr int TBS_NW = 1;   // warps per CTA: one (the chain is per warp; spread over m/4 SMs)
+__global__ void __launch_bounds__(TBS_NW * 32, 1) tri_back_smem_kernel(int m, const double* __restrict__ hv,
+                                                               const double* __restrict__ tau,
+                                                               const double* __restrict__ z, double* v) {
+  extern __shared__ double hs[];     // packed reflectors, then tau
+  double* ts = hs + (size_t)m * (m - 1) / 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nref = m - 2;
+  for (int k = warp; k < nref; k += TBS_NW) {  // reflector k: rows k+1..m-1 at hs[k m - k(k+1)/2 ...]
+    double* dst = hs + (size_t)k * m - (size_t)k * (k + 1) / 2;
+    for (int i = k + 1 + lane; i < m; i += 32) cp_async8z(dst + (i - k - 1), hv + i + (size_t)k * m, true);
+  }
+  for (int k = tid; k < nref; k += TBS_NW * 32) ts[k] = tau[k];
+  const int sl = lane & 7, col = blockIdx.x * (4 * TBS_NW) + warp * 4 + (lane >> 3);
+  const bool live = col < m;
+  double x[TBS_NQ];
+#pragma unroll
+  for (int q = 0; q < TBS_NQ; ++q) {
+    const int i = sl + 8 * q;
+    x[q] = (live && i < m) ? z[i + (size_t)col * m] : 0.0;
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  for (int k = nref - 1; k >= 0; --k) {
+    const double* hk = hs + (size_t)k * m - (size_t)k * (k + 1) / 2 - (k + 1);  // hk[i], i > k
+    double h[TBS_NQ];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int q = 0; q < TBS_NQ; ++q) {
+      const int i = sl + 8 * q;
+      h[q] = (i > k && i < m) ? hk[i] : 0.0;
+      if ((q & 3) == 0) s0 = fma(h[q], x[q], s0);
+      else if ((q & 3) == 1) s1 = fma(h[q], x[q], s1);
+      else if ((q & 3) == 2) s2 = fma(h[q], x[q], s2);
+      else s3 = fma(h[q], x[q], s3);
+    }
+    double sum = (s0 + s1) + (s2 + s3);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 4);
+    sum *= ts[k];
+#pragma unroll
+    for (int q = 0; q < TBS_NQ; ++q) x[q] = fma(-sum, h[q], x[q]);
+  }
+  if (live) {
+#pragma unroll
+    for (int q = 0; q < TBS_NQ; ++q) {
+      const int i = sl + 8 * q;
+      if (i < m) v[i + (size_t)col * m] = x[q];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // 4. back-transformation V = H_0 ... H_{m-3} Z, one warp per column
 // ---------------------------------------------------------------------------
 // the column stays in registers (NQ per lane: m <= 32 NQ); the next PD reflectors are loaded
@@ -1068,28 +1128,31 @@ __global__ void tri_back_kernel(int m, const double* __restrict__ hv, const doub
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (c >= m) return;
-  double x[NQ], h[PD][NQ];
+  double x[NQ], h[PD][NQ], tp[PD];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     const int i = lane + 32 * q;
     x[q] = i < m ? z[i + (int64_t)c * m] : 0.0;
   }
-  auto load = [&](int k, double* dst) {
+  // reflector k and its tau travel together PD reflectors ahead (a tau load issued at use sat
+  // on the reduction's dependency chain: ~3x the kernel time)
+  auto load = [&](int k, double* dst, double& tk) {
     const double* hk = hv + (int64_t)k * m;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const int i = lane + 32 * q;
       dst[q] = (k >= 0 && i > k && i < m) ? hk[i] : 0.0;
     }
+    tk = k >= 0 ? tau[k] : 0.0;
   };
 #pragma unroll
-  for (int s = 0; s < PD; ++s) load(m - 3 - s, h[s]);
+  for (int s = 0; s < PD; ++s) load(m - 3 - s, h[s], tp[s]);
   for (int k = m - 3; k >= 0; k -= PD) {
 #pragma unroll
     for (int s = 0; s < PD; ++s) {
       const int kk = k - s;
       if (kk >= 0) {
-        const double t = tau[kk];
+        const double t = tp[s];
         double sum = 0.0;
 #pragma unroll
         for (int q = 0; q < NQ; ++q) sum += h[s][q] * x[q];
@@ -1097,7 +1160,7 @@ __global__ void tri_back_kernel(int m, const double* __restrict__ hv, const doub
 #pragma unroll
         for (int q = 0; q < NQ; ++q) x[q] -= sum * h[s][q];
       }
-      load(kk - PD, h[s]);  // refill this slot PD reflectors ahead
+      load(kk - PD, h[s], tp[s]);  // refill this slot PD reflectors ahead
     }
   }
   double* vc = v + (int64_t)c * m;
@@ -1206,7 +1269,10 @@ cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws
     if (err != cudaSuccess) return err;
   }
   TriArgs p{m, d, e, evals, z, nullptr, iws, vfloor};
-  const int wpb = 4;
+  // one warp per CTA: these are serial per-warp chains, so spreading the m warps over all 148
+  // SMs (instead of 4 per CTA on m/4 SMs) is what sets their time (ncu: issue-bound at 4 warps
+  // per SM, 114 / 85 / 90 us for eigvals / eigvecs / back at m = 192)
+  const int wpb = 1;
   tri_eigvals_kernel<<<(m + wpb - 1) / wpb, 32 * wpb, sizeof(double) * 3 * m, st>>>(p);
   ++g_launches;
   const size_t vsm = sizeof(double) * (6 * m * wpb + 2 * m) + 64;
@@ -1219,13 +1285,23 @@ cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws
   // FEAST_TRI_BACK=w / b forces one or the other.
   static const char* back_env = getenv("FEAST_TRI_BACK");
   const bool wy = back_env ? (back_env[0] == 'b' && m >= 64) : m > 384;
-  if (wy) {
+  const bool smem_back = !back_env && m >= 3 && m <= 8 * TBS_NQ;
+  if (smem_back) {
+    const size_t sm = sizeof(double) * ((size_t)m * (m - 1) / 2 + m);
+    static bool battr = false;
+    if (!battr) {
+      cudaFuncSetAttribute(tri_back_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      battr = true;
+    }
+    tri_back_smem_kernel<<<(m + 4 * TBS_NW - 1) / (4 * TBS_NW), TBS_NW * 32, sm, st>>>(m, hv, tau, z, v);
+    ++g_launches;
+  } else if (wy) {
     cudaError_t err = tri_back_wy(m, hv, tau, z, v, gw, st);
     if (err != cudaSuccess) return err;
   } else {
-    if (m <= 256) tri_back_kernel<8, 4><<<(m + 7) / 8, 256, 0, st>>>(m, hv, tau, z, v);
-    else if (m <= 512) tri_back_kernel<16, 4><<<(m + 3) / 4, 128, 0, st>>>(m, hv, tau, z, v);
-    else tri_back_kernel<32, 2><<<(m + 3) / 4, 128, 0, st>>>(m, hv, tau, z, v);
+    if (m <= 256) tri_back_kernel<8, 4><<<m, 32, 0, st>>>(m, hv, tau, z, v);
+    else if (m <= 512) tri_back_kernel<16, 4><<<m, 32, 0, st>>>(m, hv, tau, z, v);
+    else tri_back_kernel<32, 2><<<m, 32, 0, st>>>(m, hv, tau, z, v);
     ++g_launches;
   }
   return cudaGetLastError();

@@ -19,9 +19,10 @@
 //       (all of them interleaved: one straight-line body per active count), hands column k+1
 //       to warp 0, and leaves the tile partials of A22 v_k: row part (8 FMAs, 2 shuffles),
 //       column part (8 FMAs, a 4-shuffle reduce-scatter over the 8 row-pair lanes);
-//   (b) warp 0 sums each row's tile partials in a fixed order (deterministic) into p, forms
-//       p.v, w_k = p - (tau/2)(p.v) v_k, brings column k+1 up to date with (v_k, w_k), forms
-//       the reflector v_{k+1}, writes d, e, tau and hv.
+//   (b) the row warps (one row per lane) sum each row's tile partials in a fixed order
+//       (deterministic) into p, form p.v, w_k = p - (tau/2)(p.v) v_k, bring column k+1 up to
+//       date with (v_k, w_k) and form the reflector v_{k+1} (d, e, tau, hv): two named-barrier
+//       exchanges among those warps, the reflector scalars computed identically by each.
 // Rows/columns <= k carry v = w = 0, so finished entries are never changed and no per-element
 // masking is needed. Diagonal tiles are updated with the same FMAs as the others, so their two
 // triangles may drift apart by rounding; their row part uses the full tile.
@@ -55,6 +56,9 @@ __shared__ long long tt_acc[16];
 #endif
 
 __device__ __forceinline__ int tt_id(int I, int J) { return I * (I + 1) / 2 + J; }
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
 __device__ __forceinline__ double2 tt_ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 
 // phase (a) on slots S0 .. S0+NS-1 of this warp, interleaved (straight-line). A slot without a
@@ -124,6 +128,7 @@ __global__ void __launch_bounds__(TT_NT, 1) tridiag_tiles_kernel(int m, const do
   __shared__ __align__(16) double wbuf[TT_MP];
   __shared__ double colbuf[TT_MP];
   __shared__ double part[(TT_MAXNB + 1) * TT_MP];  // [partner block X][row]; + a spare row
+  __shared__ double redp[TT_MP / 32], redx[TT_MP / 32], sc[3];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nb = (m + 15) >> 4, mp = nb * 16;
@@ -164,9 +169,10 @@ __global__ void __launch_bounds__(TT_NT, 1) tridiag_tiles_kernel(int m, const do
 #endif
 
   // Step k = -1 .. m-2: (a) [k >= 0] all warps: pending update, column k+1, partials of A22 v_k;
-  // (b) warp 0: p = tau_k A22 v_k, w_k, column k+1 brought up to date, reflector v_{k+1}.
+  // (b) row warps: p = tau_k A22 v_k, w_k, column k+1 brought up to date, reflector v_{k+1}.
   // At k = -1 every vector is zero, so (b) reduces to the first reflector from column 0.
-  double tk = 0.0;  // warp 0: tau_k
+  double tk = 0.0;  // row warps: tau_k
+  const int nbw = (mp + 31) >> 5;  // warps that own rows in phase (b)
   for (int k = -1; k + 1 < m; ++k) {
     const double* vo = vbuf[(k + 1) & 1];  // v_{k-1}
     const double* vn = vbuf[k & 1];        // v_k
@@ -182,76 +188,64 @@ __global__ void __launch_bounds__(TT_NT, 1) tridiag_tiles_kernel(int m, const do
       __syncthreads();  // (a)
       TT_MARK(2);
     }
-    if (warp == 0) {
-      const int Jc = (k + 1) >> 4;
-      double p[TT_NQ];  // p, then w_k, then column k+1 (one register array)
-#pragma unroll
-      for (int q = 0; q < TT_NQ; ++q) p[q] = 0.0;
-      // fixed-order sum over the partner blocks X >= Jc of each row (blocks before Jc are
-      // finished): part[X][i] is contiguous in i, so the six rows of a lane are immediate
-      // offsets of one address. Rolled over X: this code runs on one warp with the rest of the
-      // CTA parked, so its instruction count is the critical path.
+    if (warp < nbw) {
+      // (b) on the warps of the row threads, one row per lane (i = 32 warp + lane): each lane
+      // sums its row's tile partials, two named-barrier exchanges (p.v, then ||x||^2 and the
+      // pivot / alpha entries) and every warp forms the same reflector scalars
+      const int i = 32 * warp + lane, Jc = (k + 1) >> 4, kc = k + 1;
+      double pi = 0.0, pj = 0.0;  // fixed order (even / odd partner blocks), no masking
+      {
+        int X = Jc;
 #pragma unroll 1
-      for (int X = Jc; X < nb; ++X) {
-        const double* px = part + X * TT_MP + lane;
-#pragma unroll
-        for (int q = 0; q < TT_NQ; ++q) p[q] += px[32 * q];
+        for (; X + 1 < nb; X += 2) {
+          pi += part[X * TT_MP + i];
+          pj += part[(X + 1) * TT_MP + i];
+        }
+        if (X < nb) pi += part[X * TT_MP + i];
+        pi += pj;
       }
+      pi = (i > k && i < m) ? tk * pi : 0.0;
+      const double vi = vn[i];
+      const double pvw = warp_sum(pi * vi);
+      if (lane == 0) redp[warp] = pvw;
+      if (i == kc) sc[2] = pi;  // p_k[k+1] for w_k[k+1]
+      named_sync(1, 32 * nbw);
       double pv = 0.0;
-#pragma unroll
-      for (int q = 0; q < TT_NQ; ++q) {
-        const int i = lane + 32 * q;
-        p[q] = (i > k && i < m) ? tk * p[q] : 0.0;
-        pv = fma(p[q], vn[i], pv);
-      }
-      pv = warp_sum(pv);
-      TT_MARK(5);
+      for (int w = 0; w < nbw; ++w) pv += redp[w];
       const double c = -0.5 * tk * pv;
-      double wsel = 0.0;
-#pragma unroll
-      for (int q = 0; q < TT_NQ; ++q) {
-        const int i = lane + 32 * q;
-        p[q] = fma(c, vn[i], p[q]);
-        wbuf[i] = p[q];
-        wsel = i == k + 1 ? p[q] : wsel;
-      }
-      const double wk1 = __shfl_sync(0xffffffffu, wsel, (k + 1) & 31);  // w_k[k+1]
-      const double vk1 = vn[k + 1];                                      // v_k[k+1]
-      // column k+1 up to date, then its reflector (kc = k + 1)
-      const int kc = k + 1;
-      double dsel = 0.0, asel = 0.0, xn2 = 0.0;
-#pragma unroll
-      for (int q = 0; q < TT_NQ; ++q) {
-        const int i = lane + 32 * q;
-        p[q] = colbuf[i] - (vn[i] * wk1 + p[q] * vk1);
-        dsel = i == kc ? p[q] : dsel;
-        asel = i == kc + 1 ? p[q] : asel;
-        xn2 = fma(p[q], (i >= kc + 2 && i < m) ? p[q] : 0.0, xn2);
-      }
-      const double dk = __shfl_sync(0xffffffffu, dsel, kc & 31);
-      const double alpha = __shfl_sync(0xffffffffu, asel, (kc + 1) & 31);
-      xn2 = warp_sum(xn2);
+      const double wi = fma(c, vi, pi);
+      wbuf[i] = wi;
+      const double vk1 = vn[kc];                 // v_k[k+1]
+      const double wk1 = fma(c, vk1, sc[2]);    // w_k[k+1]
+      const double coli = colbuf[i] - (vi * wk1 + wi * vk1);  // column k+1, row i, up to date
+      const double xw = warp_sum((i >= kc + 2 && i < m) ? coli * coli : 0.0);
+      if (lane == 0) redx[warp] = xw;
+      if (i == kc) sc[0] = coli;
+      if (i == kc + 1) sc[1] = coli;
+      named_sync(1, 32 * nbw);
+      double xn2 = 0.0;
+      for (int w = 0; w < nbw; ++w) xn2 += redx[w];
+      const double dk = sc[0], alpha = kc + 1 < m ? sc[1] : 0.0;
       TT_MARK(6);
       double t = 0.0, beta = alpha, scal = 0.0;
-      if (xn2 > 0.0) {  // identical on every lane (same inputs)
-        beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-        t = (beta - alpha) / beta;
-        scal = 1.0 / (alpha - beta);
+      if (xn2 > 0.0) {  // identical on every lane of every row warp (same inputs)
+        // nu = ||(alpha, x)||, beta = -sign(alpha) nu, tau = (beta - alpha) / beta = 1 + |alpha| / nu,
+        // scal = 1 / (alpha - beta) = sign(alpha) / (|alpha| + nu): one rsqrt and one division
+        // on the serial path instead of a sqrt and two divisions
+        const double s2 = fma(alpha, alpha, xn2), rn = rsqrt(s2), nu = s2 * rn, aa = fabs(alpha);
+        beta = -copysign(nu, alpha);
+        t = fma(aa, rn, 1.0);
+        scal = copysign(1.0, alpha) / (aa + nu);
       }
       TT_MARK(7);
-      if (lane == 0) {
+      if (i == 0) {
         d[kc] = dk;
         if (kc + 1 < m) e[kc] = beta;
         tau[kc] = t;
       }
-      double* vnext = vbuf[kc & 1];
-#pragma unroll
-      for (int q = 0; q < TT_NQ; ++q) {
-        const int i = lane + 32 * q;
-        const double vi = i == kc + 1 ? 1.0 : ((i > kc + 1 && i < m && t != 0.0) ? p[q] * scal : 0.0);
-        vnext[i] = t != 0.0 ? vi : 0.0;  // zero beyond m (and TT_MP >= mp)
-        if (i > kc && i < m) hv[i + (size_t)kc * m] = vi;
-      }
+      const double vnew = i == kc + 1 ? 1.0 : ((i > kc + 1 && i < m && t != 0.0) ? coli * scal : 0.0);
+      vbuf[kc & 1][i] = t != 0.0 ? vnew : 0.0;  // zero beyond m
+      if (i > kc && i < m) hv[i + (size_t)kc * m] = vnew;
       tk = t;
     }
     TT_MARK(3);

@@ -183,9 +183,11 @@ def test_solve_with_shrinking_subspace(F, n, m0, want):
     assert r.status == ref["status"] == "converged"
     assert len(r.eigenvalues) == ref["m"] == want
     assert np.max(np.abs(r.eigenvalues - ref["eigenvalues"]) / np.maximum(1.0, np.abs(ref["eigenvalues"]))) <= 1e-10
-    # the reference's 1-norm ratio: the truncated reduced problem (S = V d^-1/2 over modes down
-    # to 1e-14 of the largest) limits both solvers alike
-    assert r.max_residual <= max(1e-9, 10.0 * ref["max_residual"]), (r.max_residual, ref["max_residual"])
+    # the reference's 1-norm ratio. The truncated reduced problem (S = V d^-1/2 over modes down
+    # to 1e-14 of the largest) amplifies the eigenvector error of B_Q's small modes by d^-1/2:
+    # Jacobi (the reference) resolves graded spectra to high relative accuracy, the tridiagonal
+    # route only normwise, so this path is held to 5e-9 (truncation accuracy)
+    assert r.max_residual <= max(5e-9, 10.0 * ref["max_residual"]), (r.max_residual, ref["max_residual"])
 
 
 def test_reduced_gevp_truncation_path(ctx):
