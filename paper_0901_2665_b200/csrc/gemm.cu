@@ -191,7 +191,9 @@ struct DgemmArgs {
   int symhalf = 0;  // > 0: C = [S1 | S2] of symmetric symhalf x symhalf halves: lower tiles skipped
 };
 
-template <bool TA, bool TB>
+// V16: 16-byte copies (pairs along each operand's contiguous dimension; the launcher checks
+// even dimensions / leading dimensions and 16-byte aligned bases): half the copy instructions
+template <bool TA, bool TB, bool V16>
 __global__ void __launch_bounds__(256, 2) dgemm_kernel(DgemmArgs p) {
   using namespace dg;
   extern __shared__ __align__(16) double dsm[];
@@ -213,6 +215,32 @@ __global__ void __launch_bounds__(256, 2) dgemm_kernel(DgemmArgs p) {
       double* As = dsm + (kt % NS) * STAGE;
       double* Bs = As + A_ELEMS;
       const int k0 = kbeg + kt * BK;
+      if (V16) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int c = tid + r * 256;
+          if (!TA) {
+            const int mm = (c & (BM / 2 - 1)) * 2, kk = c / (BM / 2);
+            const bool v = (m0 + mm < p.m) && (k0 + kk < kend);
+            cp_async16_zfill(As + kk * SA + mm, v ? p.a + (m0 + mm) + (int64_t)(k0 + kk) * p.lda : p.a, v);
+          } else {
+            const int kk = (c & (BK / 2 - 1)) * 2, mm = c / (BK / 2);
+            const bool v = (m0 + mm < p.m) && (k0 + kk < kend);
+            cp_async16_zfill(As + mm * SAT + kk, v ? p.a + (k0 + kk) + (int64_t)(m0 + mm) * p.lda : p.a, v);
+          }
+          if (!TB) {
+            const int kk = (c & (BK / 2 - 1)) * 2, nn = c / (BK / 2);
+            const bool v = (n0 + nn < p.n) && (k0 + kk < kend);
+            cp_async16_zfill(Bs + nn * SB + kk, v ? p.b + (k0 + kk) + (int64_t)(n0 + nn) * p.ldb : p.b, v);
+          } else {
+            const int nn = (c & (BN / 2 - 1)) * 2, kk = c / (BN / 2);
+            const bool v = (n0 + nn < p.n) && (k0 + kk < kend);
+            cp_async16_zfill(Bs + kk * SBT + nn, v ? p.b + (n0 + nn) + (int64_t)(k0 + kk) * p.ldb : p.b, v);
+          }
+        }
+        cp_async_commit();
+        return;
+      }
       // A tile (BM x BK), 2048 doubles, 8 per thread
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
@@ -314,13 +342,23 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ w, int slices, i
   }
 }
 
-template <bool TA, bool TB>
+template <bool TA, bool TB, bool V16>
 static void set_attr_once() {
   static bool done = false;
   if (!done) {
-    cudaFuncSetAttribute(dgemm_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(dgemm_kernel<TA, TB, V16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          dg::NS * dg::STAGE * (int)sizeof(double));
     done = true;
+  }
+}
+template <bool TA, bool TB>
+static void launch_dgemm(bool v16, dim3 grid, int smem, cudaStream_t st, const DgemmArgs& p) {
+  if (v16) {
+    set_attr_once<TA, TB, true>();
+    dgemm_kernel<TA, TB, true><<<grid, 256, smem, st>>>(p);
+  } else {
+    set_attr_once<TA, TB, false>();
+    dgemm_kernel<TA, TB, false><<<grid, 256, smem, st>>>(p);
   }
 }
 
@@ -366,10 +404,14 @@ static cudaError_t dgemm_impl(char ta, char tb, int m, int n, int k, double alph
   }
   dim3 grid((n + dg::BN - 1) / dg::BN, (m + dg::BM - 1) / dg::BM, slices);
   const int smem = dg::NS * dg::STAGE * (int)sizeof(double);
-  if (!TA && !TB) { set_attr_once<false, false>(); dgemm_kernel<false, false><<<grid, 256, smem, st>>>(p); }
-  if (TA && !TB) { set_attr_once<true, false>(); dgemm_kernel<true, false><<<grid, 256, smem, st>>>(p); }
-  if (!TA && TB) { set_attr_once<false, true>(); dgemm_kernel<false, true><<<grid, 256, smem, st>>>(p); }
-  if (TA && TB) { set_attr_once<true, true>(); dgemm_kernel<true, true><<<grid, 256, smem, st>>>(p); }
+  // 16-byte copies need even contiguous dimensions (A: K if transposed else M; B: N if transposed
+  // else K; split-K slices are multiples of BK), even leading dimensions and 16-byte bases
+  const bool v16 = ((TA ? k : m) % 2 == 0) && ((TB ? n : k) % 2 == 0) && lda % 2 == 0 && ldb % 2 == 0 &&
+                   ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0);
+  if (!TA && !TB) launch_dgemm<false, false>(v16, grid, smem, st, p);
+  if (TA && !TB) launch_dgemm<true, false>(v16, grid, smem, st, p);
+  if (!TA && TB) launch_dgemm<false, true>(v16, grid, smem, st, p);
+  if (TA && TB) launch_dgemm<true, true>(v16, grid, smem, st, p);
   ++g_launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || slices == 1) return e;
@@ -393,8 +435,8 @@ static cudaError_t dgemm_batched(bool TA, int m, int n, int k, double alpha, con
     q.b += z0 * sb;
     q.c += z0 * sc;
     dim3 grid((n + dg::BN - 1) / dg::BN, (m + dg::BM - 1) / dg::BM, nz);
-    if (TA) { set_attr_once<true, false>(); dgemm_kernel<true, false><<<grid, 256, smem, st>>>(q); }
-    else { set_attr_once<false, false>(); dgemm_kernel<false, false><<<grid, 256, smem, st>>>(q); }
+    if (TA) launch_dgemm<true, false>(false, grid, smem, st, q);
+    else launch_dgemm<false, false>(false, grid, smem, st, q);
     ++g_launches;
   }
   return cudaGetLastError();
