@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(CT_NT, 1) chol_tiles_kernel(int m, double* __r
   double* colj = Li + CT_MAXNB * 256;            // 16: column broadcast of the diagonal factor
   double* scr = colj + 16;                       // (CT_MAXNB / 2) * 256: dinv assembly
   __shared__ double red[CT_NW];
+  __shared__ double rsd[16];
   __shared__ int bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
@@ -131,6 +132,7 @@ __global__ void __launch_bounds__(CT_NT, 1) chol_tiles_kernel(int m, double* __r
         const double d = __shfl_sync(0xffffffffu, x[j & 7], j + 16 * (j >> 3));
         if (16 * J + j < m && (d <= 0.0 || d <= floor_)) fail = true;  // uniform
         const double rs = rsqrt(d), ljj = d * rs;
+        if (lane == 0) rsd[j] = rs;  // 1 / l_jj for the inverse below
         if (h == (j >> 3)) {  // the lanes holding column j
           const double l = r == j ? ljj : (r > j ? x[j & 7] * rs : 0.0);
           x[j & 7] = l;
@@ -166,7 +168,7 @@ __global__ void __launch_bounds__(CT_NT, 1) chol_tiles_kernel(int m, double* __r
               else if ((k & 3) == 2) s2 -= lk;
               else s3 -= lk;
             }
-            y[i] = ((s0 + s1) + (s2 + s3)) / T[ct_sw(i, i)];
+            y[i] = ((s0 + s1) + (s2 + s3)) * rsd[i];  // no division on the chain
           }
 #pragma unroll
           for (int i = 0; i < 16; ++i) Ti[ct_sw(i, c)] = y[i];

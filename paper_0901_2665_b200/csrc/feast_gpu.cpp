@@ -914,11 +914,11 @@ Reduced reduced_gevp(feast_gpu_ctx* c, int m) {
   CK(cudaMemsetAsync(c->status.p, 0, sizeof(int), c->stream));
   c->Dv.ensure((size_t)((m + 31) / 32) * 1024);
   CK(cholesky(m, c->Lm.p, 1e-13, c->status.p, c->Dv.p, c->stream));
-  int st = 0;
-  CK(cudaMemcpyAsync(&st, c->status.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  sync(c);
+  // The Cholesky path is enqueued without waiting for the pivot check: status and eigenvalues
+  // come back with ONE synchronisation, and a failed factorisation (its trailing kernels ran
+  // on a partial factor; their output is discarded) falls through to the truncation path.
   r.evals.resize(m);
-  if (!st) {
+  {
     // C = L^-1 A L^-T  via two lower solves and transposes (eigh.hpp:192-196)
     CK(cudaMemcpyAsync(c->Cm.p, c->Aq.p, sizeof(double) * mm, cudaMemcpyDeviceToDevice, c->stream));
     CK(trsm_lower(m, c->Lm.p, c->Dv.p, c->Cm.p, m, m, c->stream));
@@ -928,10 +928,14 @@ Reduced reduced_gevp(feast_gpu_ctx* c, int m) {
     CK(symmetrize(c->Cm.p, m, m, c->stream));
     CK(sym_eig(c->eig, m, c->Cm.p, c->Ev.p, c->Phi.p, c->stream));
     CK(trsm_lower_t(m, c->Lm.p, c->Dv.p, c->Phi.p, m, m, c->stream));  // Phi = L^-T W
+    int st = 0;
+    CK(cudaMemcpyAsync(&st, c->status.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(r.evals.data(), c->Ev.p, sizeof(double) * m, cudaMemcpyDeviceToHost, c->stream));
     sync(c);
-    r.mo = m;
-    return r;
+    if (!st) {
+      r.mo = m;
+      return r;
+    }
   }
   // spectral truncation fallback (eigh.hpp:204-224)
   CK(cudaMemcpyAsync(c->Cm.p, c->Bq.p, sizeof(double) * mm, cudaMemcpyDeviceToDevice, c->stream));
