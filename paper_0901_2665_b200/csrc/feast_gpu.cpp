@@ -227,6 +227,7 @@ struct feast_gpu_ctx {
   int bench_m = 0;
   bool timing = false;
   cudaEvent_t ev[8] = {};
+  cudaEvent_t pev[2][3] = {};  // feast_solve phase timing per pass parity: contour start, RR start, RR end
 
   int owned() const { return e1 - e0; }
   bool streamed() const { return batch > 0 && batch < owned(); }
@@ -1126,6 +1127,12 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
   std::vector<int> counts;
 
   auto finalize = [&](int status, const Reduced& rr, int pass) {
+    sync(c);  // the last pass's X = Q Phi, and its RR end event
+    {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, c->pev[pass & 1][1], c->pev[pass & 1][2]));
+      out->reduce_s += 1e-3 * ms;
+    }
     out->status = status;
     out->loops_used = pass;
     std::vector<int> keep;
@@ -1168,28 +1175,36 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
       out->factorize_s += secs(t0);
       trace_mark(c, "solve: factor");
     }
-    const auto t_solve = std::chrono::steady_clock::now();
+    // phase times from device events (FeastTimings, core.hpp:54-59): the only host
+    // synchronisation per pass is the one the trace check needs (the Ritz values, inside
+    // reduced_gevp). A pass's RR end event (after X = Q Phi) is read one pass later.
+    cudaEvent_t* pe = c->pev[pass & 1];
+    CK(cudaEventRecord(pe[0], c->stream));
     contour_pass(c, m);
-    sync(c);
-    out->solve_s += secs(t_solve);
+    CK(cudaEventRecord(pe[1], c->stream));
     trace_mark(c, "solve: contour pass");
 
-    const auto t_reduce = std::chrono::steady_clock::now();
     Reduced rr;
     try {
       rr = rayleigh_ritz(c, m);
-      sync(c);
+      CK(cudaEventRecord(pe[2], c->stream));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, pe[0], pe[1]));  // complete: reduced_gevp synchronised
+      out->solve_s += 1e-3 * ms;
+      if (pass > 0) {
+        cudaEvent_t* pp = c->pev[(pass - 1) & 1];
+        CK(cudaEventElapsedTime(&ms, pp[1], pp[2]));
+        out->reduce_s += 1e-3 * ms;
+      }
     } catch (const Failure& f) {
       if (f.code != FEAST_EBREAKDOWN) throw;
       out->status = FEAST_STATUS_BREAKDOWN;
       out->loops_used = pass;
-      out->reduce_s += secs(t_reduce);
       if (out->trace_history) std::memcpy(out->trace_history, history.data(), sizeof(double) * history.size());
       if (out->in_interval_counts) std::memcpy(out->in_interval_counts, counts.data(), sizeof(int) * counts.size());
       out->total_s = secs(t_start);
       return;
     }
-    out->reduce_s += secs(t_reduce);
     trace_mark(c, "solve: rayleigh-ritz");
 
     double tr = 0.0;
@@ -1278,6 +1293,8 @@ int feast_gpu_create(int device, void* stream, feast_gpu_ctx** out) {
       c->own_stream = true;
     }
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
+    for (auto& pe : c->pev)
+      for (auto& e : pe) CK(cudaEventCreate(&e));
   });
   if (rc) {
     delete c;
@@ -1304,6 +1321,9 @@ void feast_gpu_destroy(feast_gpu_ctx* c) {
   if (c->eig) eig_destroy(c->eig);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& pe : c->pev)
+    for (auto& e : pe)
+      if (e) cudaEventDestroy(e);
   if (c->comm && nccl().commDestroy) nccl().commDestroy(c->comm);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   if (c->aux) cudaStreamDestroy(c->aux);
