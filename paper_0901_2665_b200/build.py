@@ -7,7 +7,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfeastgpu.so")
-SOURCES = ["blocktri.cu", "sweep.cu", "sweep_small.cu", "sweep_tma.cu", "gemm.cu", "band_apply.cu", "dense.cu", "chol.cu", "chol_tiles.cu", "eig.cu", "jacobi.cu", "tridiag.cu", "tridiag_tiles.cu", "tri_back.cu", "misc.cu", "feast_gpu.cpp"]
+SOURCES = ["blocktri.cu", "sweep.cu", "sweep_small.cu", "sweep_tma.cu", "gemm.cu", "band_apply.cu", "dense.cu", "chol.cu", "chol_tiles.cu", "eig.cu", "jacobi.cu", "tridiag.cu", "tridiag_tiles.cu", "tri_back.cu", "misc.cu", "csr_ingest.cu", "feast_gpu.cpp"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-Xlinker", "-soname=libfeastgpu.so"]
 

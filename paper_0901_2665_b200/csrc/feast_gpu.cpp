@@ -15,6 +15,7 @@
 #include <exception>
 #include <mutex>
 #include <thread>
+#include <tuple>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
@@ -217,6 +218,8 @@ struct feast_gpu_ctx {
   DevBuf<double2> W;
   DevBuf<double> Aq, Bq, Cm, Lm, Phi, Ev, Vm, S, Tm, Dv;
   DevBuf<int> keep;
+  DevBuf<double> csr;        // CSR operators as uploaded (set_pencil's device route)
+  DevBuf<CsrStats> csrstats;
   EigWork* eig = nullptr;
   int eig_cap = 0;
   // host phase tracing (FEAST_TRACE=1: host wall clock per phase to stderr; =2: with a stream
@@ -554,11 +557,112 @@ void check_operator(const feast_operator_t* o) {
   }
 }
 
+// ---- CSR operators taken in on the device (csr_ingest.cu) ----------------------
+// The route for the common case (A and B both CSR, row pointers well formed): the CSR arrays
+// go up once through the pinned stage, csr_scan validates them and measures bandwidth, block
+// fit and 1-norm in one pass, csr_to_blocktri assembles the blocks. Errors, messages and
+// storage decisions are those of the host path above (validate_csr, csr_bandwidth,
+// csr_fits_blocktri, norm_one, to_blocktri), which serves every other combination.
+bool csr_rowptr_ok(const feast_operator_t* o) {
+  if (!o || o->kind != FEAST_STORAGE_CSR || o->n < 1 || !o->row_ptr || !o->col_idx || !o->values) return false;
+  if (o->row_ptr[0] != 0) return false;
+  for (int i = 0; i < o->n; ++i)
+    if (o->row_ptr[i + 1] < o->row_ptr[i]) return false;
+  return true;
+}
+
+struct PinnedStage;
+PinnedStage& pinned_stage();
+double* pinned_stage_lock_get(size_t count, std::unique_lock<std::mutex>& lk);
+
+// copies (dst, src, bytes) pieces on up to 8 host threads
+void parallel_copies(const std::vector<std::tuple<char*, const char*, size_t>>& segs) {
+  constexpr size_t piece = 1u << 20;
+  std::vector<std::tuple<char*, const char*, size_t>> work;
+  for (auto& [d, s, nb] : segs)
+    for (size_t off = 0; off < nb; off += piece) work.emplace_back(d + off, s + off, std::min(piece, nb - off));
+  const int nt = (int)std::min<size_t>(std::min(8u, std::max(1u, std::thread::hardware_concurrency())), work.size());
+  if (nt <= 1) {
+    for (auto& [d, s, nb] : work) std::memcpy(d, s, nb);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      for (size_t w = t; w < work.size(); w += nt) std::memcpy(std::get<0>(work[w]), std::get<1>(work[w]), std::get<2>(work[w]));
+    });
+  for (auto& x : th) x.join();
+}
+
+struct DeviceCsr {
+  const int* rp[2];
+  const int* ci[2];
+  const double* val[2];
+  CsrStats stats[2];
+};
+
+// upload A and B, scan both; throws the host path's InputError for the first bad entry of A,
+// then of B
+DeviceCsr csr_upload_scan(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operator_t* b) {
+  const int n = a->n;
+  const size_t nnz[2] = {(size_t)a->row_ptr[n], (size_t)b->row_ptr[n]};
+  const size_t ints = 2 * ((size_t)n + 1) + nnz[0] + nnz[1];
+  const size_t idoubles = (ints + 1) / 2, total = idoubles + nnz[0] + nnz[1];
+  c->csr.ensure(total);
+  c->csrstats.ensure(2);
+  DeviceCsr d;
+  int* ip = reinterpret_cast<int*>(c->csr.p);
+  double* vp = c->csr.p + idoubles;
+  const feast_operator_t* ops[2] = {a, b};
+  {
+    std::unique_lock<std::mutex> lk;
+    double* st = pinned_stage_lock_get(total, lk);
+    std::vector<std::tuple<char*, const char*, size_t>> segs;
+    int* sip = st ? reinterpret_cast<int*>(st) : nullptr;
+    size_t io = 0, vo = 0;
+    for (int t = 0; t < 2; ++t) {
+      const feast_operator_t* o = ops[t];
+      d.rp[t] = ip + io;
+      if (st) segs.emplace_back(reinterpret_cast<char*>(sip + io), reinterpret_cast<const char*>(o->row_ptr), sizeof(int) * (n + 1));
+      else CK(cudaMemcpyAsync(ip + io, o->row_ptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, c->stream));
+      io += n + 1;
+      d.ci[t] = ip + io;
+      if (st) segs.emplace_back(reinterpret_cast<char*>(sip + io), reinterpret_cast<const char*>(o->col_idx), sizeof(int) * nnz[t]);
+      else if (nnz[t]) CK(cudaMemcpyAsync(ip + io, o->col_idx, sizeof(int) * nnz[t], cudaMemcpyHostToDevice, c->stream));
+      io += nnz[t];
+      d.val[t] = vp + vo;
+      if (st) segs.emplace_back(reinterpret_cast<char*>(st + idoubles + vo), reinterpret_cast<const char*>(o->values), sizeof(double) * nnz[t]);
+      else if (nnz[t]) CK(cudaMemcpyAsync(vp + vo, o->values, sizeof(double) * nnz[t], cudaMemcpyHostToDevice, c->stream));
+      vo += nnz[t];
+    }
+    if (st) {
+      parallel_copies(segs);
+      CK(cudaMemcpyAsync(c->csr.p, st, sizeof(double) * total, cudaMemcpyHostToDevice, c->stream));
+    }
+    for (int t = 0; t < 2; ++t) CK(csr_scan(n, d.rp[t], d.ci[t], d.val[t], c->csrstats.p + t, true, c->stream));
+    CK(cudaMemcpyAsync(d.stats, c->csrstats.p, sizeof(d.stats), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);  // (also the end of the stage's use)
+  }
+  static const char* msg[3] = {"SymmetricOperator: triplet index out of range",
+                               "SymmetricOperator: missing mirror entry",
+                               "SymmetricOperator: mirror entries disagree"};
+  for (int t = 0; t < 2; ++t)
+    if (d.stats[t].first_error != ~0ull) fail(FEAST_EINPUT, msg[d.stats[t].first_error & 3]);
+  return d;
+}
+
 void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operator_t* b) {
   trace_mark(c, nullptr);
-  check_operator(a);
-  check_operator(b);
-  trace_mark(c, "set_pencil: validate operators");
+  const bool dev_csr = csr_rowptr_ok(a) && csr_rowptr_ok(b) && a->n == b->n;
+  DeviceCsr dcsr{};
+  if (dev_csr) {
+    dcsr = csr_upload_scan(c, a, b);
+    trace_mark(c, "set_pencil: CSR upload + device validation");
+  } else {
+    check_operator(a);
+    check_operator(b);
+    trace_mark(c, "set_pencil: validate operators");
+  }
   if (a->n != b->n) fail(FEAST_EINPUT, "feast_solve: operator dimensions differ");
   const int n = a->n;
   // storage policy (the reference's Auto policy, inner_solver.hpp:84-92, with the banded
@@ -572,7 +676,8 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
     } else {
       int bw = 0;
       for (const feast_operator_t* o : {a, b}) {
-        if (o->kind == FEAST_STORAGE_CSR) bw = std::max(bw, csr_bandwidth(o));
+        if (dev_csr) bw = std::max({bw, dcsr.stats[0].bandwidth, dcsr.stats[1].bandwidth});
+        else if (o->kind == FEAST_STORAGE_CSR) bw = std::max(bw, csr_bandwidth(o));
         else bw = std::max(bw, 2 * o->bsize - 1);
       }
       if ((3 * bw + 1) * 2 <= n) {
@@ -583,7 +688,8 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
         for (int cand = lo; cand <= hi && !bsz; cand *= 2) {
           bool ok = true;
           for (const feast_operator_t* o : {a, b}) {
-            if (o->kind == FEAST_STORAGE_CSR) ok = ok && csr_fits_blocktri(o, cand);
+            if (dev_csr) ok = ok && !(((dcsr.stats[0].misfit_mask | dcsr.stats[1].misfit_mask) >> (log2_exact(cand) - 4)) & 1u);
+            else if (o->kind == FEAST_STORAGE_CSR) ok = ok && csr_fits_blocktri(o, cand);
             else ok = ok && cand >= o->bsize && cand % o->bsize == 0;
           }
           if (ok) bsz = cand;
@@ -598,27 +704,39 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
   c->mcap = 0;
   c->n = n;
   trace_mark(c, "set_pencil: storage choice");
-  c->norm_a1 = norm_one(a);
+  if (dev_csr) {
+    double nrm;
+    std::memcpy(&nrm, &dcsr.stats[0].norm1_bits, sizeof(double));
+    c->norm_a1 = nrm;
+  } else {
+    c->norm_a1 = norm_one(a);
+  }
   trace_mark(c, "set_pencil: norm_1(A)");
   if (bsz) {
     c->blocktri = true;
     c->b = bsz;
     c->L = (n + bsz - 1) / bsz;
     c->npad = c->L * bsz;
-    std::vector<double> ad, al, bd, bl;
-    to_blocktri(a, bsz, c->L, false, ad, al);
-    to_blocktri(b, bsz, c->L, true, bd, bl);
-    trace_mark(c, "set_pencil: re-block A, B");
     // plain real copies [diag blocks | lower blocks] for the operator applies (bt_apply); the
     // interleaved (A, B) pairs of the factorisation are packed from them on the device
-    const size_t nd = ad.size(), nl = al.size();
+    const size_t nd = (size_t)c->L * bsz * bsz, nl = (size_t)(c->L > 1 ? c->L - 1 : 0) * bsz * bsz;
     c->A.ensure(nd + nl);
     c->Bm.ensure(nd + nl);
-    CK(cudaMemcpyAsync(c->A.p, ad.data(), sizeof(double) * nd, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->Bm.p, bd.data(), sizeof(double) * nd, cudaMemcpyHostToDevice, c->stream));
-    if (nl) {
-      CK(cudaMemcpyAsync(c->A.p + nd, al.data(), sizeof(double) * nl, cudaMemcpyHostToDevice, c->stream));
-      CK(cudaMemcpyAsync(c->Bm.p + nd, bl.data(), sizeof(double) * nl, cudaMemcpyHostToDevice, c->stream));
+    if (dev_csr) {
+      CK(csr_to_blocktri(n, bsz, c->L, dcsr.rp[0], dcsr.ci[0], dcsr.val[0], c->A.p, c->A.p + nd, false, c->stream));
+      CK(csr_to_blocktri(n, bsz, c->L, dcsr.rp[1], dcsr.ci[1], dcsr.val[1], c->Bm.p, c->Bm.p + nd, true, c->stream));
+    } else {
+      std::vector<double> ad, al, bd, bl;
+      to_blocktri(a, bsz, c->L, false, ad, al);
+      to_blocktri(b, bsz, c->L, true, bd, bl);
+      trace_mark(c, "set_pencil: re-block A, B");
+      CK(cudaMemcpyAsync(c->A.p, ad.data(), sizeof(double) * nd, cudaMemcpyHostToDevice, c->stream));
+      CK(cudaMemcpyAsync(c->Bm.p, bd.data(), sizeof(double) * nd, cudaMemcpyHostToDevice, c->stream));
+      if (nl) {
+        CK(cudaMemcpyAsync(c->A.p + nd, al.data(), sizeof(double) * nl, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->Bm.p + nd, bl.data(), sizeof(double) * nl, cudaMemcpyHostToDevice, c->stream));
+      }
+      sync(c);  // the host vectors die here
     }
     c->abdiag.ensure(nd);
     c->ablow.ensure(std::max<size_t>(nl, 1));
@@ -635,6 +753,7 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
       c->Bband.release();
     }
     sync(c);
+    c->csr.release();  // back to the stream-ordered pool (reused by the next set_pencil)
     trace_mark(c, "set_pencil: alloc + H2D");
   } else {
     c->blocktri = false;
@@ -1025,6 +1144,12 @@ PinnedStage& pinned_stage() {
   static PinnedStage* s = new PinnedStage();  // never destroyed: may be used until exit
   return *s;
 }
+// the stage for `count` doubles with its lock held in lk (nullptr: pinned memory unavailable)
+double* pinned_stage_lock_get(size_t count, std::unique_lock<std::mutex>& lk) {
+  PinnedStage& ps = pinned_stage();
+  lk = std::unique_lock<std::mutex>(ps.mu);
+  return ps.get(count);
+}
 
 void download_block(feast_gpu_ctx* c, const double* dev, int m, double* host) {
   const size_t cnt = (size_t)c->n * m;
@@ -1045,6 +1170,72 @@ void download_block(feast_gpu_ctx* c, const double* dev, int m, double* host) {
   }
   CK(cudaMemcpy2DAsync(host, sizeof(double) * c->n, dev, sizeof(double) * c->npad, sizeof(double) * c->n, m,
                        cudaMemcpyDeviceToHost, c->stream));
+}
+
+// Several result blocks at once, pipelined: column chunks of ~4 MB are DMA'd into the pinned
+// stage back to back, each followed by an event, and host threads copy chunk i into the
+// caller's block as soon as its event fires, while the later chunks are still in flight.
+struct Download {
+  const double* dev;
+  int m;
+  double* host;
+};
+void download_blocks(feast_gpu_ctx* c, const std::vector<Download>& dl) {
+  const size_t n = c->n;
+  size_t total = 0;
+  for (auto& d : dl) total += n * d.m;
+  if (total * sizeof(double) < (8u << 20)) {
+    for (auto& d : dl) download_block(c, d.dev, d.m, d.host);
+    return;
+  }
+  std::unique_lock<std::mutex> lk;
+  double* st = pinned_stage_lock_get(total, lk);
+  if (!st) {
+    lk.unlock();
+    for (auto& d : dl) download_block(c, d.dev, d.m, d.host);
+    return;
+  }
+  const int per = std::max<int>(1, (int)((4u << 20) / (sizeof(double) * n)));  // columns per chunk
+  struct Chunk {
+    double* stage;
+    double* host;
+    size_t count;
+    cudaEvent_t ev;
+  };
+  static std::vector<cudaEvent_t> evs;  // guarded by the stage lock
+  std::vector<Chunk> ch;
+  size_t off = 0;
+  for (auto& d : dl)
+    for (int j = 0; j < d.m; j += per) {
+      const int w = std::min(per, d.m - j);
+      if (ch.size() == evs.size()) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        evs.push_back(e);
+      }
+      Chunk k{st + off, d.host + n * j, n * w, evs[ch.size()]};
+      CK(cudaMemcpy2DAsync(k.stage, sizeof(double) * n, d.dev + (size_t)c->npad * j, sizeof(double) * c->npad,
+                           sizeof(double) * n, w, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaEventRecord(k.ev, c->stream));
+      ch.push_back(k);
+      off += n * w;
+    }
+  const int nt = (int)std::min<size_t>(std::min(8u, std::max(1u, std::thread::hardware_concurrency())), ch.size());
+  std::atomic<bool> bad{false};
+  auto work = [&](int t) {
+    for (size_t i = t; i < ch.size(); i += nt) {
+      if (cudaEventSynchronize(ch[i].ev) != cudaSuccess) {
+        bad = true;
+        return;
+      }
+      std::memcpy(ch[i].host, ch[i].stage, sizeof(double) * ch[i].count);
+    }
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < nt; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+  if (bad) CK(cudaStreamSynchronize(c->stream));  // raises the stream's error
 }
 
 // residual_norms (residual.hpp:29-68) of the first m columns of X (device, ld npad)
@@ -1152,8 +1343,10 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
     trace_mark(c, "finalize: gather");
     // (pinning the caller's blocks with cudaHostRegister for these copies measured slower:
     // 13.4 vs 10.2 ms for 41 MB at config 2, the registration costs more than it saves)
-    if (out->eigenvectors && k) download_block(c, c->Q.p, k, out->eigenvectors);
-    if (out->subspace) download_block(c, c->X.p, rr.mo, out->subspace);
+    std::vector<Download> dl;
+    if (out->eigenvectors && k) dl.push_back({c->Q.p, k, out->eigenvectors});
+    if (out->subspace) dl.push_back({c->X.p, rr.mo, out->subspace});
+    download_blocks(c, dl);
     trace_mark(c, "finalize: D2H eigenvectors + subspace");
     std::vector<double> res(k);
     std::vector<int32_t> ab(k);
@@ -1311,8 +1504,9 @@ void feast_gpu_destroy(feast_gpu_ctx* c) {
   cudaStreamSynchronize(c->stream);
   AllocStream as(c->stream);
   for (DevBuf<double>* d : {&c->A, &c->Bm, &c->Y, &c->Q, &c->X, &c->AQ, &c->BQ, &c->T, &c->gw, &c->Aq, &c->Bq,
-                            &c->Cm, &c->Lm, &c->Phi, &c->Ev, &c->Vm, &c->S, &c->Tm, &c->Dv, &c->Aband, &c->Bband})
-    d->release();  // every buffer, before the stream goes (the destructor would free on a dead stream)
+                            &c->Cm, &c->Lm, &c->Phi, &c->Ev, &c->Vm, &c->S, &c->Tm, &c->Dv, &c->Aband, &c->Bband, &c->csr})
+    d->release();
+  c->csrstats.release();  // every buffer, before the stream goes (the destructor would free on a dead stream)
   for (DevBuf<double2>* d : {&c->abdiag, &c->ablow, &c->dz, &c->dcoeff, &c->sinv, &c->gfac, &c->hfac, &c->lu, &c->dinv,
                              &c->scratch, &c->W, &c->fwork})
     d->release();

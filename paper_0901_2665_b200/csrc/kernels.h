@@ -169,6 +169,25 @@ cudaError_t residual_sums(int n, int m, const double* ax, const double* bx, cons
 cudaError_t random_block_device(uint64_t seed, int n, int m, double* out, int ld, cudaStream_t st);
 
 // out[i] = (a[i], b[i]): the interleaved (A, B) pairs of the block-tridiagonal factorisation
+// ---------------- CSR operators taken in on the device (csr_ingest.cu) ----------
+// Result of csr_scan over one operator: first_error = 4 * (entry index) + code of the first
+// failing entry in row-major order (~0: none), the bandwidth max |i - j|, bit s of misfit_mask
+// set when the pattern is not block-tridiagonal at block size 16 << s, and the 1-norm (max
+// absolute row sum = column sum for a symmetric pattern) as the bits of a non-negative double.
+constexpr int kCsrOutOfRange = 0, kCsrMirrorMissing = 1, kCsrMirrorDiffers = 2;
+constexpr int kCsrBlockCandidates = 6;  // 16 .. 512
+struct CsrStats {
+  unsigned long long first_error;
+  unsigned long long norm1_bits;
+  int bandwidth;
+  unsigned misfit_mask;
+};
+cudaError_t csr_scan(int n, const int* row_ptr, const int* col_idx, const double* values, CsrStats* stats,
+                     bool init, cudaStream_t st);
+// block-tridiagonal storage (L diagonal blocks, L-1 couplings C_l = M(l+1, l), b x b col-major,
+// b a power of two) from device CSR arrays; unit_padding: rows n..L*b-1 get a unit diagonal
+cudaError_t csr_to_blocktri(int n, int b, int L, const int* row_ptr, const int* col_idx, const double* values,
+                            double* diag, double* low, bool unit_padding, cudaStream_t st);
 cudaError_t interleave_pairs(const double* a, const double* b, size_t n, double2* out, cudaStream_t st);
 
 // accumulate_subspace_hermitian for real symmetric pencils (misc.cu): complex right-hand
