@@ -33,6 +33,8 @@ _cache = {}
 
 
 def available(kind="reference"):
+    if kind == "mm":
+        return os.path.exists(os.path.join(_HERE, "_ref", "ref_mm_dump"))
     return os.path.exists(LIBS[kind])
 
 
@@ -291,3 +293,25 @@ def unpack_result(out, r, n):
         timings=dict(factorize_s=r.factorize_s, solve_s=r.solve_s, reduce_s=r.reduce_s,
                      total_s=r.total_s),
     )
+
+
+class ReferenceInputError(Exception):
+    """InputError raised inside the reference library (message = what())."""
+
+
+def mm_load_reference(path):
+    """load_matrix_market_real (matrix_market.cpp:106-116) of the reference itself, run as
+    oracle/_ref/ref_mm_dump: (n, row_ptr, col_idx, values) of the symmetric-complete CSR operator."""
+    import subprocess
+    exe = os.path.join(_HERE, "_ref", "ref_mm_dump")
+    out = subprocess.run([exe, str(path)], capture_output=True, text=True, check=True).stdout
+    head, _, rest = out.partition("\n")
+    if head.startswith("ERR "):
+        raise ReferenceInputError(head[4:])
+    _, n, nnz = head.split()
+    n, nnz = int(n), int(nnz)
+    lines = rest.split("\n")
+    rp = np.array([int(x) for x in lines[:n + 1]], np.int32)
+    ci = np.array([int(x.split()[0]) for x in lines[n + 1:n + 1 + nnz]], np.int32)
+    v = np.array([float.fromhex(x.split()[1]) for x in lines[n + 1:n + 1 + nnz]], np.float64)
+    return n, rp, ci, v

@@ -241,7 +241,10 @@ namespace {
 
 void ensure_eig(feast_gpu_ctx* c, int m) {
   if (c->eig && c->eig_cap >= m) return;
-  if (c->eig) eig_destroy(c->eig);
+  if (c->eig) {
+    CK(cudaStreamSynchronize(c->stream));  // a released workspace may go to another context
+    eig_destroy(c->eig);
+  }
   c->eig = eig_create(std::max(m, 16));
   c->eig_cap = std::max(m, 16);
 }

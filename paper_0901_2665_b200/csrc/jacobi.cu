@@ -21,6 +21,9 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include <mutex>
+#include <vector>
+
 #include "kernels.h"
 
 namespace cg = cooperative_groups;
@@ -57,7 +60,15 @@ struct EigWork {
   double* tws = nullptr;   // tridiagonal route (m <= tri_max_dim): 6m^2 + 3m
   int* tiws = nullptr;     // m^2
   int grid = 0;
+  int dev = 0;
 };
+
+// Process-wide cache of released workspaces: a fresh context (every end-to-end solve opens one)
+// takes a cached set of the same size instead of seven cudaMalloc calls, and a destroyed one
+// parks its set instead of seven device-synchronising cudaFree calls.
+static std::mutex g_eig_mu;
+static std::vector<EigWork*> g_eig_cache;
+constexpr size_t kEigCacheMax = 4;
 
 static int eig_bs(int m) { return m <= 256 ? 16 : 32; }
 static int eig_mp(int m) {
@@ -69,7 +80,19 @@ static int eig_mp(int m) {
 }
 
 EigWork* eig_create(int mmax) {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  {
+    std::lock_guard<std::mutex> lk(g_eig_mu);
+    for (size_t i = 0; i < g_eig_cache.size(); ++i)
+      if (g_eig_cache[i]->mmax == mmax && g_eig_cache[i]->dev == cur) {
+        EigWork* w = g_eig_cache[i];
+        g_eig_cache.erase(g_eig_cache.begin() + i);
+        return w;
+      }
+  }
   EigWork* w = new EigWork();
+  w->dev = cur;
   w->mmax = mmax;
   const int mp = std::max(eig_mp(mmax), eig_mp(std::min(mmax, 256)));
   cudaMalloc(&w->w, sizeof(double) * mp * mp);
@@ -90,6 +113,13 @@ EigWork* eig_create(int mmax) {
 
 void eig_destroy(EigWork* w) {
   if (!w) return;
+  {
+    std::lock_guard<std::mutex> lk(g_eig_mu);  // (the caller has synchronised its stream)
+    if (g_eig_cache.size() < kEigCacheMax) {
+      g_eig_cache.push_back(w);
+      return;
+    }
+  }
   cudaFree(w->w);
   cudaFree(w->v);
   cudaFree(w->j);

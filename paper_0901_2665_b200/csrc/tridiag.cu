@@ -7,8 +7,9 @@
 //   tridiag_kernel      Householder reduction A = Q T Q^T (dsytd2, lower); the working
 //                       matrix lives in packed lower-triangular SHARED memory (m(m+1)/2
 //                       doubles, 148 KB at m = 192); one CTA of 1024 threads; reflectors out.
-//   tri_eigvals_kernel  one warp per eigenvalue: 32-way multisection of the Sturm count of
-//                       T - sigma I (dstebz) down to round-off; eigenvalue j is the j-th.
+//   tri_eigvals_kernel  a group of 1-4 warps per eigenvalue: (128 x warps)-point multisection
+//                       of the Sturm count of T - sigma I (dstebz) down to round-off;
+//                       eigenvalue j is the j-th.
 //   tri_eigvecs_kernel  one warp per cluster (|lam_i - lam_j| <= 1e-5 ||T||, cf. dstein):
 //                       inverse iteration with the partial-pivot tridiagonal LU (dgttrf /
 //                       dgtts2), modified Gram-Schmidt against earlier cluster members.
@@ -803,13 +804,14 @@ __device__ __forceinline__ double fast_rcp1(double x) {
   return fma(r, fma(-x, r, 1.0), r);
 }
 
-// four Sturm counts at once (independent chains interleaved: the division latency of one
-// chain hides behind the other three)
-__device__ __forceinline__ void sturm4(int m, const double* d, const double* e2, const double (&sg)[4], double pivmin,
-                                       int (&cnt)[4]) {
-  double q[4];
+// NCH Sturm counts at once (independent chains interleaved: the latency of one chain's
+// reciprocal and FMAs hides behind the others; the chain step is latency-bound at 4)
+template <int NCH>
+__device__ __forceinline__ void sturm_n(int m, const double* d, const double* e2, const double (&sg)[NCH],
+                                        double pivmin, int (&cnt)[NCH]) {
+  double q[NCH];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < NCH; ++u) {
     q[u] = d[0] - sg[u];
     if (fabs(q[u]) < pivmin) q[u] = -pivmin;
     cnt[u] = q[u] < 0.0;
@@ -817,7 +819,7 @@ __device__ __forceinline__ void sturm4(int m, const double* d, const double* e2,
   for (int i = 1; i < m; ++i) {
     const double di = d[i], ei = e2[i - 1];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < NCH; ++u) {
       q[u] = (di - sg[u]) - ei * fast_rcp1(q[u]);
       if (fabs(q[u]) < pivmin) q[u] = -pivmin;
       cnt[u] += q[u] < 0.0;
@@ -853,11 +855,16 @@ __device__ void tri_bounds(int m, const double* d, const double* e, double& lo, 
   hi += slack;
 }
 
+// WPE warps per eigenvalue (a named barrier per group of WPE warps), EPC = warps / WPE
+// eigenvalues per CTA: each step is a (128 WPE)-point multisection, the WPE warps of a group
+// sitting on different SM sub-partitions so the wider step costs no more than a one-warp one
+template <int WPE, int NCH>
 __global__ void tri_eigvals_kernel(TriArgs p) {
   extern __shared__ double sm[];
   double* d = sm;
   double* e2 = d + p.m;
   double* e = e2 + p.m;
+  __shared__ int s_nb[2][32];
   const int m = p.m;
   for (int i = threadIdx.x; i < m; i += blockDim.x) {
     d[i] = p.d[i];
@@ -869,29 +876,40 @@ __global__ void tri_eigvals_kernel(TriArgs p) {
   __syncthreads();
   double lo, hi, tnorm, pivmin;
   tri_bounds(m, d, e, lo, hi, tnorm, pivmin);  // from shared memory: one pass, no L2 round trips
-  const int lane = threadIdx.x & 31;
-  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = warp / WPE, wg = warp % WPE;
+  const int epc = (blockDim.x >> 5) / WPE;
+  const int j = blockIdx.x * epc + grp;
   if (j >= m) return;
-  // 128-point multisection per step (4 Sturm chains per lane): points a + w (P + 1) / 129,
-  // P = 4 lane + u, computed identically on every lane; invariant count(a) <= j < count(b)
+  constexpr int PT = 32 * NCH * WPE;       // points per step
+  constexpr double INV = 1.0 / (PT + 1);   // (exact enough: only the grid's spacing uses it)
+  // points a + w (P + 1) / (PT + 1), P = 32 NCH wg + NCH lane + u, computed identically on every
+  // lane of the group; invariant count(a) <= j < count(b)
   double a = lo, b = hi;
   for (int it = 0; it < 16; ++it) {
     const double width = b - a;
     if (width <= 2.0 * DBL_EPSILON * fmax(fabs(a), fabs(b)) + 2.0 * pivmin) break;
-    double sg[4];
-    int c[4];
+    double sg[NCH];
+    int c[NCH];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) sg[u] = a + width * (double)(4 * lane + u + 1) / 129.0;
-    sturm4(m, d, e2, sg, pivmin, c);
+    for (int u = 0; u < NCH; ++u) sg[u] = a + width * ((double)(32 * NCH * wg + NCH * lane + u + 1) * INV);
+    sturm_n<NCH>(m, d, e2, sg, pivmin, c);
     int nb = 0;  // points left of lam_j (counts are monotone in the point index)
 #pragma unroll
-    for (int u = 0; u < 4; ++u) nb += __popc(__ballot_sync(0xffffffffu, c[u] <= j));
-    const double na = nb > 0 ? a + width * (double)nb / 129.0 : a;
-    const double nbb = nb < 128 ? a + width * (double)(nb + 1) / 129.0 : b;
+    for (int u = 0; u < NCH; ++u) nb += __popc(__ballot_sync(0xffffffffu, c[u] <= j));
+    if (WPE > 1) {
+      if (lane == 0) s_nb[it & 1][warp] = nb;
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(32 * WPE) : "memory");
+      nb = 0;
+#pragma unroll
+      for (int w = 0; w < WPE; ++w) nb += s_nb[it & 1][grp * WPE + w];
+    }
+    const double na = nb > 0 ? a + width * ((double)nb * INV) : a;
+    const double nbb = nb < PT ? a + width * ((double)(nb + 1) * INV) : b;
     a = na;
     b = nbb;
   }
-  if (lane == 0) p.lam[j] = 0.5 * (a + b);
+  if (lane == 0 && wg == 0) p.lam[j] = 0.5 * (a + b);
 }
 
 // ---------------------------------------------------------------------------
@@ -1272,9 +1290,26 @@ cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws
   // one warp per CTA: these are serial per-warp chains, so spreading the m warps over all 148
   // SMs (instead of 4 per CTA on m/4 SMs) is what sets their time (ncu: issue-bound at 4 warps
   // per SM, 114 / 85 / 90 us for eigvals / eigvecs / back at m = 192)
-  const int wpb = 1;
-  tri_eigvals_kernel<<<(m + wpb - 1) / wpb, 32 * wpb, sizeof(double) * 3 * m, st>>>(p);
+  // eigenvalues: FEAST_EIGVALS="<warps per eigenvalue 1-4><eigenvalues per CTA><chains per lane
+  // 2|4|8>" (default 222: two 2-warp groups per CTA, each warp on its own SM sub-partition, two
+  // Sturm chains per lane = 128 points per step). The chain step is bound by MUFU.RCP64H
+  // throughput, so fewer chains per lane on more sub-partitions win. Measured at m = 192 (ncu,
+  // cfg2): 116 us for one warp x 4 chains, 92 us for 2 warps x 4 chains, 78 us for 2 warps x 2
+  // chains, 86 us for 3-4 warps x 2 chains, 264 us for 2 warps x 8 chains
+  static const char* ev_env = getenv("FEAST_EIGVALS");
+  const int wpe = ev_env ? ev_env[0] - '0' : 2, epc = ev_env && ev_env[1] ? ev_env[1] - '0' : 2;
+  const int nch = ev_env && ev_env[1] && ev_env[2] ? ev_env[2] - '0' : 2;
+  const unsigned evb = (unsigned)((m + epc - 1) / epc), evt = 32u * wpe * epc;
+  const size_t evs = sizeof(double) * 3 * m;
+#define FEAST_EIGVALS_CASE(W, C) \
+  if (wpe == W && nch == C) tri_eigvals_kernel<W, C><<<evb, evt, evs, st>>>(p); else
+  FEAST_EIGVALS_CASE(1, 2) FEAST_EIGVALS_CASE(2, 4) FEAST_EIGVALS_CASE(3, 2) FEAST_EIGVALS_CASE(4, 2)
+  FEAST_EIGVALS_CASE(1, 8) FEAST_EIGVALS_CASE(2, 8) FEAST_EIGVALS_CASE(1, 4) FEAST_EIGVALS_CASE(3, 4)
+  FEAST_EIGVALS_CASE(4, 4) tri_eigvals_kernel<2, 2><<<evb, evt, evs, st>>>(p);
+#undef FEAST_EIGVALS_CASE
   ++g_launches;
+  static const char* evv_env = getenv("FEAST_EIGVECS_WPB");
+  const int wpb = evv_env ? atoi(evv_env) : 1;
   const size_t vsm = sizeof(double) * (6 * m * wpb + 2 * m) + 64;
   if (vsm > 48 * 1024) cudaFuncSetAttribute(tri_eigvecs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsm);
   tri_eigvecs_kernel<<<(m + wpb - 1) / wpb, 32 * wpb, vsm, st>>>(p);
