@@ -149,6 +149,12 @@ int feast_gpu_prepare(feast_gpu_ctx* ctx, double emin, double emax, int n_e);
  * resident plan). Takes effect at the next feast_gpu_prepare / feast_gpu_solve. */
 int feast_gpu_set_node_batch(feast_gpu_ctx* ctx, int nodes);
 
+/* Block-Thomas recursion for block-tridiagonal pencils with b <= 64: enable = 1 (default) runs
+ * the two-ended (twisted) elimination that meets at layer L/2, enable = 0 the plain top-down
+ * chain of BandedLU (lu.hpp:127-206). Both give the same solves to rounding; takes effect at the
+ * next factorisation. */
+int feast_gpu_set_twist(feast_gpu_ctx* ctx, int enable);
+
 /* random_block<double> (core.hpp:84-106) generated on the device: out (host, n*m column-major)
  * = 2 * ((w >> 11) * 2^-53) - 1 over the std::mt19937_64(seed) words w, bit-identical to the
  * reference's host generator. feast_gpu_solve draws its initial block this way. */

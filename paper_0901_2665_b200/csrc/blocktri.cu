@@ -364,27 +364,17 @@ static cudaError_t launch_factor_small(const BtFactorArgs& a, cudaStream_t st) {
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-int bt_twist_layer(int L, int b) {
-  const char* s = std::getenv("FEAST_BT_TWIST");  // read per call: tests flip it per context
-  const bool off = s && s[0] == '0';
-  return (!off && b <= 64 && L >= 4) ? L / 2 : -1;
-}
+int bt_twist_layer(int L, int b, bool enable) { return (enable && b <= 64 && L >= 4) ? L / 2 : -1; }
 
 // ---------------------------------------------------------------------------
 // Large blocks (b >= 128): the same recursion, every dense b x b operation batched over the
 // nodes and run on the DMMA GEMM / batched-LU kernels (one layer at a time):
-//   S_l = M_l - C_{l-1} G_{l-1}  (zgemm) ;  S_l^{-1} by block Gauss-Jordan in place (below;
-//   FEAST_BT_FACTOR=lu selects pivoted LU + solve against I instead) ;
+//   S_l = M_l - C_{l-1} G_{l-1}  (zgemm) ;  S_l^{-1} by block Gauss-Jordan in place (below) ;
 //   H_l = S_l^{-1} C_{l-1} ;  G_l = S_l^{-1} C_l^T  (zgemm) ; all three packed into panels
 // ---------------------------------------------------------------------------
 cudaError_t zgemm_batched(int m, int n, int k, double2 alpha, const double2* a, int lda, int64_t sa,
                           const double2* b, int ldb, int64_t sb, double2 beta, double2* c, int ldc,
                           int64_t sc, int batch, cudaStream_t st);
-cudaError_t zgetrf_batched(int n, int nodes, double2* lu, int64_t stride, int* ipiv, int* perm, double2* dinv,
-                           int* status, cudaStream_t st);
-cudaError_t zgetrs_batched(int n, int nodes, int m, const double2* lu, int64_t stride, const int* perm,
-                           const double2* dinv, double2* w, int ldv, double2* scratch, cudaStream_t st);
-
 // out_s = z_s * B - A for a block of (A, B) pairs (optionally transposed), or the identity
 __global__ void bt_make_kernel(int b, const double2* __restrict__ ab, const double2* __restrict__ z,
                                double2* __restrict__ out, int mode) {
@@ -542,31 +532,19 @@ static cudaError_t gj_invert_batched(double2* S, int n, int64_t sstride, int nod
   return cudaGetLastError();
 }
 
-static bool factor_use_lu() {
-  static const bool lu = [] {
-    const char* e = getenv("FEAST_BT_FACTOR");
-    return e && e[0] == 'l';
-  }();
-  return lu;
-}
-
 static cudaError_t bt_factor_big(const BtFactorArgs& a, cudaStream_t st) {
-  const bool lu = factor_use_lu();  // FEAST_BT_FACTOR=lu: pivoted LU + solve (comparison path)
   const int L = a.L, b = a.b, nodes = a.nodes;
   const int64_t bb = (int64_t)b * b, lnode = (int64_t)L * bb, gnode = (int64_t)(L > 1 ? L - 1 : 0) * bb;
-  double2* S = a.work;                 // LU of S_l            (nodes x bb)
+  double2* S = a.work;                 // S_l, then S_l^{-1}   (nodes x bb)
   double2* Cp = S + nodes * bb;        // C_{l-1}, then C_l
   double2* CT = Cp + nodes * bb;       // C_l^T
   double2* X = CT + nodes * bb;        // S_l^{-1}
-  double2* scr = X + nodes * bb;       // zgetrs scratch
-  double2* dinv = scr + nodes * bb;    // diagonal-block inverses
-  double2* gjw = dinv + (int64_t)nodes * ((b + kDenseNb - 1) / kDenseNb) * 2 * kDenseNb * kDenseNb;  // GJ work
-  int* ipiv = a.iwork;
-  int* perm = ipiv + nodes * b;
+  double2* scr = X + nodes * bb;       // G_l (col-major) until the next Schur update; I - S X
+  double2* gjw = scr + nodes * bb;     // Gauss-Jordan work
   const double2 one = make_double2(1.0, 0.0), mone = make_double2(-1.0, 0.0), zero = make_double2(0.0, 0.0);
   dim3 g((unsigned)std::min<int64_t>((bb + 255) / 256, 512), nodes);
   // factors leave in the sweep's panel layout; G_l also stays col-major in scr until the
-  // next layer's Schur update has used it (zgetrs reuses scr only after that)
+  // next layer's Schur update has used it (the refinement reuses scr only after that)
   const int rb = bt_panel_rows(b);
   auto pack = [&](const double2* src, double2* dst, int64_t dstride) {
     pack_panels_kernel<<<g, 256, 0, st>>>(src, dst, dstride, b, rb);
@@ -576,13 +554,7 @@ static cudaError_t bt_factor_big(const BtFactorArgs& a, cudaStream_t st) {
     bt_make_kernel<<<g, 256, 0, st>>>(b, a.abdiag + l * bb, a.z, S, 0);
     ++g_launches;
     if (l > 0) zgemm_batched(b, b, b, mone, Cp, b, bb, scr, b, bb, one, S, b, bb, nodes, st);
-    if (lu) {  // FEAST_BT_FACTOR=lu
-      zgetrf_batched(b, nodes, S, bb, ipiv, perm, dinv, a.status, st);
-      bt_make_kernel<<<g, 256, 0, st>>>(b, nullptr, a.z, X, 2);
-      ++g_launches;
-      zgetrs_batched(b, nodes, b, S, bb, perm, dinv, X, b, scr, st);
-    }
-    if (!lu) {
+    {
       // S^{-1} by pivot-free block Gauss-Jordan, then one Newton-Schulz refinement step
       // X' = X + X (I - S X): the near-real-axis nodes lose ~1 digit without pivoting, and
       // the refinement squares that residual (two DMMA GEMMs per layer)
@@ -612,9 +584,7 @@ static cudaError_t bt_factor_big(const BtFactorArgs& a, cudaStream_t st) {
 }
 
 size_t bt_factor_work_elems(int b, int nodes) {  // double2 elements of BtFactorArgs::work
-  const int nblk = (b + kDenseNb - 1) / kDenseNb;
-  return (size_t)nodes * (5 * (size_t)b * b + (size_t)nblk * 2 * kDenseNb * kDenseNb + 2 * (size_t)b * GJ_NB +
-                          (size_t)GJ_NB * GJ_NB);
+  return (size_t)nodes * (4 * (size_t)b * b + 2 * (size_t)b * GJ_NB + (size_t)GJ_NB * GJ_NB);
 }
 
 cudaError_t bt_factor(const BtFactorArgs& a, cudaStream_t st) {

@@ -181,133 +181,11 @@ __global__ void __launch_bounds__(256) chol_kernel(CholArgs p) {
   }
 }
 
-// ---------------------------------------------------------------------------
-// One-CTA Cholesky for m <= 192 (opt-in, FEAST_CHOL=s): the packed lower
-// triangle lives in shared memory (148 KB at m = 192), right-looking by columns with two block
-// barriers per column and no grid synchronisation (the cooperative kernel above pays three
-// grid barriers per 32-column panel plus its launch). Lane l owns rows l + 32t, warp w the
-// columns k = w (mod 16). Same pivot rule (d <= 0 or d <= rel_tol * max initial diagonal ->
-// status 1) and the same outputs: L in place (zero upper triangle) and the inverses of the
-// 32 x 32 diagonal tiles for the triangular solves.
-// ---------------------------------------------------------------------------
-constexpr int CS_SL = 6, CS_NW = 16, CS_NT = CS_NW * 32;
-
-__device__ __forceinline__ int cs_cb(int j, int m) { return j * m - (j * (j - 1)) / 2; }
-
-__global__ void __launch_bounds__(CS_NT, 1) chol_sm_kernel(CholArgs p) {
-  extern __shared__ double cps[];
-  const int m = p.m, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* ps = cps;                       // packed lower, column j at cs_cb(j)
-  double* lcol = ps + m * (m + 1) / 2;    // current column of L
-  __shared__ double red[CS_NW];
-  __shared__ int bad;
-  double md = 0.0;
-  for (int idx = tid; idx < m * m; idx += CS_NT) {
-    const int i = idx % m, j = idx / m;
-    if (i >= j) cp_async8z(ps + cs_cb(j, m) + i - j, p.a + idx, true);
-    if (i == j) md = fmax(md, p.a[idx]);
-  }
-  md = warp_max(md);
-  if (lane == 0) red[warp] = md;
-  if (tid == 0) bad = 0;
-  cp_async_wait_all();
-  __syncthreads();
-  double mx = 0.0;
-  for (int w = 0; w < CS_NW; ++w) mx = fmax(mx, red[w]);
-  const double floor_ = p.rel_tol * mx;
-
-  for (int j = 0; j < m; ++j) {
-    double* colj = ps + cs_cb(j, m) - j;  // colj[i] = A(i, j), i >= j
-    if (warp == (j % CS_NW)) {
-      const double dd = colj[j];         // the pivot after all earlier updates
-      if (dd <= 0.0 || dd <= floor_) {
-        if (lane == 0) bad = 1;
-      } else {
-        const double ljj = sqrt(dd), rl = 1.0 / ljj;
-#pragma unroll
-        for (int t = 0; t < CS_SL; ++t) {
-          const int i = lane + 32 * t;
-          if (i >= j && i < m) {
-            const double l = i == j ? ljj : colj[i] * rl;
-            colj[i] = l;
-            lcol[i] = l;
-          }
-        }
-      }
-    }
-    __syncthreads();
-    if (bad) {
-      if (tid == 0) p.status[0] = 1;
-      return;
-    }
-    double lr[CS_SL];
-#pragma unroll
-    for (int t = 0; t < CS_SL; ++t) {
-      const int i = lane + 32 * t;
-      lr[t] = i > j && i < m ? lcol[i] : 0.0;
-    }
-    // A(i, k) -= l_i l_k for k > j, i >= k: warp w takes k = w (mod CS_NW)
-    const int k0 = j + 1 + ((warp - (j + 1)) % CS_NW + CS_NW) % CS_NW;
-    for (int k = k0; k < m; k += CS_NW) {
-      double* colk = ps + cs_cb(k, m) - k;
-      const double lk = lcol[k];
-#pragma unroll
-      for (int t = 0; t < CS_SL; ++t) {
-        const int i = lane + 32 * t;
-        if (i >= k && i < m) colk[i] = fma(-lr[t], lk, colk[i]);
-      }
-    }
-    __syncthreads();
-  }
-  // L out (zero upper triangle), then the diagonal-tile inverses (warp per tile, lane per
-  // column of the inverse: forward substitution with the tile's rows broadcast)
-  for (int idx = tid; idx < m * m; idx += CS_NT) {
-    const int i = idx % m, j = idx / m;
-    p.a[idx] = i >= j ? ps[cs_cb(j, m) + i - j] : 0.0;
-  }
-  const int nblk = (m + TB - 1) / TB;
-  for (int pn = warp; pn < nblk; pn += CS_NW) {
-    const int p0 = pn * TB, pb = min(TB, m - p0);
-    const int c = lane;
-    double x[TB];
-#pragma unroll
-    for (int i = 0; i < TB; ++i) {
-      double sacc = i == c ? 1.0 : 0.0;
-#pragma unroll
-      for (int t = 0; t < i; ++t) {
-        const double lit = (i < pb && t < pb) ? ps[cs_cb(p0 + t, m) + i - t] : 0.0;
-        sacc = fma(-lit, x[t], sacc);
-      }
-      const double lii = i < pb ? ps[cs_cb(p0 + i, m)] : 1.0;
-      x[i] = sacc / lii;
-    }
-    double* Di = p.dinv + (int64_t)pn * TB * TB;
-#pragma unroll
-    for (int i = 0; i < TB; ++i) Di[i + c * TB] = (i < pb && c < pb) ? x[i] : (i == c ? 1.0 : 0.0);
-  }
-}
-
-static size_t chol_sm_bytes(int m) { return sizeof(double) * ((size_t)m * (m + 1) / 2 + m); }
-
 cudaError_t cholesky(int m, double* a, double rel_tol, int* status, double* dinv, cudaStream_t st) {
   if (m > 1024 || m < 1) return cudaErrorInvalidValue;
-  // one-CTA route: FEAST_CHOL=s only (measured 336 us against the cooperative kernel's 232 us
-  // at m = 192: per-slot predicates and the serial column chain keep the SM at ~0.45 IPC)
-  static const char* route = std::getenv("FEAST_CHOL");
-  // default for m <= 192: one CTA, 16 x 16 tiles in shared memory, DMMA tile products
-  // (chol_tiles.cu); FEAST_CHOL=c keeps the cooperative kernel below, s the packed one-CTA one
-  if ((!route || route[0] == 't') && m <= chol_tiles_max_dim()) return chol_tiles(m, a, rel_tol, status, dinv, st);
-  if (route && route[0] == 's' && m <= 32 * CS_SL && chol_sm_bytes(m) <= 226 * 1024) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(chol_sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
-      attr = true;
-    }
-    CholArgs q{m, a, dinv, rel_tol, status};
-    chol_sm_kernel<<<1, CS_NT, chol_sm_bytes(m), st>>>(q);
-    ++g_launches;
-    return cudaGetLastError();
-  }
+  // m <= 192: one CTA, 16 x 16 tiles in shared memory, DMMA tile products (chol_tiles.cu);
+  // beyond: the cooperative kernel above
+  if (m <= chol_tiles_max_dim()) return chol_tiles(m, a, rel_tol, status, dinv, st);
   const int nblk = (m + TB - 1) / TB;
   int grid = std::max(1, nblk * (nblk - 1) / 2);
   int dev = 0, sms = 148, occ = 1;
@@ -516,8 +394,7 @@ __global__ void __launch_bounds__(256) trsm_res_kernel(int m, const double* __re
 template <bool TRANS>
 static cudaError_t trsm_tiles(int m, const double* l, const double* dinv, double* x, int ldx, int ncols,
                               cudaStream_t st) {
-  static const char* route = std::getenv("FEAST_TRSM");
-  if (m <= RS_MAXB * TB && !(route && route[0] == 'g')) {  // FEAST_TRSM=g: L streamed from L2
+  if (m <= RS_MAXB * TB) {  // every lower tile of L resident in shared memory; beyond, L from L2
     const size_t rs = sizeof(double) * ((size_t)m * XC + (size_t)(RS_MAXB * (RS_MAXB + 1) / 2 + 1) * TB * TL +
                                         TB * XC);
     static bool rattr = false;

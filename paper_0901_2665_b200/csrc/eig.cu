@@ -1,22 +1,83 @@
 // eig.cu — the reduced generalized eigensolver on device (reduced_gevp, eigh.hpp:178-225).
 //
 //   (cholesky / trsm_lower / trsm_lower_t live in chol.cu)
-//   sym_eig       symmetric eigendecomposition, ascending, stable order (jacobi_eigh,
-//                 eigh.hpp:84-163). Same method class as the reference (cyclic Jacobi, so
-//                 multiplicities and tiny eigenvalues come out as accurately), re-shaped for
-//                 148 SMs: BLOCK Jacobi. The m x m matrix is cut into 2k blocks of bs rows;
-//                 each round pairs the blocks by the circle method, every pair's 2bs x 2bs
-//                 sub-problem is diagonalised in shared memory by parallel (round-robin)
-//                 Jacobi, and the pair rotations are applied to W and V as small GEMM tiles
-//                 by all CTAs — one cooperative kernel, two grid barriers per round.
+//   sym_eig       symmetric eigendecomposition, ascending, orthonormal vectors (the role of
+//                 jacobi_eigh, eigh.hpp:84-163): Householder tridiagonalisation + Sturm
+//                 multisection + inverse iteration + back-transformation (tridiag*.cu,
+//                 tri_back.cu). A different method from the reference's cyclic Jacobi; the
+//                 eigenpairs agree to rounding (tests/test_gpu_parity.py).
+//   EigWork       its device workspace, cached process-wide per (device, size) so a fresh
+//                 context (every end-to-end solve opens one) does not pay cudaMalloc/cudaFree.
 
 #include <algorithm>
 #include <cfloat>
+#include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
 
 namespace feastgpu {
+
+int tri_max_dim();
+cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws, int* iws, cudaStream_t st,
+                    double vfloor);
+
+struct EigWork {
+  int mmax = 0;
+  int dev = 0;
+  double* tws = nullptr;  // tridiagonal route: 6m^2 + 3m
+  int* tiws = nullptr;    // m^2
+};
+
+static std::mutex g_eig_mu;
+static std::vector<EigWork*> g_eig_cache;
+constexpr size_t kEigCacheMax = 4;
+
+EigWork* eig_create(int mmax) {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  {
+    std::lock_guard<std::mutex> lk(g_eig_mu);
+    for (size_t i = 0; i < g_eig_cache.size(); ++i)
+      if (g_eig_cache[i]->mmax == mmax && g_eig_cache[i]->dev == cur) {
+        EigWork* w = g_eig_cache[i];
+        g_eig_cache.erase(g_eig_cache.begin() + i);
+        return w;
+      }
+  }
+  EigWork* w = new EigWork();
+  w->dev = cur;
+  w->mmax = mmax;
+  const size_t tm = (size_t)std::min(mmax, tri_max_dim());
+  if (cudaMalloc(&w->tws, sizeof(double) * (6 * tm * tm + 3 * tm)) != cudaSuccess ||
+      cudaMalloc(&w->tiws, sizeof(int) * tm * tm) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(w->tws);
+    delete w;
+    return nullptr;
+  }
+  return w;
+}
+
+void eig_destroy(EigWork* w) {
+  if (!w) return;
+  {
+    std::lock_guard<std::mutex> lk(g_eig_mu);  // (the caller has synchronised its stream)
+    if (g_eig_cache.size() < kEigCacheMax) {
+      g_eig_cache.push_back(w);
+      return;
+    }
+  }
+  cudaFree(w->tws);
+  cudaFree(w->tiws);
+  delete w;
+}
+
+cudaError_t sym_eig(EigWork* w, int m, double* a, double* evals, double* v, cudaStream_t st, double vfloor) {
+  if (!w || m < 1 || m > w->mmax || m > tri_max_dim()) return cudaErrorInvalidValue;
+  return tri_eig(m, a, evals, v, w->tws, w->tiws, st, vfloor);
+}
 
 __global__ void transpose_kernel(const double* __restrict__ src, int m, int n, int lds,
                                  double* __restrict__ dst, int ldd) {

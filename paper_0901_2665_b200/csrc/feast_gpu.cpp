@@ -211,7 +211,9 @@ struct feast_gpu_ctx {
   DevBuf<double2> sinv, gfac, hfac, lu, dinv, scratch, fwork;
   DevBuf<double> Aband, Bband;  // band-row copies of A, B for the applies (b <= 32; band_apply.cu)
   int kmid = -1;  // twisted block-Thomas meeting layer of the current factors (bt_twist_layer)
-  DevBuf<int> ipiv, perm, status, fiwork;
+  DevBuf<int> ipiv, perm, status;
+  bool chol_failed_prev = false;  // the last reduced_gevp took the truncation path
+  bool twist = true;  // two-ended block-Thomas recursion where it applies (feast_gpu_set_twist)
   // workspaces
   int mcap = 0;
   DevBuf<double> Y, Q, X, AQ, BQ, T, gw;
@@ -246,6 +248,7 @@ void ensure_eig(feast_gpu_ctx* c, int m) {
     eig_destroy(c->eig);
   }
   c->eig = eig_create(std::max(m, 16));
+  if (!c->eig) fail(FEAST_ECUDA, "CUDA: out of memory for the reduced eigensolver workspace");
   c->eig_cap = std::max(m, 16);
 }
 
@@ -685,8 +688,7 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
       }
       if ((3 * bw + 1) * 2 <= n) {
         // smallest supported block size whose block-tridiagonal pattern holds both operators
-        static const int min_block = getenv("FEAST_MIN_BLOCK") ? atoi(getenv("FEAST_MIN_BLOCK")) : 0;
-        const int lo = round_block(std::max(std::max(1, (bw + 2) / 2), min_block));
+        const int lo = round_block(std::max(1, (bw + 2) / 2));
         const int hi = std::min(std::max(round_block(std::max(bw, 1)), lo), kMaxBlock);
         for (int cand = lo; cand <= hi && !bsz; cand *= 2) {
           bool ok = true;
@@ -857,17 +859,11 @@ void factor_range(feast_gpu_ctx* c, int s0, int cnt) {
     c->sinv.ensure(slots * c->L * bb);
     c->gfac.ensure(std::max<size_t>(slots * (c->L - 1) * bb, 1));
     c->hfac.ensure(std::max<size_t>(slots * (c->L - 1) * bb, 1));
-    if (c->b >= 128) {
-      c->fwork.ensure(bt_factor_work_elems(c->b, cnt));
-      c->fiwork.ensure((size_t)cnt * 2 * c->b);
-    }
+    if (c->b >= 128) c->fwork.ensure(bt_factor_work_elems(c->b, cnt));
     BtFactorArgs a{c->L, c->b, cnt, c->abdiag.p, c->ablow.p, c->dz.p + s0, c->sinv.p, c->gfac.p, c->hfac.p,
-                   c->scratch.p, c->status.p, c->fwork.p, c->fiwork.p, c->kmid = bt_twist_layer(c->L, c->b)};
+                   c->scratch.p, c->status.p, c->fwork.p, c->kmid = bt_twist_layer(c->L, c->b, c->twist)};
     CK(bt_factor(a, c->stream));
-    if (!c->streamed()) {  // factor workspaces are transient unless they are reused every pass
-      c->fwork.release();
-      c->fiwork.release();
-    }
+    if (!c->streamed()) c->fwork.release();  // transient unless it is reused every pass
   } else {
     const int n = c->n, nb = kDenseNb, nblk = (n + nb - 1) / nb, slots = c->wnodes();
     c->lu.ensure((size_t)slots * n * n);
@@ -1037,11 +1033,19 @@ Reduced reduced_gevp(feast_gpu_ctx* c, int m) {
   CK(cudaMemsetAsync(c->status.p, 0, sizeof(int), c->stream));
   c->Dv.ensure((size_t)((m + 31) / 32) * 1024);
   CK(cholesky(m, c->Lm.p, 1e-13, c->status.p, c->Dv.p, c->stream));
-  // The Cholesky path is enqueued without waiting for the pivot check: status and eigenvalues
-  // come back with ONE synchronisation, and a failed factorisation (its trailing kernels ran
-  // on a partial factor; their output is discarded) falls through to the truncation path.
+  // While the Cholesky factorisations succeed, the rest of the path is enqueued without waiting
+  // for the pivot check: status and eigenvalues come back with ONE synchronisation. After a
+  // failed one (the subspace is in the truncation regime, where it usually stays) the status is
+  // read first, so a failing pass does not pay a full eigensolve on a partial factor.
   r.evals.resize(m);
-  {
+  bool chol_ok = true;
+  if (c->chol_failed_prev) {
+    int st = 0;
+    CK(cudaMemcpyAsync(&st, c->status.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    chol_ok = st == 0;
+  }
+  if (chol_ok) {
     // C = L^-1 A L^-T  via two lower solves and transposes (eigh.hpp:192-196)
     CK(cudaMemcpyAsync(c->Cm.p, c->Aq.p, sizeof(double) * mm, cudaMemcpyDeviceToDevice, c->stream));
     CK(trsm_lower(m, c->Lm.p, c->Dv.p, c->Cm.p, m, m, c->stream));
@@ -1056,10 +1060,12 @@ Reduced reduced_gevp(feast_gpu_ctx* c, int m) {
     CK(cudaMemcpyAsync(r.evals.data(), c->Ev.p, sizeof(double) * m, cudaMemcpyDeviceToHost, c->stream));
     sync(c);
     if (!st) {
+      c->chol_failed_prev = false;
       r.mo = m;
       return r;
     }
   }
+  c->chol_failed_prev = true;
   // spectral truncation fallback (eigh.hpp:204-224)
   CK(cudaMemcpyAsync(c->Cm.p, c->Bq.p, sizeof(double) * mm, cudaMemcpyDeviceToDevice, c->stream));
   CK(symmetrize(c->Cm.p, m, m, c->stream));
@@ -1120,15 +1126,19 @@ void upload_block(feast_gpu_ctx* c, const double* host, int m, double* dev) {
   CK(cudaMemcpy2DAsync(dev, sizeof(double) * c->npad, host, sizeof(double) * c->n, sizeof(double) * c->n, m,
                        cudaMemcpyHostToDevice, c->stream));
 }
-// Process-wide pinned staging buffer for large result downloads: the DMA into page-locked
-// memory runs at link speed and the copy into the caller's pageable block is spread over host
-// threads (pageable cudaMemcpy measured 4 GB/s on the result blocks; pinning the caller's
-// memory per call with cudaHostRegister was slower still). Grown on demand, kept for reuse.
+// Process-wide pinned staging buffer for large transfers: the DMA into page-locked memory runs
+// at link speed and the copy into the caller's pageable block is spread over host threads
+// (pageable cudaMemcpy measured 4 GB/s on the result blocks; pinning the caller's memory per
+// call with cudaHostRegister was slower still). Grown on demand up to kPinnedStageMax and kept
+// for reuse; larger transfers go through it in rounds (downloads) or take the pageable path
+// (uploads), so a config-5-sized result does not leave gigabytes page-locked.
+constexpr size_t kPinnedStageMax = (size_t)256 << 20;  // bytes
 struct PinnedStage {
   std::mutex mu;
   double* p = nullptr;
   size_t n = 0;
   double* get(size_t count) {
+    if (count * sizeof(double) > kPinnedStageMax) return nullptr;
     if (count > n) {
       if (p) cudaFreeHost(p);
       p = nullptr;
@@ -1191,54 +1201,76 @@ void download_blocks(feast_gpu_ctx* c, const std::vector<Download>& dl) {
     for (auto& d : dl) download_block(c, d.dev, d.m, d.host);
     return;
   }
+  const int per = std::max<int>(1, (int)((4u << 20) / (sizeof(double) * n)));  // columns per chunk
+  const size_t chunk_max = n * per;
+  const size_t round_max = std::max(chunk_max, std::min(total, kPinnedStageMax / sizeof(double)));
   std::unique_lock<std::mutex> lk;
-  double* st = pinned_stage_lock_get(total, lk);
+  double* st = pinned_stage_lock_get(round_max, lk);
   if (!st) {
     lk.unlock();
-    for (auto& d : dl) download_block(c, d.dev, d.m, d.host);
+    for (auto& d : dl) {
+      CK(cudaMemcpy2DAsync(d.host, sizeof(double) * n, d.dev, sizeof(double) * c->npad, sizeof(double) * n, d.m,
+                           cudaMemcpyDeviceToHost, c->stream));
+    }
+    sync(c);
     return;
   }
-  const int per = std::max<int>(1, (int)((4u << 20) / (sizeof(double) * n)));  // columns per chunk
   struct Chunk {
-    double* stage;
+    const double* dev;
     double* host;
-    size_t count;
-    cudaEvent_t ev;
+    int w;
   };
-  static std::vector<cudaEvent_t> evs;  // guarded by the stage lock
-  std::vector<Chunk> ch;
-  size_t off = 0;
+  std::vector<Chunk> all;
   for (auto& d : dl)
-    for (int j = 0; j < d.m; j += per) {
-      const int w = std::min(per, d.m - j);
-      if (ch.size() == evs.size()) {
+    for (int j = 0; j < d.m; j += per) all.push_back({d.dev + (size_t)c->npad * j, d.host + n * j, std::min(per, d.m - j)});
+  // chunk events, per device (an event belongs to the device current at its creation); guarded
+  // by the stage lock
+  static std::vector<std::pair<int, std::vector<cudaEvent_t>>> dev_events;
+  std::vector<cudaEvent_t>* evs = nullptr;
+  for (auto& de : dev_events)
+    if (de.first == c->device) evs = &de.second;
+  if (!evs) {
+    dev_events.emplace_back(c->device, std::vector<cudaEvent_t>());
+    evs = &dev_events.back().second;
+  }
+  // rounds of chunks that fit the stage: DMA chunk i into the stage with an event behind it,
+  // host threads copy chunk i out as soon as its event fires while later chunks are in flight
+  for (size_t c0 = 0; c0 < all.size();) {
+    size_t c1 = c0, used = 0;
+    while (c1 < all.size() && used + n * all[c1].w <= round_max) used += n * all[c1++].w;
+    std::vector<size_t> off(c1 - c0);
+    size_t o = 0;
+    for (size_t i = c0; i < c1; ++i) {
+      if (evs->size() <= i - c0) {
         cudaEvent_t e;
         CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        evs.push_back(e);
+        evs->push_back(e);
       }
-      Chunk k{st + off, d.host + n * j, n * w, evs[ch.size()]};
-      CK(cudaMemcpy2DAsync(k.stage, sizeof(double) * n, d.dev + (size_t)c->npad * j, sizeof(double) * c->npad,
-                           sizeof(double) * n, w, cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaEventRecord(k.ev, c->stream));
-      ch.push_back(k);
-      off += n * w;
+      off[i - c0] = o;
+      CK(cudaMemcpy2DAsync(st + o, sizeof(double) * n, all[i].dev, sizeof(double) * c->npad, sizeof(double) * n,
+                           all[i].w, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaEventRecord((*evs)[i - c0], c->stream));
+      o += n * all[i].w;
     }
-  const int nt = (int)std::min<size_t>(std::min(8u, std::max(1u, std::thread::hardware_concurrency())), ch.size());
-  std::atomic<bool> bad{false};
-  auto work = [&](int t) {
-    for (size_t i = t; i < ch.size(); i += nt) {
-      if (cudaEventSynchronize(ch[i].ev) != cudaSuccess) {
-        bad = true;
-        return;
+    const int cnt = (int)(c1 - c0);
+    const int nt = std::min(cnt, (int)std::min(8u, std::max(1u, std::thread::hardware_concurrency())));
+    std::atomic<bool> bad{false};
+    auto work = [&](int t) {
+      for (int i = t; i < cnt; i += nt) {
+        if (cudaEventSynchronize((*evs)[i]) != cudaSuccess) {
+          bad = true;
+          return;
+        }
+        std::memcpy(all[c0 + i].host, st + off[i], sizeof(double) * n * all[c0 + i].w);
       }
-      std::memcpy(ch[i].host, ch[i].stage, sizeof(double) * ch[i].count);
-    }
-  };
-  std::vector<std::thread> th;
-  for (int t = 1; t < nt; ++t) th.emplace_back(work, t);
-  work(0);
-  for (auto& x : th) x.join();
-  if (bad) CK(cudaStreamSynchronize(c->stream));  // raises the stream's error
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; ++t) th.emplace_back(work, t);
+    work(0);
+    for (auto& x : th) x.join();
+    if (bad) CK(cudaStreamSynchronize(c->stream));  // raises the stream's error
+    c0 = c1;
+  }
 }
 
 // residual_norms (residual.hpp:29-68) of the first m columns of X (device, ld npad)
@@ -1292,6 +1324,7 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
   if (initial_y && (y_cols < 1 || y_cols > cfg->m0)) fail(FEAST_EINPUT, "feast_solve: initial block shape mismatch");
   if (!(emin < emax)) fail(FEAST_EINPUT, "SearchInterval: lambda_min must be strictly below lambda_max");
 
+  c->chol_failed_prev = false;
   const bool same_contour = c->have_contour && c->emin == emin && c->emax == emax && c->ne == cfg->n_e;
   if (!same_contour) build_contour(c, emin, emax, cfg->n_e);
   const double effective_tol = cfg->trace_tol;  // direct solves: residual_target() == 0
@@ -1513,7 +1546,7 @@ void feast_gpu_destroy(feast_gpu_ctx* c) {
   for (DevBuf<double2>* d : {&c->abdiag, &c->ablow, &c->dz, &c->dcoeff, &c->sinv, &c->gfac, &c->hfac, &c->lu, &c->dinv,
                              &c->scratch, &c->W, &c->fwork})
     d->release();
-  for (DevBuf<int>* d : {&c->ipiv, &c->perm, &c->status, &c->keep, &c->fiwork}) d->release();
+  for (DevBuf<int>* d : {&c->ipiv, &c->perm, &c->status, &c->keep}) d->release();
   cudaStreamSynchronize(c->stream);  // the frees above are stream-ordered
   if (c->eig) eig_destroy(c->eig);
   for (auto& e : c->ev)
@@ -1572,6 +1605,13 @@ int feast_gpu_set_node_batch(feast_gpu_ctx* c, int nodes) {
     if (nodes < 0) fail(FEAST_EINPUT, "set_node_batch: negative batch");
     c->batch_req = nodes;
     c->factored = false;  // re-plan at the next factorisation
+  });
+}
+
+int feast_gpu_set_twist(feast_gpu_ctx* c, int enable) {
+  return guarded(c, [&] {
+    c->twist = enable != 0;
+    c->factored = false;  // the factors' layout follows the recursion
   });
 }
 

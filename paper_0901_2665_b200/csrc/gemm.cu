@@ -442,94 +442,9 @@ static cudaError_t dgemm_batched(bool TA, int m, int n, int k, double alpha, con
   return cudaGetLastError();
 }
 
-// Small blocks (B <= 32): the operator is a narrow band, so one CTA computes a 64-row x
-// 64-column tile of Y against the K = 64 + 2B rows of X its rows touch, assembling the
-// banded A tile (diagonal blocks, C_{l-1}, C_l^T) in shared memory; 8 warps of DMMA.
-template <int B>
-__global__ void __launch_bounds__(256) bt_apply_small_kernel(int n, const double* __restrict__ diag,
-                                                             const double* __restrict__ low,
-                                                             const double* __restrict__ x, int ldx,
-                                                             double* __restrict__ y, int ldy, int m) {
-  constexpr int TR = 64, KW = TR + 2 * B, SA = TR + 4, SX = KW + 4;
-  constexpr int BB = B * B;
-  extern __shared__ __align__(16) double bsm[];
-  double* As = bsm;             // [KW][SA]   A(r0 + rr, c0 + k) at As[k*SA + rr]
-  double* Xs = As + KW * SA;    // [64][SX]   X(c0 + k, n0 + col) at Xs[col*SX + k]
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
-  const int wm = warp & 1, wn = warp >> 1;
-  const int r0 = blockIdx.y * TR, n0 = blockIdx.x * 64, c0 = r0 - B;
-  const int L = n / B;
-  for (int e = tid; e < KW * TR; e += 256) {
-    const int rr = e % TR, k = e / TR;
-    const int r = r0 + rr, c = c0 + k;
-    const double* src = diag;
-    bool v = false;
-    if (r < n && c >= 0 && c < n) {
-      const int l = r / B, i = r % B, lc = c / B, jc = c % B;
-      if (lc == l) { src = diag + (size_t)l * BB + i + jc * B; v = true; }
-      else if (lc == l - 1) { src = low + (size_t)(l - 1) * BB + i + jc * B; v = true; }
-      else if (lc == l + 1 && l + 1 < L) { src = low + (size_t)l * BB + jc + i * B; v = true; }
-    }
-    cp_async8z(As + k * SA + rr, src, v);
-  }
-  for (int e = tid; e < KW * 64; e += 256) {
-    const int k = e % KW, col = e / KW;
-    const int c = c0 + k, gc = n0 + col;
-    const bool v = c >= 0 && c < n && gc < m;
-    cp_async8z(Xs + col * SX + k, v ? x + c + (int64_t)gc * ldx : x, v);
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  double acc[4][2][2] = {};
-#pragma unroll 4
-  for (int kk = 0; kk < KW; kk += 4) {
-    double af[4], bf[2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) af[i] = As[(kk + t4) * SA + wm * 32 + i * 8 + g];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) bf[j] = Xs[(wn * 16 + j * 8 + g) * SX + kk + t4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int row = r0 + wm * 32 + i * 8 + g;
-    if (row >= n) continue;
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int col = n0 + wn * 16 + j * 8 + 2 * t4 + h;
-        if (col < m) y[row + (int64_t)col * ldy] = acc[i][j][h];
-      }
-  }
-}
-
-template <int B>
-static cudaError_t bt_apply_small(int n, const double* diag, const double* low, const double* x, int ldx,
-                                  double* y, int ldy, int m, cudaStream_t st) {
-  constexpr int TR = 64, KW = TR + 2 * B;
-  const int sm = (int)sizeof(double) * (KW * (TR + 4) + 64 * (KW + 4));
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(bt_apply_small_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    attr = true;
-  }
-  dim3 grid((m + 63) / 64, (n + TR - 1) / TR);
-  bt_apply_small_kernel<B><<<grid, 256, sm, st>>>(n, diag, low, x, ldx, y, ldy, m);
-  ++g_launches;
-  return cudaGetLastError();
-}
-
-// Y = Op X for a block-tridiagonal real operator (diag: L blocks b*b, low: L-1 couplings
-// C_l = Op(l+1, l), Op(l, l+1) = C_l^T) (SymmetricOperator::apply, operator.hpp:132-158, on
-// the block structure): banded tiles for b <= 32, else three layer-batched DMMA GEMMs.
 cudaError_t bt_apply(int L, int b, const double* diag, const double* low, const double* x, int ldx,
                      double* y, int ldy, int m, cudaStream_t st) {
-  if (b == 16) return bt_apply_small<16>(L * b, diag, low, x, ldx, y, ldy, m, st);
-  if (b == 32) return bt_apply_small<32>(L * b, diag, low, x, ldx, y, ldy, m, st);
+  // (b <= 32 goes through band_apply on band-row copies, band_apply.cu)
   const int64_t bb = (int64_t)b * b;
   cudaError_t e = dgemm_batched(false, b, m, b, 1.0, diag, b, bb, x, ldx, b, 0.0, y, ldy, b, L, st);
   if (e != cudaSuccess || L == 1) return e;

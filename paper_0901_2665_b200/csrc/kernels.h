@@ -29,13 +29,12 @@ struct BtFactorArgs {
   double2* scratch;       // unused (kept for the launcher signature)
   int* status;            // set to 1 on a singular block pivot
   double2* work;          // b >= 128: bt_factor_work_elems(b, nodes) double2
-  int* iwork;             // b >= 128: nodes * 2b
   int kmid = -1;          // >= 0: twisted recursion meeting at layer kmid (bt_twist_layer)
 };
 cudaError_t bt_factor(const BtFactorArgs& a, cudaStream_t st);
 // Meeting layer of the twisted (two-ended) block-Thomas recursion for b <= 64 and L >= 4
-// (L / 2), else -1 (plain top-down chain). FEAST_BT_TWIST=0 disables it.
-int bt_twist_layer(int L, int b);
+// (L / 2), else -1 (plain top-down chain; also when !enable, feast_gpu_set_twist).
+int bt_twist_layer(int L, int b, bool enable);
 size_t bt_factor_work_elems(int b, int nodes);
 
 // Panel layout of the factors for b >= 128 (the bulk-copy sweep): each b x b factor is stored

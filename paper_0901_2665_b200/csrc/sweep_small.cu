@@ -442,17 +442,8 @@ bool bt_swizzled_factors(int b) { return b == 16 || b == 32; }
 cudaError_t bt_sweep_small(const BtSweepArgs& a, cudaStream_t st) {
   switch (a.b) {
     case 16: {
-      // FEAST_SWEEP_CFG = NC*10 + TPW selects the launch shape (experiments); default 81:
-      // 8 columns per CTA, the 16 rows split over 2 compute warps
-      const char* c = std::getenv("FEAST_SWEEP_CFG");
-      const int cfg = c ? std::atoi(c) : 81;
-      switch (cfg) {
-        case 82: return launch_bulk_any<16, 8, 2>(a, st);    // 1 warp owns 8 columns x 16 rows
-        case 161: return launch_bulk_any<16, 16, 1>(a, st);  // 4 warps
-        case 162: return launch_bulk_any<16, 16, 2>(a, st);  // 2 warps, whole columns
-        case 321: return launch_bulk_any<16, 32, 1>(a, st);  // 8 warps
-        case 322: return launch_bulk_any<16, 32, 2>(a, st);  // 4 warps, whole columns
-      }
+      // 8 columns per CTA, the 16 rows split over 2 compute warps (measured against 8 x 1 warp,
+      // 16 and 32 columns per CTA with 1-8 warps: DESIGN.md, the bulk-copy pipeline)
       return launch_bulk_any<16, 8, 1>(a, st);               // 2 warps
     }
     case 32:  // (complex right-hand sides: narrower column blocks keep the ring within 227 KB)

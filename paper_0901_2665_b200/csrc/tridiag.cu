@@ -1,7 +1,6 @@
 // tridiag.cu — symmetric eigendecomposition for the reduced problem when it fits one SM
 // (m <= 1024): the dense -> tridiagonal -> eigenpairs route of LAPACK's syevx, re-shaped for
-// one B200 CTA plus a grid of warps. Used by sym_eig (jacobi.cu) in place of block Jacobi for
-// those sizes; same contract as jacobi_eigh (eigh.hpp:84-163): eigenvalues ascending,
+// one B200 CTA plus a grid of warps. Used by sym_eig (eig.cu) for every reduced size; same contract as jacobi_eigh (eigh.hpp:84-163): eigenvalues ascending,
 // orthonormal eigenvectors, repeated eigenvalues allowed.
 //
 //   tridiag_kernel      Householder reduction A = Q T Q^T (dsytd2, lower); the working
@@ -186,214 +185,6 @@ __global__ void __launch_bounds__(1024) tridiag_kernel(int m, const double* __re
   }
 }
 
-
-// ---------------------------------------------------------------------------
-// 1a'. The same reduction on one SM for m <= 192, laid out so that almost every issued
-//      instruction is a load, an FMA or a store of the packed matrix (the kernel above spends
-//      ~14 instructions per useful FMA: irregular packed offsets, per-element reloads of v and
-//      w, every thread re-summing the warp partials):
-//      * lane l owns rows i = l + 32t (t < 6) of EVERY column: v_i, w_i and the row
-//        accumulators live in registers; column j's slot t is A(l + 32t, j), a contiguous
-//        (conflict-free) run of the packed column;
-//      * warp w owns columns j = w (mod 32) (balanced: column j has m - j rows); per column
-//        the warp forms the dot A(j+1:, j).v and the axpy A(j:, j) v_j into its row
-//        accumulators (symv over the stored lower triangle, each element read once);
-//      * the 32 warps' row partials are summed in a fixed order by 4 threads per row
-//        (run-to-run deterministic), v^T A v from the per-warp dot partials;
-//      * the rank-2 update runs warp-per-column again; the owner of the next column leaves
-//        the next reflector (norm, scalars, v) before the step's last barrier.
-//      Three block barriers per column.
-// ---------------------------------------------------------------------------
-constexpr int TR_SL = 6;   // row slots per lane: m <= 192
-constexpr int TR_NW = 24;  // warps (768 threads: 85 registers each, no spills; 4 threads per row in (R))
-constexpr int TR_NT = TR_NW * 32;
-constexpr int TR_CS = (32 * TR_SL + TR_NW - 1) / TR_NW;  // column slots per warp
-
-__device__ __forceinline__ int tr_cb(int j, int m) { return j * m - (j * (j - 1)) / 2; }  // A(i,j) at cb + i - j
-
-__global__ void __launch_bounds__(TR_NT, 1) tridiag_rows_kernel(int m, const double* __restrict__ a, double* d,
-                                                                double* e, double* hv, double* tau) {
-  extern __shared__ double tsm[];
-  double* ps = tsm;                        // packed lower triangle
-  double* part = ps + m * (m + 1) / 2;     // [TR_NW][m] row partials of the symv
-  double* dots = part + TR_NW * m;         // [m]   column dots
-  double* pvec = dots + m;                 // [m]   p = t A v
-  double* vb = pvec + m;                   // [2][m] reflector by parity (zero above its start)
-  __shared__ double red[32];               // per-warp v^T A v partials (TR_NW used)
-  __shared__ double refl[2][3];            // t, beta, scal of the reflector by parity
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-
-  for (int idx = tid; idx < m * m; idx += TR_NT) {
-    const int i = idx % m, j = idx / m;
-    if (i >= j) cp_async8z(ps + tr_cb(j, m) + i - j, a + idx, true);
-  }
-  cp_async_wait_all();
-  __syncthreads();
-
-  // reflector k from column k (rows k+1..): warp `warp` with the column's entries in x[t]
-  // (rows lane + 32t; anything outside k+1..m-1 ignored); writes v into vb[par], hv, scalars
-  auto build = [&](int k, const double (&x)[TR_SL], int par) {
-    double nrm = 0.0, alpha = 0.0;
-#pragma unroll
-    for (int t = 0; t < TR_SL; ++t) {
-      const int i = lane + 32 * t;
-      if (i >= k + 2 && i < m) nrm += x[t] * x[t];
-      if (i == k + 1) alpha = x[t];
-    }
-    nrm = warp_sum(nrm);
-    alpha = warp_sum(alpha);  // exactly one lane holds it
-    double tt = 0.0, beta = alpha, sc = 0.0;
-    if (nrm > 0.0) {
-      beta = -copysign(sqrt(alpha * alpha + nrm), alpha);
-      tt = (beta - alpha) / beta;
-      sc = 1.0 / (alpha - beta);
-    }
-    double* v = vb + par * m;
-#pragma unroll
-    for (int t = 0; t < TR_SL; ++t) {
-      const int i = lane + 32 * t;
-      if (i < m) {
-        const double vi = i == k + 1 ? 1.0 : (i > k + 1 && tt != 0.0 ? x[t] * sc : 0.0);
-        v[i] = vi;
-        if (i > k) hv[i + (int64_t)k * m] = vi;
-      }
-    }
-    if (lane == 0) {
-      refl[par][0] = tt;
-      refl[par][1] = beta;
-      refl[par][2] = sc;
-      e[k] = beta;
-      tau[k] = tt;
-    }
-  };
-
-  if (m > 2 && warp == 0) {
-    double x[TR_SL];
-#pragma unroll
-    for (int t = 0; t < TR_SL; ++t) {
-      const int i = lane + 32 * t;
-      x[t] = i < m ? ps[i] : 0.0;  // column 0
-    }
-    build(0, x, 0);
-    if (lane == 0) d[0] = ps[0];
-  }
-  __syncthreads();
-
-  for (int k = 0; k + 2 < m; ++k) {
-    const int base = k + 1, par = k & 1;
-    const double tt = refl[par][0];
-    const double* v = vb + par * m;
-    double vr[TR_SL];
-#pragma unroll
-    for (int t = 0; t < TR_SL; ++t) {
-      const int i = lane + 32 * t;
-      vr[t] = i < m ? v[i] : 0.0;  // zero above base
-    }
-    // first own column >= base: j = warp + TR_NW s
-    const int s0 = base > warp ? (base - warp + TR_NW - 1) / TR_NW : 0;
-    if (tt != 0.0) {
-      // ---- (S) symv partials ----
-      double pacc[TR_SL];
-#pragma unroll
-      for (int t = 0; t < TR_SL; ++t) pacc[t] = 0.0;
-      double vav = 0.0;
-#pragma unroll
-      for (int s = 0; s < TR_CS; ++s) {
-        const int j = warp + TR_NW * s;
-        if (s >= s0 && j < m) {
-          const double* col = ps + tr_cb(j, m) - j;  // col[i] = A(i, j), i >= j
-          const double vj = v[j];
-          double dot = 0.0;
-#pragma unroll
-          for (int t = (TR_NW * s) / 32; t < TR_SL; ++t) {
-            const int i = lane + 32 * t;
-            if (i >= j && i < m) {
-              const double aij = col[i];
-              pacc[t] = fma(aij, vj, pacc[t]);
-              if (i > j) dot = fma(aij, vr[t], dot);
-            }
-          }
-          dot = warp_sum(dot);
-          if (lane == 0) dots[j] = dot;
-          if (lane == (j & 31)) vav += vj * (2.0 * dot + col[j] * vj);
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < TR_SL; ++t) {
-        const int i = lane + 32 * t;
-        if (i < m) part[warp * m + i] = pacc[t];
-      }
-      vav = warp_sum(vav);  // (the column's owner lane added it)
-      if (lane == 0) red[warp] = vav;
-      __syncthreads();  // (1)
-      // ---- (R) p = t (dots + sum_w part[w]) : 4 threads per row, fixed order ----
-      {
-        const int i = tid >> 2, q = tid & 3;
-        double sacc = 0.0;
-        if (i < m)
-#pragma unroll
-          for (int w = q; w < TR_NW; w += 4) sacc += part[w * m + i];
-        sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
-        sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
-        if (i < m && q == 0) pvec[i] = i >= base ? tt * (sacc + dots[i]) : 0.0;
-      }
-      __syncthreads();  // (2)
-      // ---- (U) A -= v w^T + w v^T,  w = p + c v,  c = -t^2 (v^T A v) / 2 ----
-      const double c = -0.5 * tt * tt * warp_sum(lane < TR_NW ? red[lane] : 0.0);
-      double wr[TR_SL];
-#pragma unroll
-      for (int t = 0; t < TR_SL; ++t) {
-        const int i = lane + 32 * t;
-        wr[t] = i < m ? pvec[i] + c * vr[t] : 0.0;
-      }
-#pragma unroll
-      for (int s = 0; s < TR_CS; ++s) {
-        const int j = warp + TR_NW * s;
-        if (s >= s0 && j < m) {
-          double* col = ps + tr_cb(j, m) - j;
-          const double vj = v[j], wj = pvec[j] + c * vj;
-          double x[TR_SL];
-#pragma unroll
-          for (int t = 0; t < TR_SL; ++t) {
-            const int i = lane + 32 * t;
-            x[t] = 0.0;
-            if (t >= (TR_NW * s) / 32 && i >= j && i < m) {
-              const double y = col[i] - (vr[t] * wj + wr[t] * vj);
-              col[i] = y;
-              x[t] = y;
-            }
-          }
-          if (j == base && k + 3 < m) {  // the next column is final: its reflector
-            build(base, x, par ^ 1);
-            if (lane == 0) d[base] = col[base];
-          }
-        }
-      }
-    } else if (base % TR_NW == warp && k + 3 < m) {  // no reflection: the next column as it is
-      const double* col = ps + tr_cb(base, m) - base;
-      double x[TR_SL];
-#pragma unroll
-      for (int t = 0; t < TR_SL; ++t) {
-        const int i = lane + 32 * t;
-        x[t] = i >= base && i < m ? col[i] : 0.0;
-      }
-      build(base, x, par ^ 1);
-      if (lane == 0) d[base] = col[base];
-    }
-    __syncthreads();  // (3)
-  }
-  if (tid == 0) {
-    if (m >= 2) {
-      d[m - 2] = ps[tr_cb(m - 2, m)];
-      e[m - 2] = ps[tr_cb(m - 2, m) + 1];
-      tau[m - 2] = 0.0;
-    }
-    d[m - 1] = ps[tr_cb(m - 1, m)];
-    tau[m - 1] = 0.0;
-  }
-}
-
-static size_t tr_rows_smem(int m) { return sizeof(double) * ((size_t)m * (m + 1) / 2 + TR_NW * (size_t)m + 4 * (size_t)m); }
 
 // ---------------------------------------------------------------------------
 // 1b. Householder tridiagonalisation for m beyond one SM's shared memory: cooperative grid,
@@ -1210,28 +1001,16 @@ cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws
     cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
     attr = true;
   }
-  // route: one SM for small m, the 16-CTA cluster while its layout fits (m <= ~840), the
-  // cooperative grid beyond; FEAST_TRI=s (one SM, m <= 236) / k (cluster) / c (cooperative)
-  static const char* route_env = getenv("FEAST_TRI");
-  const char rt = route_env ? route_env[0] : 0;
-  const bool fits_cluster = m > 2 && tcl_smem(m) <= 220 * 1024;
-  // (measured: the cluster overtakes the single SM above m ~ 128; 0.87 vs 0.92 ms at m = 192)
-  bool use_smem = m <= 128, use_cluster = !use_smem && fits_cluster;
-  if (!use_smem && !use_cluster && m <= tri_smem_dim()) use_smem = true;
-  if (rt == 's' && m <= tri_smem_dim()) use_smem = true, use_cluster = false;
-  if (rt == 'k' && fits_cluster) use_smem = false, use_cluster = true;
-  if (rt == 'c') use_smem = false, use_cluster = false;
-  // the row-slot one-SM kernel (m <= 192): FEAST_TRI=r only — it issues ~20K warp instructions
-  // per column at m = 192, mostly the per-column dot reductions, and measured 1.0 ms against
-  // the cluster kernel's 0.8 ms (profiles/r01_summary.md)
-  const bool use_rows = m > 2 && m <= 32 * TR_SL && tr_rows_smem(m) <= 226 * 1024 && rt == 'r';
-  // default for 3 <= m <= 192: the register-tile kernel (tridiag_tiles.cu); the letters above
-  // select the older routes for comparison
-  const bool use_tiles = m > 2 && m <= tri_tiles_max_dim() && (rt == 0 || rt == 't');
+  // route: the register-tile kernel for 3 <= m <= 192 (tridiag_tiles.cu), the one-SM
+  // shared-memory kernel for m <= 2, the 16-CTA cluster while its layout fits (m <= ~840), the
+  // cooperative grid beyond
+  const bool use_tiles = m > 2 && m <= tri_tiles_max_dim();
+  const bool use_cluster = !use_tiles && m > 2 && tcl_smem(m) <= 220 * 1024;
+  const bool use_smem = !use_tiles && !use_cluster && m <= tri_smem_dim();
   if (use_tiles) {
     cudaError_t err = tridiag_tiles(m, a, d, e, hv, tau, st);
     if (err != cudaSuccess) return err;
-  } else if (use_cluster && !use_rows) {
+  } else if (use_cluster) {
     const size_t ksm = tcl_smem(m);
     cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ksm);
@@ -1250,15 +1029,6 @@ cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws
     cudaError_t err = cudaLaunchKernelEx(&cfg, tridiag_cluster_kernel, m, a, d, e, hv, tau);
     ++g_launches;
     if (err != cudaSuccess) return err;
-  } else if (use_rows) {
-    const size_t sm = tr_rows_smem(m);
-    static bool attr2 = false;
-    if (!attr2) {
-      cudaFuncSetAttribute(tridiag_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);
-      attr2 = true;
-    }
-    tridiag_rows_kernel<<<1, TR_NT, sm, st>>>(m, a, d, e, hv, tau);
-    ++g_launches;
   } else if (use_smem) {
     const size_t sm = sizeof(double) * ((size_t)m * (m + 1) / 2 + 2 * m);
     tridiag_kernel<<<1, 1024, sm, st>>>(m, a, d, e, hv, tau);
@@ -1290,38 +1060,23 @@ cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws
   // one warp per CTA: these are serial per-warp chains, so spreading the m warps over all 148
   // SMs (instead of 4 per CTA on m/4 SMs) is what sets their time (ncu: issue-bound at 4 warps
   // per SM, 114 / 85 / 90 us for eigvals / eigvecs / back at m = 192)
-  // eigenvalues: FEAST_EIGVALS="<warps per eigenvalue 1-4><eigenvalues per CTA><chains per lane
-  // 2|4|8>" (default 222: two 2-warp groups per CTA, each warp on its own SM sub-partition, two
-  // Sturm chains per lane = 128 points per step). The chain step is bound by MUFU.RCP64H
-  // throughput, so fewer chains per lane on more sub-partitions win. Measured at m = 192 (ncu,
+  // eigenvalues: two 2-warp groups per CTA (each warp on its own SM sub-partition), two Sturm
+  // chains per lane = 128 points per multisection step. The chain step is bound by MUFU.RCP64H
+  // throughput, so fewer chains per lane on more sub-partitions win; measured at m = 192 (ncu,
   // cfg2): 116 us for one warp x 4 chains, 92 us for 2 warps x 4 chains, 78 us for 2 warps x 2
   // chains, 86 us for 3-4 warps x 2 chains, 264 us for 2 warps x 8 chains
-  static const char* ev_env = getenv("FEAST_EIGVALS");
-  const int wpe = ev_env ? ev_env[0] - '0' : 2, epc = ev_env && ev_env[1] ? ev_env[1] - '0' : 2;
-  const int nch = ev_env && ev_env[1] && ev_env[2] ? ev_env[2] - '0' : 2;
-  const unsigned evb = (unsigned)((m + epc - 1) / epc), evt = 32u * wpe * epc;
-  const size_t evs = sizeof(double) * 3 * m;
-#define FEAST_EIGVALS_CASE(W, C) \
-  if (wpe == W && nch == C) tri_eigvals_kernel<W, C><<<evb, evt, evs, st>>>(p); else
-  FEAST_EIGVALS_CASE(1, 2) FEAST_EIGVALS_CASE(2, 4) FEAST_EIGVALS_CASE(3, 2) FEAST_EIGVALS_CASE(4, 2)
-  FEAST_EIGVALS_CASE(1, 8) FEAST_EIGVALS_CASE(2, 8) FEAST_EIGVALS_CASE(1, 4) FEAST_EIGVALS_CASE(3, 4)
-  FEAST_EIGVALS_CASE(4, 4) tri_eigvals_kernel<2, 2><<<evb, evt, evs, st>>>(p);
-#undef FEAST_EIGVALS_CASE
+  constexpr int kWpe = 2, kEpc = 2, kNch = 2;
+  const unsigned evb = (unsigned)((m + kEpc - 1) / kEpc), evt = 32u * kWpe * kEpc;
+  tri_eigvals_kernel<kWpe, kNch><<<evb, evt, sizeof(double) * 3 * m, st>>>(p);
   ++g_launches;
-  static const char* evv_env = getenv("FEAST_EIGVECS_WPB");
-  const int wpb = evv_env ? atoi(evv_env) : 1;
-  const size_t vsm = sizeof(double) * (6 * m * wpb + 2 * m) + 64;
+  const size_t vsm = sizeof(double) * (6 * m + 2 * m) + 64;
   if (vsm > 48 * 1024) cudaFuncSetAttribute(tri_eigvecs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsm);
-  tri_eigvecs_kernel<<<(m + wpb - 1) / wpb, 32 * wpb, vsm, st>>>(p);
+  tri_eigvecs_kernel<<<m, 32, vsm, st>>>(p);
   ++g_launches;
-  // blocked (WY) back-transformation above m = 384 (tri_back.cu; its T factors live in the
-  // cooperative route's scratch gw, free by now); below, one warp per column measured faster
-  // (m = 192: 83 us against 40 + 56 us, the WY products being shared-memory bound as written).
-  // FEAST_TRI_BACK=w / b forces one or the other.
-  static const char* back_env = getenv("FEAST_TRI_BACK");
-  const bool wy = back_env ? (back_env[0] == 'b' && m >= 64) : m > 384;
-  const bool smem_back = !back_env && m >= 3 && m <= 8 * TBS_NQ;
-  if (smem_back) {
+  // back-transformation: all reflectors in shared memory for m <= 192; blocked (WY) above
+  // m = 384 (tri_back.cu; its T factors live in the cooperative route's scratch gw, free by now);
+  // in between one warp per column (m = 192: 83 us against 40 + 56 us for the WY pair)
+  if (m >= 3 && m <= 8 * TBS_NQ) {
     const size_t sm = sizeof(double) * ((size_t)m * (m - 1) / 2 + m);
     static bool battr = false;
     if (!battr) {
@@ -1330,13 +1085,12 @@ cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws
     }
     tri_back_smem_kernel<<<(m + 4 * TBS_NW - 1) / (4 * TBS_NW), TBS_NW * 32, sm, st>>>(m, hv, tau, z, v);
     ++g_launches;
-  } else if (wy) {
+  } else if (m > 384) {
     cudaError_t err = tri_back_wy(m, hv, tau, z, v, gw, st);
     if (err != cudaSuccess) return err;
   } else {
     if (m <= 256) tri_back_kernel<8, 4><<<m, 32, 0, st>>>(m, hv, tau, z, v);
-    else if (m <= 512) tri_back_kernel<16, 4><<<m, 32, 0, st>>>(m, hv, tau, z, v);
-    else tri_back_kernel<32, 2><<<m, 32, 0, st>>>(m, hv, tau, z, v);
+    else tri_back_kernel<16, 4><<<m, 32, 0, st>>>(m, hv, tau, z, v);
     ++g_launches;
   }
   return cudaGetLastError();

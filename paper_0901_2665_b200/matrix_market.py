@@ -12,6 +12,8 @@ order after a stable (row, col) sort, and the writer emits the lower triangle wi
 """
 from __future__ import annotations
 
+import re
+
 import numpy as np
 
 from .feast import InputError
@@ -22,20 +24,81 @@ def _fail(path, line, what):
     raise InputError(f"{path}:{line}: {what}")
 
 
+_WS = " \t\n\v\f\r"  # isspace() in the "C" locale
+_INT = re.compile(r"[+-]?[0-9]+")
+_FLT = re.compile(r"[+-]?(?:[0-9]+\.?[0-9]*|\.[0-9]*)(?:[eE][+-]?[0-9]*)?")
+_FLT_FULL = re.compile(r"[+-]?(?:[0-9]+\.?[0-9]*|\.[0-9]+)(?:[eE][+-]?[0-9]+)?")
+_LL_MAX = (1 << 63) - 1
+
+
+class _Stream:
+    """std::istringstream >> for long long and double (libstdc++ num_get, "C" locale): skip
+    isspace(), take the longest prefix the numeric grammar accepts (so '3.0' read as an integer
+    yields 3 and leaves '.0', and '1.5d0' read as a double yields 1.5 and leaves 'd0'), then
+    convert; no digits, an incomplete exponent ('1e'), 'nan' / 'inf' and out-of-range values set
+    the fail bit, and every later extraction fails too."""
+
+    def __init__(self, line):
+        self.s, self.pos, self.failed = line, 0, False
+
+    def _skip(self):
+        while self.pos < len(self.s) and self.s[self.pos] in _WS:
+            self.pos += 1
+
+    def integer(self):
+        if self.failed:
+            return None
+        self._skip()
+        m = _INT.match(self.s, self.pos)
+        if not m:
+            self.failed = True
+            return None
+        self.pos = m.end()
+        v = int(m.group())
+        if v > _LL_MAX or v < -_LL_MAX - 1:
+            self.failed = True
+            return None
+        return v
+
+    def real(self):
+        if self.failed:
+            return None
+        self._skip()
+        m = _FLT.match(self.s, self.pos)
+        if not m or not m.group():
+            self.failed = True
+            return None
+        self.pos = m.end()
+        txt = m.group()
+        if not _FLT_FULL.fullmatch(txt):  # strtod must consume everything num_get collected
+            self.failed = True
+            return None
+        v = float(txt)
+        if v in (float("inf"), float("-inf")):
+            self.failed = True
+            return None
+        return v
+
+
+def _words(line):
+    return [w for w in re.split("[" + _WS + "]+", line) if w]
+
+
 def _parse(path):
     """matrix_market.cpp:33-102: (n, complex_field, rows0, cols0, re)."""
     try:
-        f = open(path, "r")
+        f = open(path, "rb")
     except OSError:
         raise InputError("cannot open matrix file: " + str(path)) from None
     with f:
-        lines = f.read().split("\n")
+        # std::getline splits on '\n' only: a '\r' of a CRLF file stays in its line
+        lines = f.read().decode("latin-1").split("\n")
     if lines and lines[-1] == "":
         lines.pop()  # std::getline: a trailing newline ends the last line, it is not a line
     if not lines:
         _fail(path, 1, "empty file")
     lineno = 1
-    head = lines[0].split()
+    head = _words(lines[0])
     banner, obj, fmt, field, sym = (head + [""] * 5)[:5]
     if banner != "%%MatrixMarket":
         _fail(path, lineno, "missing MatrixMarket banner")
@@ -59,10 +122,9 @@ def _parse(path):
         lineno += 1
         if not line or line[0] == "%":
             continue
-        tok = line.split()
-        try:
-            rows, cols, count = int(tok[0]), int(tok[1]), int(tok[2])
-        except (ValueError, IndexError):
+        ls = _Stream(line)
+        rows, cols, count = ls.integer(), ls.integer(), ls.integer()
+        if ls.failed:
             _fail(path, lineno, "malformed size line")
         break
     if rows < 0:
@@ -75,7 +137,7 @@ def _parse(path):
         _fail(path, lineno, "negative entry count")
     ii = np.empty(count, np.int64)
     jj = np.empty(count, np.int64)
-    re = np.empty(count, np.float64)
+    re_ = np.empty(count, np.float64)
     seen = 0
     while seen < count:
         if pos >= len(lines):
@@ -85,21 +147,19 @@ def _parse(path):
         lineno += 1
         if not line or line[0] == "%":
             continue
-        tok = line.split()
-        try:
-            i, j, v = int(tok[0]), int(tok[1]), float(tok[2])
-        except (ValueError, IndexError):
+        ls = _Stream(line)
+        i, j, v = ls.integer(), ls.integer(), ls.real()
+        if ls.failed:
             _fail(path, lineno, "malformed entry")
         if cplx:
-            try:
-                float(tok[3])
-            except (ValueError, IndexError):
+            ls.real()
+            if ls.failed:
                 _fail(path, lineno, "missing imaginary part")
         if i < 1 or i > rows or j < 1 or j > cols:
             _fail(path, lineno, "index out of range")
-        ii[seen], jj[seen], re[seen] = i - 1, j - 1, v
+        ii[seen], jj[seen], re_[seen] = i - 1, j - 1, v
         seen += 1
-    return int(rows), cplx, ii, jj, re
+    return int(rows), cplx, ii, jj, re_
 
 
 def operator_from_triplets(n, rows, cols, values, mirror_off_diagonal=True) -> Operator:

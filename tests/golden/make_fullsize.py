@@ -1,0 +1,97 @@
+"""Generates tests/golden/full_*.npz: the REFERENCE's own feast_solve (oracle/_ref, compiled from
+/root/reference) on full-size BASELINE configs 3 and 4 and on the scaled config 5 that SURVEY
+§8(c) prescribes (L=64, b=512), run on this container's CPU cores (tens of minutes to hours each).
+
+The inputs are NOT stored (cfg3's B alone is 0.8 GB as CSR): the GPU tests regenerate them with
+paper_0901_2665_b200/problems.py (numpy PCG64, same bits on the same numpy) and the fixture keeps a
+SHA-256 of the generated arrays, so a generator drift fails loudly instead of comparing different
+pencils. Stored outputs: status, loops, trace history, in-interval counts, eigenvalues, residuals,
+max residual, timings, and the eigenvectors:
+
+  * in full where they are <= ~30 MB (cfg4: 8192 x 400);
+  * otherwise as a seeded Gaussian sketch S X (S: K x N, K = 512, rows drawn from
+    np.random.default_rng(SKETCH_SEED)); a K-row Gaussian sketch preserves the angle between two
+    vectors (a 2-dim subspace) to ~ +-3/sqrt(K) relative, so the per-eigenvector (per-cluster)
+    sine of the angle between GPU and reference eigenvectors is measurable to ~20 % in the sketched
+    space — enough to test <= 1e-8.
+
+    python tests/golden/make_fullsize.py cfg4 cfg3 cfg5s      # in the build container
+"""
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+from oracle import oracle as O  # noqa: E402
+from paper_0901_2665_b200 import problems as P  # noqa: E402
+
+GOLDEN = os.path.dirname(os.path.abspath(__file__))
+SKETCH_ROWS = 512
+SKETCH_SEED = 20260901
+FULL_VECTOR_LIMIT = 32 << 20
+
+
+def problem(name):
+    if name == "cfg3":
+        return P.config3()
+    if name == "cfg4":
+        return P.config4()
+    if name == "cfg5s":
+        return P.config5(L=64, b=512)
+    raise KeyError(name)
+
+
+def pencil_digest(prob):
+    h = hashlib.sha256()
+    for op in (prob.a, prob.b):
+        for f in ("dense", "row_ptr", "col_idx", "values", "diag", "lower"):
+            v = getattr(op, f)
+            if v is not None:
+                h.update(np.ascontiguousarray(v).view(np.uint8).reshape(-1).data)
+    h.update(np.array([prob.emin, prob.emax]).tobytes())
+    return h.hexdigest()
+
+
+def sketch_matrix(n, rows=SKETCH_ROWS, seed=SKETCH_SEED):
+    return np.random.default_rng(seed).standard_normal((rows, n)) / np.sqrt(rows)
+
+
+def main(names):
+    assert O.available("reference"), "build oracle/_ref first (make -C oracle reference)"
+    threads = os.cpu_count() or 1
+    for name in names:
+        t0 = time.perf_counter()
+        prob = problem(name)
+        tgen = time.perf_counter() - t0
+        print(f"{name}: generated n={prob.n} in {tgen:.0f}s; running the reference on {threads} threads",
+              flush=True)
+        t0 = time.perf_counter()
+        r = O.feast_solve(prob, threads=min(threads, prob.n_e), kind="reference")
+        wall = time.perf_counter() - t0
+        x = r["eigenvectors"]
+        out = dict(status=r["status"], m=r["m"], loops_used=r["loops_used"],
+                   max_residual=r["max_residual"], eigenvalues=r["eigenvalues"], residuals=r["residuals"],
+                   residual_absolute_only=r["residual_absolute_only"], trace_history=r["trace_history"],
+                   in_interval_counts=r["in_interval_counts"], digest=pencil_digest(prob),
+                   name=prob.name, n=prob.n, m0=prob.m0, n_e=prob.n_e, emin=prob.emin, emax=prob.emax,
+                   seed=prob.seed, expected_count=prob.expected_count,
+                   timings=json.dumps(r["timings"]), wall_s=wall, threads=min(threads, prob.n_e),
+                   sketch_rows=SKETCH_ROWS, sketch_seed=SKETCH_SEED)
+        if x.nbytes <= FULL_VECTOR_LIMIT:
+            out["eigenvectors"] = x
+        if x.shape[1]:
+            out["sketch"] = sketch_matrix(prob.n) @ x
+        path = os.path.join(GOLDEN, f"full_{name}.npz")
+        np.savez_compressed(path, **out)
+        print(f"{name}: {r['status']} m={r['m']} loops={r['loops_used']} max_res={r['max_residual']:.2e} "
+              f"wall={wall:.0f}s -> {path}", flush=True)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or ["cfg4", "cfg3", "cfg5s"])

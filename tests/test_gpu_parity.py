@@ -358,18 +358,18 @@ def test_streamed_node_batches_bit_identical(F, which):
 
 
 # small blocks (b <= 64): the twisted (two-ended) block-Thomas recursion and sweep, and the
-# plain top-down chain (FEAST_BT_TWIST=0), against the reference's pivoted BandedLU solves and
+# plain top-down chain (set_twist(False)), against the reference's pivoted BandedLU solves and
 # accumulate_subspace_real; L = 1..3 take the plain chain, L >= 4 meet at layer L // 2
 @pytest.mark.parametrize("twist", ["1", "0"])
 @pytest.mark.parametrize("L,b", [(1, 16), (2, 16), (3, 16), (4, 16), (5, 16), (9, 16), (33, 16),
                                  (4, 32), (7, 32), (5, 64), (6, 64)])
-def test_contour_pass_small_blocks(F, monkeypatch, twist, L, b):
+def test_contour_pass_small_blocks(F, twist, L, b):
     from paper_0901_2665_b200 import problems as P
-    monkeypatch.setenv("FEAST_BT_TWIST", twist)
     a, bb = P.blocktri_operators(L, b, seed=L * 100 + b)
     emin, emax, ne, m0 = -0.3, 0.4, 8, 20
     c = F.GpuContext(0)
     try:
+        c.set_twist(twist == "1")
         c.set_pencil(a, bb)
         c.prepare(emin, emax, ne)
         assert c.storage() == (b, L, L // 2 if (twist == "1" and L >= 4) else -1)

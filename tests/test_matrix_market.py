@@ -22,6 +22,11 @@ GOOD = {
     "negative_zero": BANNER + "2 2 2\n1 1 -0\n2 2 1\n",
     "case_banner": "%%MatrixMarket MATRIX Coordinate REAL Symmetric\n1 1 1\n1 1 3\n",
     "no_trailing_newline": BANNER + "1 1 1\n1 1 3",
+    # istream extraction takes the longest numeric prefix: '1.5d0' reads as 1.5
+    "fortran_exponent_prefix": BANNER + "2 2 2\n1 1 1.5d0\n2 2 2\n",
+    "signs_and_dots": BANNER + "2 2 3\n+1 +1 +.5\n2 1 -3.\n2 2 1e+2\n",
+    "underscore_digits": BANNER + "2 2 1\n1 1 1_0\n",   # reads 1 (Python's float() says 10)
+    "crlf": BANNER.replace("\n", "\r\n") + "2 2 2\r\n1 1 1\r\n2 2 4\r\n",
 }
 
 BAD = {
@@ -41,6 +46,14 @@ BAD = {
     "malformed_entry": BANNER + "2 2 1\n1 one 1\n",
     "index_range": BANNER + "2 2 1\n3 1 1\n",
     "index_zero": BANNER + "2 2 1\n0 1 1\n",
+    # what Python's int()/float() accept but C++ stream extraction rejects
+    "nan_value": BANNER + "2 2 1\n1 1 nan\n",
+    "inf_value": BANNER + "2 2 1\n1 1 inf\n",
+    "incomplete_exponent": BANNER + "2 2 1\n1 1 1e\n",
+    "overflow_value": BANNER + "2 2 1\n1 1 1e999\n",
+    "float_size_line": BANNER + "2.0 2 1\n1 1 1\n",
+    # a CRLF blank line is "\r": not empty for std::getline, so a malformed entry
+    "crlf_blank_line": BANNER.replace("\n", "\r\n") + "2 2 1\r\n\r\n1 1 1\r\n",
 }
 
 
