@@ -81,4 +81,6 @@ def load_fixture(path):
 def fixtures():
     if not os.path.isdir(GOLDEN):
         return []
-    return sorted(os.path.join(GOLDEN, f) for f in os.listdir(GOLDEN) if f.endswith(".npz"))
+    # (full_*.npz are the full-size reference runs of tests/golden/make_fullsize.py: outputs only)
+    return sorted(os.path.join(GOLDEN, f) for f in os.listdir(GOLDEN)
+                  if f.endswith(".npz") and not f.startswith("full_"))
