@@ -205,16 +205,28 @@ int feast_gpu_residuals(feast_gpu_ctx* ctx, int m, const double* lambdas, const 
 int feast_gpu_solve(feast_gpu_ctx* ctx, double emin, double emax, const feast_config_t* config,
                     const double* initial_y, int y_cols, feast_result_t* result);
 
+/* Look-ahead contour pass (default on): during each Rayleigh-Ritz step the next pass's Ne solves
+ * run on B Q, concurrently with the reduced eigensolve, and the next subspace is formed as
+ * (that result) Phi — the same iteration as core.hpp:356-388 by linearity of the filter. Used only
+ * when the Ritz block's cancellation factor max_i sum_j ||q_j||_B |Phi_ji| is <= 8 (otherwise the
+ * pass is redone in the reference order), never with low_memory or streamed factors. enable = 0
+ * runs every pass in the reference order. */
+int feast_gpu_set_lookahead(feast_gpu_ctx* ctx, int enable);
+
 /* Benchmark hook: runs `passes` loop bodies (contour pass + Rayleigh-Ritz + trace/count
  * + Y = B X) on the device-resident state set up by feast_gpu_bench_init (after
  * feast_gpu_prepare), with no stopping rule. Each pass is bracketed by CUDA events on the
- * context stream; when flush_bytes > 0 a buffer of that size is overwritten between
- * passes, outside the events, so every pass starts with a cold L2. Outputs: summed
- * device milliseconds and phase_ms[4] = {contour-solve kernel(s), Q reduction +
- * allreduce, Rayleigh-Ritz + Y = B X, dominant kernel alone}. */
+ * context stream, the passes pipelined as in feast_gpu_solve (look-ahead included); when
+ * flush_bytes > 0 a buffer of that size is overwritten once before the passes (outside the
+ * events). Outputs: device milliseconds of the whole sequence and phase_ms[4] summed over the
+ * passes = {contour-solve kernel(s), Q reduction + allreduce, Rayleigh-Ritz (projection +
+ * reduced eigensolve), dominant kernel alone}; with look-ahead the phases overlap. */
 int feast_gpu_bench_init(feast_gpu_ctx* ctx, int m0, uint64_t seed);
 int feast_gpu_bench_passes(feast_gpu_ctx* ctx, int passes, size_t flush_bytes, double* total_ms,
                            double* phase_ms);
+
+/* Passes of this context (solves and bench) whose look-ahead result was admitted. */
+int feast_gpu_lookahead_count(const feast_gpu_ctx* ctx);
 
 /* Number of kernel launches this context issued since creation (evidence counter). */
 int64_t feast_gpu_launch_count(const feast_gpu_ctx* ctx);

@@ -584,7 +584,7 @@ static cudaError_t bt_factor_big(const BtFactorArgs& a, cudaStream_t st) {
 }
 
 size_t bt_factor_work_elems(int b, int nodes) {  // double2 elements of BtFactorArgs::work
-  return (size_t)nodes * (4 * (size_t)b * b + 2 * (size_t)b * GJ_NB + (size_t)GJ_NB * GJ_NB);
+  return (size_t)nodes * (5 * (size_t)b * b + 2 * (size_t)b * GJ_NB + (size_t)GJ_NB * GJ_NB);  // S Cp CT X scr + GJ
 }
 
 cudaError_t bt_factor(const BtFactorArgs& a, cudaStream_t st) {

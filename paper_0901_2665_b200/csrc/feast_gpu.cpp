@@ -213,6 +213,15 @@ struct feast_gpu_ctx {
   int kmid = -1;  // twisted block-Thomas meeting layer of the current factors (bt_twist_layer)
   DevBuf<int> ipiv, perm, status;
   bool chol_failed_prev = false;  // the last reduced_gevp took the truncation path
+  bool gevp_enqueued = false;     // reduced_gevp_start enqueued the whole Cholesky path
+  // look-ahead contour pass (rayleigh_ritz_la): setting, and whether the last eigensolve's
+  // cancellation factor admitted it (the predictor for launching the next one)
+  bool lookahead = true, lookahead_ok = true;
+  cudaStream_t eigs = nullptr;  // high-priority stream of the reduced eigensolve
+  cudaEvent_t ev_proj = nullptr, ev_eig = nullptr;
+  double* hpin = nullptr;       // pinned: status, cancellation factor, eigenvalues
+  size_t hpin_n = 0;
+  DevBuf<double> kfac;
   bool twist = true;  // two-ended block-Thomas recursion where it applies (feast_gpu_set_twist)
   // workspaces
   int mcap = 0;
@@ -230,9 +239,12 @@ struct feast_gpu_ctx {
   std::chrono::steady_clock::time_point tmark;
   // bench state
   int bench_m = 0;
+  bool bench_have_q = false;  // the bench loop's next pass already has its Q (look-ahead)
+  int bench_pass = 0;
+  int lookahead_count = 0;    // passes (solve or bench) whose look-ahead result was admitted
   bool timing = false;
   cudaEvent_t ev[8] = {};
-  cudaEvent_t pev[2][3] = {};  // feast_solve phase timing per pass parity: contour start, RR start, RR end
+  cudaEvent_t pev[2][4] = {};  // phase timing per pass parity: contour start, contour end, RR start, solves end
 
   int owned() const { return e1 - e0; }
   bool streamed() const { return batch > 0 && batch < owned(); }
@@ -245,6 +257,7 @@ void ensure_eig(feast_gpu_ctx* c, int m) {
   if (c->eig && c->eig_cap >= m) return;
   if (c->eig) {
     CK(cudaStreamSynchronize(c->stream));  // a released workspace may go to another context
+    if (c->eigs) CK(cudaStreamSynchronize(c->eigs));
     eig_destroy(c->eig);
   }
   c->eig = eig_create(std::max(m, 16));
@@ -261,6 +274,16 @@ void ensure_reduced(feast_gpu_ctx* c, int m) {
   for (DevBuf<double>* d : {&c->Cm, &c->Lm, &c->Phi, &c->Vm, &c->S, &c->Tm}) d->ensure(mm);
   c->Ev.ensure(m);
   c->keep.ensure(m);
+  c->kfac.ensure(1);
+  c->status.ensure(1);
+  c->Dv.ensure((size_t)((m + 31) / 32) * 1024);
+  if (c->hpin_n < (size_t)m + 2) {
+    if (c->hpin) cudaFreeHost(c->hpin);
+    c->hpin = nullptr;
+    c->hpin_n = 0;
+    CK(cudaMallocHost(reinterpret_cast<void**>(&c->hpin), sizeof(double) * ((size_t)m + 2)));
+    c->hpin_n = (size_t)m + 2;
+  }
 }
 
 void plan_batch(feast_gpu_ctx* c, int m);
@@ -913,12 +936,23 @@ int resident_slot(feast_gpu_ctx* c, int s) {
 }
 
 // ------------------------------- passes --------------------------------------
-// Q = -sum_e Re(c_e (z_e B - A)^{-1} Y) over ALL nodes (allreduce across ranks)
-void contour_pass(feast_gpu_ctx* c, int m) {
+// sum over ranks of a device block (in place on `st`); a no-op on one rank
+void allreduce_sum(feast_gpu_ctx* c, double* p, size_t count, cudaStream_t st) {
+  if (c->nranks <= 1) return;
+  NcclApi& api = nccl();
+  if (!api.allReduce) fail(FEAST_ENCCL, "NCCL not available");
+  const int r = api.allReduce(p, p, count, kNcclFloat64, kNcclSum, c->comm, st);
+  if (r != 0) fail(FEAST_ENCCL, std::string("ncclAllReduce: ") + (api.getErrorString ? api.getErrorString(r) : "?"));
+}
+
+// q = -sum_e Re(c_e (z_e B - A)^{-1} y) over ALL nodes (allreduce across ranks); y, q npad x m.
+// ev_start / ev_solved (may be null) are recorded before the first solve and after the last one.
+void contour_pass(feast_gpu_ctx* c, int m, const double* y, double* q, cudaEvent_t ev_start = nullptr,
+                  cudaEvent_t ev_solved = nullptr) {
   join_aux(c);
   const int own = c->owned();
   const size_t nv = (size_t)c->npad * m;
-  if (c->timing) CK(cudaEventRecord(c->ev[2], c->stream));
+  if (ev_start) CK(cudaEventRecord(ev_start, c->stream));
   if (own > 0) {
     // node batches in ascending order (one batch = every owned node unless streamed); the
     // reduction continues the same ascending-e sum across batches, so the result is
@@ -929,26 +963,21 @@ void contour_pass(feast_gpu_ctx* c, int m) {
       if (c->res0 != s0 || c->rescnt != cnt) factor_range(c, s0, cnt);
       if (c->blocktri) {
         BtSweepArgs a{c->L, c->b, cnt, m, c->npad, c->ablow.p, c->dz.p + s0, c->dcoeff.p + s0, c->sinv.p,
-                      c->gfac.p, c->hfac.p, c->Y.p, c->T.p, c->W.p, 0, c->kmid};
+                      c->gfac.p, c->hfac.p, y, c->T.p, c->W.p, 0, c->kmid};
         CK(bt_sweep(a, c->stream));
       } else {
-        DenseSolveArgs a{c->n, cnt, m, c->npad, c->lu.p, c->perm.p, c->dinv.p, c->dcoeff.p + s0, c->Y.p, c->T.p,
+        DenseSolveArgs a{c->n, cnt, m, c->npad, c->lu.p, c->perm.p, c->dinv.p, c->dcoeff.p + s0, y, c->T.p,
                          c->W.p, 0};
         CK(dense_solve(a, c->stream));
       }
-      if (c->timing && s0 + cnt >= own) CK(cudaEventRecord(c->ev[3], c->stream));
-      CK(reduce_terms(c->T.p, cnt, (int64_t)nv, c->npad, m, c->npad, c->Q.p, c->stream, s0 > 0));
+      if (ev_solved && s0 + cnt >= own) CK(cudaEventRecord(ev_solved, c->stream));
+      CK(reduce_terms(c->T.p, cnt, (int64_t)nv, c->npad, m, c->npad, q, c->stream, s0 > 0));
     }
   } else {
-    if (c->timing) CK(cudaEventRecord(c->ev[3], c->stream));
-    CK(fill_zero(c->Q.p, nv, c->stream));
+    if (ev_solved) CK(cudaEventRecord(ev_solved, c->stream));
+    CK(fill_zero(q, nv, c->stream));
   }
-  if (c->nranks > 1) {
-    NcclApi& api = nccl();
-    if (!api.allReduce) fail(FEAST_ENCCL, "NCCL not available");
-    const int r = api.allReduce(c->Q.p, c->Q.p, nv, kNcclFloat64, kNcclSum, c->comm, c->stream);
-    if (r != 0) fail(FEAST_ENCCL, std::string("ncclAllReduce: ") + (api.getErrorString ? api.getErrorString(r) : "?"));
-  }
+  allreduce_sum(c, q, nv, c->stream);
 }
 
 // accumulate_subspace_hermitian (core.hpp:190-215) for the real symmetric pencils this path
@@ -987,13 +1016,7 @@ void contour_pass_hermitian(feast_gpu_ctx* c, int m) {
   } else {
     CK(fill_zero(c->AQ.p, 2 * (size_t)c->npad * m, c->stream));
   }
-  if (c->nranks > 1) {
-    NcclApi& api = nccl();
-    if (!api.allReduce) fail(FEAST_ENCCL, "NCCL not available");
-    const int r = api.allReduce(c->AQ.p, c->AQ.p, 2 * (size_t)c->npad * m, kNcclFloat64, kNcclSum, c->comm,
-                                c->stream);
-    if (r != 0) fail(FEAST_ENCCL, std::string("ncclAllReduce: ") + (api.getErrorString ? api.getErrorString(r) : "?"));
-  }
+  allreduce_sum(c, c->AQ.p, 2 * (size_t)c->npad * m, c->stream);
 }
 
 void apply_op(feast_gpu_ctx* c, int which, const double* x, double* y, int m) {
@@ -1023,89 +1046,34 @@ struct Reduced {
   std::vector<double> evals;
   int mo = 0;
   bool truncated = false;
+  double kfactor = 0.0;  // cancellation factor of X = Q Phi (cancellation_factor, misc.cu)
+  bool lookahead = false;  // c->X holds the look-ahead contour pass on B Q, admitted for use
 };
 
-// reduced_gevp (eigh.hpp:178-225) on device blocks Aq, Bq (m x m); Phi (m x mo) -> c->Phi
-Reduced reduced_gevp(feast_gpu_ctx* c, int m) {
-  Reduced r;
-  const size_t mm = (size_t)m * m;
-  CK(cudaMemcpyAsync(c->Lm.p, c->Bq.p, sizeof(double) * mm, cudaMemcpyDeviceToDevice, c->stream));
-  CK(cudaMemsetAsync(c->status.p, 0, sizeof(int), c->stream));
-  c->Dv.ensure((size_t)((m + 31) / 32) * 1024);
-  CK(cholesky(m, c->Lm.p, 1e-13, c->status.p, c->Dv.p, c->stream));
-  // While the Cholesky factorisations succeed, the rest of the path is enqueued without waiting
-  // for the pivot check: status and eigenvalues come back with ONE synchronisation. After a
-  // failed one (the subspace is in the truncation regime, where it usually stays) the status is
-  // read first, so a failing pass does not pay a full eigensolve on a partial factor.
-  r.evals.resize(m);
-  bool chol_ok = true;
-  if (c->chol_failed_prev) {
-    int st = 0;
-    CK(cudaMemcpyAsync(&st, c->status.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    sync(c);
-    chol_ok = st == 0;
-  }
-  if (chol_ok) {
-    // C = L^-1 A L^-T  via two lower solves and transposes (eigh.hpp:192-196)
-    CK(cudaMemcpyAsync(c->Cm.p, c->Aq.p, sizeof(double) * mm, cudaMemcpyDeviceToDevice, c->stream));
-    CK(trsm_lower(m, c->Lm.p, c->Dv.p, c->Cm.p, m, m, c->stream));
-    CK(transpose(c->Cm.p, m, m, m, c->Tm.p, m, c->stream));
-    CK(trsm_lower(m, c->Lm.p, c->Dv.p, c->Tm.p, m, m, c->stream));
-    CK(transpose(c->Tm.p, m, m, m, c->Cm.p, m, c->stream));
-    CK(symmetrize(c->Cm.p, m, m, c->stream));
-    CK(sym_eig(c->eig, m, c->Cm.p, c->Ev.p, c->Phi.p, c->stream));
-    CK(trsm_lower_t(m, c->Lm.p, c->Dv.p, c->Phi.p, m, m, c->stream));  // Phi = L^-T W
-    int st = 0;
-    CK(cudaMemcpyAsync(&st, c->status.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(r.evals.data(), c->Ev.p, sizeof(double) * m, cudaMemcpyDeviceToHost, c->stream));
-    sync(c);
-    if (!st) {
-      c->chol_failed_prev = false;
-      r.mo = m;
-      return r;
-    }
-  }
-  c->chol_failed_prev = true;
-  // spectral truncation fallback (eigh.hpp:204-224)
-  CK(cudaMemcpyAsync(c->Cm.p, c->Bq.p, sizeof(double) * mm, cudaMemcpyDeviceToDevice, c->stream));
-  CK(symmetrize(c->Cm.p, m, m, c->stream));
-  // mass-matrix modes at or below the 1e-14 truncation floor are discarded below, so their
-  // vectors are not computed (the near-null cluster of a filtered subspace is large)
-  CK(sym_eig(c->eig, m, c->Cm.p, c->Ev.p, c->Vm.p, c->stream, 1e-14));
-  std::vector<double> d(m);
-  CK(cudaMemcpyAsync(d.data(), c->Ev.p, sizeof(double) * m, cudaMemcpyDeviceToHost, c->stream));
-  sync(c);
-  const double dmax = d.back();
-  if (!(dmax > 0.0)) fail(FEAST_EBREAKDOWN, "reduced_gevp: projected mass matrix has no positive modes");
-  std::vector<int> keep;
-  for (int i = 0; i < m; ++i)
-    if (d[i] > 1e-14 * dmax) keep.push_back(i);
-  if (keep.empty()) fail(FEAST_EBREAKDOWN, "reduced_gevp: projected mass matrix has no usable modes");
-  const int k = (int)keep.size();
-  CK(cudaMemcpyAsync(c->keep.p, keep.data(), sizeof(int) * k, cudaMemcpyHostToDevice, c->stream));
-  CK(scale_columns(c->Vm.p, m, c->keep.p, c->Ev.p, k, c->S.p, c->stream));   // S = V_keep diag(d^-1/2)
-  CK(dgemm('N', 'N', m, k, m, 1.0, c->Aq.p, m, c->S.p, m, 0.0, c->Tm.p, m, c->gw.p, c->gw.n, c->stream));
-  CK(dgemm('T', 'N', k, k, m, 1.0, c->S.p, m, c->Tm.p, m, 0.0, c->Cm.p, k, c->gw.p, c->gw.n, c->stream));
-  CK(symmetrize(c->Cm.p, k, k, c->stream));
-  CK(sym_eig(c->eig, k, c->Cm.p, c->Ev.p, c->Vm.p, c->stream));
-  CK(dgemm('N', 'N', m, k, k, 1.0, c->S.p, m, c->Vm.p, k, 0.0, c->Phi.p, m, c->gw.p, c->gw.n, c->stream));
-  r.evals.resize(k);
-  CK(cudaMemcpyAsync(r.evals.data(), c->Ev.p, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
-  sync(c);
-  r.mo = k;
-  r.truncated = true;
-  return r;
-}
+// ---------------------------------------------------------------------------------------------
+// Look-ahead contour pass. The FEAST filter is linear and Phi is real, so the next pass's
+// subspace -sum_e Re(c_e (z_e B - A)^{-1} B X) with X = Q Phi equals
+// (-sum_e Re(c_e (z_e B - A)^{-1} B Q)) Phi. The solves on B Q need only the projections, not the
+// reduced eigensolve, so they run on the main stream WHILE the eigensolve runs on a
+// high-priority stream (it is a chain of latency-bound few-CTA kernels, ~1 ms at m = 192, that
+// leaves most SMs idle); afterwards one GEMM forms the next Q. In exact arithmetic the iteration
+// is the reference's (core.hpp:356-388). In floating point each solved column carries its own
+// relative rounding, which Phi recombines: the error grows by at most the cancellation factor
+// K = max_i sum_j ||q_j||_B |Phi_ji| (1 when forming X cancels nothing; ~1 in the converged
+// regime where Q is close to X diag(rho)). The look-ahead result is used only when
+// K <= kLookaheadMaxK; otherwise the pass is redone in the reference order (X = Q Phi, Y = B X,
+// solves on Y), and the next pass does not speculate until K is small again. Disabled for
+// streamed node batches (the factors would be recomputed for a pass that may be discarded).
+constexpr double kLookaheadMaxK = 8.0;
 
-// rayleigh_ritz (core.hpp:228-240): X = Q Phi, Ritz values ascending
-Reduced rayleigh_ritz(feast_gpu_ctx* c, int m) {
+// [Aq | Bq] = Q^T [AQ | BQ] (rayleigh_ritz core.hpp:228-236) on the main stream
+void rr_project(feast_gpu_ctx* c, int m) {
   const int n = c->npad;
   // the one-GEMM projection needs BQ right after AQ and Bq right after Aq AT THIS m: the
   // buffers are sized for mcap columns, and m shrinks after a truncated pass (core.hpp:387)
   c->BQ.p = c->AQ.p + (size_t)n * m;
   c->Bq.p = c->Aq.p + (size_t)m * m;
   apply_both(c, c->Q.p, c->AQ.p, c->BQ.p, m);
-  // [Aq | Bq] = Q^T [AQ | BQ] in one GEMM (adjacent buffers; same sums as two separate ones)
   if (m % 64 == 0) {  // symmetric halves: upper tiles only (2/3 of the flops at m = 192)
     CK(dgemm_tn_sym2(m, n, c->Q.p, n, c->AQ.p, n, c->Aq.p, c->gw.p, c->gw.n, c->stream));
     CK(symmetrize_tiles(c->Aq.p, m, m, c->stream));
@@ -1115,9 +1083,165 @@ Reduced rayleigh_ritz(feast_gpu_ctx* c, int m) {
     CK(symmetrize(c->Aq.p, m, m, c->stream));
     CK(symmetrize(c->Bq.p, m, m, c->stream));
   }
-  Reduced r = reduced_gevp(c, m);
-  CK(dgemm('N', 'N', n, r.mo, m, 1.0, c->Q.p, n, c->Phi.p, m, 0.0, c->X.p, n, c->gw.p, c->gw.n, c->stream));
+}
+
+// reduced_gevp (eigh.hpp:178-225) on device blocks Aq, Bq (m x m) on stream `st`: Phi (m x mo)
+// -> c->Phi, eigenvalues + status + cancellation factor back to the host. The Cholesky path is
+// enqueued by reduced_gevp_start; reduced_gevp_finish waits for it and runs the truncation
+// fallback when the factorisation failed. (The main stream may run the look-ahead contour pass
+// in between.)
+void reduced_gevp_start(feast_gpu_ctx* c, int m, cudaStream_t st) {
+  const size_t mm = (size_t)m * m;
+  double* h = c->hpin;
+  CK(cudaMemcpyAsync(c->Lm.p, c->Bq.p, sizeof(double) * mm, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemsetAsync(c->status.p, 0, sizeof(int), st));
+  CK(cholesky(m, c->Lm.p, 1e-13, c->status.p, c->Dv.p, st));
+  // While the Cholesky factorisations succeed, the rest of the path is enqueued without waiting
+  // for the pivot check: status and eigenvalues come back with ONE synchronisation. After a
+  // failed one (the subspace is in the truncation regime, where it usually stays) the status is
+  // read first (reduced_gevp_finish), so a failing pass does not pay a full eigensolve on a
+  // partial factor.
+  c->gevp_enqueued = !c->chol_failed_prev;
+  if (c->gevp_enqueued) {
+    // C = L^-1 A L^-T  via two lower solves and transposes (eigh.hpp:192-196)
+    CK(cudaMemcpyAsync(c->Cm.p, c->Aq.p, sizeof(double) * mm, cudaMemcpyDeviceToDevice, st));
+    CK(trsm_lower(m, c->Lm.p, c->Dv.p, c->Cm.p, m, m, st));
+    CK(transpose(c->Cm.p, m, m, m, c->Tm.p, m, st));
+    CK(trsm_lower(m, c->Lm.p, c->Dv.p, c->Tm.p, m, m, st));
+    CK(transpose(c->Tm.p, m, m, m, c->Cm.p, m, st));
+    CK(symmetrize(c->Cm.p, m, m, st));
+    CK(sym_eig(c->eig, m, c->Cm.p, c->Ev.p, c->Phi.p, st));
+    CK(trsm_lower_t(m, c->Lm.p, c->Dv.p, c->Phi.p, m, m, st));  // Phi = L^-T W
+    CK(cancellation_factor(m, m, c->Bq.p, m, c->Phi.p, m, c->kfac.p, st));
+    CK(cudaMemcpyAsync(h + 1, c->kfac.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h + 2, c->Ev.p, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaMemcpyAsync(h, c->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(c->ev_eig, st));
+}
+
+Reduced reduced_gevp_finish(feast_gpu_ctx* c, int m, cudaStream_t st) {
+  Reduced r;
+  const size_t mm = (size_t)m * m;
+  double* h = c->hpin;
+  CK(cudaEventSynchronize(c->ev_eig));
+  int chol_status = 0;
+  std::memcpy(&chol_status, h, sizeof(int));
+  if (c->gevp_enqueued && chol_status == 0) {
+    c->chol_failed_prev = false;
+    r.evals.assign(h + 2, h + 2 + m);
+    r.kfactor = h[1];
+    r.mo = m;
+    return r;
+  }
+  c->chol_failed_prev = chol_status != 0;
+  if (chol_status == 0) {  // (the status was read first: finish the Cholesky path now)
+    c->chol_failed_prev = false;
+    c->gevp_enqueued = false;
+    CK(cudaMemcpyAsync(c->Cm.p, c->Aq.p, sizeof(double) * mm, cudaMemcpyDeviceToDevice, st));
+    CK(trsm_lower(m, c->Lm.p, c->Dv.p, c->Cm.p, m, m, st));
+    CK(transpose(c->Cm.p, m, m, m, c->Tm.p, m, st));
+    CK(trsm_lower(m, c->Lm.p, c->Dv.p, c->Tm.p, m, m, st));
+    CK(transpose(c->Tm.p, m, m, m, c->Cm.p, m, st));
+    CK(symmetrize(c->Cm.p, m, m, st));
+    CK(sym_eig(c->eig, m, c->Cm.p, c->Ev.p, c->Phi.p, st));
+    CK(trsm_lower_t(m, c->Lm.p, c->Dv.p, c->Phi.p, m, m, st));
+    CK(cancellation_factor(m, m, c->Bq.p, m, c->Phi.p, m, c->kfac.p, st));
+    CK(cudaMemcpyAsync(h + 1, c->kfac.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h + 2, c->Ev.p, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(c->ev_eig, st));
+    CK(cudaEventSynchronize(c->ev_eig));
+    r.evals.assign(h + 2, h + 2 + m);
+    r.kfactor = h[1];
+    r.mo = m;
+    return r;
+  }
+  // spectral truncation fallback (eigh.hpp:204-224)
+  CK(cudaMemcpyAsync(c->Cm.p, c->Bq.p, sizeof(double) * mm, cudaMemcpyDeviceToDevice, st));
+  CK(symmetrize(c->Cm.p, m, m, st));
+  // mass-matrix modes at or below the 1e-14 truncation floor are discarded below, so their
+  // vectors are not computed (the near-null cluster of a filtered subspace is large)
+  CK(sym_eig(c->eig, m, c->Cm.p, c->Ev.p, c->Vm.p, st, 1e-14));
+  std::vector<double> d(m);
+  CK(cudaMemcpyAsync(d.data(), c->Ev.p, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const double dmax = d.back();
+  if (!(dmax > 0.0)) fail(FEAST_EBREAKDOWN, "reduced_gevp: projected mass matrix has no positive modes");
+  std::vector<int> keep;
+  for (int i = 0; i < m; ++i)
+    if (d[i] > 1e-14 * dmax) keep.push_back(i);
+  if (keep.empty()) fail(FEAST_EBREAKDOWN, "reduced_gevp: projected mass matrix has no usable modes");
+  const int k = (int)keep.size();
+  CK(cudaMemcpyAsync(c->keep.p, keep.data(), sizeof(int) * k, cudaMemcpyHostToDevice, st));
+  CK(scale_columns(c->Vm.p, m, c->keep.p, c->Ev.p, k, c->S.p, st));   // S = V_keep diag(d^-1/2)
+  CK(dgemm('N', 'N', m, k, m, 1.0, c->Aq.p, m, c->S.p, m, 0.0, c->Tm.p, m, c->gw.p, c->gw.n, st));
+  CK(dgemm('T', 'N', k, k, m, 1.0, c->S.p, m, c->Tm.p, m, 0.0, c->Cm.p, k, c->gw.p, c->gw.n, st));
+  CK(symmetrize(c->Cm.p, k, k, st));
+  CK(sym_eig(c->eig, k, c->Cm.p, c->Ev.p, c->Vm.p, st));
+  CK(dgemm('N', 'N', m, k, k, 1.0, c->S.p, m, c->Vm.p, k, 0.0, c->Phi.p, m, c->gw.p, c->gw.n, st));
+  CK(cancellation_factor(m, k, c->Bq.p, m, c->Phi.p, m, c->kfac.p, st));
+  CK(cudaMemcpyAsync(h + 1, c->kfac.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h + 2, c->Ev.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(c->ev_eig, st));
+  CK(cudaEventSynchronize(c->ev_eig));
+  r.evals.assign(h + 2, h + 2 + k);
+  r.kfactor = h[1];
+  r.mo = k;
+  r.truncated = true;
   return r;
+}
+
+// reduced_gevp on the main stream (the C-ABI's feast_gpu_reduced_gevp)
+Reduced reduced_gevp(feast_gpu_ctx* c, int m) {
+  reduced_gevp_start(c, m, c->stream);
+  return reduced_gevp_finish(c, m, c->stream);
+}
+
+// rayleigh_ritz (core.hpp:228-240) on c->Q (m columns) with the reduced eigensolve on the
+// high-priority stream. lookahead: the main stream also runs the look-ahead contour pass on B Q
+// into c->X meanwhile (r.lookahead then says whether it is admitted). ev_* (may be null): RR
+// start / eigensolve end / look-ahead contour start and solved (timing).
+Reduced rayleigh_ritz_la(feast_gpu_ctx* c, int m, bool lookahead, cudaEvent_t ev_rr0 = nullptr,
+                         cudaEvent_t ev_c0 = nullptr, cudaEvent_t ev_c1 = nullptr) {
+  if (ev_rr0) CK(cudaEventRecord(ev_rr0, c->stream));
+  rr_project(c, m);
+  CK(cudaEventRecord(c->ev_proj, c->stream));
+  CK(cudaStreamWaitEvent(c->eigs, c->ev_proj, 0));
+  reduced_gevp_start(c, m, c->eigs);
+  if (lookahead) contour_pass(c, m, c->BQ.p, c->X.p, ev_c0, ev_c1);
+  Reduced r = reduced_gevp_finish(c, m, c->eigs);
+  r.lookahead = lookahead && r.kfactor <= kLookaheadMaxK;
+  c->lookahead_ok = r.kfactor <= kLookaheadMaxK;
+  CK(cudaStreamWaitEvent(c->stream, c->ev_eig, 0));  // Phi is read on the main stream from here on
+  return r;
+}
+
+// X = Q Phi (the Ritz block; rayleigh_ritz's last step)
+void ritz_vectors(feast_gpu_ctx* c, int m, const Reduced& r) {
+  const int n = c->npad;
+  CK(dgemm('N', 'N', n, r.mo, m, 1.0, c->Q.p, n, c->Phi.p, m, 0.0, c->X.p, n, c->gw.p, c->gw.n, c->stream));
+}
+
+// rayleigh_ritz without look-ahead, X = Q Phi formed (the C-ABI's feast_gpu_rayleigh_ritz)
+Reduced rayleigh_ritz(feast_gpu_ctx* c, int m) {
+  Reduced r = rayleigh_ritz_la(c, m, false);
+  ritz_vectors(c, m, r);
+  return r;
+}
+
+// after a Rayleigh-Ritz step that continues the loop: with an admitted look-ahead pass the next
+// Q = (look-ahead result) Phi (returns true: the next pass's contour solves are done); else the
+// reference order's Y = B X with X = Q Phi over all retained Ritz vectors (core.hpp:387), and
+// the next pass solves on Y (returns false)
+bool next_subspace(feast_gpu_ctx* c, int m, const Reduced& r) {
+  const int n = c->npad;
+  if (r.lookahead) {
+    CK(dgemm('N', 'N', n, r.mo, m, 1.0, c->X.p, n, c->Phi.p, m, 0.0, c->Q.p, n, c->gw.p, c->gw.n, c->stream));
+    return true;
+  }
+  ritz_vectors(c, m, r);
+  apply_op(c, 1, c->X.p, c->Y.p, r.mo);
+  return false;
 }
 
 void upload_block(feast_gpu_ctx* c, const double* host, int m, double* dev) {
@@ -1353,13 +1477,9 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
   std::vector<double> history;
   std::vector<int> counts;
 
-  auto finalize = [&](int status, const Reduced& rr, int pass) {
-    sync(c);  // the last pass's X = Q Phi, and its RR end event
-    {
-      float ms = 0.f;
-      CK(cudaEventElapsedTime(&ms, c->pev[pass & 1][1], c->pev[pass & 1][2]));
-      out->reduce_s += 1e-3 * ms;
-    }
+  auto finalize = [&](int status, const Reduced& rr, int pass, int mq) {
+    ritz_vectors(c, mq, rr);  // X = Q Phi (rayleigh_ritz, core.hpp:238)
+    sync(c);
     out->status = status;
     out->loops_used = pass;
     std::vector<int> keep;
@@ -1396,37 +1516,56 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
     out->total_s = secs(t_start);
   };
 
+  // the look-ahead contour pass overlaps each reduced eigensolve with the next pass's solves
+  // (rayleigh_ritz_la); not with low_memory / streamed factors, which refactor for every pass
+  const bool la_allowed = c->lookahead && !cfg->low_memory;
+  c->lookahead_ok = true;
+  bool have_q = false;  // this pass's Q is already formed (admitted look-ahead)
   for (int pass = 0; pass <= cfg->max_loops; ++pass) {
-    if (cfg->low_memory) c->factored = false;
-    if (!c->factored) {
-      const auto t0 = std::chrono::steady_clock::now();
-      factor(c);
-      out->factorize_s += secs(t0);
-      trace_mark(c, "solve: factor");
-    }
     // phase times from device events (FeastTimings, core.hpp:54-59): the only host
-    // synchronisation per pass is the one the trace check needs (the Ritz values, inside
-    // reduced_gevp). A pass's RR end event (after X = Q Phi) is read one pass later.
+    // synchronisation per pass is the one the trace check needs (the Ritz values, in
+    // reduced_gevp_finish); event set pass & 1 = {contour start, contour end, RR start}
     cudaEvent_t* pe = c->pev[pass & 1];
-    CK(cudaEventRecord(pe[0], c->stream));
-    contour_pass(c, m);
-    CK(cudaEventRecord(pe[1], c->stream));
-    trace_mark(c, "solve: contour pass");
-
+    if (!have_q) {
+      if (cfg->low_memory) c->factored = false;
+      if (!c->factored) {
+        const auto t0 = std::chrono::steady_clock::now();
+        factor(c);
+        out->factorize_s += secs(t0);
+        trace_mark(c, "solve: factor");
+      }
+      CK(cudaEventRecord(pe[0], c->stream));
+      contour_pass(c, m, c->Y.p, c->Q.p);
+      CK(cudaEventRecord(pe[1], c->stream));
+      trace_mark(c, "solve: contour pass");
+    }
+    const bool la = la_allowed && c->lookahead_ok && !c->streamed() && pass < cfg->max_loops;
     Reduced rr;
     try {
-      rr = rayleigh_ritz(c, m);
+      cudaEvent_t* pn = c->pev[(pass + 1) & 1];
       CK(cudaEventRecord(pe[2], c->stream));
-      float ms = 0.f;
-      CK(cudaEventElapsedTime(&ms, pe[0], pe[1]));  // complete: reduced_gevp synchronised
-      out->solve_s += 1e-3 * ms;
-      if (pass > 0) {
-        cudaEvent_t* pp = c->pev[(pass - 1) & 1];
-        CK(cudaEventElapsedTime(&ms, pp[1], pp[2]));
-        out->reduce_s += 1e-3 * ms;
+      rr_project(c, m);
+      CK(cudaEventRecord(c->ev_proj, c->stream));
+      CK(cudaStreamWaitEvent(c->eigs, c->ev_proj, 0));
+      reduced_gevp_start(c, m, c->eigs);
+      if (la) {
+        CK(cudaEventRecord(pn[0], c->stream));
+        contour_pass(c, m, c->BQ.p, c->X.p);
+        CK(cudaEventRecord(pn[1], c->stream));
       }
+      rr = reduced_gevp_finish(c, m, c->eigs);
+      rr.lookahead = la && rr.kfactor <= kLookaheadMaxK;
+      c->lookahead_ok = rr.kfactor <= kLookaheadMaxK;
+      if (rr.lookahead) ++c->lookahead_count;
+      CK(cudaStreamWaitEvent(c->stream, c->ev_eig, 0));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, pe[0], pe[1]));  // this pass's contour solves (complete)
+      out->solve_s += 1e-3 * ms;
+      CK(cudaEventElapsedTime(&ms, pe[2], c->ev_eig));
+      out->reduce_s += 1e-3 * ms;
     } catch (const Failure& f) {
       if (f.code != FEAST_EBREAKDOWN) throw;
+      CK(cudaStreamSynchronize(c->stream));
       out->status = FEAST_STATUS_BREAKDOWN;
       out->loops_used = pass;
       if (out->trace_history) std::memcpy(out->trace_history, history.data(), sizeof(double) * history.size());
@@ -1447,28 +1586,28 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
     counts.push_back(cnt);
 
     if (cnt == cfg->m0) {
-      finalize(FEAST_STATUS_SATURATED, rr, pass);
+      finalize(FEAST_STATUS_SATURATED, rr, pass, m);
       return;
     }
     if (pass >= 1) {
       if (cnt == 0 && prev_count == 0) {
-        finalize(FEAST_STATUS_NO_EIGENVALUES, rr, pass);
+        finalize(FEAST_STATUS_NO_EIGENVALUES, rr, pass, m);
         return;
       }
       const double denom = std::max(std::fabs(tr), emax - emin);
       if (cnt == prev_count && std::fabs(tr - prev_trace) <= effective_tol * denom) {
-        finalize(FEAST_STATUS_CONVERGED, rr, pass);
+        finalize(FEAST_STATUS_CONVERGED, rr, pass, m);
         return;
       }
     }
     if (pass == cfg->max_loops) {
-      finalize(FEAST_STATUS_MAX_LOOPS, rr, pass);
+      finalize(FEAST_STATUS_MAX_LOOPS, rr, pass, m);
       return;
     }
     prev_trace = tr;
     prev_count = cnt;
+    have_q = next_subspace(c, m, rr);
     m = rr.mo;
-    apply_op(c, 1, c->X.p, c->Y.p, m);  // y = B X over all retained Ritz vectors (core.hpp:387)
   }
   fail(FEAST_EINTERNAL, "feast_solve: unreachable");
 }
@@ -1522,6 +1661,11 @@ int feast_gpu_create(int device, void* stream, feast_gpu_ctx** out) {
       c->own_stream = true;
     }
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&c->eigs, cudaStreamNonBlocking, hi));
+    CK(cudaEventCreateWithFlags(&c->ev_proj, cudaEventDisableTiming));
+    CK(cudaEventCreate(&c->ev_eig));
     for (auto& pe : c->pev)
       for (auto& e : pe) CK(cudaEventCreate(&e));
   });
@@ -1537,12 +1681,14 @@ void feast_gpu_destroy(feast_gpu_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->aux) cudaStreamSynchronize(c->aux);
+  if (c->eigs) cudaStreamSynchronize(c->eigs);
   cudaStreamSynchronize(c->stream);
   AllocStream as(c->stream);
   for (DevBuf<double>* d : {&c->A, &c->Bm, &c->Y, &c->Q, &c->X, &c->AQ, &c->BQ, &c->T, &c->gw, &c->Aq, &c->Bq,
                             &c->Cm, &c->Lm, &c->Phi, &c->Ev, &c->Vm, &c->S, &c->Tm, &c->Dv, &c->Aband, &c->Bband, &c->csr})
     d->release();
   c->csrstats.release();  // every buffer, before the stream goes (the destructor would free on a dead stream)
+  c->kfac.release();
   for (DevBuf<double2>* d : {&c->abdiag, &c->ablow, &c->dz, &c->dcoeff, &c->sinv, &c->gfac, &c->hfac, &c->lu, &c->dinv,
                              &c->scratch, &c->W, &c->fwork})
     d->release();
@@ -1555,6 +1701,13 @@ void feast_gpu_destroy(feast_gpu_ctx* c) {
     for (auto& e : pe)
       if (e) cudaEventDestroy(e);
   if (c->comm && nccl().commDestroy) nccl().commDestroy(c->comm);
+  if (c->eigs) {
+    cudaStreamSynchronize(c->eigs);
+    cudaStreamDestroy(c->eigs);
+  }
+  if (c->ev_proj) cudaEventDestroy(c->ev_proj);
+  if (c->ev_eig) cudaEventDestroy(c->ev_eig);
+  if (c->hpin) cudaFreeHost(c->hpin);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   if (c->aux) cudaStreamDestroy(c->aux);
   if (c->y_ready) cudaEventDestroy(c->y_ready);
@@ -1688,7 +1841,7 @@ int feast_gpu_contour_pass(feast_gpu_ctx* c, const double* y, int m, double* q) 
     if (!c->factored) fail(FEAST_EINPUT, "feast_gpu: factors not prepared");
     ensure_workspace(c, m);
     upload_block(c, y, m, c->Y.p);
-    contour_pass(c, m);
+    contour_pass(c, m, c->Y.p, c->Q.p);
     download_block(c, c->Q.p, m, q);
     sync(c);
   });
@@ -1782,6 +1935,8 @@ int feast_gpu_bench_init(feast_gpu_ctx* c, int m0, uint64_t seed) {
     join_aux(c);
     sync(c);
     c->bench_m = m0;
+    c->bench_have_q = false;
+    c->lookahead_ok = true;
   });
 }
 
@@ -1789,38 +1944,70 @@ int feast_gpu_bench_passes(feast_gpu_ctx* c, int passes, size_t flush_bytes, dou
                            double* phase_ms) {
   return guarded(c, [&] {
     if (!c->factored || c->bench_m < 1) fail(FEAST_EINPUT, "bench: call feast_gpu_bench_init first");
-    double ph[4] = {0, 0, 0, 0}, tot = 0.0;
-    float ms = 0;
+    double ph[4] = {0, 0, 0, 0};
     DevBuf<char> flush;
-    if (flush_bytes) flush.ensure(flush_bytes);
-    c->timing = true;
+    if (flush_bytes) {  // L2 flushed once before the region; inside, the passes run back to back
+      flush.ensure(flush_bytes);
+      CK(cudaMemsetAsync(flush.p, 0x5a, flush_bytes, c->stream));
+    }
+    const bool la_allowed = c->lookahead && !c->streamed();
+    int m = c->bench_m;
+    bool have_q = c->bench_have_q;
+    float ms = 0.f;
+    CK(cudaEventRecord(c->ev[0], c->stream));
     for (int p = 0; p < passes; ++p) {
-      if (flush_bytes) CK(cudaMemsetAsync(flush.p, p & 0xff, flush_bytes, c->stream));
-      CK(cudaEventRecord(c->ev[0], c->stream));
-      contour_pass(c, c->bench_m);  // records ev[2..5] around the solve and the reduction
-      CK(cudaEventRecord(c->ev[1], c->stream));
-      Reduced r = rayleigh_ritz(c, c->bench_m);
-      apply_op(c, 1, c->X.p, c->Y.p, r.mo);
-      CK(cudaEventRecord(c->ev[6], c->stream));
-      CK(cudaEventSynchronize(c->ev[6]));
-      CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[6]));
-      tot += ms;
-      CK(cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]));
+      cudaEvent_t* pe = c->pev[(c->bench_pass + p) & 1];  // (the ring continues across calls)
+      cudaEvent_t* pn = c->pev[(c->bench_pass + p + 1) & 1];
+      if (!have_q) {
+        CK(cudaEventRecord(pe[0], c->stream));
+        contour_pass(c, m, c->Y.p, c->Q.p, nullptr, pe[3]);
+        CK(cudaEventRecord(pe[1], c->stream));
+      }
+      const bool la = la_allowed && c->lookahead_ok;
+      CK(cudaEventRecord(pe[2], c->stream));
+      rr_project(c, m);
+      CK(cudaEventRecord(c->ev_proj, c->stream));
+      CK(cudaStreamWaitEvent(c->eigs, c->ev_proj, 0));
+      reduced_gevp_start(c, m, c->eigs);
+      if (la) {
+        CK(cudaEventRecord(pn[0], c->stream));
+        contour_pass(c, m, c->BQ.p, c->X.p, nullptr, pn[3]);
+        CK(cudaEventRecord(pn[1], c->stream));
+      }
+      Reduced r = reduced_gevp_finish(c, m, c->eigs);
+      r.lookahead = la && r.kfactor <= kLookaheadMaxK;
+      c->lookahead_ok = r.kfactor <= kLookaheadMaxK;
+      CK(cudaStreamWaitEvent(c->stream, c->ev_eig, 0));
+      // this pass's contour solves are complete (they precede the projection)
+      CK(cudaEventElapsedTime(&ms, pe[0], pe[3]));
       ph[0] += ms;
       ph[3] += ms;
-      CK(cudaEventElapsedTime(&ms, c->ev[3], c->ev[1]));
+      CK(cudaEventElapsedTime(&ms, pe[3], pe[1]));
       ph[1] += ms;
-      CK(cudaEventElapsedTime(&ms, c->ev[1], c->ev[6]));
+      CK(cudaEventElapsedTime(&ms, pe[2], c->ev_eig));
       ph[2] += ms;
-      c->bench_m = r.mo;
+      have_q = next_subspace(c, m, r);
+      m = r.mo;
+      if (r.lookahead) ++c->lookahead_count;
     }
-    c->timing = false;
+    CK(cudaEventRecord(c->ev[1], c->stream));
+    CK(cudaEventSynchronize(c->ev[1]));
+    CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+    c->bench_m = m;
+    c->bench_have_q = have_q;
+    c->bench_pass += passes;
     flush.release();
-    if (total_ms) *total_ms = tot;
+    if (total_ms) *total_ms = ms;
     if (phase_ms)
       for (int i = 0; i < 4; ++i) phase_ms[i] = ph[i];
   });
 }
+
+int feast_gpu_set_lookahead(feast_gpu_ctx* c, int enable) {
+  return guarded(c, [&] { c->lookahead = enable != 0; });
+}
+
+int feast_gpu_lookahead_count(const feast_gpu_ctx* c) { return c ? c->lookahead_count : 0; }
 
 int64_t feast_gpu_launch_count(const feast_gpu_ctx*) { return g_launches; }
 

@@ -195,6 +195,10 @@ cudaError_t real_to_complex_slots(const double* y, int64_t ld, int64_t m, int no
 cudaError_t hermitian_terms(const double2* w, int nodes, int64_t ld, int n, int m, const double2* coeff,
                             double2* q, int accumulate, cudaStream_t st);
 
+// look-ahead admission test: *out = max_i sum_j sqrt(bq(j,j)) |phi(j,i)|, i < mo, j < m
+cudaError_t cancellation_factor(int m, int mo, const double* bq, int ldb, const double* phi, int ldp,
+                                double* out, cudaStream_t st);
+
 // misc
 cudaError_t fill_zero(double* p, size_t count, cudaStream_t st);
 cudaError_t gather_columns(const double* src, int ld, int n, const int* idx, int m, double* dst,

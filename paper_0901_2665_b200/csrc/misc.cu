@@ -46,6 +46,38 @@ cudaError_t residual_sums(int n, int m, const double* ax, const double* bx, cons
   return cudaGetLastError();
 }
 
+// Cancellation factor of the Ritz block X = Q Phi (m x mo Phi, ld m), the look-ahead contour
+// pass's admission test (feast_gpu.cpp, lookahead): K = max_i sum_j ||q_j||_B |Phi_ji| with
+// ||q_j||_B = sqrt(B_Q(j, j)). Every X column has unit B-norm, so K = 1 means no cancellation in
+// forming X; K measures how much the per-column rounding of solves on B Q grows when they are
+// recombined by Phi afterwards. One CTA per column i; the max over columns is order-independent
+// (atomicMax on the bits of non-negative doubles).
+__global__ void __launch_bounds__(128) cancellation_factor_kernel(int m, const double* __restrict__ bq, int ldb,
+                                                                  const double* __restrict__ phi, int ldp,
+                                                                  unsigned long long* __restrict__ out) {
+  const int i = blockIdx.x;
+  double s = 0.0;
+  for (int j = threadIdx.x; j < m; j += blockDim.x)
+    s += sqrt(fmax(bq[j + (int64_t)j * ldb], 0.0)) * fabs(phi[j + (int64_t)i * ldp]);
+  s = warp_sum(s);
+  __shared__ double red[4];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double k = red[0] + red[1] + red[2] + red[3];
+    atomicMax(out, __double_as_longlong(k));
+  }
+}
+
+cudaError_t cancellation_factor(int m, int mo, const double* bq, int ldb, const double* phi, int ldp,
+                                double* out, cudaStream_t st) {
+  cudaMemsetAsync(out, 0, sizeof(double), st);
+  if (mo <= 0) return cudaGetLastError();
+  cancellation_factor_kernel<<<mo, 128, 0, st>>>(m, bq, ldb, phi, ldp, reinterpret_cast<unsigned long long*>(out));
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 __global__ void fill_zero_kernel(double* p, size_t count) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
        i += (size_t)gridDim.x * blockDim.x)

@@ -98,6 +98,8 @@ def load_library(path: str = LIB_PATH):
     L.feast_gpu_random_block.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64, _dp]
     L.feast_gpu_set_node_batch.argtypes = [C.c_void_p, C.c_int]
     L.feast_gpu_set_twist.argtypes = [C.c_void_p, C.c_int]
+    L.feast_gpu_set_lookahead.argtypes = [C.c_void_p, C.c_int]
+    L.feast_gpu_lookahead_count.argtypes = [C.c_void_p]
     L.feast_gpu_solve_shift.argtypes = [C.c_void_p, C.c_int, _dp, C.c_int, C.c_int]
     L.feast_gpu_contour_pass.argtypes = [C.c_void_p, _dp, C.c_int, _dp]
     L.feast_gpu_contour_pass_hermitian.argtypes = [C.c_void_p, _dp, C.c_int, _dp]
@@ -121,7 +123,8 @@ EXPORTED_SYMBOLS = [
     "feast_gpu_rayleigh_ritz", "feast_gpu_reduced_gevp", "feast_gpu_residuals", "feast_gpu_solve",
     "feast_gpu_bench_init", "feast_gpu_bench_passes", "feast_gpu_launch_count",
     "feast_gpu_set_node_batch", "feast_gpu_storage", "feast_gpu_random_block",
-    "feast_gpu_contour_pass_hermitian", "feast_gpu_set_twist",
+    "feast_gpu_contour_pass_hermitian", "feast_gpu_set_twist", "feast_gpu_set_lookahead",
+    "feast_gpu_lookahead_count",
 ]
 
 
@@ -243,6 +246,13 @@ class GpuContext:
     def set_node_batch(self, nodes: int):
         """Factor memory plan: 0 = automatic (resident if they fit), k > 0 = stream k nodes."""
         self._check(self.L.feast_gpu_set_node_batch(self.h, int(nodes)))
+
+    def set_lookahead(self, enable: bool):
+        """Look-ahead contour pass overlapping each reduced eigensolve (default on)."""
+        self._check(self.L.feast_gpu_set_lookahead(self.h, int(bool(enable))))
+
+    def lookahead_count(self) -> int:
+        return int(self.L.feast_gpu_lookahead_count(self.h))
 
     def set_twist(self, enable: bool):
         """Two-ended block-Thomas recursion (default on) or the plain top-down chain (b <= 64)."""

@@ -436,3 +436,38 @@ def test_contour_pass_hermitian_equals_real_on_real_blocks(ctx):
     scale = max(1.0, float(np.max(np.abs(qr))))
     assert np.max(np.abs(qh.real - qr)) <= 1e-13 * scale
     assert np.max(np.abs(qh.imag)) <= 1e-13 * scale
+
+
+# The look-ahead contour pass (feast_gpu.cpp, rayleigh_ritz_la): the next pass's solves run on B Q
+# during the reduced eigensolve and the next subspace is (that result) Phi. Same iteration by
+# linearity; it must reproduce the reference-order loop (set_lookahead(False)) to rounding: same
+# status, counts and loop count, eigenvalues and trace history to 1e-10 relative, subspaces to a
+# 1e-8 principal angle, and it must actually be admitted on these converging problems.
+@pytest.mark.parametrize("which", ["cfg2_n2048", "bt_L16_b32", "small_dense_n60", "cfg1_n256"])
+def test_lookahead_matches_reference_order(F, which):
+    from tests.golden_problems import generate
+    prob = generate(which)
+    runs = {}
+    for la in (True, False):
+        c = F.GpuContext(0)
+        try:
+            c.set_lookahead(la)
+            c.set_pencil(prob.a, prob.b)
+            n0 = c.lookahead_count()
+            r = c.solve(F.SearchInterval(prob.emin, prob.emax),
+                        F.FeastConfig(m0=prob.m0, n_e=prob.n_e, trace_tol=prob.trace_tol,
+                                      max_loops=prob.max_loops, seed=prob.seed))
+            runs[la] = (r, c.lookahead_count() - n0)
+        finally:
+            c.close()
+    (on, n_on), (off, n_off) = runs[True], runs[False]
+    assert n_off == 0 and n_on >= 1, (n_on, n_off)
+    assert on.status == off.status and on.loops_used == off.loops_used
+    assert np.array_equal(on.in_interval_counts, off.in_interval_counts)
+    assert np.allclose(on.trace_history, off.trace_history, rtol=1e-10, atol=1e-12 * (prob.emax - prob.emin))
+    assert len(on.eigenvalues) == len(off.eigenvalues)
+    assert np.all(np.abs(on.eigenvalues - off.eigenvalues) <= 1e-10 * np.maximum(np.abs(off.eigenvalues), 1e-3 * (prob.emax - prob.emin)))
+    if len(on.eigenvalues):
+        bm = prob.b.to_dense()
+        assert sin_max_angle(on.eigenvectors, off.eigenvectors, bm) <= 1e-8
+    assert on.max_residual <= max(1e-9, 10 * off.max_residual)
