@@ -131,6 +131,23 @@ const char* feast_gpu_last_error(const feast_gpu_ctx* ctx);
 int feast_gpu_nccl_unique_id(void* id_out_128_bytes);
 int feast_gpu_set_comm(feast_gpu_ctx* ctx, const void* nccl_unique_id, int rank, int nranks);
 
+/* Loopback rank group: several contexts of ONE process (one host thread each, any devices)
+ * joined as ranks 0..nranks-1 with the same collectives as the NCCL group (device copies and
+ * host barriers). It runs the sharded loop and the row-distributed Rayleigh-Ritz step on a
+ * single GPU, which is how they are tested here; production runs one process per GPU with
+ * feast_gpu_set_comm. With nranks = 1 and a non-zero id, feast_gpu_set_comm builds a one-rank
+ * NCCL communicator, so the NCCL calls themselves also run on one GPU. */
+typedef struct feast_gpu_group feast_gpu_group;
+int feast_gpu_group_create(int nranks, feast_gpu_group** out);
+void feast_gpu_group_destroy(feast_gpu_group* group);
+int feast_gpu_set_group(feast_gpu_ctx* ctx, feast_gpu_group* group, int rank);
+
+/* Rayleigh-Ritz across the ranks of a group (default 1): each rank applies A, B and projects on
+ * its row slab (whole layers for block-tridiagonal pencils), one allreduce of the 2 M0^2 reduced
+ * values, the reduced eigensolve replicated, the N x M0 blocks the solves need allgathered by
+ * slabs. 0 = replicated Rayleigh-Ritz on every rank (rayleigh_ritz, core.hpp:228-240). */
+int feast_gpu_set_row_distribution(feast_gpu_ctx* ctx, int enable);
+
 /* Uploads the pencil (A symmetric, B symmetric positive definite). CSR inputs
  * whose pattern is block-tridiagonal are stored block-tridiagonal; other CSR
  * inputs are densified (the reference's Dense policy, inner_solver.hpp:88-92). */

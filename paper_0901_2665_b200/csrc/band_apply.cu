@@ -38,7 +38,7 @@ __global__ void band_rows_kernel(int L, int B, const double* __restrict__ diag, 
 }
 
 template <int B, bool TWO>
-__global__ void __launch_bounds__(256) band_apply_kernel(int n, const double* __restrict__ ab1,
+__global__ void __launch_bounds__(256) band_apply_kernel(int n, int rbeg, int rend, const double* __restrict__ ab1,
                                                          const double* __restrict__ ab2,
                                                          const double* __restrict__ x, int ldx, double* y1,
                                                          double* y2, int ldy, int m) {
@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(256) band_apply_kernel(int n, const double* __
   double* As1 = Xs + NCOL * SX;     // [RT][SA]: band row r0 + rr at As1[rr * SA]
   double* As2 = As1 + RT * SA;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
-  const int r0 = blockIdx.y * RT, n0 = blockIdx.x * NCOL, c0 = r0 - B;
+  const int r0 = rbeg + blockIdx.y * RT, n0 = blockIdx.x * NCOL, c0 = r0 - B;
   for (int e = tid; e < NCOL * (XR / 2); e += 256) {
     const int col = e / (XR / 2), ch = e - col * (XR / 2), row = c0 + 2 * ch, gc = n0 + col;
     const bool v = gc < m && row >= 0 && row < n;
@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(256) band_apply_kernel(int n, const double* __
   }
   for (int e = tid; e < RT * (W / 2); e += 256) {
     const int rr = e / (W / 2), ch = e - rr * (W / 2);
-    const bool v = r0 + rr < n;
+    const bool v = r0 + rr < rend;
     cp_async16z(As1 + rr * SA + 2 * ch, v ? ab1 + (int64_t)(r0 + rr) * W + 2 * ch : ab1, v);
     if (TWO) cp_async16z(As2 + rr * SA + 2 * ch, v ? ab2 + (int64_t)(r0 + rr) * W + 2 * ch : ab2, v);
   }
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(256) band_apply_kernel(int n, const double* __
     double* y = pass ? y2 : y1;
     for (int e = tid; e < NCOL * (RT / 2); e += 256) {
       const int col = e / (RT / 2), pr = e - col * (RT / 2), row = r0 + 2 * pr, gc = n0 + col;
-      if (gc < m && row < n)
+      if (gc < m && row < rend)
         *reinterpret_cast<double2*>(y + row + (int64_t)gc * ldy) = *reinterpret_cast<const double2*>(Ys + col * SY + 2 * pr);
     }
   }
@@ -114,8 +114,8 @@ cudaError_t band_rows(int L, int b, const double* diag, const double* low, doubl
 }
 
 template <int B, bool TWO>
-static cudaError_t launch_band(int n, const double* ab1, const double* ab2, const double* x, int ldx, double* y1,
-                               double* y2, int ldy, int m, cudaStream_t st) {
+static cudaError_t launch_band(int n, int rbeg, int rend, const double* ab1, const double* ab2, const double* x,
+                               int ldx, double* y1, double* y2, int ldy, int m, cudaStream_t st) {
   constexpr int RT = 64, NCOL = 64, W = 3 * B, XR = RT + 2 * B;
   const int sm = (int)sizeof(double) * (NCOL * (XR + 4) + (TWO ? 2 : 1) * RT * (W + 4));
   static bool attr = false;
@@ -123,20 +123,24 @@ static cudaError_t launch_band(int n, const double* ab1, const double* ab2, cons
     cudaFuncSetAttribute(band_apply_kernel<B, TWO>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     attr = true;
   }
-  dim3 grid((m + NCOL - 1) / NCOL, (n + RT - 1) / RT);
-  band_apply_kernel<B, TWO><<<grid, 256, sm, st>>>(n, ab1, ab2, x, ldx, y1, y2, ldy, m);
+  if (rend <= rbeg || m <= 0) return cudaSuccess;
+  dim3 grid((m + NCOL - 1) / NCOL, (rend - rbeg + RT - 1) / RT);
+  band_apply_kernel<B, TWO><<<grid, 256, sm, st>>>(n, rbeg, rend, ab1, ab2, x, ldx, y1, y2, ldy, m);
   ++g_launches;
   return cudaGetLastError();
 }
 
-// y1 = A x (and y2 = B x when ab2 != nullptr); b = 16 or 32, n = L b, ldx / ldy even
+// rows [l0 b, l1 b) of y1 = A x (and y2 = B x when ab2 != nullptr); b = 16 or 32, n = L b,
+// ldx / ldy even; x is read on rows [l0 b - b, l1 b + b) within [0, n)
 cudaError_t band_apply(int L, int b, const double* ab1, const double* ab2, const double* x, int ldx, double* y1,
-                       double* y2, int ldy, int m, cudaStream_t st) {
+                       double* y2, int ldy, int m, cudaStream_t st, int l0, int l1) {
   const int n = L * b;
-  if (b == 16) return ab2 ? launch_band<16, true>(n, ab1, ab2, x, ldx, y1, y2, ldy, m, st)
-                          : launch_band<16, false>(n, ab1, ab2, x, ldx, y1, y2, ldy, m, st);
-  if (b == 32) return ab2 ? launch_band<32, true>(n, ab1, ab2, x, ldx, y1, y2, ldy, m, st)
-                          : launch_band<32, false>(n, ab1, ab2, x, ldx, y1, y2, ldy, m, st);
+  if (l1 < 0) l1 = L;
+  const int rb = l0 * b, re = l1 * b;
+  if (b == 16) return ab2 ? launch_band<16, true>(n, rb, re, ab1, ab2, x, ldx, y1, y2, ldy, m, st)
+                          : launch_band<16, false>(n, rb, re, ab1, ab2, x, ldx, y1, y2, ldy, m, st);
+  if (b == 32) return ab2 ? launch_band<32, true>(n, rb, re, ab1, ab2, x, ldx, y1, y2, ldy, m, st)
+                          : launch_band<32, false>(n, rb, re, ab1, ab2, x, ldx, y1, y2, ldy, m, st);
   return cudaErrorInvalidValue;
 }
 

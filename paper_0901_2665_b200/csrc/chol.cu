@@ -393,8 +393,10 @@ __global__ void __launch_bounds__(256) trsm_res_kernel(int m, const double* __re
 
 template <bool TRANS>
 static cudaError_t trsm_tiles(int m, const double* l, const double* dinv, double* x, int ldx, int ncols,
-                              cudaStream_t st) {
-  if (m <= RS_MAXB * TB) {  // every lower tile of L resident in shared memory; beyond, L from L2
+                              cudaStream_t st, bool low_smem) {
+  // every lower tile of L resident in shared memory (~200 KB: a whole SM); beyond, or when the
+  // solve must share SMs with a concurrent kernel (low_smem), L streamed from L2
+  if (m <= RS_MAXB * TB && !low_smem) {
     const size_t rs = sizeof(double) * ((size_t)m * XC + (size_t)(RS_MAXB * (RS_MAXB + 1) / 2 + 1) * TB * TL +
                                         TB * XC);
     static bool rattr = false;
@@ -415,12 +417,12 @@ static cudaError_t trsm_tiles(int m, const double* l, const double* dinv, double
 }
 
 cudaError_t trsm_lower(int m, const double* l, const double* dinv, double* x, int ldx, int ncols,
-                       cudaStream_t st) {
-  return trsm_tiles<false>(m, l, dinv, x, ldx, ncols, st);
+                       cudaStream_t st, bool low_smem) {
+  return trsm_tiles<false>(m, l, dinv, x, ldx, ncols, st, low_smem);
 }
 cudaError_t trsm_lower_t(int m, const double* l, const double* dinv, double* x, int ldx, int ncols,
-                         cudaStream_t st) {
-  return trsm_tiles<true>(m, l, dinv, x, ldx, ncols, st);
+                         cudaStream_t st, bool low_smem) {
+  return trsm_tiles<true>(m, l, dinv, x, ldx, ncols, st, low_smem);
 }
 
 }  // namespace feastgpu

@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <atomic>
 #include <exception>
+#include <condition_variable>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <tuple>
@@ -58,6 +60,7 @@ struct NcclApi {
   int (*getUniqueId)(void*) = nullptr;
   int (*commInitRank)(void**, int, const void* /*by value 128B*/, int) = nullptr;
   int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*allGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
   int (*commDestroy)(void*) = nullptr;
   const char* (*getErrorString)(int) = nullptr;
 };
@@ -75,6 +78,7 @@ NcclApi& nccl() {
       api.getUniqueId = (int (*)(void*))dlsym(api.h, "ncclGetUniqueId");
       api.allReduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
           api.h, "ncclAllReduce");
+      api.allGather = (int (*)(const void*, void*, size_t, int, void*, cudaStream_t))dlsym(api.h, "ncclAllGather");
       api.commDestroy = (int (*)(void*))dlsym(api.h, "ncclCommDestroy");
       api.getErrorString = (const char* (*)(int))dlsym(api.h, "ncclGetErrorString");
     }
@@ -82,6 +86,119 @@ NcclApi& nccl() {
   return api;
 }
 constexpr int kNcclFloat64 = 8, kNcclSum = 0;
+
+// ----------------------------------------------------------------------------
+// Collectives of one context's rank group. NcclComm is the product path (one process per GPU,
+// NVLink / NVSwitch; NCCL picks NVLS on NVSwitch systems). LocalComm is a loopback group of
+// contexts inside ONE process (one host thread per context, any devices): the same collective
+// semantics through device copies and host barriers — no kernel ever waits on another rank's
+// kernel — so the sharded loop and the row-distributed Rayleigh-Ritz run, and are tested, on a
+// single GPU (tests/test_gpu_sharding.py).
+// ----------------------------------------------------------------------------
+struct Comm {
+  virtual ~Comm() = default;
+  // p <- sum over ranks of p (count doubles, in place), identical on every rank
+  virtual void allreduce(double* p, size_t count, cudaStream_t st) = 0;
+  // recv[r * count .. (r + 1) * count) <- rank r's send (count doubles)
+  virtual void allgather(const double* send, double* recv, size_t count, cudaStream_t st) = 0;
+  // this rank failed: release the others (a loopback group's barriers; NCCL ranks see the abort
+  // of the process)
+  virtual void abort() {}
+};
+
+struct NcclComm : Comm {
+  void* comm = nullptr;
+  ~NcclComm() override {
+    if (comm && nccl().commDestroy) nccl().commDestroy(comm);
+  }
+  static void check(int r, const char* what) {
+    if (r != 0) fail(FEAST_ENCCL, std::string(what) + ": " + (nccl().getErrorString ? nccl().getErrorString(r) : "?"));
+  }
+  void allreduce(double* p, size_t count, cudaStream_t st) override {
+    if (!nccl().allReduce) fail(FEAST_ENCCL, "NCCL not available");
+    check(nccl().allReduce(p, p, count, kNcclFloat64, kNcclSum, comm, st), "ncclAllReduce");
+  }
+  void allgather(const double* send, double* recv, size_t count, cudaStream_t st) override {
+    if (!nccl().allGather) fail(FEAST_ENCCL, "NCCL not available");
+    check(nccl().allGather(send, recv, count, kNcclFloat64, comm, st), "ncclAllGather");
+  }
+};
+
+}  // namespace
+
+struct feast_gpu_group {
+  int nranks = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t generation = 0;
+  bool broken = false;
+  double* stage = nullptr;  // nranks slots (device memory of the first rank's device)
+  size_t slot = 0;          // doubles per slot
+  // all ranks meet here; a rank that fails breaks the group so the others fail instead of hanging
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (broken) fail(FEAST_ENCCL, "local group: another rank failed");
+    const uint64_t g = generation;
+    if (++arrived == nranks) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+      return;
+    }
+    if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return generation != g || broken; }) || broken) {
+      broken = true;
+      cv.notify_all();
+      fail(FEAST_ENCCL, "local group: barrier timed out or another rank failed");
+    }
+  }
+  void breakup() {
+    std::lock_guard<std::mutex> lk(mu);
+    broken = true;
+    cv.notify_all();
+  }
+};
+
+namespace {
+
+struct LocalComm : Comm {
+  feast_gpu_group* g;
+  int rank;
+  LocalComm(feast_gpu_group* grp, int r) : g(grp), rank(r) {}
+  void abort() override { g->breakup(); }
+  void stage_ready(size_t count) {  // every rank enters; rank 0 sizes the slots
+    g->barrier();
+    if (rank == 0 && g->slot < count) {
+      if (g->stage) CK(cudaFree(g->stage));
+      g->stage = nullptr;
+      g->slot = 0;
+      CK(cudaMalloc(reinterpret_cast<void**>(&g->stage), sizeof(double) * count * g->nranks));
+      g->slot = count;
+    }
+    g->barrier();
+  }
+  void allreduce(double* p, size_t count, cudaStream_t st) override {
+    CK(cudaStreamSynchronize(st));
+    stage_ready(count);
+    CK(cudaMemcpyAsync(g->stage + rank * g->slot, p, sizeof(double) * count, cudaMemcpyDefault, st));
+    CK(cudaStreamSynchronize(st));
+    g->barrier();
+    CK(sum_slices(g->stage, g->nranks, (int64_t)g->slot, count, p, st));  // rank order: same bits everywhere
+    CK(cudaStreamSynchronize(st));
+    g->barrier();
+  }
+  void allgather(const double* send, double* recv, size_t count, cudaStream_t st) override {
+    CK(cudaStreamSynchronize(st));
+    stage_ready(count);
+    CK(cudaMemcpyAsync(g->stage + rank * g->slot, send, sizeof(double) * count, cudaMemcpyDefault, st));
+    CK(cudaStreamSynchronize(st));
+    g->barrier();
+    for (int r = 0; r < g->nranks; ++r)
+      CK(cudaMemcpyAsync(recv + r * count, g->stage + r * g->slot, sizeof(double) * count, cudaMemcpyDefault, st));
+    CK(cudaStreamSynchronize(st));
+    g->barrier();
+  }
+};
 
 // ----------------------------------------------------------------------------
 // Gauss-Legendre + half-circle contour (restates quadrature.cpp:14-87): Newton on the
@@ -186,9 +303,11 @@ struct feast_gpu_ctx {
   cudaEvent_t y_ready = nullptr;  // recorded on aux; the main stream waits on it before the first pass
   bool y_pending = false;
   std::string err;
-  // multi-GPU
-  void* comm = nullptr;
+  // multi-GPU: rank group (NCCL, or a loopback group of contexts in one process)
+  std::unique_ptr<Comm> comm;
   int rank = 0, nranks = 1;
+  bool row_dist = true;  // row-distributed Rayleigh-Ritz across the ranks (feast_gpu_set_row_distribution)
+  DevBuf<double> G;      // allgather staging (row-distributed)
   // pencil
   bool have_pencil = false;
   int n = 0, npad = 0;
@@ -218,7 +337,7 @@ struct feast_gpu_ctx {
   // cancellation factor admitted it (the predictor for launching the next one)
   bool lookahead = true, lookahead_ok = true;
   cudaStream_t eigs = nullptr;  // high-priority stream of the reduced eigensolve
-  cudaEvent_t ev_proj = nullptr, ev_eig = nullptr;
+  cudaEvent_t ev_proj = nullptr, ev_eig = nullptr, ev_pre_eig = nullptr;
   double* hpin = nullptr;       // pinned: status, cancellation factor, eigenvalues
   size_t hpin_n = 0;
   DevBuf<double> kfac;
@@ -936,13 +1055,9 @@ int resident_slot(feast_gpu_ctx* c, int s) {
 }
 
 // ------------------------------- passes --------------------------------------
-// sum over ranks of a device block (in place on `st`); a no-op on one rank
+// sum over ranks of a device block (in place on `st`); a no-op without a rank group
 void allreduce_sum(feast_gpu_ctx* c, double* p, size_t count, cudaStream_t st) {
-  if (c->nranks <= 1) return;
-  NcclApi& api = nccl();
-  if (!api.allReduce) fail(FEAST_ENCCL, "NCCL not available");
-  const int r = api.allReduce(p, p, count, kNcclFloat64, kNcclSum, c->comm, st);
-  if (r != 0) fail(FEAST_ENCCL, std::string("ncclAllReduce: ") + (api.getErrorString ? api.getErrorString(r) : "?"));
+  if (c->comm) c->comm->allreduce(p, count, st);
 }
 
 // q = -sum_e Re(c_e (z_e B - A)^{-1} y) over ALL nodes (allreduce across ranks); y, q npad x m.
@@ -1019,27 +1134,114 @@ void contour_pass_hermitian(feast_gpu_ctx* c, int m) {
   allreduce_sum(c, c->AQ.p, 2 * (size_t)c->npad * m, c->stream);
 }
 
-void apply_op(feast_gpu_ctx* c, int which, const double* x, double* y, int m) {
-  if (c->blocktri && c->b <= 32) {
-    CK(band_apply(c->L, c->b, which ? c->Bband.p : c->Aband.p, nullptr, x, c->npad, y, nullptr, c->npad, m,
-                  c->stream));
-  } else if (c->blocktri) {
-    const double* base = which ? c->Bm.p : c->A.p;
-    CK(bt_apply(c->L, c->b, base, base + (size_t)c->L * c->b * c->b, x, c->npad, y, c->npad, m, c->stream));
-  } else {
-    CK(dgemm('N', 'N', c->n, m, c->n, 1.0, which ? c->Bm.p : c->A.p, c->n, x, c->npad, 0.0, y, c->npad,
-             c->gw.p, c->gw.n, c->stream));
+// ------------------------------- row slabs -------------------------------------
+// Row-distributed Rayleigh-Ritz: with R ranks, rank r owns a row slab of the
+// N x M0 blocks (block-tridiagonal: whole layers [l0, l1); dense: an equal row range). It forms
+// A Q and B Q on its slab only (the block-tridiagonal applies read one layer of Q on each side,
+// the halo; dense applies read all of Q), the partial projections of its slab, and ONE allreduce
+// of the 2 M0^2 values gives every rank [A_Q | B_Q]; the reduced eigensolve is replicated. The
+// N x M0 blocks that the solves need in full (B Q for the look-ahead pass, Y = B X otherwise) are
+// allgathered by slabs. The N-proportional Rayleigh-Ritz work (applies, projections, Q Phi) so
+// divides by R.
+struct Slab {
+  int r0 = 0, r1 = 0;  // owned rows
+  int h0 = 0, h1 = 0;  // rows of Q this rank keeps valid (owned + halo)
+  int l0 = 0, l1 = -1; // owned layers (block-tridiagonal)
+};
+
+bool row_distributed(const feast_gpu_ctx* c) { return c->comm && c->nranks > 1 && c->row_dist; }
+
+Slab slab_of(const feast_gpu_ctx* c, int rank) {
+  Slab s;
+  if (!row_distributed(c)) {
+    s.r1 = s.h1 = c->npad;
+    s.l1 = c->blocktri ? c->L : -1;
+    return s;
   }
+  if (c->blocktri) {
+    s.l0 = (int)((int64_t)c->L * rank / c->nranks);
+    s.l1 = (int)((int64_t)c->L * (rank + 1) / c->nranks);
+    s.r0 = s.l0 * c->b;
+    s.r1 = s.l1 * c->b;
+    s.h0 = std::max(s.l0 - 1, 0) * c->b;
+    s.h1 = std::min(s.l1 + 1, c->L) * c->b;
+  } else {
+    s.r0 = (int)((int64_t)c->npad * rank / c->nranks);
+    s.r1 = (int)((int64_t)c->npad * (rank + 1) / c->nranks);
+    s.h0 = 0;
+    s.h1 = c->npad;
+  }
+  return s;
 }
 
-// A x and B x (one pass over x for small blocks)
-void apply_both(feast_gpu_ctx* c, const double* x, double* ya, double* yb, int m) {
+int slab_max_rows(const feast_gpu_ctx* c) {
+  int mx = 0;
+  for (int r = 0; r < c->nranks; ++r) {
+    const Slab s = slab_of(c, r);
+    mx = std::max(mx, s.r1 - s.r0);
+  }
+  return mx;
+}
+
+// rows [s.r0, s.r1) of y = Op x (x valid on [s.h0, s.h1))
+void apply_op(feast_gpu_ctx* c, int which, const double* x, double* y, int m, const Slab& s) {
+  if (s.r1 <= s.r0 || m <= 0) return;
   if (c->blocktri && c->b <= 32) {
-    CK(band_apply(c->L, c->b, c->Aband.p, c->Bband.p, x, c->npad, ya, yb, c->npad, m, c->stream));
+    CK(band_apply(c->L, c->b, which ? c->Bband.p : c->Aband.p, nullptr, x, c->npad, y, nullptr, c->npad, m,
+                  c->stream, s.l0, s.l1));
+  } else if (c->blocktri) {
+    const double* base = which ? c->Bm.p : c->A.p;
+    CK(bt_apply(c->L, c->b, base, base + (size_t)c->L * c->b * c->b, x, c->npad, y, c->npad, m, c->stream, s.l0,
+                s.l1));
+  } else {
+    CK(dgemm('N', 'N', s.r1 - s.r0, m, c->n, 1.0, (which ? c->Bm.p : c->A.p) + s.r0, c->n, x, c->npad, 0.0,
+             y + s.r0, c->npad, c->gw.p, c->gw.n, c->stream));
+  }
+}
+void apply_op(feast_gpu_ctx* c, int which, const double* x, double* y, int m) {
+  Slab all;
+  all.r1 = all.h1 = c->npad;
+  all.l1 = c->blocktri ? c->L : -1;
+  apply_op(c, which, x, y, m, all);
+}
+
+// A x and B x on rows of s (one pass over x for small blocks)
+void apply_both(feast_gpu_ctx* c, const double* x, double* ya, double* yb, int m, const Slab& s) {
+  if (c->blocktri && c->b <= 32) {
+    if (s.r1 > s.r0 && m > 0)
+      CK(band_apply(c->L, c->b, c->Aband.p, c->Bband.p, x, c->npad, ya, yb, c->npad, m, c->stream, s.l0, s.l1));
     return;
   }
-  apply_op(c, 0, x, ya, m);
-  apply_op(c, 1, x, yb, m);
+  apply_op(c, 0, x, ya, m, s);
+  apply_op(c, 1, x, yb, m, s);
+}
+void apply_both(feast_gpu_ctx* c, const double* x, double* ya, double* yb, int m) {
+  Slab all;
+  all.r1 = all.h1 = c->npad;
+  all.l1 = c->blocktri ? c->L : -1;
+  apply_both(c, x, ya, yb, m, all);
+}
+
+// every rank's slab of M (npad x m) into every rank's M: pack, allgather, unpack
+void allgather_rows(feast_gpu_ctx* c, double* M, int m) {
+  if (!row_distributed(c) || m <= 0) return;
+  const int sm = slab_max_rows(c);
+  const size_t cnt = (size_t)sm * m;
+  c->G.ensure(cnt * (c->nranks + 1));
+  double* send = c->G.p;
+  double* recv = send + cnt;
+  const Slab me = slab_of(c, c->rank);
+  const size_t ld = sizeof(double) * c->npad;
+  if (me.r1 > me.r0)
+    CK(cudaMemcpy2DAsync(send, sizeof(double) * sm, M + me.r0, ld, sizeof(double) * (me.r1 - me.r0), m,
+                         cudaMemcpyDeviceToDevice, c->stream));
+  c->comm->allgather(send, recv, cnt, c->stream);
+  for (int r = 0; r < c->nranks; ++r) {
+    const Slab o = slab_of(c, r);
+    if (r == c->rank || o.r1 <= o.r0) continue;
+    CK(cudaMemcpy2DAsync(M + o.r0, ld, recv + r * cnt, sizeof(double) * sm, sizeof(double) * (o.r1 - o.r0), m,
+                         cudaMemcpyDeviceToDevice, c->stream));
+  }
 }
 
 struct Reduced {
@@ -1066,31 +1268,48 @@ struct Reduced {
 // streamed node batches (the factors would be recomputed for a pass that may be discarded).
 constexpr double kLookaheadMaxK = 8.0;
 
-// [Aq | Bq] = Q^T [AQ | BQ] (rayleigh_ritz core.hpp:228-236) on the main stream
+// [Aq | Bq] = Q^T [AQ | BQ] (rayleigh_ritz core.hpp:228-236) on the main stream; row-distributed:
+// each rank projects its slab and one allreduce of the 2 m^2 partial sums completes it
 void rr_project(feast_gpu_ctx* c, int m) {
   const int n = c->npad;
   // the one-GEMM projection needs BQ right after AQ and Bq right after Aq AT THIS m: the
   // buffers are sized for mcap columns, and m shrinks after a truncated pass (core.hpp:387)
   c->BQ.p = c->AQ.p + (size_t)n * m;
   c->Bq.p = c->Aq.p + (size_t)m * m;
-  apply_both(c, c->Q.p, c->AQ.p, c->BQ.p, m);
-  if (m % 64 == 0) {  // symmetric halves: upper tiles only (2/3 of the flops at m = 192)
-    CK(dgemm_tn_sym2(m, n, c->Q.p, n, c->AQ.p, n, c->Aq.p, c->gw.p, c->gw.n, c->stream));
+  const Slab s = slab_of(c, c->rank);
+  const int k = s.r1 - s.r0;
+  apply_both(c, c->Q.p, c->AQ.p, c->BQ.p, m, s);
+  const bool sym = m % 64 == 0;  // symmetric halves: upper tiles only (2/3 of the flops at m = 192)
+  if (k == 0)
+    CK(fill_zero(c->Aq.p, 2 * (size_t)m * m, c->stream));
+  else if (sym)
+    CK(dgemm_tn_sym2(m, k, c->Q.p + s.r0, n, c->AQ.p + s.r0, n, c->Aq.p, c->gw.p, c->gw.n, c->stream));
+  else
+    CK(dgemm('T', 'N', m, 2 * m, k, 1.0, c->Q.p + s.r0, n, c->AQ.p + s.r0, n, 0.0, c->Aq.p, m, c->gw.p, c->gw.n,
+             c->stream));
+  if (row_distributed(c)) c->comm->allreduce(c->Aq.p, 2 * (size_t)m * m, c->stream);
+  if (sym) {
     CK(symmetrize_tiles(c->Aq.p, m, m, c->stream));
     CK(symmetrize_tiles(c->Bq.p, m, m, c->stream));
   } else {
-    CK(dgemm('T', 'N', m, 2 * m, n, 1.0, c->Q.p, n, c->AQ.p, n, 0.0, c->Aq.p, m, c->gw.p, c->gw.n, c->stream));
     CK(symmetrize(c->Aq.p, m, m, c->stream));
     CK(symmetrize(c->Bq.p, m, m, c->stream));
   }
 }
+
+// the look-ahead pass solves on B Q, which a row-distributed step holds by slabs
+void lookahead_input(feast_gpu_ctx* c, int m) { allgather_rows(c, c->BQ.p, m); }
 
 // reduced_gevp (eigh.hpp:178-225) on device blocks Aq, Bq (m x m) on stream `st`: Phi (m x mo)
 // -> c->Phi, eigenvalues + status + cancellation factor back to the host. The Cholesky path is
 // enqueued by reduced_gevp_start; reduced_gevp_finish waits for it and runs the truncation
 // fallback when the factorisation failed. (The main stream may run the look-ahead contour pass
 // in between.)
-void reduced_gevp_start(feast_gpu_ctx* c, int m, cudaStream_t st) {
+// concurrent: the look-ahead contour pass will run beside the eigensolve. It is held back until
+// the eigensolve reaches the tridiagonalisation (event c->ev_pre_eig): that kernel keeps the matrix
+// in registers and needs a whole SM, which the solves' CTAs would otherwise occupy for their entire
+// chains; the kernels after it take the routes that leave room on shared SMs (low_smem).
+void reduced_gevp_start(feast_gpu_ctx* c, int m, cudaStream_t st, bool concurrent = false) {
   const size_t mm = (size_t)m * m;
   double* h = c->hpin;
   CK(cudaMemcpyAsync(c->Lm.p, c->Bq.p, sizeof(double) * mm, cudaMemcpyDeviceToDevice, st));
@@ -1110,11 +1329,14 @@ void reduced_gevp_start(feast_gpu_ctx* c, int m, cudaStream_t st) {
     CK(trsm_lower(m, c->Lm.p, c->Dv.p, c->Tm.p, m, m, st));
     CK(transpose(c->Tm.p, m, m, m, c->Cm.p, m, st));
     CK(symmetrize(c->Cm.p, m, m, st));
-    CK(sym_eig(c->eig, m, c->Cm.p, c->Ev.p, c->Phi.p, st));
-    CK(trsm_lower_t(m, c->Lm.p, c->Dv.p, c->Phi.p, m, m, st));  // Phi = L^-T W
+    if (concurrent) CK(cudaEventRecord(c->ev_pre_eig, st));
+    CK(sym_eig(c->eig, m, c->Cm.p, c->Ev.p, c->Phi.p, st, 0.0, concurrent));
+    CK(trsm_lower_t(m, c->Lm.p, c->Dv.p, c->Phi.p, m, m, st, concurrent));  // Phi = L^-T W
     CK(cancellation_factor(m, m, c->Bq.p, m, c->Phi.p, m, c->kfac.p, st));
     CK(cudaMemcpyAsync(h + 1, c->kfac.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(h + 2, c->Ev.p, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
+  } else if (concurrent) {
+    CK(cudaEventRecord(c->ev_pre_eig, st));
   }
   CK(cudaMemcpyAsync(h, c->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaEventRecord(c->ev_eig, st));
@@ -1207,8 +1429,12 @@ Reduced rayleigh_ritz_la(feast_gpu_ctx* c, int m, bool lookahead, cudaEvent_t ev
   rr_project(c, m);
   CK(cudaEventRecord(c->ev_proj, c->stream));
   CK(cudaStreamWaitEvent(c->eigs, c->ev_proj, 0));
-  reduced_gevp_start(c, m, c->eigs);
-  if (lookahead) contour_pass(c, m, c->BQ.p, c->X.p, ev_c0, ev_c1);
+  reduced_gevp_start(c, m, c->eigs, lookahead);
+  if (lookahead) {
+    lookahead_input(c, m);
+    CK(cudaStreamWaitEvent(c->stream, c->ev_pre_eig, 0));
+    contour_pass(c, m, c->BQ.p, c->X.p, ev_c0, ev_c1);
+  }
   Reduced r = reduced_gevp_finish(c, m, c->eigs);
   r.lookahead = lookahead && r.kfactor <= kLookaheadMaxK;
   c->lookahead_ok = r.kfactor <= kLookaheadMaxK;
@@ -1216,10 +1442,14 @@ Reduced rayleigh_ritz_la(feast_gpu_ctx* c, int m, bool lookahead, cudaEvent_t ev
   return r;
 }
 
-// X = Q Phi (the Ritz block; rayleigh_ritz's last step)
+// X = Q Phi (the Ritz block; rayleigh_ritz's last step), all rows on every rank
 void ritz_vectors(feast_gpu_ctx* c, int m, const Reduced& r) {
   const int n = c->npad;
-  CK(dgemm('N', 'N', n, r.mo, m, 1.0, c->Q.p, n, c->Phi.p, m, 0.0, c->X.p, n, c->gw.p, c->gw.n, c->stream));
+  const Slab s = slab_of(c, c->rank);
+  if (s.r1 > s.r0)
+    CK(dgemm('N', 'N', s.r1 - s.r0, r.mo, m, 1.0, c->Q.p + s.r0, n, c->Phi.p, m, 0.0, c->X.p + s.r0, n, c->gw.p,
+             c->gw.n, c->stream));
+  allgather_rows(c, c->X.p, r.mo);
 }
 
 // rayleigh_ritz without look-ahead, X = Q Phi formed (the C-ABI's feast_gpu_rayleigh_ritz)
@@ -1235,12 +1465,17 @@ Reduced rayleigh_ritz(feast_gpu_ctx* c, int m) {
 // the next pass solves on Y (returns false)
 bool next_subspace(feast_gpu_ctx* c, int m, const Reduced& r) {
   const int n = c->npad;
+  const Slab s = slab_of(c, c->rank);  // row-distributed: only the rows the next projection reads
   if (r.lookahead) {
-    CK(dgemm('N', 'N', n, r.mo, m, 1.0, c->X.p, n, c->Phi.p, m, 0.0, c->Q.p, n, c->gw.p, c->gw.n, c->stream));
+    CK(dgemm('N', 'N', s.h1 - s.h0, r.mo, m, 1.0, c->X.p + s.h0, n, c->Phi.p, m, 0.0, c->Q.p + s.h0, n, c->gw.p,
+             c->gw.n, c->stream));
     return true;
   }
-  ritz_vectors(c, m, r);
-  apply_op(c, 1, c->X.p, c->Y.p, r.mo);
+  if (s.h1 > s.h0)
+    CK(dgemm('N', 'N', s.h1 - s.h0, r.mo, m, 1.0, c->Q.p + s.h0, n, c->Phi.p, m, 0.0, c->X.p + s.h0, n, c->gw.p,
+             c->gw.n, c->stream));
+  apply_op(c, 1, c->X.p, c->Y.p, r.mo, s);
+  allgather_rows(c, c->Y.p, r.mo);
   return false;
 }
 
@@ -1517,8 +1752,10 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
   };
 
   // the look-ahead contour pass overlaps each reduced eigensolve with the next pass's solves
-  // (rayleigh_ritz_la); not with low_memory / streamed factors, which refactor for every pass
-  const bool la_allowed = c->lookahead && !cfg->low_memory;
+  // (rayleigh_ritz_la); not with streamed factors (a discarded look-ahead would have refactored
+  // every batch). low_memory keeps it and refactors before it, so results stay bit-identical to
+  // the default (test_core.cpp:341-376)
+  const bool la_allowed = c->lookahead;
   c->lookahead_ok = true;
   bool have_q = false;  // this pass's Q is already formed (admitted look-ahead)
   for (int pass = 0; pass <= cfg->max_loops; ++pass) {
@@ -1547,8 +1784,16 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
       rr_project(c, m);
       CK(cudaEventRecord(c->ev_proj, c->stream));
       CK(cudaStreamWaitEvent(c->eigs, c->ev_proj, 0));
-      reduced_gevp_start(c, m, c->eigs);
+      reduced_gevp_start(c, m, c->eigs, la);
       if (la) {
+        lookahead_input(c, m);
+        if (cfg->low_memory) {
+          const auto t0 = std::chrono::steady_clock::now();
+          c->factored = false;
+          factor(c);
+          out->factorize_s += secs(t0);
+        }
+        CK(cudaStreamWaitEvent(c->stream, c->ev_pre_eig, 0));
         CK(cudaEventRecord(pn[0], c->stream));
         contour_pass(c, m, c->BQ.p, c->X.p);
         CK(cudaEventRecord(pn[1], c->stream));
@@ -1621,9 +1866,11 @@ int guarded(feast_gpu_ctx* c, F&& f) {
     return FEAST_OK;
   } catch (const Failure& e) {
     if (c) c->err = e.what();
+    if (c && c->comm) c->comm->abort();
     return e.code;
   } catch (const std::exception& e) {
     if (c) c->err = e.what();
+    if (c && c->comm) c->comm->abort();
     return FEAST_EINTERNAL;
   }
 }
@@ -1665,6 +1912,7 @@ int feast_gpu_create(int device, void* stream, feast_gpu_ctx** out) {
     CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CK(cudaStreamCreateWithPriority(&c->eigs, cudaStreamNonBlocking, hi));
     CK(cudaEventCreateWithFlags(&c->ev_proj, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_pre_eig, cudaEventDisableTiming));
     CK(cudaEventCreate(&c->ev_eig));
     for (auto& pe : c->pev)
       for (auto& e : pe) CK(cudaEventCreate(&e));
@@ -1685,7 +1933,7 @@ void feast_gpu_destroy(feast_gpu_ctx* c) {
   cudaStreamSynchronize(c->stream);
   AllocStream as(c->stream);
   for (DevBuf<double>* d : {&c->A, &c->Bm, &c->Y, &c->Q, &c->X, &c->AQ, &c->BQ, &c->T, &c->gw, &c->Aq, &c->Bq,
-                            &c->Cm, &c->Lm, &c->Phi, &c->Ev, &c->Vm, &c->S, &c->Tm, &c->Dv, &c->Aband, &c->Bband, &c->csr})
+                            &c->Cm, &c->Lm, &c->Phi, &c->Ev, &c->Vm, &c->S, &c->Tm, &c->Dv, &c->Aband, &c->Bband, &c->csr, &c->G})
     d->release();
   c->csrstats.release();  // every buffer, before the stream goes (the destructor would free on a dead stream)
   c->kfac.release();
@@ -1700,12 +1948,13 @@ void feast_gpu_destroy(feast_gpu_ctx* c) {
   for (auto& pe : c->pev)
     for (auto& e : pe)
       if (e) cudaEventDestroy(e);
-  if (c->comm && nccl().commDestroy) nccl().commDestroy(c->comm);
+  c->comm.reset();
   if (c->eigs) {
     cudaStreamSynchronize(c->eigs);
     cudaStreamDestroy(c->eigs);
   }
   if (c->ev_proj) cudaEventDestroy(c->ev_proj);
+  if (c->ev_pre_eig) cudaEventDestroy(c->ev_pre_eig);
   if (c->ev_eig) cudaEventDestroy(c->ev_eig);
   if (c->hpin) cudaFreeHost(c->hpin);
   if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -1725,19 +1974,51 @@ int feast_gpu_nccl_unique_id(void* id_out) {
 int feast_gpu_set_comm(feast_gpu_ctx* c, const void* uid, int rank, int nranks) {
   return guarded(c, [&] {
     if (nranks < 1 || rank < 0 || rank >= nranks) fail(FEAST_EINPUT, "set_comm: bad rank/nranks");
+    c->comm.reset();
     c->rank = rank;
     c->nranks = nranks;
     c->have_contour = false;
     c->factored = false;
-    if (nranks > 1) {
+    c->mcap = 0;
+    // a communicator whenever an id is given: with nranks = 1 the NCCL path runs on one GPU
+    if (uid && (nranks > 1 || std::any_of((const char*)uid, (const char*)uid + 128, [](char x) { return x != 0; }))) {
       NcclApi& api = nccl();
-      auto init = (nccl_init_fn)dlsym(api.h, "ncclCommInitRank");
+      auto init = api.h ? (nccl_init_fn)dlsym(api.h, "ncclCommInitRank") : nullptr;
       if (!init) fail(FEAST_ENCCL, "NCCL not available");
       NcclUid id;
       std::memcpy(id.internal, uid, 128);
-      const int r = init(&c->comm, nranks, id, rank);
+      auto nc = std::make_unique<NcclComm>();
+      const int r = init(&nc->comm, nranks, id, rank);
       if (r != 0) fail(FEAST_ENCCL, "ncclCommInitRank failed");
+      c->comm = std::move(nc);
+    } else if (nranks > 1) {
+      fail(FEAST_EINPUT, "set_comm: an NCCL unique id is required for nranks > 1");
     }
+  });
+}
+
+int feast_gpu_group_create(int nranks, feast_gpu_group** out) {
+  if (!out || nranks < 1) return FEAST_EINPUT;
+  *out = new feast_gpu_group();
+  (*out)->nranks = nranks;
+  return FEAST_OK;
+}
+
+void feast_gpu_group_destroy(feast_gpu_group* g) {
+  if (!g) return;
+  if (g->stage) cudaFree(g->stage);
+  delete g;
+}
+
+int feast_gpu_set_group(feast_gpu_ctx* c, feast_gpu_group* g, int rank) {
+  return guarded(c, [&] {
+    if (!g || rank < 0 || rank >= g->nranks) fail(FEAST_EINPUT, "set_group: bad group/rank");
+    c->comm = std::make_unique<LocalComm>(g, rank);
+    c->rank = rank;
+    c->nranks = g->nranks;
+    c->have_contour = false;
+    c->factored = false;
+    c->mcap = 0;
   });
 }
 
@@ -1968,8 +2249,10 @@ int feast_gpu_bench_passes(feast_gpu_ctx* c, int passes, size_t flush_bytes, dou
       rr_project(c, m);
       CK(cudaEventRecord(c->ev_proj, c->stream));
       CK(cudaStreamWaitEvent(c->eigs, c->ev_proj, 0));
-      reduced_gevp_start(c, m, c->eigs);
+      reduced_gevp_start(c, m, c->eigs, la);
       if (la) {
+        lookahead_input(c, m);
+        CK(cudaStreamWaitEvent(c->stream, c->ev_pre_eig, 0));
         CK(cudaEventRecord(pn[0], c->stream));
         contour_pass(c, m, c->BQ.p, c->X.p, nullptr, pn[3]);
         CK(cudaEventRecord(pn[1], c->stream));
@@ -2001,6 +2284,10 @@ int feast_gpu_bench_passes(feast_gpu_ctx* c, int passes, size_t flush_bytes, dou
     if (phase_ms)
       for (int i = 0; i < 4; ++i) phase_ms[i] = ph[i];
   });
+}
+
+int feast_gpu_set_row_distribution(feast_gpu_ctx* c, int enable) {
+  return guarded(c, [&] { c->row_dist = enable != 0; });
 }
 
 int feast_gpu_set_lookahead(feast_gpu_ctx* c, int enable) {

@@ -443,14 +443,26 @@ static cudaError_t dgemm_batched(bool TA, int m, int n, int k, double alpha, con
 }
 
 cudaError_t bt_apply(int L, int b, const double* diag, const double* low, const double* x, int ldx,
-                     double* y, int ldy, int m, cudaStream_t st) {
-  // (b <= 32 goes through band_apply on band-row copies, band_apply.cu)
+                     double* y, int ldy, int m, cudaStream_t st, int l0, int l1) {
+  // (b <= 32 goes through band_apply on band-row copies, band_apply.cu); layers [l0, l1) of y:
+  // y_l = D_l x_l + C_{l-1} x_{l-1} + C_l^T x_{l+1}
+  if (l1 < 0) l1 = L;
+  if (l1 <= l0) return cudaSuccess;
   const int64_t bb = (int64_t)b * b;
-  cudaError_t e = dgemm_batched(false, b, m, b, 1.0, diag, b, bb, x, ldx, b, 0.0, y, ldy, b, L, st);
-  if (e != cudaSuccess || L == 1) return e;
-  e = dgemm_batched(false, b, m, b, 1.0, low, b, bb, x, ldx, b, 1.0, y + b, ldy, b, L - 1, st);
+  cudaError_t e = dgemm_batched(false, b, m, b, 1.0, diag + l0 * bb, b, bb, x + (int64_t)l0 * b, ldx, b, 0.0,
+                                y + (int64_t)l0 * b, ldy, b, l1 - l0, st);
   if (e != cudaSuccess) return e;
-  return dgemm_batched(true, b, m, b, 1.0, low, b, bb, x + b, ldx, b, 1.0, y, ldy, b, L - 1, st);
+  const int a0 = std::max(l0, 1);  // y_l += C_{l-1} x_{l-1}, l in [a0, l1)
+  if (l1 > a0) {
+    e = dgemm_batched(false, b, m, b, 1.0, low + (a0 - 1) * bb, b, bb, x + (int64_t)(a0 - 1) * b, ldx, b, 1.0,
+                      y + (int64_t)a0 * b, ldy, b, l1 - a0, st);
+    if (e != cudaSuccess) return e;
+  }
+  const int u1 = std::min(l1, L - 1);  // y_l += C_l^T x_{l+1}, l in [l0, u1)
+  if (u1 > l0)
+    e = dgemm_batched(true, b, m, b, 1.0, low + l0 * bb, b, bb, x + (int64_t)(l0 + 1) * b, ldx, b, 1.0,
+                      y + (int64_t)l0 * b, ldy, b, u1 - l0, st);
+  return e;
 }
 
 __global__ void symmetrize_kernel(double* c, int m, int ld) {

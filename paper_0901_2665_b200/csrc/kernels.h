@@ -67,9 +67,10 @@ cudaError_t bt_sweep(const BtSweepArgs& a, cudaStream_t st);
 cudaError_t reduce_terms(const double* t, int nodes, int64_t slice, int n, int m, int ld,
                          double* q, cudaStream_t st, int accumulate = 0);
 
-// block-tridiagonal real operator apply: Y = Op * X (layer-batched DMMA GEMMs)
+// block-tridiagonal real operator apply: Y = Op * X (layer-batched DMMA GEMMs), layers [l0, l1)
+// of Y (l1 < 0: all)
 cudaError_t bt_apply(int L, int b, const double* diag, const double* low, const double* x, int ldx,
-                     double* y, int ldy, int m, cudaStream_t st);
+                     double* y, int ldy, int m, cudaStream_t st, int l0 = 0, int l1 = -1);
 
 // ---------------- dense shifted solves (batched complex LU) -------------------
 struct DenseFactorArgs {
@@ -116,9 +117,10 @@ cudaError_t symmetrize(double* c, int m, int ld, cudaStream_t st);
 
 // band-row copy of a block-tridiagonal operator (b = 16, 32): row l b + i = [C_{l-1} | D_l | C_l^T](i, :)
 cudaError_t band_rows(int L, int b, const double* diag, const double* low, double* ab, cudaStream_t st);
-// y1 = A x, and y2 = B x in the same pass when ab2 != nullptr (band rows from band_rows)
+// y1 = A x, and y2 = B x in the same pass when ab2 != nullptr (band rows from band_rows), layers
+// [l0, l1) of y (l1 < 0: all)
 cudaError_t band_apply(int L, int b, const double* ab1, const double* ab2, const double* x, int ldx, double* y1,
-                       double* y2, int ldy, int m, cudaStream_t st);
+                       double* y2, int ldy, int m, cudaStream_t st, int l0 = 0, int l1 = -1);
 
 // ---------------- reduced generalized eigensolver ----------------------------
 struct EigWork;  // opaque, sized for mmax
@@ -128,7 +130,7 @@ void eig_destroy(EigWork* w);
 // into `evals` (device), vectors into `v` (device, m x m), stable order. vfloor > 0: the
 // tridiagonal route computes vectors only for evals > vfloor * max(evals) (others zero).
 cudaError_t sym_eig(EigWork* w, int m, double* a, double* evals, double* v, cudaStream_t st,
-                    double vfloor = 0.0);
+                    double vfloor = 0.0, bool low_smem = false);
 // Householder tridiagonalisation of a symmetric m x m matrix (3 <= m <= tri_tiles_max_dim())
 // on one SM with the matrix in registers: d[m], e[m-1], tau[m], reflectors in hv (m x m)
 int tri_tiles_max_dim();
@@ -145,12 +147,13 @@ cudaError_t chol_tiles(int m, double* a, double rel_tol, int* status, double* di
 // (status must be zero on entry). dinv receives the inverses of the 32x32 diagonal tiles of
 // L (ceil(m/32) * 1024 doubles), consumed by the triangular solves.
 cudaError_t cholesky(int m, double* a, double rel_tol, int* status, double* dinv, cudaStream_t st);
-// X <- L^{-1} X   (L lower m x m from cholesky(), X m x ncols)
+// X <- L^{-1} X   (L lower m x m from cholesky(), X m x ncols); low_smem: a route that leaves
+// room on each SM for a concurrent kernel (the look-ahead contour pass)
 cudaError_t trsm_lower(int m, const double* l, const double* dinv, double* x, int ldx, int ncols,
-                       cudaStream_t st);
+                       cudaStream_t st, bool low_smem = false);
 // X <- L^{-T} X
 cudaError_t trsm_lower_t(int m, const double* l, const double* dinv, double* x, int ldx, int ncols,
-                         cudaStream_t st);
+                         cudaStream_t st, bool low_smem = false);
 // transpose copy: dst(n x m) = src(m x n)^T
 cudaError_t transpose(const double* src, int m, int n, int lds, double* dst, int ldd,
                       cudaStream_t st);
@@ -198,6 +201,9 @@ cudaError_t hermitian_terms(const double2* w, int nodes, int64_t ld, int n, int 
 // look-ahead admission test: *out = max_i sum_j sqrt(bq(j,j)) |phi(j,i)|, i < mo, j < m
 cudaError_t cancellation_factor(int m, int mo, const double* bq, int ldb, const double* phi, int ldp,
                                 double* out, cudaStream_t st);
+
+// dst = sum of `slices` blocks of `count` doubles at src + r * stride, in slice order
+cudaError_t sum_slices(const double* src, int slices, int64_t stride, size_t count, double* dst, cudaStream_t st);
 
 // misc
 cudaError_t fill_zero(double* p, size_t count, cudaStream_t st);

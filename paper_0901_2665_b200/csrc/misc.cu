@@ -78,6 +78,25 @@ cudaError_t cancellation_factor(int m, int mo, const double* bq, int ldb, const 
   return cudaGetLastError();
 }
 
+// dst[i] = sum_{r < slices} src[r * stride + i], summed in slice order (the loopback group's
+// allreduce: every rank adds the same slots in the same order, so all get the same bits)
+__global__ void sum_slices_kernel(const double* __restrict__ src, int slices, int64_t stride, size_t count,
+                                  double* __restrict__ dst) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    double acc = src[i];
+    for (int r = 1; r < slices; ++r) acc += src[r * stride + i];
+    dst[i] = acc;
+  }
+}
+
+cudaError_t sum_slices(const double* src, int slices, int64_t stride, size_t count, double* dst, cudaStream_t st) {
+  if (!count) return cudaSuccess;
+  sum_slices_kernel<<<(unsigned)std::min<size_t>((count + 255) / 256, 4096), 256, 0, st>>>(src, slices, stride,
+                                                                                         count, dst);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 __global__ void fill_zero_kernel(double* p, size_t count) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
        i += (size_t)gridDim.x * blockDim.x)

@@ -987,7 +987,7 @@ int tri_max_dim() { return 1024; }
 
 // a (m x m, overwritten is allowed), eigenvalues ascending -> evals, vectors -> v (m x m)
 cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws, int* iws, cudaStream_t st,
-                    double vfloor) {
+                    double vfloor, bool low_smem) {
   if (m < 1 || m > tri_max_dim()) return cudaErrorInvalidValue;
   double* d = ws;
   double* e = d + m;
@@ -1073,10 +1073,11 @@ cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws
   if (vsm > 48 * 1024) cudaFuncSetAttribute(tri_eigvecs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsm);
   tri_eigvecs_kernel<<<m, 32, vsm, st>>>(p);
   ++g_launches;
-  // back-transformation: all reflectors in shared memory for m <= 192; blocked (WY) above
-  // m = 384 (tri_back.cu; its T factors live in the cooperative route's scratch gw, free by now);
-  // in between one warp per column (m = 192: 83 us against 40 + 56 us for the WY pair)
-  if (m >= 3 && m <= 8 * TBS_NQ) {
+  // back-transformation: all reflectors in shared memory for m <= 192 (147 KB per CTA: a whole
+  // SM, so not beside a concurrent kernel, low_smem); blocked (WY) above m = 384 (tri_back.cu; its
+  // T factors live in the cooperative route's scratch gw, free by now); otherwise one warp per
+  // column with the reflectors from L2 (m = 192: 83 us against 71 us from shared memory)
+  if (m >= 3 && m <= 8 * TBS_NQ && !low_smem) {
     const size_t sm = sizeof(double) * ((size_t)m * (m - 1) / 2 + m);
     static bool battr = false;
     if (!battr) {

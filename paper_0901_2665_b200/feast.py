@@ -99,6 +99,10 @@ def load_library(path: str = LIB_PATH):
     L.feast_gpu_set_node_batch.argtypes = [C.c_void_p, C.c_int]
     L.feast_gpu_set_twist.argtypes = [C.c_void_p, C.c_int]
     L.feast_gpu_set_lookahead.argtypes = [C.c_void_p, C.c_int]
+    L.feast_gpu_set_row_distribution.argtypes = [C.c_void_p, C.c_int]
+    L.feast_gpu_group_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+    L.feast_gpu_group_destroy.argtypes = [C.c_void_p]
+    L.feast_gpu_set_group.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
     L.feast_gpu_lookahead_count.argtypes = [C.c_void_p]
     L.feast_gpu_solve_shift.argtypes = [C.c_void_p, C.c_int, _dp, C.c_int, C.c_int]
     L.feast_gpu_contour_pass.argtypes = [C.c_void_p, _dp, C.c_int, _dp]
@@ -124,7 +128,8 @@ EXPORTED_SYMBOLS = [
     "feast_gpu_bench_init", "feast_gpu_bench_passes", "feast_gpu_launch_count",
     "feast_gpu_set_node_batch", "feast_gpu_storage", "feast_gpu_random_block",
     "feast_gpu_contour_pass_hermitian", "feast_gpu_set_twist", "feast_gpu_set_lookahead",
-    "feast_gpu_lookahead_count",
+    "feast_gpu_lookahead_count", "feast_gpu_set_row_distribution", "feast_gpu_group_create",
+    "feast_gpu_group_destroy", "feast_gpu_set_group",
 ]
 
 
@@ -246,6 +251,15 @@ class GpuContext:
     def set_node_batch(self, nodes: int):
         """Factor memory plan: 0 = automatic (resident if they fit), k > 0 = stream k nodes."""
         self._check(self.L.feast_gpu_set_node_batch(self.h, int(nodes)))
+
+    def set_group(self, group: "LocalGroup", rank: int):
+        """Join a loopback rank group (contexts of this process, one host thread each)."""
+        self._check(self.L.feast_gpu_set_group(self.h, group.h, rank))
+        self._group = group
+
+    def set_row_distribution(self, enable: bool):
+        """Row-distributed Rayleigh-Ritz across the ranks (default on)."""
+        self._check(self.L.feast_gpu_set_row_distribution(self.h, int(bool(enable))))
 
     def set_lookahead(self, enable: bool):
         """Look-ahead contour pass overlapping each reduced eigensolve (default on)."""
@@ -393,6 +407,29 @@ class GpuContext:
 
     def launch_count(self) -> int:
         return int(self.L.feast_gpu_launch_count(self.h))
+
+
+class LocalGroup:
+    """feast_gpu_group: a loopback rank group of contexts inside one process (the collectives of
+    the NCCL group through device copies and host barriers; include/feast_gpu.h)."""
+
+    def __init__(self, nranks: int):
+        self.L = load_library()
+        h = C.c_void_p()
+        if self.L.feast_gpu_group_create(int(nranks), C.byref(h)) != 0:
+            raise InputError("feast_gpu_group_create failed")
+        self.h, self.nranks = h, nranks
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.feast_gpu_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def shard_nodes(n_e: int, rank: int, nranks: int):
