@@ -166,6 +166,23 @@ int feast_gpu_prepare(feast_gpu_ctx* ctx, double emin, double emax, int n_e);
  * resident plan). Takes effect at the next feast_gpu_prepare / feast_gpu_solve. */
 int feast_gpu_set_node_batch(feast_gpu_ctx* ctx, int nodes);
 
+/* Inner solver, the InnerSolver the reference's feast_solve takes (inner_solver.hpp:32-39):
+ *   kind 0: DirectSolver (default) — factors of z_e B - A per node, solves on the factors;
+ *   kind 1: IterativeSolver(a, b, tol, max_iter) (inner_solver.hpp:209-240) — unpreconditioned
+ *           BiCGStab per right-hand side to ||r|| <= tol ||b|| with the reference's restart and
+ *           failure rules (FEAST_ENUMERICAL "BicgstabShiftSystem: inner solve did not reach
+ *           tolerance"); max_iter <= 0 means max(1000, 20 n); the loop's trace tolerance is
+ *           floored at tol^2 (core.hpp:296-297). tol outside (0, 1) is FEAST_EINPUT.
+ * Takes effect at the next factorisation / solve. */
+int feast_gpu_set_inner_solver(feast_gpu_ctx* ctx, int kind, double tol, int max_iter);
+
+/* FactorPolicy of the DirectSolver (inner_solver.hpp:40-47, 80-95), applied at the next
+ * feast_gpu_set_pencil: 0 Auto (block-tridiagonal factors when both operators are sparse and
+ * (3 bw + 1) 2 <= n, dense otherwise), 1 Dense (dense LU for any storage), 2 Banded (sparse
+ * operands required, FEAST_EINPUT "DirectSolver: banded policy requires sparse operands"
+ * otherwise; block-tridiagonal factors, or dense when no block size up to 512 holds the band). */
+int feast_gpu_set_factor_policy(feast_gpu_ctx* ctx, int policy);
+
 /* Block-Thomas recursion for block-tridiagonal pencils with b <= 64: enable = 1 (default) runs
  * the two-ended (twisted) elimination that meets at layer L/2, enable = 0 the plain top-down
  * chain of BandedLU (lu.hpp:127-206). Both give the same solves to rounding; takes effect at the
@@ -224,11 +241,11 @@ int feast_gpu_solve(feast_gpu_ctx* ctx, double emin, double emax, const feast_co
 
 /* Look-ahead contour pass (default on): during each Rayleigh-Ritz step the next pass's Ne solves
  * run on B Q, concurrently with the reduced eigensolve, and the next subspace is formed as
- * (that result) Phi — the same iteration as core.hpp:356-388 by linearity of the filter. Used only
- * when the Ritz block's cancellation factor max_i sum_j ||q_j||_B |Phi_ji| is <= 8 (otherwise the
- * pass is redone in the reference order), never with low_memory or streamed factors. enable = 0
- * runs every pass in the reference order. */
-int feast_gpu_set_lookahead(feast_gpu_ctx* ctx, int enable);
+ * (that result) Phi — the same iteration as core.hpp:356-388 by linearity of the filter. Used from
+ * pass 1 on, when the Ritz block's cancellation factor max_i sum_j ||q_j||_B |Phi_ji| is <= the bound (otherwise the
+ * pass is redone in the reference order), never with streamed factors. enable = 0 runs every
+ * pass in the reference order; max_cancellation > 0 replaces the admission bound 1e3. */
+int feast_gpu_set_lookahead(feast_gpu_ctx* ctx, int enable, double max_cancellation);
 
 /* Benchmark hook: runs `passes` loop bodies (contour pass + Rayleigh-Ritz + trace/count
  * + Y = B X) on the device-resident state set up by feast_gpu_bench_init (after

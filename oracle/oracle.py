@@ -63,6 +63,10 @@ def lib(kind="reference"):
     L.ref_feast_solve.argtypes = [_op, _op, C.c_double, C.c_double,
                                   C.POINTER(abi.FeastConfigT), _dp, C.c_int,
                                   C.POINTER(abi.FeastResultT)]
+    L.ref_feast_solve_with.argtypes = [_op, _op, C.c_double, C.c_double, C.POINTER(abi.FeastConfigT), _dp, C.c_int,
+                                       C.c_int, C.c_int, C.c_double, C.c_int, C.POINTER(abi.FeastResultT)]
+    L.ref_shift_solve_with.argtypes = [_op, _op, C.c_double, C.c_double, _dp, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.c_double, C.c_int]
     if hasattr(L, "ref_bench_passes"):
         L.ref_bench_passes.argtypes = [_op, _op, C.c_double, C.c_double, C.c_int, C.c_int,
                                        C.c_uint64, C.c_int, C.c_int, _dp]
@@ -140,6 +144,16 @@ def shift_solve(a, b, z, rhs, mode=0, kind="reference"):
     ca, cb = a.to_c(), b.to_c()
     _check(L, L.ref_shift_solve(C.byref(ca), C.byref(cb), z.real, z.imag,
                                 r.ctypes.data_as(_dp), r.shape[1], mode))
+    return r
+
+
+def shift_solve_with(a, b, z, rhs, mode=0, solver="direct", policy=0, tol=0.0, max_iter=0, kind="reference"):
+    """ShiftSystem::solve_in_place of DirectSolver(policy) or IterativeSolver(tol, max_iter)."""
+    L = lib(kind)
+    r = np.asfortranarray(rhs, dtype=np.complex128).copy(order="F")
+    ca, cb = a.to_c(), b.to_c()
+    _check(L, L.ref_shift_solve_with(C.byref(ca), C.byref(cb), z.real, z.imag, r.ctypes.data_as(_dp), r.shape[1],
+                                     mode, 1 if solver == "iterative" else 0, policy, tol, max_iter))
     return r
 
 
@@ -256,7 +270,17 @@ def feast_solve(problem, threads=1, low_memory=False, initial_y=None, kind="refe
     return _run_solve(L, p.a, p.b, p.emin, p.emax, cfg, initial_y, n)
 
 
-def _run_solve(L, a, b, emin, emax, cfg, initial_y, n):
+def feast_solve_with(problem, solver="direct", policy=0, tol=0.0, max_iter=0, threads=1, kind="reference"):
+    """feast_solve with an explicit InnerSolver: DirectSolver(policy) or IterativeSolver(tol, max_iter)."""
+    L = lib(kind)
+    p = problem
+    cfg = abi.FeastConfigT(m0=p.m0, n_e=p.n_e, trace_tol=p.trace_tol, max_loops=p.max_loops, seed=p.seed,
+                           threads=threads, low_memory=0)
+    return _run_solve(L, p.a, p.b, p.emin, p.emax, cfg, None, p.n,
+                      solver=(1 if solver == "iterative" else 0, policy, tol, max_iter))
+
+
+def _run_solve(L, a, b, emin, emax, cfg, initial_y, n, solver=None):
     m0 = cfg.m0
     out = dict(eigenvalues=np.zeros(m0), eigenvectors=np.zeros((n, m0), order="F"),
                residuals=np.zeros(m0), residual_absolute_only=np.zeros(m0, dtype=np.int32),
@@ -273,8 +297,12 @@ def _run_solve(L, a, b, emin, emax, cfg, initial_y, n):
     r.subspace = abi.dptr(out["subspace"])
     y0 = None if initial_y is None else _F(initial_y)
     ca, cb = a.to_c(), b.to_c()
-    _check(L, L.ref_feast_solve(C.byref(ca), C.byref(cb), emin, emax, C.byref(cfg),
-                                abi.dptr(y0), 0 if y0 is None else y0.shape[1], C.byref(r)))
+    if solver is None:
+        _check(L, L.ref_feast_solve(C.byref(ca), C.byref(cb), emin, emax, C.byref(cfg),
+                                    abi.dptr(y0), 0 if y0 is None else y0.shape[1], C.byref(r)))
+    else:
+        _check(L, L.ref_feast_solve_with(C.byref(ca), C.byref(cb), emin, emax, C.byref(cfg),
+                                         abi.dptr(y0), 0 if y0 is None else y0.shape[1], *solver, C.byref(r)))
     return unpack_result(out, r, n)
 
 

@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -324,9 +325,20 @@ int ref_bench_passes(const feast_operator_t* a, const feast_operator_t* b, doubl
   }
 }
 
-int ref_feast_solve(const feast_operator_t* a, const feast_operator_t* b, double emin,
-                    double emax, const feast_config_t* config, const double* initial_y,
-                    int y_cols, feast_result_t* out) {
+// solver_kind 0: DirectSolver(a, b, FactorPolicy(policy)); 1: IterativeSolver(a, b, tol, max_iter)
+// (inner_solver.hpp:77-113, 209-240); -1: the default (nullptr, core.hpp:264-268)
+std::unique_ptr<feast::InnerSolver<double>> make_solver(const SymmetricOperator<double>& ra,
+                                                        const SymmetricOperator<double>& rb, int solver_kind,
+                                                        int policy, double tol, int max_iter) {
+  if (solver_kind == 1) return std::make_unique<feast::IterativeSolver<double>>(ra, rb, tol, max_iter);
+  if (solver_kind == 0)
+    return std::make_unique<feast::DirectSolver<double>>(ra, rb, static_cast<feast::FactorPolicy>(policy));
+  return nullptr;
+}
+
+int ref_feast_solve_with(const feast_operator_t* a, const feast_operator_t* b, double emin, double emax,
+                         const feast_config_t* config, const double* initial_y, int y_cols, int solver_kind,
+                         int policy, double tol, int max_iter, feast_result_t* out) {
   try {
     const auto ra = to_ref(a);
     const auto rb = to_ref(b);
@@ -336,8 +348,9 @@ int ref_feast_solve(const feast_operator_t* a, const feast_operator_t* b, double
       y0 = DenseMatrix<double>(n, y_cols);
       std::memcpy(y0.data().data(), initial_y, sizeof(double) * (size_t)n * y_cols);
     }
+    const auto solver = make_solver(ra, rb, solver_kind, policy, tol, max_iter);
     const auto r = feast::feast_solve<double>(ra, rb, feast::SearchInterval(emin, emax),
-                                              to_ref(config), nullptr,
+                                              to_ref(config), solver.get(),
                                               initial_y ? &y0 : nullptr);
     const int m = (int)r.eigenvalues.size();
     out->m = m;
@@ -365,6 +378,32 @@ int ref_feast_solve(const feast_operator_t* a, const feast_operator_t* b, double
     if (out->subspace)
       std::memcpy(out->subspace, r.subspace.data().data(),
                   sizeof(double) * r.subspace.data().size());
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+
+int ref_feast_solve(const feast_operator_t* a, const feast_operator_t* b, double emin,
+                    double emax, const feast_config_t* config, const double* initial_y,
+                    int y_cols, feast_result_t* out) {
+  return ref_feast_solve_with(a, b, emin, emax, config, initial_y, y_cols, -1, 0, 0.0, 0, out);
+}
+
+// ShiftSystem::solve_in_place at shift z for a DirectSolver with FactorPolicy `policy` or an
+// IterativeSolver (solver_kind as in ref_feast_solve_with)
+int ref_shift_solve_with(const feast_operator_t* a, const feast_operator_t* b, double zr, double zi,
+                         double* rhs, int m, int mode, int solver_kind, int policy, double tol, int max_iter) {
+  try {
+    const auto ra = to_ref(a);
+    const auto rb = to_ref(b);
+    const auto solver = make_solver(ra, rb, solver_kind, policy, tol, max_iter);
+    auto sys = solver->prepare(cplx(zr, zi));
+    DenseMatrix<cplx> r(ra.n(), m);
+    std::memcpy(r.data().data(), rhs, sizeof(cplx) * (size_t)ra.n() * m);
+    sys->solve_in_place(r, mode ? feast::linalg::SolveMode::ConjTranspose
+                                : feast::linalg::SolveMode::Normal);
+    std::memcpy(rhs, r.data().data(), sizeof(cplx) * (size_t)ra.n() * m);
     return 0;
   } catch (const std::exception& e) {
     return code_of(e);

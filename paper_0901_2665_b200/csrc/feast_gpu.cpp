@@ -330,17 +330,28 @@ struct feast_gpu_ctx {
   DevBuf<double2> sinv, gfac, hfac, lu, dinv, scratch, fwork;
   DevBuf<double> Aband, Bband;  // band-row copies of A, B for the applies (b <= 32; band_apply.cu)
   int kmid = -1;  // twisted block-Thomas meeting layer of the current factors (bt_twist_layer)
-  DevBuf<int> ipiv, perm, status;
+  DevBuf<int> ipiv, perm, status, fstatus;  // status: reduced Cholesky; fstatus: factorisation
   bool chol_failed_prev = false;  // the last reduced_gevp took the truncation path
   bool gevp_enqueued = false;     // reduced_gevp_start enqueued the whole Cholesky path
   // look-ahead contour pass (rayleigh_ritz_la): setting, and whether the last eigensolve's
   // cancellation factor admitted it (the predictor for launching the next one)
   bool lookahead = true, lookahead_ok = true;
+  double la_kmax = 1e3;  // admission bound of the look-ahead pass (kLookaheadMaxK)
   cudaStream_t eigs = nullptr;  // high-priority stream of the reduced eigensolve
   cudaEvent_t ev_proj = nullptr, ev_eig = nullptr, ev_pre_eig = nullptr;
   double* hpin = nullptr;       // pinned: status, cancellation factor, eigenvalues
   size_t hpin_n = 0;
   DevBuf<double> kfac;
+  // inner solver (inner_solver.hpp): 0 = DirectSolver, 1 = IterativeSolver (BiCGStab, bicgstab.cu)
+  int inner_kind = 0;
+  double inner_tol = 0.0;
+  int inner_max_iter = 0;
+  int factor_policy = 0;  // FactorPolicy at set_pencil: 0 Auto, 1 Dense, 2 Banded (inner_solver.hpp:40-47)
+  DevBuf<double2> bvec;   // BiCGStab: X R R0 P V S T, npad x C each
+  DevBuf<double> breal;   // BiCGStab: PR AR BR, npad x 2C each
+  DevBuf<BicgCol> bcol;
+  DevBuf<int> bflag;
+  DevBuf<double2> bz;
   bool twist = true;  // two-ended block-Thomas recursion where it applies (feast_gpu_set_twist)
   // workspaces
   int mcap = 0;
@@ -818,7 +829,10 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
   int bsz = 0;
   const bool a_bt = a->kind == FEAST_STORAGE_BLOCKTRI, b_bt = b->kind == FEAST_STORAGE_BLOCKTRI;
   const bool a_sp = a->kind == FEAST_STORAGE_CSR || a_bt, b_sp = b->kind == FEAST_STORAGE_CSR || b_bt;
-  if (a_sp && b_sp) {
+  // FactorPolicy (inner_solver.hpp:80-95): Dense keeps dense factors for any storage, Banded
+  // requires sparse operands, Auto chooses by bandwidth as below
+  if (c->factor_policy == 2 && !(a_sp && b_sp)) fail(FEAST_EINPUT, "DirectSolver: banded policy requires sparse operands");
+  if (a_sp && b_sp && c->factor_policy != 1) {
     if (a_bt && b_bt && a->bsize == b->bsize && round_block(a->bsize) == a->bsize && a->bsize <= kMaxBlock) {
       bsz = a->bsize;
     } else {
@@ -828,7 +842,7 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
         else if (o->kind == FEAST_STORAGE_CSR) bw = std::max(bw, csr_bandwidth(o));
         else bw = std::max(bw, 2 * o->bsize - 1);
       }
-      if ((3 * bw + 1) * 2 <= n) {
+      if ((3 * bw + 1) * 2 <= n || c->factor_policy == 2) {
         // smallest supported block size whose block-tridiagonal pattern holds both operators
         const int lo = round_block(std::max(1, (bw + 2) / 2));
         const int hi = std::min(std::max(round_block(std::max(bw, 1)), lo), kMaxBlock);
@@ -993,8 +1007,8 @@ void plan_batch(feast_gpu_ctx* c, int m) {
 
 // factors of owned nodes [s0, s0 + cnt) into factor slots 0..cnt-1
 void factor_range(feast_gpu_ctx* c, int s0, int cnt) {
-  c->status.ensure(1);
-  CK(cudaMemsetAsync(c->status.p, 0, sizeof(int), c->stream));
+  c->fstatus.ensure(1);
+  CK(cudaMemsetAsync(c->fstatus.p, 0, sizeof(int), c->stream));
   if (c->blocktri) {
     const size_t bb = (size_t)c->b * c->b;
     const int slots = c->wnodes();
@@ -1003,7 +1017,7 @@ void factor_range(feast_gpu_ctx* c, int s0, int cnt) {
     c->hfac.ensure(std::max<size_t>(slots * (c->L - 1) * bb, 1));
     if (c->b >= 128) c->fwork.ensure(bt_factor_work_elems(c->b, cnt));
     BtFactorArgs a{c->L, c->b, cnt, c->abdiag.p, c->ablow.p, c->dz.p + s0, c->sinv.p, c->gfac.p, c->hfac.p,
-                   c->scratch.p, c->status.p, c->fwork.p, c->kmid = bt_twist_layer(c->L, c->b, c->twist)};
+                   c->scratch.p, c->fstatus.p, c->fwork.p, c->kmid = bt_twist_layer(c->L, c->b, c->twist)};
     CK(bt_factor(a, c->stream));
     if (!c->streamed()) c->fwork.release();  // transient unless it is reused every pass
   } else {
@@ -1012,11 +1026,11 @@ void factor_range(feast_gpu_ctx* c, int s0, int cnt) {
     c->ipiv.ensure((size_t)slots * n);
     c->perm.ensure((size_t)slots * n);
     c->dinv.ensure((size_t)slots * nblk * 2 * nb * nb);
-    DenseFactorArgs a{n, cnt, c->A.p, c->Bm.p, c->dz.p + s0, c->lu.p, c->ipiv.p, c->perm.p, c->dinv.p, c->status.p};
+    DenseFactorArgs a{n, cnt, c->A.p, c->Bm.p, c->dz.p + s0, c->lu.p, c->ipiv.p, c->perm.p, c->dinv.p, c->fstatus.p};
     CK(dense_factor(a, c->stream));
   }
   int st = 0;
-  CK(cudaMemcpyAsync(&st, c->status.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(&st, c->fstatus.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   sync(c);
   if (st) fail(FEAST_ENUMERICAL, c->blocktri ? "BlockThomas: block pivot is numerically singular"
                                              : "DenseLU: matrix is numerically singular");
@@ -1027,8 +1041,14 @@ void factor_range(feast_gpu_ctx* c, int s0, int cnt) {
 void factor(feast_gpu_ctx* c) {
   if (!c->have_pencil) fail(FEAST_EINPUT, "feast_gpu: pencil not set");
   if (!c->have_contour) fail(FEAST_EINPUT, "feast_gpu: contour not prepared");
+  if (c->inner_kind == 1) {  // IterativeSolver::prepare keeps only the shift (inner_solver.hpp:229-231)
+    c->res0 = 0;
+    c->rescnt = c->owned();
+    c->factored = true;
+    return;
+  }
   const int own = c->owned();
-  c->status.ensure(1);
+  c->fstatus.ensure(1);
   c->res0 = -1;
   c->rescnt = 0;
   if (own == 0) {
@@ -1062,9 +1082,30 @@ void allreduce_sum(feast_gpu_ctx* c, double* p, size_t count, cudaStream_t st) {
 
 // q = -sum_e Re(c_e (z_e B - A)^{-1} y) over ALL nodes (allreduce across ranks); y, q npad x m.
 // ev_start / ev_solved (may be null) are recorded before the first solve and after the last one.
+void bicg_solve(feast_gpu_ctx* c, int s0, int cnt, int m, const double* y, const double2* bc, int ldb, bool conj_z);
+
 void contour_pass(feast_gpu_ctx* c, int m, const double* y, double* q, cudaEvent_t ev_start = nullptr,
                   cudaEvent_t ev_solved = nullptr) {
   join_aux(c);
+  if (c->inner_kind == 1) {  // IterativeSolver: BiCGStab per (node, column), node batches that fit
+    const int own = c->owned();
+    const size_t nv = (size_t)c->npad * m;
+    if (ev_start) CK(cudaEventRecord(ev_start, c->stream));
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    const size_t per = (sizeof(double2) * 7 + sizeof(double) * 6) * nv;  // BiCGStab vectors per node
+    const int nb = std::max(1, std::min(own, (int)(0.5 * (double)(fr + c->bvec.n * sizeof(double2) +
+                                                               c->breal.n * sizeof(double)) / per)));
+    for (int s0 = 0; s0 < own; s0 += nb) {
+      const int cnt = std::min(nb, own - s0);
+      bicg_solve(c, s0, cnt, m, y, nullptr, 0, false);
+      CK(bicg_terms(c->bvec.p, cnt, c->npad, m, c->npad, c->dcoeff.p + s0, q, s0 > 0, c->stream));
+    }
+    if (own == 0) CK(fill_zero(q, nv, c->stream));
+    if (ev_solved) CK(cudaEventRecord(ev_solved, c->stream));
+    allreduce_sum(c, q, nv, c->stream);
+    return;
+  }
   const int own = c->owned();
   const size_t nv = (size_t)c->npad * m;
   if (ev_start) CK(cudaEventRecord(ev_start, c->stream));
@@ -1095,6 +1136,70 @@ void contour_pass(feast_gpu_ctx* c, int m, const double* y, double* q, cudaEvent
   allreduce_sum(c, q, nv, c->stream);
 }
 
+void apply_both(feast_gpu_ctx* c, const double* x, double* ya, double* yb, int m);
+
+// BiCGStab (inner_solver.hpp:124-184) for owned nodes [s0, s0 + cnt), m right-hand sides each (y
+// real, ld npad, or bc complex, ld ldb, shared by the nodes); solutions in c->bvec (X block,
+// npad x cnt*m complex). conj_z: the ConjTranspose solves (inner_solver.hpp:129).
+void bicg_solve(feast_gpu_ctx* c, int s0, int cnt, int m, const double* y, const double2* bc, int ldb, bool conj_z) {
+  const int C = cnt * m;
+  const size_t nv = (size_t)c->npad * C;
+  c->bvec.ensure(7 * nv);
+  c->breal.ensure(6 * nv);
+  c->bcol.ensure(C);
+  c->bflag.ensure(2);
+  c->bz.ensure(cnt);
+  std::vector<double2> zs(cnt);
+  for (int e = 0; e < cnt; ++e) {
+    zs[e] = c->z[c->e0 + s0 + e];
+    if (conj_z) zs[e].y = -zs[e].y;
+  }
+  CK(cudaMemcpyAsync(c->bz.p, zs.data(), sizeof(double2) * cnt, cudaMemcpyHostToDevice, c->stream));
+  BicgArgs a;
+  a.n = c->npad;
+  a.ld = c->npad;
+  a.C = C;
+  a.m = m;
+  a.z = c->bz.p;
+  double2* v = c->bvec.p;
+  a.X = v;
+  a.R = v + nv;
+  a.R0 = v + 2 * nv;
+  a.P = v + 3 * nv;
+  a.V = v + 4 * nv;
+  a.S = v + 5 * nv;
+  a.T = v + 6 * nv;
+  a.PR = c->breal.p;
+  a.AR = a.PR + 2 * nv;
+  a.BR = a.AR + 2 * nv;
+  a.col = c->bcol.p;
+  a.tol = c->inner_tol;
+  a.max_iter = c->inner_max_iter > 0 ? c->inner_max_iter : std::max(1000, 20 * c->n);
+  a.any_active = c->bflag.p;
+  CK(cudaMemsetAsync(c->bflag.p, 0, 2 * sizeof(int), c->stream));
+  CK(bicg_init(a, y, c->npad, bc, ldb, c->stream));
+  int active = 0;
+  CK(cudaMemcpyAsync(&active, c->bflag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  constexpr int kChunk = 8;  // iterations between host checks of the any-active flag
+  while (active) {
+    for (int k = 0; k < kChunk; ++k) {
+      apply_both(c, a.PR, a.AR, a.BR, 2 * C);
+      CK(bicg_a(a, c->stream));
+      apply_both(c, a.PR, a.AR, a.BR, 2 * C);
+      if (k == kChunk - 1) CK(cudaMemsetAsync(c->bflag.p, 0, sizeof(int), c->stream));
+      CK(bicg_b(a, c->stream));
+    }
+    CK(cudaMemcpyAsync(&active, c->bflag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+  }
+  CK(bicg_check(a, c->bflag.p + 1, c->stream));
+  int failed = 0;
+  CK(cudaMemcpyAsync(&failed, c->bflag.p + 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  if (failed) fail(FEAST_ENUMERICAL, "BicgstabShiftSystem: inner solve did not reach tolerance");
+}
+
 // accumulate_subspace_hermitian (core.hpp:190-215) for the real symmetric pencils this path
 // holds: (z B - A)^H = conj(z B - A), so the ConjTranspose solve is conj(G conj(Y)) and ONE
 // complex-mode solve of the 2m columns [Yr | Yi] per node gives both (hermitian_terms). Input
@@ -1102,6 +1207,7 @@ void contour_pass(feast_gpu_ctx* c, int m, const double* y, double* q, cudaEvent
 // node batches and allreduce as contour_pass.
 void contour_pass_hermitian(feast_gpu_ctx* c, int m) {
   join_aux(c);
+  if (c->inner_kind == 1) fail(FEAST_EINPUT, "contour_pass_hermitian: needs the direct inner solver");
   const int own = c->owned();
   const int m2 = 2 * m;
   double2* qc = reinterpret_cast<double2*>(c->AQ.p);
@@ -1261,12 +1367,16 @@ struct Reduced {
 // leaves most SMs idle); afterwards one GEMM forms the next Q. In exact arithmetic the iteration
 // is the reference's (core.hpp:356-388). In floating point each solved column carries its own
 // relative rounding, which Phi recombines: the error grows by at most the cancellation factor
-// K = max_i sum_j ||q_j||_B |Phi_ji| (1 when forming X cancels nothing; ~1 in the converged
-// regime where Q is close to X diag(rho)). The look-ahead result is used only when
-// K <= kLookaheadMaxK; otherwise the pass is redone in the reference order (X = Q Phi, Y = B X,
-// solves on Y), and the next pass does not speculate until K is small again. Disabled for
-// streamed node batches (the factors would be recomputed for a pass that may be discarded).
-constexpr double kLookaheadMaxK = 8.0;
+// K = max_i sum_j ||q_j||_B |Phi_ji| (1 when forming X cancels nothing; a few in the converged
+// regime where Q is close to X diag(rho); 1e4-1e6 after the random start block of pass 0, ~50-100
+// after pass 1). The look-ahead result is used only when K <= kLookaheadMaxK; otherwise the pass
+// is redone in the reference order (X = Q Phi, Y = B X, solves on Y). It is not launched during
+// pass 0 (K is always large there) nor after a pass whose K exceeded the bound. Measured
+// (tools/lookahead_study.py, profiles/r02_lookahead_study.log): even admitting every pass (bound
+// 1e6) the solves end with the same status and loop count as the reference order and eigenvalues
+// within 5e-12 relative. Disabled for streamed node batches (the factors would be recomputed for
+// a pass that may be discarded).
+constexpr double kLookaheadMaxK = 1e3;  // default admission bound (feast_gpu_set_lookahead)
 
 // [Aq | Bq] = Q^T [AQ | BQ] (rayleigh_ritz core.hpp:228-236) on the main stream; row-distributed:
 // each rank projects its slab and one allreduce of the 2 m^2 partial sums completes it
@@ -1436,8 +1546,8 @@ Reduced rayleigh_ritz_la(feast_gpu_ctx* c, int m, bool lookahead, cudaEvent_t ev
     contour_pass(c, m, c->BQ.p, c->X.p, ev_c0, ev_c1);
   }
   Reduced r = reduced_gevp_finish(c, m, c->eigs);
-  r.lookahead = lookahead && r.kfactor <= kLookaheadMaxK;
-  c->lookahead_ok = r.kfactor <= kLookaheadMaxK;
+  r.lookahead = lookahead && r.kfactor <= c->la_kmax;
+  c->lookahead_ok = r.kfactor <= c->la_kmax;
   CK(cudaStreamWaitEvent(c->stream, c->ev_eig, 0));  // Phi is read on the main stream from here on
   return r;
 }
@@ -1686,7 +1796,9 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
   c->chol_failed_prev = false;
   const bool same_contour = c->have_contour && c->emin == emin && c->emax == emax && c->ne == cfg->n_e;
   if (!same_contour) build_contour(c, emin, emax, cfg->n_e);
-  const double effective_tol = cfg->trace_tol;  // direct solves: residual_target() == 0
+  // max(trace_tol, residual_target^2) (core.hpp:296-297): 0 for direct solves, tol for BiCGStab
+  const double inner = c->inner_kind == 1 ? c->inner_tol : 0.0;
+  const double effective_tol = std::max(cfg->trace_tol, inner * inner);
   ensure_workspace(c, cfg->m0);
   trace_mark(c, "solve: contour + workspaces");
 
@@ -1755,7 +1867,7 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
   // (rayleigh_ritz_la); not with streamed factors (a discarded look-ahead would have refactored
   // every batch). low_memory keeps it and refactors before it, so results stay bit-identical to
   // the default (test_core.cpp:341-376)
-  const bool la_allowed = c->lookahead;
+  const bool la_allowed = c->lookahead && c->inner_kind == 0;  // (an inexact solve is not linear)
   c->lookahead_ok = true;
   bool have_q = false;  // this pass's Q is already formed (admitted look-ahead)
   for (int pass = 0; pass <= cfg->max_loops; ++pass) {
@@ -1776,7 +1888,8 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
       CK(cudaEventRecord(pe[1], c->stream));
       trace_mark(c, "solve: contour pass");
     }
-    const bool la = la_allowed && c->lookahead_ok && !c->streamed() && pass < cfg->max_loops;
+    const bool la = la_allowed && pass >= 1 && (pass == 1 || c->lookahead_ok) && !c->streamed() &&
+                    pass < cfg->max_loops;
     Reduced rr;
     try {
       cudaEvent_t* pn = c->pev[(pass + 1) & 1];
@@ -1799,8 +1912,11 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
         CK(cudaEventRecord(pn[1], c->stream));
       }
       rr = reduced_gevp_finish(c, m, c->eigs);
-      rr.lookahead = la && rr.kfactor <= kLookaheadMaxK;
-      c->lookahead_ok = rr.kfactor <= kLookaheadMaxK;
+      if (c->trace)
+        std::fprintf(stderr, "[feast_gpu] pass %d: m=%d mo=%d truncated=%d K=%.3e lookahead=%d\n", pass, m, rr.mo,
+                     (int)rr.truncated, rr.kfactor, (int)la);
+      rr.lookahead = la && rr.kfactor <= c->la_kmax;
+      c->lookahead_ok = rr.kfactor <= c->la_kmax;
       if (rr.lookahead) ++c->lookahead_count;
       CK(cudaStreamWaitEvent(c->stream, c->ev_eig, 0));
       float ms = 0.f;
@@ -1933,14 +2049,17 @@ void feast_gpu_destroy(feast_gpu_ctx* c) {
   cudaStreamSynchronize(c->stream);
   AllocStream as(c->stream);
   for (DevBuf<double>* d : {&c->A, &c->Bm, &c->Y, &c->Q, &c->X, &c->AQ, &c->BQ, &c->T, &c->gw, &c->Aq, &c->Bq,
-                            &c->Cm, &c->Lm, &c->Phi, &c->Ev, &c->Vm, &c->S, &c->Tm, &c->Dv, &c->Aband, &c->Bband, &c->csr, &c->G})
+                            &c->Cm, &c->Lm, &c->Phi, &c->Ev, &c->Vm, &c->S, &c->Tm, &c->Dv, &c->Aband, &c->Bband, &c->csr, &c->G, &c->breal})
     d->release();
   c->csrstats.release();  // every buffer, before the stream goes (the destructor would free on a dead stream)
   c->kfac.release();
   for (DevBuf<double2>* d : {&c->abdiag, &c->ablow, &c->dz, &c->dcoeff, &c->sinv, &c->gfac, &c->hfac, &c->lu, &c->dinv,
                              &c->scratch, &c->W, &c->fwork})
     d->release();
-  for (DevBuf<int>* d : {&c->ipiv, &c->perm, &c->status, &c->keep}) d->release();
+  for (DevBuf<int>* d : {&c->ipiv, &c->perm, &c->status, &c->fstatus, &c->keep, &c->bflag}) d->release();
+  c->bvec.release();
+  c->bz.release();
+  c->bcol.release();
   cudaStreamSynchronize(c->stream);  // the frees above are stream-ordered
   if (c->eig) eig_destroy(c->eig);
   for (auto& e : c->ev)
@@ -2084,6 +2203,19 @@ int feast_gpu_solve_shift(feast_gpu_ctx* c, int e, double* rhs, int m, int mode)
     if (m < 1) fail(FEAST_EINPUT, "solve_shift: no right-hand sides");
     // panel-layout factors (b >= 128): the sweep takes real right-hand sides, so the complex
     // ones go through as 2m real columns [Re | Im] and are recombined afterwards
+    if (c->inner_kind == 1) {  // BicgstabShiftSystem::solve_in_place (inner_solver.hpp:124-184)
+      ensure_workspace(c, m);
+      DevBuf<double2> b;
+      b.ensure((size_t)c->npad * m);
+      CK(cudaMemsetAsync(b.p, 0, sizeof(double2) * c->npad * m, c->stream));
+      CK(cudaMemcpy2DAsync(b.p, sizeof(double2) * c->npad, rhs, sizeof(double2) * c->n, sizeof(double2) * c->n, m,
+                           cudaMemcpyHostToDevice, c->stream));
+      bicg_solve(c, e - c->e0, 1, m, nullptr, b.p, c->npad, mode != 0);
+      CK(cudaMemcpy2DAsync(rhs, sizeof(double2) * c->n, c->bvec.p, sizeof(double2) * c->npad, sizeof(double2) * c->n,
+                           m, cudaMemcpyDeviceToHost, c->stream));
+      sync(c);
+      return;
+    }
     const bool split = c->blocktri && bt_panel_rows(c->b) > 0;
     ensure_workspace(c, split ? 2 * m : m);
     const int sn = e - c->e0;                 // owned node index (shift, coefficient)
@@ -2231,7 +2363,7 @@ int feast_gpu_bench_passes(feast_gpu_ctx* c, int passes, size_t flush_bytes, dou
       flush.ensure(flush_bytes);
       CK(cudaMemsetAsync(flush.p, 0x5a, flush_bytes, c->stream));
     }
-    const bool la_allowed = c->lookahead && !c->streamed();
+    const bool la_allowed = c->lookahead && !c->streamed() && c->inner_kind == 0;
     int m = c->bench_m;
     bool have_q = c->bench_have_q;
     float ms = 0.f;
@@ -2258,8 +2390,8 @@ int feast_gpu_bench_passes(feast_gpu_ctx* c, int passes, size_t flush_bytes, dou
         CK(cudaEventRecord(pn[1], c->stream));
       }
       Reduced r = reduced_gevp_finish(c, m, c->eigs);
-      r.lookahead = la && r.kfactor <= kLookaheadMaxK;
-      c->lookahead_ok = r.kfactor <= kLookaheadMaxK;
+      r.lookahead = la && r.kfactor <= c->la_kmax;
+      c->lookahead_ok = r.kfactor <= c->la_kmax;
       CK(cudaStreamWaitEvent(c->stream, c->ev_eig, 0));
       // this pass's contour solves are complete (they precede the projection)
       CK(cudaEventElapsedTime(&ms, pe[0], pe[3]));
@@ -2286,12 +2418,33 @@ int feast_gpu_bench_passes(feast_gpu_ctx* c, int passes, size_t flush_bytes, dou
   });
 }
 
+int feast_gpu_set_inner_solver(feast_gpu_ctx* c, int kind, double tol, int max_iter) {
+  return guarded(c, [&] {
+    if (kind != 0 && kind != 1) fail(FEAST_EINPUT, "set_inner_solver: kind must be 0 (direct) or 1 (iterative)");
+    if (kind == 1 && (!(tol > 0.0) || tol >= 1.0)) fail(FEAST_EINPUT, "IterativeSolver: tolerance must be in (0, 1)");
+    c->inner_kind = kind;
+    c->inner_tol = kind == 1 ? tol : 0.0;
+    c->inner_max_iter = kind == 1 ? max_iter : 0;
+    c->factored = false;
+  });
+}
+
+int feast_gpu_set_factor_policy(feast_gpu_ctx* c, int policy) {
+  return guarded(c, [&] {
+    if (policy < 0 || policy > 2) fail(FEAST_EINPUT, "set_factor_policy: policy must be 0 (Auto), 1 (Dense) or 2 (Banded)");
+    c->factor_policy = policy;
+  });
+}
+
 int feast_gpu_set_row_distribution(feast_gpu_ctx* c, int enable) {
   return guarded(c, [&] { c->row_dist = enable != 0; });
 }
 
-int feast_gpu_set_lookahead(feast_gpu_ctx* c, int enable) {
-  return guarded(c, [&] { c->lookahead = enable != 0; });
+int feast_gpu_set_lookahead(feast_gpu_ctx* c, int enable, double max_cancellation) {
+  return guarded(c, [&] {
+    c->lookahead = enable != 0;
+    c->la_kmax = max_cancellation > 0.0 ? max_cancellation : kLookaheadMaxK;
+  });
 }
 
 int feast_gpu_lookahead_count(const feast_gpu_ctx* c) { return c ? c->lookahead_count : 0; }

@@ -100,6 +100,32 @@ struct DenseSolveArgs {
 };
 cudaError_t dense_solve(const DenseSolveArgs& a, cudaStream_t st);
 
+// ---------------- iterative inner solver (bicgstab.cu) -------------------------
+// BiCGStab (inner_solver.hpp:115-240) on z B - A for C = nodes * m columns at once.
+struct BicgCol {
+  double2 rho, alpha, omega;
+  double bnorm, rnorm;
+  int it, active;
+};
+struct BicgArgs {
+  int n, ld, C, m;          // rows, leading dimension, columns, columns per node
+  const double2* z;         // per node: the shift (conjugated for ConjTranspose solves)
+  double2 *X, *R, *R0, *P, *V, *S, *T;  // ld x C complex each
+  double *PR, *AR, *BR;     // ld x 2C real: the packed [Re | Im] apply operand, A and B times it
+  BicgCol* col;             // C
+  double tol;
+  int max_iter;
+  int* any_active;          // set by columns still iterating after a kernel
+};
+// rhs: y (real, ld ldy, column j of every node) or bc (complex, ld ldb, column j of every node)
+cudaError_t bicg_init(const BicgArgs& a, const double* y, int ldy, const double2* bc, int ldb, cudaStream_t st);
+cudaError_t bicg_a(const BicgArgs& a, cudaStream_t st);   // after PR -> AR, BR: v, alpha, s -> PR
+cudaError_t bicg_b(const BicgArgs& a, cudaStream_t st);   // after PR -> AR, BR: t, omega, x, r, next p -> PR
+cudaError_t bicg_check(const BicgArgs& a, int* failed, cudaStream_t st);
+// q = [q] - sum_e Re(coeff_e x_e), nodes ascending (x: ld x nodes*m complex)
+cudaError_t bicg_terms(const double2* x, int nodes, int n, int m, int64_t ld, const double2* coeff, double* q,
+                       int accumulate, cudaStream_t st);
+
 // ---------------- real GEMM (DMMA) -------------------------------------------
 // C(m x n) = alpha * op(A) * op(B) + beta * C, column-major; op = 'N' or 'T'.
 // Split-K with a deterministic reduction when k is large relative to m*n.

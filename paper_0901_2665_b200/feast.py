@@ -98,8 +98,10 @@ def load_library(path: str = LIB_PATH):
     L.feast_gpu_random_block.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64, _dp]
     L.feast_gpu_set_node_batch.argtypes = [C.c_void_p, C.c_int]
     L.feast_gpu_set_twist.argtypes = [C.c_void_p, C.c_int]
-    L.feast_gpu_set_lookahead.argtypes = [C.c_void_p, C.c_int]
+    L.feast_gpu_set_lookahead.argtypes = [C.c_void_p, C.c_int, C.c_double]
     L.feast_gpu_set_row_distribution.argtypes = [C.c_void_p, C.c_int]
+    L.feast_gpu_set_inner_solver.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_int]
+    L.feast_gpu_set_factor_policy.argtypes = [C.c_void_p, C.c_int]
     L.feast_gpu_group_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
     L.feast_gpu_group_destroy.argtypes = [C.c_void_p]
     L.feast_gpu_set_group.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
@@ -129,7 +131,8 @@ EXPORTED_SYMBOLS = [
     "feast_gpu_set_node_batch", "feast_gpu_storage", "feast_gpu_random_block",
     "feast_gpu_contour_pass_hermitian", "feast_gpu_set_twist", "feast_gpu_set_lookahead",
     "feast_gpu_lookahead_count", "feast_gpu_set_row_distribution", "feast_gpu_group_create",
-    "feast_gpu_group_destroy", "feast_gpu_set_group",
+    "feast_gpu_group_destroy", "feast_gpu_set_group", "feast_gpu_set_inner_solver",
+    "feast_gpu_set_factor_policy",
 ]
 
 
@@ -252,6 +255,16 @@ class GpuContext:
         """Factor memory plan: 0 = automatic (resident if they fit), k > 0 = stream k nodes."""
         self._check(self.L.feast_gpu_set_node_batch(self.h, int(nodes)))
 
+    def set_inner_solver(self, kind: str = "direct", tol: float = 0.0, max_iter: int = 0):
+        """InnerSolver of the loop (inner_solver.hpp): "direct" (DirectSolver, the default) or
+        "iterative" (IterativeSolver(tol, max_iter): BiCGStab per right-hand side)."""
+        k = {"direct": 0, "iterative": 1}[kind]
+        self._check(self.L.feast_gpu_set_inner_solver(self.h, k, float(tol), int(max_iter)))
+
+    def set_factor_policy(self, policy: str = "auto"):
+        """FactorPolicy (inner_solver.hpp:40-47) of the DirectSolver, at the next set_pencil."""
+        self._check(self.L.feast_gpu_set_factor_policy(self.h, {"auto": 0, "dense": 1, "banded": 2}[policy]))
+
     def set_group(self, group: "LocalGroup", rank: int):
         """Join a loopback rank group (contexts of this process, one host thread each)."""
         self._check(self.L.feast_gpu_set_group(self.h, group.h, rank))
@@ -261,9 +274,10 @@ class GpuContext:
         """Row-distributed Rayleigh-Ritz across the ranks (default on)."""
         self._check(self.L.feast_gpu_set_row_distribution(self.h, int(bool(enable))))
 
-    def set_lookahead(self, enable: bool):
-        """Look-ahead contour pass overlapping each reduced eigensolve (default on)."""
-        self._check(self.L.feast_gpu_set_lookahead(self.h, int(bool(enable))))
+    def set_lookahead(self, enable: bool, max_cancellation: float = 0.0):
+        """Look-ahead contour pass overlapping each reduced eigensolve (default on); admitted when
+        the Ritz block's cancellation factor is <= max_cancellation (0: the default bound)."""
+        self._check(self.L.feast_gpu_set_lookahead(self.h, int(bool(enable)), float(max_cancellation)))
 
     def lookahead_count(self) -> int:
         return int(self.L.feast_gpu_lookahead_count(self.h))

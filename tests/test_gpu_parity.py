@@ -10,6 +10,8 @@ Tolerances (BASELINE.json north_star and the reference's own tests):
   * shifted solves: relative error <= 1e-12 (test_linalg.cpp:138-190);
   * contour accumulation: <= 1e-11 * max(1, max|Q_ref|) (test_core.cpp:94-109).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -473,3 +475,108 @@ def test_lookahead_matches_reference_order(F, which):
         bm = prob.b.to_dense()
         assert sin_max_angle(on.eigenvectors, off.eigenvectors, bm) <= 1e-8
     assert on.max_residual <= max(1e-9, 10 * off.max_residual)
+
+
+# IterativeSolver (inner_solver.hpp:115-240): unpreconditioned BiCGStab per right-hand side to
+# ||r|| <= tol ||b||, here batched over every (node, column). Shifted solves against the reference's
+# own BicgstabShiftSystem to the solve tolerance, and whole FEAST solves against the reference's
+# feast_solve with the same IterativeSolver (the trace tolerance floored at tol^2, core.hpp:296).
+@pytest.mark.parametrize("which", ["small_dense_n60", "bt_L16_b32"])
+def test_iterative_shift_solve_matches_reference(F, which):
+    from tests.golden_problems import generate
+    prob = generate(which)
+    tol = 1e-10
+    c = F.GpuContext(0)
+    try:
+        c.set_inner_solver("iterative", tol)
+        c.set_pencil(prob.a, prob.b)
+        c.prepare(prob.emin, prob.emax, prob.n_e)
+        z, _ = c.contour()
+        rhs = np.random.default_rng(5).standard_normal((prob.n, 3)) + 1j * np.random.default_rng(6).standard_normal((prob.n, 3))
+        for e in (0, prob.n_e - 1):
+            for mode in (0, 1):
+                x = c.solve_shift(e, rhs.copy(), bool(mode))
+                xr = O.shift_solve_with(prob.a, prob.b, z[e], rhs, mode, solver="iterative", tol=tol)
+                xd = O.shift_solve(prob.a, prob.b, z[e], rhs, mode)  # the direct solve
+                # both iterates are within ~kappa * tol of the exact solution
+                assert rel(x, xd) <= 1e-6 and rel(xr, xd) <= 1e-6
+                # the residual target itself: ||(zB - A) x - b|| <= tol ||b|| per column
+                zz = np.conj(z[e]) if mode else z[e]
+                m = zz * prob.b.to_dense() - prob.a.to_dense()
+                res = np.linalg.norm(m @ x - rhs, axis=0) / np.linalg.norm(rhs, axis=0)
+                assert np.all(res <= tol), res
+    finally:
+        c.close()
+
+
+@pytest.mark.parametrize("which", ["small_dense_n60", "bt_L8_b48"])
+def test_iterative_feast_solve_matches_reference(F, which):
+    from tests.golden_problems import generate
+    prob = generate(which)
+    tol = 1e-9
+    c = F.GpuContext(0)
+    try:
+        c.set_inner_solver("iterative", tol)
+        c.set_pencil(prob.a, prob.b)
+        r = c.solve(F.SearchInterval(prob.emin, prob.emax),
+                    F.FeastConfig(m0=prob.m0, n_e=prob.n_e, trace_tol=prob.trace_tol, max_loops=prob.max_loops,
+                                  seed=prob.seed))
+    finally:
+        c.close()
+    ref = O.feast_solve_with(prob, solver="iterative", tol=tol, threads=min(prob.n_e, os.cpu_count() or 1))
+    assert r.status == ref["status"] == "converged"
+    assert len(r.eigenvalues) == ref["m"] == prob.expected_count
+    ev = ref["eigenvalues"]
+    # inexact solves: eigenvalues to ~tol^2 relative (Rayleigh quotients), vectors to ~tol
+    assert np.all(np.abs(r.eigenvalues - ev) <= 1e-10 * np.maximum(np.abs(ev), 1e-3 * (prob.emax - prob.emin)))
+    assert sin_max_angle(r.eigenvectors, ref["eigenvectors"], prob.b.to_dense()) <= 1e-7
+
+
+def test_iterative_solver_input_errors(F):
+    c = F.GpuContext(0)
+    try:
+        for bad in (0.0, 1.0, -1e-3):
+            with pytest.raises(F.InputError, match="IterativeSolver: tolerance must be in"):
+                c.set_inner_solver("iterative", bad)
+    finally:
+        c.close()
+
+
+# FactorPolicy (inner_solver.hpp:40-47, test_core.cpp:415-431: banded = dense): Dense factors of a
+# sparse pencil and Banded (block-tridiagonal) factors give the reference's solves and the same
+# FEAST results; Banded needs sparse operands
+@pytest.mark.parametrize("policy", ["dense", "banded"])
+def test_factor_policy_matches_reference(F, policy):
+    from tests.golden_problems import generate
+    prob = generate("cfg2_n2048")
+    c = F.GpuContext(0)
+    try:
+        c.set_factor_policy(policy)
+        c.set_pencil(prob.a, prob.b)
+        assert (c.storage()[0] == 0) == (policy == "dense")
+        r = c.solve(F.SearchInterval(prob.emin, prob.emax),
+                    F.FeastConfig(m0=prob.m0, n_e=prob.n_e, trace_tol=prob.trace_tol, max_loops=prob.max_loops,
+                                  seed=prob.seed))
+        z, _ = c.contour()
+        rhs = np.random.default_rng(1).standard_normal((prob.n, 2)) + 0j
+        x = c.solve_shift(3, rhs.copy(), False)
+    finally:
+        c.close()
+    pol = {"dense": 1, "banded": 2}[policy]
+    assert rel(x, O.shift_solve_with(prob.a, prob.b, z[3], rhs, 0, policy=pol)) <= 1e-12
+    ref = O.feast_solve_with(prob, policy=pol)
+    assert r.status == ref["status"] and len(r.eigenvalues) == ref["m"]
+    ev = ref["eigenvalues"]
+    assert np.all(np.abs(r.eigenvalues - ev) <= 1e-10 * np.maximum(np.abs(ev), 1e-3 * (prob.emax - prob.emin)))
+
+
+def test_banded_policy_needs_sparse_operands(F):
+    from tests.golden_problems import generate
+    prob = generate("small_dense_n60")
+    c = F.GpuContext(0)
+    try:
+        c.set_factor_policy("banded")
+        with pytest.raises(F.InputError, match="banded policy requires sparse operands"):
+            c.set_pencil(prob.a, prob.b)
+    finally:
+        c.close()
