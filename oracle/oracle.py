@@ -63,10 +63,12 @@ def lib(kind="reference"):
     L.ref_feast_solve.argtypes = [_op, _op, C.c_double, C.c_double,
                                   C.POINTER(abi.FeastConfigT), _dp, C.c_int,
                                   C.POINTER(abi.FeastResultT)]
-    L.ref_feast_solve_with.argtypes = [_op, _op, C.c_double, C.c_double, C.POINTER(abi.FeastConfigT), _dp, C.c_int,
-                                       C.c_int, C.c_int, C.c_double, C.c_int, C.POINTER(abi.FeastResultT)]
-    L.ref_shift_solve_with.argtypes = [_op, _op, C.c_double, C.c_double, _dp, C.c_int, C.c_int, C.c_int, C.c_int,
-                                       C.c_double, C.c_int]
+    if hasattr(L, "ref_feast_solve_with"):  # the reference build only (explicit InnerSolver)
+        L.ref_feast_solve_with.argtypes = [_op, _op, C.c_double, C.c_double, C.POINTER(abi.FeastConfigT), _dp,
+                                           C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
+                                           C.POINTER(abi.FeastResultT)]
+        L.ref_shift_solve_with.argtypes = [_op, _op, C.c_double, C.c_double, _dp, C.c_int, C.c_int, C.c_int,
+                                           C.c_int, C.c_double, C.c_int]
     if hasattr(L, "ref_bench_passes"):
         L.ref_bench_passes.argtypes = [_op, _op, C.c_double, C.c_double, C.c_int, C.c_int,
                                        C.c_uint64, C.c_int, C.c_int, _dp]
