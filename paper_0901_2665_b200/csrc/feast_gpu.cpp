@@ -383,6 +383,36 @@ struct feast_gpu_ctx {
 
 namespace {
 
+// Small page-locked buffers (the per-pass status / eigenvalue read-back) from a process-wide pool:
+// cudaMallocHost / cudaFreeHost cost milliseconds and synchronise, and an end-to-end solve opens
+// a fresh context every time.
+std::mutex g_pin_mu;
+std::vector<std::pair<double*, size_t>> g_pin_free;
+double* pinned_small_get(size_t count, size_t& got) {
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    for (size_t i = 0; i < g_pin_free.size(); ++i)
+      if (g_pin_free[i].second >= count) {
+        double* p = g_pin_free[i].first;
+        got = g_pin_free[i].second;
+        g_pin_free.erase(g_pin_free.begin() + i);
+        return p;
+      }
+  }
+  double* p = nullptr;
+  const size_t n = std::max<size_t>(count, 1026);  // (M0 up to 1024 + 2 scalars)
+  CK(cudaMallocHost(reinterpret_cast<void**>(&p), sizeof(double) * n));
+  got = n;
+  return p;
+}
+void pinned_small_release(double*& p, size_t& n) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_free.emplace_back(p, n);
+  p = nullptr;
+  n = 0;
+}
+
 void ensure_eig(feast_gpu_ctx* c, int m) {
   if (c->eig && c->eig_cap >= m) return;
   if (c->eig) {
@@ -408,11 +438,8 @@ void ensure_reduced(feast_gpu_ctx* c, int m) {
   c->status.ensure(1);
   c->Dv.ensure((size_t)((m + 31) / 32) * 1024);
   if (c->hpin_n < (size_t)m + 2) {
-    if (c->hpin) cudaFreeHost(c->hpin);
-    c->hpin = nullptr;
-    c->hpin_n = 0;
-    CK(cudaMallocHost(reinterpret_cast<void**>(&c->hpin), sizeof(double) * ((size_t)m + 2)));
-    c->hpin_n = (size_t)m + 2;
+    pinned_small_release(c->hpin, c->hpin_n);
+    c->hpin = pinned_small_get((size_t)m + 2, c->hpin_n);
   }
 }
 
@@ -2075,7 +2102,7 @@ void feast_gpu_destroy(feast_gpu_ctx* c) {
   if (c->ev_proj) cudaEventDestroy(c->ev_proj);
   if (c->ev_pre_eig) cudaEventDestroy(c->ev_pre_eig);
   if (c->ev_eig) cudaEventDestroy(c->ev_eig);
-  if (c->hpin) cudaFreeHost(c->hpin);
+  pinned_small_release(c->hpin, c->hpin_n);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   if (c->aux) cudaStreamDestroy(c->aux);
   if (c->y_ready) cudaEventDestroy(c->y_ready);

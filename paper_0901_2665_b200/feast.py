@@ -373,6 +373,7 @@ class GpuContext:
     def solve(self, interval: SearchInterval, config: FeastConfig, initial_y=None) -> FeastResult:
         """feast_solve (core.hpp:264-391) on the uploaded pencil."""
         n, m0 = self.n, config.m0
+        self.n_e = config.n_e
         nl = max(config.max_loops, 0) + 1
         out = dict(eigenvalues=np.zeros(max(m0, 1)), eigenvectors=np.empty((n, max(m0, 1)), order="F"),
                    residuals=np.zeros(max(m0, 1)), absonly=np.zeros(max(m0, 1), dtype=np.int32),
