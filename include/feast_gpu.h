@@ -247,6 +247,19 @@ int feast_gpu_solve(feast_gpu_ctx* ctx, double emin, double emax, const feast_co
  * pass in the reference order; max_cancellation > 0 replaces the admission bound 1e3. */
 int feast_gpu_set_lookahead(feast_gpu_ctx* ctx, int enable, double max_cancellation);
 
+/* Warm-started parameter sweep, run_sweep (run.cpp:63-125): for each step k the pencil
+ * (A0 + steps[k] S, B) (add_scaled, operator.hpp:282-304) is solved over [emin, emax]; a
+ * converged step's Ritz block, topped up with random_block(n, m0 - cols, seed + 1000003 (k + 1))
+ * columns when truncation shrank it, times B starts the next step. Operators, factors and the
+ * warm block stay on the device (A = A0 + t S is formed there). results[k] is filled like
+ * feast_gpu_solve's (caller-allocated arrays); step_codes[k] = FEAST_OK, or FEAST_ENUMERICAL for
+ * a step whose solve raised NumericalError (the next step then starts cold, as in the
+ * reference); any other error ends the sweep with that code. The storage is chosen for the
+ * union of the A0, S and B patterns; the pencil stays set afterwards (at the last step's A). */
+int feast_gpu_sweep(feast_gpu_ctx* ctx, const feast_operator_t* a0, const feast_operator_t* b,
+                    const feast_operator_t* s, const double* steps, int nsteps, double emin, double emax,
+                    const feast_config_t* config, feast_result_t* results, int* step_codes);
+
 /* Benchmark hook: runs `passes` loop bodies (contour pass + Rayleigh-Ritz + trace/count
  * + Y = B X) on the device-resident state set up by feast_gpu_bench_init (after
  * feast_gpu_prepare), with no stopping rule. Each pass is bracketed by CUDA events on the

@@ -328,6 +328,7 @@ struct feast_gpu_ctx {
   bool factored = false;
   int batch_req = 0, batch = 0, res0 = -1, rescnt = 0;
   DevBuf<double2> sinv, gfac, hfac, lu, dinv, scratch, fwork;
+  DevBuf<double> A0, Sop;       // feast_gpu_sweep: the unperturbed A and the perturbation S (A's layout)
   DevBuf<double> Aband, Bband;  // band-row copies of A, B for the applies (b <= 32; band_apply.cu)
   int kmid = -1;  // twisted block-Thomas meeting layer of the current factors (bt_twist_layer)
   DevBuf<int> ipiv, perm, status, fstatus;  // status: reduced Cholesky; fstatus: factorisation
@@ -837,9 +838,17 @@ DeviceCsr csr_upload_scan(feast_gpu_ctx* c, const feast_operator_t* a, const fea
   return d;
 }
 
-void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operator_t* b) {
+// s (may be null): a perturbation A + t S will be formed on the device (feast_gpu_sweep); the
+// storage is chosen for the union of the three patterns and S is stored like A (c->Sop), with a
+// copy of A (c->A0)
+void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operator_t* b,
+                const feast_operator_t* s = nullptr) {
   trace_mark(c, nullptr);
-  const bool dev_csr = csr_rowptr_ok(a) && csr_rowptr_ok(b) && a->n == b->n;
+  if (s) {
+    check_operator(s);
+    if (s->n != a->n) fail(FEAST_EINPUT, "run_sweep: perturbation dimension mismatch");
+  }
+  const bool dev_csr = !s && csr_rowptr_ok(a) && csr_rowptr_ok(b) && a->n == b->n;
   DeviceCsr dcsr{};
   if (dev_csr) {
     dcsr = csr_upload_scan(c, a, b);
@@ -855,16 +864,20 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
   // factorisation replaced by block-tridiagonal block Thomas)
   int bsz = 0;
   const bool a_bt = a->kind == FEAST_STORAGE_BLOCKTRI, b_bt = b->kind == FEAST_STORAGE_BLOCKTRI;
-  const bool a_sp = a->kind == FEAST_STORAGE_CSR || a_bt, b_sp = b->kind == FEAST_STORAGE_CSR || b_bt;
+  const bool a_sp = (a->kind == FEAST_STORAGE_CSR || a_bt) && (!s || s->kind != FEAST_STORAGE_DENSE),
+             b_sp = b->kind == FEAST_STORAGE_CSR || b_bt;
+  std::vector<const feast_operator_t*> ops{a, b};
+  if (s) ops.push_back(s);
   // FactorPolicy (inner_solver.hpp:80-95): Dense keeps dense factors for any storage, Banded
   // requires sparse operands, Auto chooses by bandwidth as below
   if (c->factor_policy == 2 && !(a_sp && b_sp)) fail(FEAST_EINPUT, "DirectSolver: banded policy requires sparse operands");
   if (a_sp && b_sp && c->factor_policy != 1) {
-    if (a_bt && b_bt && a->bsize == b->bsize && round_block(a->bsize) == a->bsize && a->bsize <= kMaxBlock) {
+    if (a_bt && b_bt && a->bsize == b->bsize && round_block(a->bsize) == a->bsize && a->bsize <= kMaxBlock &&
+        (!s || (s->kind == FEAST_STORAGE_BLOCKTRI && s->bsize == a->bsize))) {
       bsz = a->bsize;
     } else {
       int bw = 0;
-      for (const feast_operator_t* o : {a, b}) {
+      for (const feast_operator_t* o : ops) {
         if (dev_csr) bw = std::max({bw, dcsr.stats[0].bandwidth, dcsr.stats[1].bandwidth});
         else if (o->kind == FEAST_STORAGE_CSR) bw = std::max(bw, csr_bandwidth(o));
         else bw = std::max(bw, 2 * o->bsize - 1);
@@ -875,7 +888,7 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
         const int hi = std::min(std::max(round_block(std::max(bw, 1)), lo), kMaxBlock);
         for (int cand = lo; cand <= hi && !bsz; cand *= 2) {
           bool ok = true;
-          for (const feast_operator_t* o : {a, b}) {
+          for (const feast_operator_t* o : ops) {
             if (dev_csr) ok = ok && !(((dcsr.stats[0].misfit_mask | dcsr.stats[1].misfit_mask) >> (log2_exact(cand) - 4)) & 1u);
             else if (o->kind == FEAST_STORAGE_CSR) ok = ok && csr_fits_blocktri(o, cand);
             else ok = ok && cand >= o->bsize && cand % o->bsize == 0;
@@ -917,6 +930,14 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
       std::vector<double> ad, al, bd, bl;
       to_blocktri(a, bsz, c->L, false, ad, al);
       to_blocktri(b, bsz, c->L, true, bd, bl);
+      if (s) {
+        std::vector<double> sd, sl;
+        to_blocktri(s, bsz, c->L, false, sd, sl);
+        c->Sop.ensure(nd + nl);
+        CK(cudaMemcpyAsync(c->Sop.p, sd.data(), sizeof(double) * nd, cudaMemcpyHostToDevice, c->stream));
+        if (nl) CK(cudaMemcpyAsync(c->Sop.p + nd, sl.data(), sizeof(double) * nl, cudaMemcpyHostToDevice, c->stream));
+        sync(c);
+      }
       trace_mark(c, "set_pencil: re-block A, B");
       CK(cudaMemcpyAsync(c->A.p, ad.data(), sizeof(double) * nd, cudaMemcpyHostToDevice, c->stream));
       CK(cudaMemcpyAsync(c->Bm.p, bd.data(), sizeof(double) * nd, cudaMemcpyHostToDevice, c->stream));
@@ -964,9 +985,41 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
       CK(cudaMemcpyAsync(c->Bm.p, d.data(), sizeof(double) * d.size(), cudaMemcpyHostToDevice, c->stream));
       sync(c);
     }
+    if (s) {
+      c->Sop.ensure((size_t)n * n);
+      auto d = to_dense(s);
+      CK(cudaMemcpyAsync(c->Sop.p, d.data(), sizeof(double) * d.size(), cudaMemcpyHostToDevice, c->stream));
+      sync(c);
+    }
     sync(c);
   }
+  if (s) {  // the unperturbed A, kept for A0 + t S
+    c->A0.ensure(c->A.n);
+    CK(cudaMemcpyAsync(c->A0.p, c->A.p, sizeof(double) * c->A.n, cudaMemcpyDeviceToDevice, c->stream));
+    sync(c);
+  } else {
+    c->A0.release();
+    c->Sop.release();
+  }
   c->have_pencil = true;
+}
+
+// A = A0 + t S on the device (add_scaled, operator.hpp:282-304), with the derived copies (the
+// (A, B) pairs of the factorisation, the band rows) and ||A||_1 brought up to date
+void perturb_pencil(feast_gpu_ctx* c, double t) {
+  const size_t cnt = c->A.n;
+  CK(axpby(c->A0.p, c->Sop.p, t, cnt, c->A.p, c->stream));
+  if (c->blocktri) {
+    const size_t nd = (size_t)c->L * c->b * c->b, nl = (size_t)(c->L > 1 ? c->L - 1 : 0) * c->b * c->b;
+    CK(interleave_pairs(c->A.p, c->Bm.p, nd, c->abdiag.p, c->stream));
+    if (nl) CK(interleave_pairs(c->A.p + nd, c->Bm.p + nd, nl, c->ablow.p, c->stream));
+    if (c->b <= 32) CK(band_rows(c->L, c->b, c->A.p, c->A.p + nd, c->Aband.p, c->stream));
+  }
+  c->kfac.ensure(1);
+  CK(operator_norm1(c->blocktri ? c->L : 0, c->blocktri ? c->b : c->n, c->A.p, c->kfac.p, c->stream));
+  CK(cudaMemcpyAsync(&c->norm_a1, c->kfac.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  c->factored = false;
 }
 
 // ------------------------------- contour + factors ---------------------------
@@ -1805,8 +1858,9 @@ double secs(std::chrono::steady_clock::time_point t0) {
 }
 
 // The FEAST loop (core.hpp:264-391), state resident on the device.
+// y_dev: the initial block (y_cols columns) is already in c->Y (feast_gpu_sweep's warm start)
 void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_t* cfg,
-                 const double* initial_y, int y_cols, feast_result_t* out) {
+                 const double* initial_y, int y_cols, feast_result_t* out, bool y_dev = false) {
   const auto t_start = std::chrono::steady_clock::now();
   trace_mark(c, nullptr);
   if (!c->have_pencil) fail(FEAST_EINPUT, "feast_gpu: pencil not set");
@@ -1817,7 +1871,8 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
   if (cfg->max_loops < 1) fail(FEAST_EINPUT, "feast_solve: max_loops must be positive");
   if (!(cfg->trace_tol > 0.0)) fail(FEAST_EINPUT, "feast_solve: trace_tol must be positive");
   if (cfg->threads < 1) fail(FEAST_EINPUT, "feast_solve: threads must be positive");
-  if (initial_y && (y_cols < 1 || y_cols > cfg->m0)) fail(FEAST_EINPUT, "feast_solve: initial block shape mismatch");
+  if ((initial_y || y_dev) && (y_cols < 1 || y_cols > cfg->m0))
+    fail(FEAST_EINPUT, "feast_solve: initial block shape mismatch");
   if (!(emin < emax)) fail(FEAST_EINPUT, "SearchInterval: lambda_min must be strictly below lambda_max");
 
   c->chol_failed_prev = false;
@@ -1831,8 +1886,10 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
 
   *out = feast_result_t{out->eigenvalues, out->eigenvectors, out->residuals, out->residual_absolute_only,
                         out->trace_history, out->in_interval_counts, out->subspace};
-  int m = initial_y ? y_cols : cfg->m0;
-  {
+  int m = (initial_y || y_dev) ? y_cols : cfg->m0;
+  if (y_dev) {
+    trace_mark(c, "solve: initial block resident");
+  } else {
     std::vector<double> y(initial_y ? (size_t)n * m : 0);
     if (initial_y) std::memcpy(y.data(), initial_y, sizeof(double) * y.size());
     if (initial_y) {
@@ -2000,6 +2057,50 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
   fail(FEAST_EINTERNAL, "feast_solve: unreachable");
 }
 
+// run_sweep (run.cpp:63-125) with the operators and the warm-start block resident on the device:
+// step k solves (A0 + steps[k] S, B) after A = A0 + t S is formed in place; a converged step's
+// Ritz block (c->X, still on the device after finalize), topped up with seeded random columns when
+// truncation shrank it (seed + 1000003 (k + 1)), times B is the next step's start block. A step
+// that fails with NumericalError is reported (codes[k]) and the next one starts cold, as in the
+// reference; other errors end the sweep.
+void sweep(feast_gpu_ctx* c, const feast_operator_t* a0, const feast_operator_t* b, const feast_operator_t* s,
+           const double* steps, int nsteps, double emin, double emax, const feast_config_t* cfg,
+           feast_result_t* results, int* codes) {
+  if (!a0 || !b || !s || !cfg || !results || !codes) fail(FEAST_EINPUT, "feast_gpu_sweep: null argument");
+  if (nsteps < 1 || !steps) fail(FEAST_EINPUT, "run_sweep: no steps given");
+  set_pencil(c, a0, b, s);
+  bool have_warm = false;
+  int warm_cols = 0;
+  for (int k = 0; k < nsteps; ++k) {
+    perturb_pencil(c, steps[k]);
+    codes[k] = FEAST_OK;
+    try {
+      feast_solve(c, emin, emax, cfg, nullptr, have_warm ? warm_cols : 0, &results[k], have_warm);
+    } catch (const Failure& f) {
+      if (f.code != FEAST_ENUMERICAL) throw;
+      codes[k] = FEAST_ENUMERICAL;
+      c->err = f.what();
+      have_warm = false;
+      continue;
+    }
+    const feast_result_t& r = results[k];
+    if (r.status == FEAST_STATUS_CONVERGED && r.subspace_cols > 0) {
+      const int cols = r.subspace_cols, m0 = cfg->m0;
+      if (cols < m0) {  // X (npad x m0 buffer) gets the seeded columns after the Ritz block
+        if (c->npad != c->n) CK(fill_zero(c->X.p + (size_t)c->npad * cols, (size_t)c->npad * (m0 - cols), c->stream));
+        CK(random_block_device(cfg->seed + 1000003ull * (uint64_t)(k + 1), c->n, m0 - cols,
+                               c->X.p + (size_t)c->npad * cols, c->npad, c->stream));
+      }
+      apply_op(c, 1, c->X.p, c->Y.p, m0);  // warm = B * block
+      have_warm = true;
+      warm_cols = m0;
+    } else {
+      have_warm = false;
+    }
+  }
+  sync(c);
+}
+
 template <typename F>
 int guarded(feast_gpu_ctx* c, F&& f) {
   AllocStream as(c ? c->stream : nullptr);
@@ -2076,7 +2177,7 @@ void feast_gpu_destroy(feast_gpu_ctx* c) {
   cudaStreamSynchronize(c->stream);
   AllocStream as(c->stream);
   for (DevBuf<double>* d : {&c->A, &c->Bm, &c->Y, &c->Q, &c->X, &c->AQ, &c->BQ, &c->T, &c->gw, &c->Aq, &c->Bq,
-                            &c->Cm, &c->Lm, &c->Phi, &c->Ev, &c->Vm, &c->S, &c->Tm, &c->Dv, &c->Aband, &c->Bband, &c->csr, &c->G, &c->breal})
+                            &c->Cm, &c->Lm, &c->Phi, &c->Ev, &c->Vm, &c->S, &c->Tm, &c->Dv, &c->Aband, &c->Bband, &c->csr, &c->G, &c->breal, &c->A0, &c->Sop})
     d->release();
   c->csrstats.release();  // every buffer, before the stream goes (the destructor would free on a dead stream)
   c->kfac.release();
@@ -2443,6 +2544,12 @@ int feast_gpu_bench_passes(feast_gpu_ctx* c, int passes, size_t flush_bytes, dou
     if (phase_ms)
       for (int i = 0; i < 4; ++i) phase_ms[i] = ph[i];
   });
+}
+
+int feast_gpu_sweep(feast_gpu_ctx* c, const feast_operator_t* a0, const feast_operator_t* b,
+                    const feast_operator_t* s, const double* steps, int nsteps, double emin, double emax,
+                    const feast_config_t* config, feast_result_t* results, int* step_codes) {
+  return guarded(c, [&] { sweep(c, a0, b, s, steps, nsteps, emin, emax, config, results, step_codes); });
 }
 
 int feast_gpu_set_inner_solver(feast_gpu_ctx* c, int kind, double tol, int max_iter) {

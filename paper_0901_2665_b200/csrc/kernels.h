@@ -231,6 +231,11 @@ cudaError_t cancellation_factor(int m, int mo, const double* bq, int ldb, const 
 // dst = sum of `slices` blocks of `count` doubles at src + r * stride, in slice order
 cudaError_t sum_slices(const double* src, int slices, int64_t stride, size_t count, double* dst, cudaStream_t st);
 
+// out = x + t y
+cudaError_t axpby(const double* x, const double* y, double t, size_t n, double* out, cudaStream_t st);
+// *out = ||A||_1 of block-tridiagonal storage [diag | lower] (L layers of b) or dense (L = 0, n = b)
+cudaError_t operator_norm1(int L, int b, const double* a, double* out, cudaStream_t st);
+
 // misc
 cudaError_t fill_zero(double* p, size_t count, cudaStream_t st);
 cudaError_t gather_columns(const double* src, int ld, int n, const int* idx, int m, double* dst,

@@ -97,6 +97,49 @@ cudaError_t sum_slices(const double* src, int slices, int64_t stride, size_t cou
   return cudaGetLastError();
 }
 
+// out = x + t y (add_scaled, operator.hpp:282-304, on the device storage of A0 and S)
+__global__ void axpby_kernel(const double* __restrict__ x, const double* __restrict__ y, double t, size_t n,
+                             double* __restrict__ out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    out[i] = x[i] + y[i] * t;
+}
+
+cudaError_t axpby(const double* x, const double* y, double t, size_t n, double* out, cudaStream_t st) {
+  if (!n) return cudaSuccess;
+  axpby_kernel<<<(unsigned)std::min<size_t>((n + 255) / 256, 4096), 256, 0, st>>>(x, y, t, n, out);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// ||A||_1 = max absolute row sum of a symmetric operator (operator.hpp:195-212): block-tridiagonal
+// storage (L > 0: row i of layer l = [C_{l-1} | D_l | C_l^T](i, :)) or dense n x n (L = 0, b = n);
+// one thread per row, max by atomicMax on the bits of non-negative doubles
+__global__ void operator_norm1_kernel(int L, int b, const double* __restrict__ a, unsigned long long* out) {
+  const int64_t rows = L > 0 ? (int64_t)L * b : b;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    if (L > 0) {
+      const int l = (int)(r / b), i = (int)(r % b);
+      const int64_t bb = (int64_t)b * b, nd = (int64_t)L * bb;
+      for (int j = 0; j < b; ++j) s += fabs(a[l * bb + i + (int64_t)j * b]);
+      if (l > 0) for (int j = 0; j < b; ++j) s += fabs(a[nd + (l - 1) * bb + i + (int64_t)j * b]);
+      if (l + 1 < L) for (int j = 0; j < b; ++j) s += fabs(a[nd + l * bb + j + (int64_t)i * b]);
+    } else {
+      for (int j = 0; j < b; ++j) s += fabs(a[r + (int64_t)j * b]);
+    }
+    atomicMax(out, __double_as_longlong(s));
+  }
+}
+
+cudaError_t operator_norm1(int L, int b, const double* a, double* out, cudaStream_t st) {
+  cudaMemsetAsync(out, 0, sizeof(double), st);
+  const int64_t rows = L > 0 ? (int64_t)L * b : b;
+  operator_norm1_kernel<<<(unsigned)std::min<int64_t>((rows + 255) / 256, 4096), 256, 0, st>>>(
+      L, b, a, reinterpret_cast<unsigned long long*>(out));
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 __global__ void fill_zero_kernel(double* p, size_t count) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
        i += (size_t)gridDim.x * blockDim.x)

@@ -102,6 +102,8 @@ def load_library(path: str = LIB_PATH):
     L.feast_gpu_set_row_distribution.argtypes = [C.c_void_p, C.c_int]
     L.feast_gpu_set_inner_solver.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_int]
     L.feast_gpu_set_factor_policy.argtypes = [C.c_void_p, C.c_int]
+    L.feast_gpu_sweep.argtypes = [C.c_void_p, _op, _op, _op, _dp, C.c_int, C.c_double, C.c_double,
+                                  C.POINTER(abi.FeastConfigT), C.c_void_p, _ip]
     L.feast_gpu_group_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
     L.feast_gpu_group_destroy.argtypes = [C.c_void_p]
     L.feast_gpu_set_group.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
@@ -132,7 +134,7 @@ EXPORTED_SYMBOLS = [
     "feast_gpu_contour_pass_hermitian", "feast_gpu_set_twist", "feast_gpu_set_lookahead",
     "feast_gpu_lookahead_count", "feast_gpu_set_row_distribution", "feast_gpu_group_create",
     "feast_gpu_group_destroy", "feast_gpu_set_group", "feast_gpu_set_inner_solver",
-    "feast_gpu_set_factor_policy",
+    "feast_gpu_set_factor_policy", "feast_gpu_sweep",
 ]
 
 
@@ -201,6 +203,43 @@ class FeastResult:
 def _cols(a, n, k):
     """The first k columns of a Fortran-ordered n x m0 output block, as a view (no copy)."""
     return a[:n, :k]
+
+
+def _result_buffers(n, config):
+    """Caller-allocated arrays of a feast_result_t (include/feast_gpu.h)."""
+    m0 = config.m0
+    nl = max(config.max_loops, 0) + 1
+    out = dict(eigenvalues=np.zeros(max(m0, 1)), eigenvectors=np.empty((n, max(m0, 1)), order="F"),
+               residuals=np.zeros(max(m0, 1)), absonly=np.zeros(max(m0, 1), dtype=np.int32),
+               trace=np.zeros(nl), counts=np.zeros(nl, dtype=np.int32),
+               subspace=np.empty((n, max(m0, 1)), order="F"))
+    r = abi.FeastResultT()
+    r.eigenvalues = abi.dptr(out["eigenvalues"])
+    r.eigenvectors = abi.dptr(out["eigenvectors"])
+    r.residuals = abi.dptr(out["residuals"])
+    r.residual_absolute_only = abi.iptr(out["absonly"])
+    r.trace_history = abi.dptr(out["trace"])
+    r.in_interval_counts = abi.iptr(out["counts"])
+    r.subspace = abi.dptr(out["subspace"])
+    return out, r
+
+
+def _result_of(out, r, n):
+    m, k, loops = r.m, r.subspace_cols, r.loops_used
+    nh = loops if r.status == 4 else loops + 1  # breakdown returns before pushing (core.hpp:347-353)
+    return FeastResult(
+        eigenvalues=out["eigenvalues"][:m].copy(),
+        eigenvectors=_cols(out["eigenvectors"], n, m),
+        residuals=out["residuals"][:m].copy(),
+        residual_absolute_only=out["absonly"][:m].astype(bool),
+        max_residual=r.max_residual,
+        loops_used=loops,
+        trace_history=out["trace"][:nh].copy(),
+        in_interval_counts=out["counts"][:nh].copy(),
+        status=abi.STATUS_NAMES[r.status],
+        subspace=_cols(out["subspace"], n, k) if k else np.zeros((n, 0)),
+        timings=FeastTimings(r.factorize_s, r.solve_s, r.reduce_s, r.total_s),
+    )
 
 
 class GpuContext:
@@ -372,42 +411,40 @@ class GpuContext:
 
     def solve(self, interval: SearchInterval, config: FeastConfig, initial_y=None) -> FeastResult:
         """feast_solve (core.hpp:264-391) on the uploaded pencil."""
-        n, m0 = self.n, config.m0
+        n = self.n
         self.n_e = config.n_e
-        nl = max(config.max_loops, 0) + 1
-        out = dict(eigenvalues=np.zeros(max(m0, 1)), eigenvectors=np.empty((n, max(m0, 1)), order="F"),
-                   residuals=np.zeros(max(m0, 1)), absonly=np.zeros(max(m0, 1), dtype=np.int32),
-                   trace=np.zeros(nl), counts=np.zeros(nl, dtype=np.int32),
-                   subspace=np.empty((n, max(m0, 1)), order="F"))
-        r = abi.FeastResultT()
-        r.eigenvalues = abi.dptr(out["eigenvalues"])
-        r.eigenvectors = abi.dptr(out["eigenvectors"])
-        r.residuals = abi.dptr(out["residuals"])
-        r.residual_absolute_only = abi.iptr(out["absonly"])
-        r.trace_history = abi.dptr(out["trace"])
-        r.in_interval_counts = abi.iptr(out["counts"])
-        r.subspace = abi.dptr(out["subspace"])
+        out, r = _result_buffers(n, config)
         y0 = None if initial_y is None else np.asfortranarray(initial_y, dtype=np.float64)
         if y0 is not None and y0.shape[0] != n:
             raise InputError("feast_solve: initial block shape mismatch")
         cfg = config.to_c()
         self._check(self.L.feast_gpu_solve(self.h, interval.lo, interval.hi, C.byref(cfg), abi.dptr(y0),
                                            0 if y0 is None else y0.shape[1], C.byref(r)))
-        m, k, loops = r.m, r.subspace_cols, r.loops_used
-        nh = loops if r.status == 4 else loops + 1  # breakdown returns before pushing (core.hpp:347-353)
-        return FeastResult(
-            eigenvalues=out["eigenvalues"][:m].copy(),
-            eigenvectors=_cols(out["eigenvectors"], n, m),
-            residuals=out["residuals"][:m].copy(),
-            residual_absolute_only=out["absonly"][:m].astype(bool),
-            max_residual=r.max_residual,
-            loops_used=loops,
-            trace_history=out["trace"][:nh].copy(),
-            in_interval_counts=out["counts"][:nh].copy(),
-            status=abi.STATUS_NAMES[r.status],
-            subspace=_cols(out["subspace"], n, k) if k else np.zeros((n, 0)),
-            timings=FeastTimings(r.factorize_s, r.solve_s, r.reduce_s, r.total_s),
-        )
+        return _result_of(out, r, n)
+
+    def sweep(self, a0, b, s, steps, interval: SearchInterval, config: FeastConfig):
+        """run_sweep (run.cpp:63-125) on the device: one FeastResult per step, or the
+        NumericalError a failed step raised (the next step then starts cold)."""
+        steps = np.ascontiguousarray(steps, dtype=np.float64)
+        n, k = a0.n, len(steps)
+        self._ca, self._cb, self._cs = a0.to_c(), b.to_c(), s.to_c()
+        bufs = [_result_buffers(n, config) for _ in range(k)]
+        res = (abi.FeastResultT * max(k, 1))()
+        for i, (_, r) in enumerate(bufs):
+            res[i] = r
+        codes = np.zeros(max(k, 1), dtype=np.int32)
+        cfg = config.to_c()
+        self._check(self.L.feast_gpu_sweep(self.h, C.byref(self._ca), C.byref(self._cb), C.byref(self._cs),
+                                           abi.dptr(steps), k, interval.lo, interval.hi, C.byref(cfg), res,
+                                           abi.iptr(codes)))
+        self.n, self.n_e = n, config.n_e
+        out = []
+        for i in range(k):
+            if codes[i] != 0:
+                out.append(_CODES.get(int(codes[i]), Error)(f"step {i}: NumericalError"))
+            else:
+                out.append(_result_of(bufs[i][0], res[i], n))
+        return out
 
     def bench_init(self, m0: int, seed: int = 42):
         self._check(self.L.feast_gpu_bench_init(self.h, m0, seed))
