@@ -221,7 +221,7 @@ def max_over_ranks(dist, v):
     return float(t[0])
 
 
-def time_passes(F, prob, args, local, world, rank, dist, flush):
+def time_passes(F, prob, args, local, world, rank, dist, flush, region=None):
     """Device-timed passes on a prepared context: (ctx, total ms over args.steps passes (max over
     ranks), phase ms, launches, factor seconds (wall clock around prepare, max over ranks), b)."""
     ctx = comm_context(F, local, world, rank, dist)
@@ -237,7 +237,10 @@ def time_passes(F, prob, args, local, world, rank, dist, flush):
     if dist:
         dist.barrier()
     l0, a0 = ctx.launch_count(), ctx.lookahead_count()
+    t0 = time.monotonic()
     ms, ph = ctx.bench_passes(args.steps, flush)
+    if region is not None:  # the monotonic interval of the timed passes (clock samples)
+        region.extend([t0, time.monotonic()])
     launches = ctx.launch_count() - l0
     ctx.lookahead_used = ctx.lookahead_count() - a0
     ms = max_over_ranks(dist, ms)
@@ -345,9 +348,10 @@ def main():
     flush = args.flush_mib << 20
     with ClockSampler(local) as clk:
         clk.wait_ready()
-        t_region = time.monotonic()
-        ctx, ms, ph, launches, t_factor, b_used = time_passes(F, prob, args, local, world, rank, dist, flush)
-        t_region = (t_region, time.monotonic())
+        region = []
+        ctx, ms, ph, launches, t_factor, b_used = time_passes(F, prob, args, local, world, rank, dist, flush,
+                                                              region)
+        t_region = tuple(region)
         time.sleep(0.15)  # the sample straddling the end of the region
     ctx.close()
     value = args.steps / (ms / 1e3)

@@ -759,6 +759,7 @@ bool csr_rowptr_ok(const feast_operator_t* o) {
 }
 
 struct PinnedStage;
+constexpr size_t kPinnedStageMax = (size_t)256 << 20;  // bytes (PinnedStage)
 PinnedStage& pinned_stage();
 double* pinned_stage_lock_get(size_t count, std::unique_lock<std::mutex>& lk);
 
@@ -836,6 +837,39 @@ DeviceCsr csr_upload_scan(feast_gpu_ctx* c, const feast_operator_t* a, const fea
   for (int t = 0; t < 2; ++t)
     if (d.stats[t].first_error != ~0ull) fail(FEAST_EINPUT, msg[d.stats[t].first_error & 3]);
   return d;
+}
+
+// host -> device copy of `bytes` from pageable memory through the pinned stage: two halves
+// alternate, host threads fill one while the DMA drains the other (synchronous on return)
+void upload_chunked(feast_gpu_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  const size_t half = std::min<size_t>(kPinnedStageMax / 2, ((bytes + 1) / 2 + 63) / 64 * 64);
+  std::unique_lock<std::mutex> lk;
+  double* st = pinned_stage_lock_get(2 * half / sizeof(double), lk);
+  if (!st) {
+    lk.unlock();
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+    sync(c);
+    return;
+  }
+  cudaEvent_t ev[2];
+  CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  bool used[2] = {false, false};
+  char* stage[2] = {reinterpret_cast<char*>(st), reinterpret_cast<char*>(st) + half};
+  size_t off = 0;
+  for (int k = 0; off < bytes; ++k, off += half) {
+    const int h = k & 1;
+    const size_t len = std::min(half, bytes - off);
+    if (used[h]) CK(cudaEventSynchronize(ev[h]));
+    parallel_copies({{stage[h], reinterpret_cast<const char*>(src) + off, len}});
+    CK(cudaMemcpyAsync(reinterpret_cast<char*>(dst) + off, stage[h], len, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaEventRecord(ev[h], c->stream));
+    used[h] = true;
+  }
+  sync(c);
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
 }
 
 // s (may be null): a perturbation A + t S will be formed on the device (feast_gpu_sweep); the
@@ -926,6 +960,17 @@ void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operato
     if (dev_csr) {
       CK(csr_to_blocktri(n, bsz, c->L, dcsr.rp[0], dcsr.ci[0], dcsr.val[0], c->A.p, c->A.p + nd, false, c->stream));
       CK(csr_to_blocktri(n, bsz, c->L, dcsr.rp[1], dcsr.ci[1], dcsr.val[1], c->Bm.p, c->Bm.p + nd, true, c->stream));
+    } else if (!s && a->kind == FEAST_STORAGE_BLOCKTRI && b->kind == FEAST_STORAGE_BLOCKTRI && a->bsize == bsz &&
+               b->bsize == bsz && a->nblocks == c->L) {
+      // already in this storage (e.g. a memory-mapped FEASTOP1 file, pencil_io.py): stream the
+      // blocks up through the pinned stage, no host-side copy of the operator
+      upload_chunked(c, c->A.p, a->diag, sizeof(double) * nd);
+      upload_chunked(c, c->Bm.p, b->diag, sizeof(double) * nd);
+      if (nl) {
+        upload_chunked(c, c->A.p + nd, a->lower, sizeof(double) * nl);
+        upload_chunked(c, c->Bm.p + nd, b->lower, sizeof(double) * nl);
+      }
+      trace_mark(c, "set_pencil: block upload");
     } else {
       std::vector<double> ad, al, bd, bl;
       to_blocktri(a, bsz, c->L, false, ad, al);
@@ -1681,7 +1726,6 @@ void upload_block(feast_gpu_ctx* c, const double* host, int m, double* dev) {
 // call with cudaHostRegister was slower still). Grown on demand up to kPinnedStageMax and kept
 // for reuse; larger transfers go through it in rounds (downloads) or take the pageable path
 // (uploads), so a config-5-sized result does not leave gigabytes page-locked.
-constexpr size_t kPinnedStageMax = (size_t)256 << 20;  // bytes
 struct PinnedStage {
   std::mutex mu;
   double* p = nullptr;
