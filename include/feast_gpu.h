@@ -52,8 +52,12 @@ typedef enum {
 typedef enum {
   FEAST_STORAGE_DENSE = 0,    /* n*n column-major, exactly symmetric            */
   FEAST_STORAGE_CSR = 1,      /* symmetric-complete CSR, int32 indices          */
-  FEAST_STORAGE_BLOCKTRI = 2  /* nblocks diagonal b*b blocks + (nblocks-1) lower
+  FEAST_STORAGE_BLOCKTRI = 2, /* nblocks diagonal b*b blocks + (nblocks-1) lower
                                  couplings C_l = M(l+1, l); M(l, l+1) = C_l^T   */
+  /* complex Hermitian operators (feast_gpu_set_pencil_hermitian): `dense` / `values` hold
+     interleaved (re, im) pairs, std::complex<double> layout (types.hpp:12)          */
+  FEAST_STORAGE_DENSE_Z = 16, /* n*n complex column-major, exactly Hermitian      */
+  FEAST_STORAGE_CSR_Z = 17    /* Hermitian-complete CSR, nnz complex values       */
 } feast_storage_t;
 
 typedef struct {
@@ -152,6 +156,22 @@ int feast_gpu_set_row_distribution(feast_gpu_ctx* ctx, int enable);
  * whose pattern is block-tridiagonal are stored block-tridiagonal; other CSR
  * inputs are densified (the reference's Dense policy, inner_solver.hpp:88-92). */
 int feast_gpu_set_pencil(feast_gpu_ctx* ctx, const feast_operator_t* a, const feast_operator_t* b);
+
+/* Complex Hermitian pencils (feast_solve<cplx>, core.hpp:264-391 with T = std::complex<double>;
+ * SymmetricOperator<cplx>, operator.hpp:33-268): A Hermitian, B Hermitian positive definite, both
+ * FEAST_STORAGE_DENSE_Z or FEAST_STORAGE_CSR_Z. Validation messages as the reference's
+ * (conjugate symmetry, real diagonal). The pencil is carried as the real symmetric pencil of
+ * twice the size (each entry x + iy as the block [[x, -y], [y, x]]), on which every solver
+ * path of this library runs; feast_gpu_solve_hermitian reads it back as the complex pencil. */
+int feast_gpu_set_pencil_hermitian(feast_gpu_ctx* ctx, const feast_operator_t* a, const feast_operator_t* b);
+
+/* feast_solve<cplx> on a Hermitian pencil: m0 complex subspace columns (m0 <= 512), the start
+ * block random_block<cplx>(n, m0, seed) (real then imaginary part per entry, core.hpp:84-106) or
+ * initial_y (n*y_cols complex, interleaved). Results as feast_gpu_solve's, except that
+ * eigenvectors (n*m0) and subspace (n*m0) hold COMPLEX entries (2 doubles each, interleaved);
+ * residuals use complex moduli (residual.hpp:29-68). */
+int feast_gpu_solve_hermitian(feast_gpu_ctx* ctx, double emin, double emax, const feast_config_t* config,
+                              const double* initial_y, int y_cols, feast_result_t* result);
 
 /* Contour on the upper half circle over [emin, emax] with n_e Gauss-Legendre
  * nodes (quadrature.cpp:69-87), then factors every node this rank owns

@@ -69,6 +69,9 @@ def lib(kind="reference"):
                                            C.POINTER(abi.FeastResultT)]
         L.ref_shift_solve_with.argtypes = [_op, _op, C.c_double, C.c_double, _dp, C.c_int, C.c_int, C.c_int,
                                            C.c_int, C.c_double, C.c_int]
+    if hasattr(L, "ref_feast_solve_hermitian"):
+        L.ref_feast_solve_hermitian.argtypes = [_op, _op, C.c_double, C.c_double, C.POINTER(abi.FeastConfigT), _dp,
+                                                C.c_int, C.POINTER(abi.FeastResultT)]
     if hasattr(L, "ref_bench_passes"):
         L.ref_bench_passes.argtypes = [_op, _op, C.c_double, C.c_double, C.c_int, C.c_int,
                                        C.c_uint64, C.c_int, C.c_int, _dp]
@@ -280,6 +283,39 @@ def feast_solve_with(problem, solver="direct", policy=0, tol=0.0, max_iter=0, th
                            threads=threads, low_memory=0)
     return _run_solve(L, p.a, p.b, p.emin, p.emax, cfg, None, p.n,
                       solver=(1 if solver == "iterative" else 0, policy, tol, max_iter))
+
+
+def feast_solve_hermitian(a, b, emin, emax, m0, n_e=8, trace_tol=1e-13, max_loops=20, seed=42, initial_y=None,
+                          threads=1, kind="reference"):
+    """feast_solve<cplx> of the reference on a Hermitian pencil (Operator kinds DENSE_Z / CSR_Z):
+    dict like feast_solve's, eigenvectors / subspace complex."""
+    L = lib(kind)
+    n = a.n
+    cfg = abi.FeastConfigT(m0=m0, n_e=n_e, trace_tol=trace_tol, max_loops=max_loops, seed=seed, threads=threads,
+                           low_memory=0)
+    out = dict(eigenvalues=np.zeros(m0), eigenvectors=np.zeros((n, m0), dtype=np.complex128, order="F"),
+               residuals=np.zeros(m0), residual_absolute_only=np.zeros(m0, dtype=np.int32),
+               trace_history=np.zeros(max_loops + 1), in_interval_counts=np.zeros(max_loops + 1, dtype=np.int32),
+               subspace=np.zeros((n, m0), dtype=np.complex128, order="F"))
+    r = abi.FeastResultT()
+    r.eigenvalues = abi.dptr(out["eigenvalues"])
+    r.eigenvectors = abi.zptr(out["eigenvectors"])
+    r.residuals = abi.dptr(out["residuals"])
+    r.residual_absolute_only = abi.iptr(out["residual_absolute_only"])
+    r.trace_history = abi.dptr(out["trace_history"])
+    r.in_interval_counts = abi.iptr(out["in_interval_counts"])
+    r.subspace = abi.zptr(out["subspace"])
+    y0 = None if initial_y is None else np.asfortranarray(initial_y, dtype=np.complex128)
+    ca, cb = a.to_c(), b.to_c()
+    _check(L, L.ref_feast_solve_hermitian(C.byref(ca), C.byref(cb), emin, emax, C.byref(cfg), abi.zptr(y0),
+                                          0 if y0 is None else y0.shape[1], C.byref(r)))
+    m, k, loops = r.m, r.subspace_cols, r.loops_used
+    return dict(status=abi.STATUS_NAMES[r.status], m=m, loops_used=loops,
+                eigenvalues=out["eigenvalues"][:m].copy(), eigenvectors=out["eigenvectors"][:, :m].copy(),
+                residuals=out["residuals"][:m].copy(), max_residual=r.max_residual,
+                trace_history=out["trace_history"][: loops + 1].copy(),
+                in_interval_counts=out["in_interval_counts"][: loops + 1].copy(),
+                subspace=out["subspace"][:, :k].copy())
 
 
 def _run_solve(L, a, b, emin, emax, cfg, initial_y, n, solver=None):

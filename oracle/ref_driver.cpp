@@ -325,6 +325,23 @@ int ref_bench_passes(const feast_operator_t* a, const feast_operator_t* b, doubl
   }
 }
 
+// complex Hermitian operator (FEAST_STORAGE_DENSE_Z / CSR_Z, interleaved) -> SymmetricOperator<cplx>
+SymmetricOperator<cplx> to_ref_z(const feast_operator_t* op) {
+  const int n = op->n;
+  if (op->kind == FEAST_STORAGE_DENSE_Z) {
+    DenseMatrix<cplx> m(n, n);
+    std::memcpy(m.data().data(), op->dense, sizeof(cplx) * (size_t)n * n);
+    return SymmetricOperator<cplx>::from_dense(std::move(m));
+  }
+  if (op->kind != FEAST_STORAGE_CSR_Z) throw feast::InputError("ref_driver: not a Hermitian operator");
+  std::vector<Triplet<cplx>> t;
+  t.reserve(op->row_ptr[n]);
+  for (int i = 0; i < n; ++i)
+    for (int k = op->row_ptr[i]; k < op->row_ptr[i + 1]; ++k)
+      t.push_back({i, op->col_idx[k], cplx(op->values[2 * (size_t)k], op->values[2 * (size_t)k + 1])});
+  return SymmetricOperator<cplx>::from_triplets(n, std::move(t), TripletLayout::Full);
+}
+
 // solver_kind 0: DirectSolver(a, b, FactorPolicy(policy)); 1: IterativeSolver(a, b, tol, max_iter)
 // (inner_solver.hpp:77-113, 209-240); -1: the default (nullptr, core.hpp:264-268)
 std::unique_ptr<feast::InnerSolver<double>> make_solver(const SymmetricOperator<double>& ra,
@@ -388,6 +405,50 @@ int ref_feast_solve(const feast_operator_t* a, const feast_operator_t* b, double
                     double emax, const feast_config_t* config, const double* initial_y,
                     int y_cols, feast_result_t* out) {
   return ref_feast_solve_with(a, b, emin, emax, config, initial_y, y_cols, -1, 0, 0.0, 0, out);
+}
+
+// feast_solve<cplx> (core.hpp:264-391) on a Hermitian pencil; eigenvectors / subspace complex
+// (interleaved), initial_y complex n x y_cols or null
+int ref_feast_solve_hermitian(const feast_operator_t* a, const feast_operator_t* b, double emin, double emax,
+                              const feast_config_t* config, const double* initial_y, int y_cols,
+                              feast_result_t* out) {
+  try {
+    const auto ra = to_ref_z(a);
+    const auto rb = to_ref_z(b);
+    const int n = ra.n();
+    DenseMatrix<cplx> y0;
+    if (initial_y) {
+      y0 = DenseMatrix<cplx>(n, y_cols);
+      std::memcpy(y0.data().data(), initial_y, sizeof(cplx) * (size_t)n * y_cols);
+    }
+    const auto r = feast::feast_solve<cplx>(ra, rb, feast::SearchInterval(emin, emax), to_ref(config), nullptr,
+                                            initial_y ? &y0 : nullptr);
+    const int m = (int)r.eigenvalues.size();
+    out->m = m;
+    out->subspace_cols = r.subspace.cols();
+    out->loops_used = r.loops_used;
+    out->status = (int)r.status;
+    out->max_residual = r.max_residual;
+    out->factorize_s = r.timings.factorize_s;
+    out->solve_s = r.timings.solve_s;
+    out->reduce_s = r.timings.reduce_s;
+    out->total_s = r.timings.total_s;
+    if (out->eigenvalues) std::memcpy(out->eigenvalues, r.eigenvalues.data(), sizeof(double) * m);
+    if (out->eigenvectors)
+      std::memcpy(out->eigenvectors, r.eigenvectors.data().data(), sizeof(cplx) * r.eigenvectors.data().size());
+    if (out->residuals) std::memcpy(out->residuals, r.residuals.data(), sizeof(double) * m);
+    if (out->residual_absolute_only)
+      for (int j = 0; j < m; ++j) out->residual_absolute_only[j] = r.residual_absolute_only[j];
+    if (out->trace_history)
+      std::memcpy(out->trace_history, r.trace_history.data(), sizeof(double) * r.trace_history.size());
+    if (out->in_interval_counts)
+      for (size_t k = 0; k < r.in_interval_counts.size(); ++k) out->in_interval_counts[k] = r.in_interval_counts[k];
+    if (out->subspace)
+      std::memcpy(out->subspace, r.subspace.data().data(), sizeof(cplx) * r.subspace.data().size());
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
 }
 
 // ShiftSystem::solve_in_place at shift z for a DirectSolver with FactorPolicy `policy` or an

@@ -18,6 +18,8 @@ FEAST_EINTERNAL = 9
 STORAGE_DENSE = 0
 STORAGE_CSR = 1
 STORAGE_BLOCKTRI = 2
+STORAGE_DENSE_Z = 16   # complex Hermitian, interleaved (feast_gpu_set_pencil_hermitian)
+STORAGE_CSR_Z = 17
 
 # feast_run_status_t == feast::FeastStatus order (core.hpp:35-41)
 STATUS_NAMES = ["converged", "max-loops", "no-eigenvalues-in-interval",
@@ -80,6 +82,14 @@ def dptr(a):
     if a is None:
         return C.cast(None, _dp)
     assert a.dtype.name == "float64" and a.flags["C_CONTIGUOUS"] or a.flags["F_CONTIGUOUS"]
+    return a.ctypes.data_as(_dp)
+
+
+def zptr(a):
+    """double* over the interleaved (re, im) pairs of a contiguous complex128 array (or NULL)."""
+    if a is None:
+        return C.cast(None, _dp)
+    assert a.dtype.name == "complex128" and (a.flags["C_CONTIGUOUS"] or a.flags["F_CONTIGUOUS"])
     return a.ctypes.data_as(_dp)
 
 

@@ -353,6 +353,8 @@ struct feast_gpu_ctx {
   DevBuf<BicgCol> bcol;
   DevBuf<int> bflag;
   DevBuf<double2> bz;
+  bool hermitian = false;  // set_pencil_hermitian: the doubled real pencil of a complex one
+  int nz = 0;              // its complex dimension
   bool twist = true;  // two-ended block-Thomas recursion where it applies (feast_gpu_set_twist)
   // workspaces
   int mcap = 0;
@@ -744,6 +746,138 @@ void check_operator(const feast_operator_t* o) {
   }
 }
 
+// ---- Hermitian pencils -------------------------------------
+// A complex Hermitian operator (kinds FEAST_STORAGE_DENSE_Z / FEAST_STORAGE_CSR_Z: complex
+// entries interleaved) is carried as the real symmetric operator of twice the size whose entry
+// a_ij = x + iy is the 2 x 2 block [[x, -y], [y, x]] at rows (2i, 2i+1), columns (2j, 2j+1). An
+// interleaved complex vector IS a real vector of that operator, multiplication by i is the
+// rotation J (re, im) -> (-im, re) that commutes with both operators, and a complex eigenpair
+// (lambda, phi) is the pair of real ones (lambda, phi), (lambda, J phi). The FEAST loop of the
+// complex pencil (core.hpp:264-391 with T = cplx) is then the real loop on the doubled pencil,
+// started from [Y | J Y] and read through one representative per Ritz pair (feast_solve's pair
+// mode) — every kernel, the look-ahead pass and the multi-rank path carry over unchanged.
+void validate_hermitian(const feast_operator_t* o) {
+  if (!o) fail(FEAST_EINPUT, "set_pencil: null operator");
+  if (o->n < 1) fail(FEAST_EINPUT, "feast_solve: empty operator");
+  const int n = o->n;
+  if (o->kind == FEAST_STORAGE_DENSE_Z) {  // from_dense (operator.hpp:45-62)
+    if (!o->dense) fail(FEAST_EINPUT, "set_pencil: dense data missing");
+    const double* m = o->dense;
+    for (int j = 0; j < n; ++j) {
+      for (int i = 0; i <= j; ++i) {
+        const size_t ij = 2 * ((size_t)i + (size_t)j * n), ji = 2 * ((size_t)j + (size_t)i * n);
+        if (m[ij] != m[ji] || m[ij + 1] != -m[ji + 1]) fail(FEAST_EINPUT, "SymmetricOperator: matrix is not symmetric");
+      }
+      if (m[2 * ((size_t)j + (size_t)j * n) + 1] != 0.0) fail(FEAST_EINPUT, "SymmetricOperator: diagonal must be real");
+    }
+    return;
+  }
+  if (o->kind != FEAST_STORAGE_CSR_Z) fail(FEAST_EINPUT, "set_pencil_hermitian: operators must be DENSE_Z or CSR_Z");
+  if (!o->row_ptr || !o->col_idx || !o->values) fail(FEAST_EINPUT, "set_pencil: CSR data missing");
+  if (o->row_ptr[0] != 0) fail(FEAST_EINPUT, "SymmetricOperator: bad row_ptr");
+  for (int i = 0; i < n; ++i)
+    if (o->row_ptr[i + 1] < o->row_ptr[i]) fail(FEAST_EINPUT, "SymmetricOperator: bad row_ptr");
+  const double* v = o->values;
+  for (int i = 0; i < n; ++i)  // validate_sparse_symmetry (operator.hpp:237-262)
+    for (int k = o->row_ptr[i]; k < o->row_ptr[i + 1]; ++k) {
+      const int j = o->col_idx[k];
+      if (j < 0 || j >= n) fail(FEAST_EINPUT, "SymmetricOperator: triplet index out of range");
+      if (i == j) {
+        if (v[2 * (size_t)k + 1] != 0.0) fail(FEAST_EINPUT, "SymmetricOperator: diagonal must be real");
+        continue;
+      }
+      if (j < i) continue;
+      bool found = false;
+      for (int k2 = o->row_ptr[j]; k2 < o->row_ptr[j + 1]; ++k2)
+        if (o->col_idx[k2] == i) {
+          if (v[2 * (size_t)k2] != v[2 * (size_t)k] || v[2 * (size_t)k2 + 1] != -v[2 * (size_t)k + 1])
+            fail(FEAST_EINPUT, "SymmetricOperator: mirror entries disagree");
+          found = true;
+          break;
+        }
+      if (!found) fail(FEAST_EINPUT, "SymmetricOperator: missing mirror entry");
+    }
+}
+
+double norm_one_hermitian(const feast_operator_t* o) {  // norm_one (operator.hpp:195-212), |complex|
+  const int n = o->n;
+  double best = 0.0;
+  if (o->kind == FEAST_STORAGE_DENSE_Z) {
+    for (int j = 0; j < n; ++j) {
+      double s = 0.0;
+      for (int i = 0; i < n; ++i) {
+        const size_t q = 2 * ((size_t)i + (size_t)j * n);
+        s += std::hypot(o->dense[q], o->dense[q + 1]);
+      }
+      best = std::max(best, s);
+    }
+  } else {
+    for (int i = 0; i < n; ++i) {
+      double s = 0.0;
+      for (int k = o->row_ptr[i]; k < o->row_ptr[i + 1]; ++k) s += std::hypot(o->values[2 * (size_t)k], o->values[2 * (size_t)k + 1]);
+      best = std::max(best, s);
+    }
+  }
+  return best;
+}
+
+struct EmbeddedOp {
+  std::vector<int> rp, ci;
+  std::vector<double> val, dense;
+  feast_operator_t op{};
+};
+
+// the real symmetric operator of twice the size (2 x 2 blocks [[x, -y], [y, x]])
+void embed_hermitian(const feast_operator_t* o, EmbeddedOp& e) {
+  const int n = o->n, n2 = 2 * n;
+  e.op = feast_operator_t{};
+  e.op.n = n2;
+  if (o->kind == FEAST_STORAGE_DENSE_Z) {
+    e.dense.assign((size_t)n2 * n2, 0.0);
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i) {
+        const size_t q = 2 * ((size_t)i + (size_t)j * n);
+        const double x = o->dense[q], y = o->dense[q + 1];
+        double* d = e.dense.data();
+        d[(2 * i) + (size_t)(2 * j) * n2] = x;
+        d[(2 * i + 1) + (size_t)(2 * j) * n2] = y;
+        d[(2 * i) + (size_t)(2 * j + 1) * n2] = -y;
+        d[(2 * i + 1) + (size_t)(2 * j + 1) * n2] = x;
+      }
+    e.op.kind = FEAST_STORAGE_DENSE;
+    e.op.dense = e.dense.data();
+    return;
+  }
+  // CSR: rows sorted by column; exact-zero parts are dropped, and since an entry and its mirror
+  // carry the same value the pattern stays symmetric-complete
+  e.rp.assign(n2 + 1, 0);
+  std::vector<std::pair<int, double>> row;
+  for (int i = 0; i < n; ++i) {
+    for (int half = 0; half < 2; ++half) {  // rows 2i (re) and 2i + 1 (im)
+      row.clear();
+      for (int k = o->row_ptr[i]; k < o->row_ptr[i + 1]; ++k) {
+        const int j = o->col_idx[k];
+        const double x = o->values[2 * (size_t)k], y = o->values[2 * (size_t)k + 1];
+        const double c0 = half ? y : x, c1 = half ? x : -y;  // columns 2j, 2j + 1
+        if (c0 != 0.0) row.emplace_back(2 * j, c0);  // (the mirror entry has the same value)
+        if (c1 != 0.0) row.emplace_back(2 * j + 1, c1);
+      }
+      std::sort(row.begin(), row.end(), [](const std::pair<int, double>& a, const std::pair<int, double>& b) {
+        return a.first < b.first;
+      });
+      for (auto& [col, val] : row) {
+        e.ci.push_back(col);
+        e.val.push_back(val);
+      }
+      e.rp[2 * i + half + 1] = (int)e.ci.size();
+    }
+  }
+  e.op.kind = FEAST_STORAGE_CSR;
+  e.op.row_ptr = e.rp.data();
+  e.op.col_idx = e.ci.data();
+  e.op.values = e.val.data();
+}
+
 // ---- CSR operators taken in on the device (csr_ingest.cu) ----------------------
 // The route for the common case (A and B both CSR, row pointers well formed): the CSR arrays
 // go up once through the pinned stage, csr_scan validates them and measures bandwidth, block
@@ -878,6 +1012,7 @@ void upload_chunked(feast_gpu_ctx* c, void* dst, const void* src, size_t bytes) 
 void set_pencil(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operator_t* b,
                 const feast_operator_t* s = nullptr) {
   trace_mark(c, nullptr);
+  c->hermitian = false;
   if (s) {
     check_operator(s);
     if (s->n != a->n) fail(FEAST_EINPUT, "run_sweep: perturbation dimension mismatch");
@@ -1436,6 +1571,12 @@ void apply_op(feast_gpu_ctx* c, int which, const double* x, double* y, int m) {
   apply_op(c, which, x, y, m, all);
 }
 
+// y = B x on all rows (m columns)
+cudaError_t apply_op_cols(feast_gpu_ctx* c, const double* x, double* y, int m) {
+  apply_op(c, 1, x, y, m);
+  return cudaSuccess;
+}
+
 // A x and B x on rows of s (one pass over x for small blocks)
 void apply_both(feast_gpu_ctx* c, const double* x, double* ya, double* yb, int m, const Slab& s) {
   if (c->blocktri && c->b <= 32) {
@@ -1876,7 +2017,7 @@ void residuals(feast_gpu_ctx* c, int m, const double* lam_host, const double* xd
   sums.ensure(3 * (size_t)m);
   CK(cudaMemcpyAsync(lam.p, lam_host, sizeof(double) * m, cudaMemcpyHostToDevice, c->stream));
   apply_both(c, xdev, c->AQ.p, c->BQ.p, m);
-  CK(residual_sums(c->n, m, c->AQ.p, c->BQ.p, xdev, c->npad, lam.p, sums.p, c->stream));
+  CK(residual_sums(c->n, m, c->AQ.p, c->BQ.p, xdev, c->npad, lam.p, sums.p, c->stream, c->hermitian));
   std::vector<double> h(3 * (size_t)m);
   CK(cudaMemcpyAsync(h.data(), sums.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, c->stream));
   sync(c);
@@ -1885,7 +2026,7 @@ void residuals(feast_gpu_ctx* c, int m, const double* lam_host, const double* xd
   const double eps = 2.220446049250313e-16;
   for (int j = 0; j < m; ++j) {
     const double num = h[3 * j], den = h[3 * j + 1], xn = h[3 * j + 2];
-    const double floor = 4.0 * c->n * eps * c->norm_a1 * xn;
+    const double floor = 4.0 * (c->hermitian ? c->nz : c->n) * eps * c->norm_a1 * xn;
     if (den <= std::max(1e-300, floor)) {
       res[j] = num;
       if (absonly) absonly[j] = 1;
@@ -1901,6 +2042,80 @@ double secs(std::chrono::steady_clock::time_point t0) {
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+// Pair mode, degenerate eigenvalues: a complex eigenvalue of multiplicity s is a real one of
+// multiplicity 2s, and one representative per real pair need not span the complex eigenspace.
+// For each cluster of in-interval representatives (relative gap <= 1e-10) the 2s real Ritz
+// vectors of the cluster are read as complex vectors and B-orthonormalised by modified
+// Gram-Schmidt in the complex inner product, accepting a candidate only while it keeps half its
+// B-norm (a J-partner of an accepted vector keeps none); the s accepted vectors replace the
+// cluster's columns of c->Q (eigenvectors of the result, keep order). Clusters are rare (exact
+// multiplicities); the small host computation touches only their columns.
+void hermitian_clusters(feast_gpu_ctx* c, const std::vector<double>& lam, const std::vector<int>& keep,
+                        const Reduced& rr) {
+  const int k = (int)keep.size();
+  std::vector<std::pair<int, int>> cl;  // [first, last] positions in keep
+  for (int j = 0; j < k;) {
+    int e = j;
+    while (e + 1 < k && lam[e + 1] - lam[e] <= 1e-10 * std::max(1.0, std::fabs(lam[e]))) ++e;
+    if (e > j) cl.emplace_back(j, e);
+    j = e + 1;
+  }
+  if (cl.empty()) return;
+  const size_t n2 = c->n, ld = c->npad;
+  for (auto [j0, j1] : cl) {
+    const int s = j1 - j0 + 1;
+    const int r0 = keep[j0], r1 = std::min(keep[j1] + 1, rr.mo - 1);  // real Ritz columns r0 .. r1
+    const int nc = r1 - r0 + 1;
+    std::vector<double> x(n2 * nc), bx(n2 * nc);
+    CK(apply_op_cols(c, c->X.p + ld * r0, c->AQ.p, nc));  // B x (AQ is free in finalize)
+    CK(cudaMemcpy2DAsync(x.data(), sizeof(double) * n2, c->X.p + ld * r0, sizeof(double) * ld, sizeof(double) * n2, nc,
+                         cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpy2DAsync(bx.data(), sizeof(double) * n2, c->AQ.p, sizeof(double) * ld, sizeof(double) * n2, nc,
+                         cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    auto dot = [&](const double* a, const double* b) {  // a^H b over interleaved complex entries
+      double re = 0.0, im = 0.0;
+      for (size_t i = 0; i + 1 < n2; i += 2) {
+        re += a[i] * b[i] + a[i + 1] * b[i + 1];
+        im += a[i] * b[i + 1] - a[i + 1] * b[i];
+      }
+      return std::make_pair(re, im);
+    };
+    std::vector<int> acc;
+    for (int q = 0; q < nc && (int)acc.size() < s; ++q) {
+      double* u = x.data() + n2 * q;
+      double* bu = bx.data() + n2 * q;
+      for (int a : acc) {
+        const double* v = x.data() + n2 * a;
+        const double* bv = bx.data() + n2 * a;
+        const auto al = dot(v, bu);  // <v, u>_B
+        for (size_t i = 0; i + 1 < n2; i += 2) {
+          const double ur = u[i] - (al.first * v[i] - al.second * v[i + 1]);
+          const double ui = u[i + 1] - (al.first * v[i + 1] + al.second * v[i]);
+          u[i] = ur;
+          u[i + 1] = ui;
+          const double br = bu[i] - (al.first * bv[i] - al.second * bv[i + 1]);
+          const double bi = bu[i + 1] - (al.first * bv[i + 1] + al.second * bv[i]);
+          bu[i] = br;
+          bu[i + 1] = bi;
+        }
+      }
+      const double nrm2 = dot(u, bu).first;
+      if (!(nrm2 > 0.25)) continue;
+      const double inv = 1.0 / std::sqrt(nrm2);
+      for (size_t i = 0; i < n2; ++i) {
+        u[i] *= inv;
+        bu[i] *= inv;
+      }
+      acc.push_back(q);
+    }
+    for (int t = 0; t < (int)acc.size(); ++t)
+      CK(cudaMemcpyAsync(c->Q.p + ld * (j0 + t), x.data() + n2 * acc[t], sizeof(double) * n2, cudaMemcpyHostToDevice,
+                         c->stream));
+    sync(c);
+  }
+}
+
 // The FEAST loop (core.hpp:264-391), state resident on the device.
 // y_dev: the initial block (y_cols columns) is already in c->Y (feast_gpu_sweep's warm start)
 void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_t* cfg,
@@ -1910,8 +2125,13 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
   if (!c->have_pencil) fail(FEAST_EINPUT, "feast_gpu: pencil not set");
   if (!cfg || !out) fail(FEAST_EINPUT, "feast_gpu_solve: null argument");
   const int n = c->n;
-  if (cfg->m0 < 1 || cfg->m0 > n) fail(FEAST_EINPUT, "feast_solve: m0 must be in [1, n]");
-  if (cfg->m0 > 1024) fail(FEAST_EINPUT, "feast_solve: m0 exceeds the supported reduced size");
+  // Hermitian pencils (pair mode): the real loop on the doubled pencil with 2 m0 columns, read
+  // through one representative per Ritz pair (set_pencil_hermitian)
+  const bool pair = c->hermitian;
+  const int step = pair ? 2 : 1;
+  if (cfg->m0 < 1 || cfg->m0 > (pair ? c->nz : n)) fail(FEAST_EINPUT, "feast_solve: m0 must be in [1, n]");
+  if (cfg->m0 * step > 1024) fail(FEAST_EINPUT, "feast_solve: m0 exceeds the supported reduced size");
+  if (pair && y_dev) fail(FEAST_EINPUT, "run_sweep: sweeps are defined for real pencils");
   if (cfg->max_loops < 1) fail(FEAST_EINPUT, "feast_solve: max_loops must be positive");
   if (!(cfg->trace_tol > 0.0)) fail(FEAST_EINPUT, "feast_solve: trace_tol must be positive");
   if (cfg->threads < 1) fail(FEAST_EINPUT, "feast_solve: threads must be positive");
@@ -1925,7 +2145,7 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
   // max(trace_tol, residual_target^2) (core.hpp:296-297): 0 for direct solves, tol for BiCGStab
   const double inner = c->inner_kind == 1 ? c->inner_tol : 0.0;
   const double effective_tol = std::max(cfg->trace_tol, inner * inner);
-  ensure_workspace(c, cfg->m0);
+  ensure_workspace(c, cfg->m0 * step);
   trace_mark(c, "solve: contour + workspaces");
 
   *out = feast_result_t{out->eigenvalues, out->eigenvectors, out->residuals, out->residual_absolute_only,
@@ -1941,8 +2161,14 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
       sync(c);
       trace_mark(c, "solve: initial block H2D");
     } else {
+      // (pair mode: random_block<cplx>(n, m0) is the real stream random_block(2n, m0), interleaved)
       device_random_block(c, m, cfg->seed);  // overlaps the factorisation (side stream)
       trace_mark(c, "solve: initial block (device mt19937_64)");
+    }
+    if (pair) {  // [Y | J Y]: the complex block as the real columns of the doubled pencil
+      join_aux(c);
+      CK(rotate_pairs(c->Y.p, c->n, c->npad, m, c->Y.p + (size_t)c->npad * m, c->stream));
+      m *= 2;
     }
   }
   if (!same_contour || !c->factored) c->factored = false;
@@ -1958,11 +2184,11 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
     out->status = status;
     out->loops_used = pass;
     std::vector<int> keep;
-    for (int i = 0; i < rr.mo; ++i)
+    for (int i = 0; i < rr.mo; i += step)
       if (emin <= rr.evals[i] && rr.evals[i] <= emax) keep.push_back(i);
     const int k = (int)keep.size();
     out->m = k;
-    out->subspace_cols = rr.mo;
+    out->subspace_cols = pair ? (rr.mo + 1) / 2 : rr.mo;
     std::vector<double> lam(k);
     for (int j = 0; j < k; ++j) lam[j] = rr.evals[keep[j]];
     if (out->eigenvalues) std::memcpy(out->eigenvalues, lam.data(), sizeof(double) * k);
@@ -1974,9 +2200,17 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
     trace_mark(c, "finalize: gather");
     // (pinning the caller's blocks with cudaHostRegister for these copies measured slower:
     // 13.4 vs 10.2 ms for 41 MB at config 2, the registration costs more than it saves)
+    if (pair) {
+      if (k) hermitian_clusters(c, lam, keep, rr);  // complex-orthonormal degenerate eigenvectors
+      // the subspace: one representative per Ritz pair, into the free AQ buffer
+      std::vector<int> rep;
+      for (int i = 0; i < rr.mo; i += 2) rep.push_back(i);
+      CK(cudaMemcpyAsync(c->keep.p, rep.data(), sizeof(int) * rep.size(), cudaMemcpyHostToDevice, c->stream));
+      CK(gather_columns(c->X.p, c->npad, c->npad, c->keep.p, (int)rep.size(), c->AQ.p, c->npad, c->stream));
+    }
     std::vector<Download> dl;
     if (out->eigenvectors && k) dl.push_back({c->Q.p, k, out->eigenvectors});
-    if (out->subspace) dl.push_back({c->X.p, rr.mo, out->subspace});
+    if (out->subspace) dl.push_back({pair ? c->AQ.p : c->X.p, out->subspace_cols, out->subspace});
     download_blocks(c, dl);
     trace_mark(c, "finalize: D2H eigenvectors + subspace");
     std::vector<double> res(k);
@@ -2066,7 +2300,7 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
 
     double tr = 0.0;
     int cnt = 0;
-    for (int i = 0; i < rr.mo; ++i)
+    for (int i = 0; i < rr.mo; i += step)  // (pair mode: one representative per Ritz pair)
       if (emin <= rr.evals[i] && rr.evals[i] <= emax) {
         tr += rr.evals[i];
         ++cnt;
@@ -2509,7 +2743,10 @@ int feast_gpu_residuals(feast_gpu_ctx* c, int m, const double* lambdas, const do
 
 int feast_gpu_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_t* config,
                     const double* initial_y, int y_cols, feast_result_t* result) {
-  return guarded(c, [&] { feast_solve(c, emin, emax, config, initial_y, y_cols, result); });
+  return guarded(c, [&] {
+    if (c->hermitian) fail(FEAST_EINPUT, "feast_gpu_solve: the pencil is Hermitian (feast_gpu_solve_hermitian)");
+    feast_solve(c, emin, emax, config, initial_y, y_cols, result);
+  });
 }
 
 int feast_gpu_bench_init(feast_gpu_ctx* c, int m0, uint64_t seed) {
@@ -2594,6 +2831,29 @@ int feast_gpu_sweep(feast_gpu_ctx* c, const feast_operator_t* a0, const feast_op
                     const feast_operator_t* s, const double* steps, int nsteps, double emin, double emax,
                     const feast_config_t* config, feast_result_t* results, int* step_codes) {
   return guarded(c, [&] { sweep(c, a0, b, s, steps, nsteps, emin, emax, config, results, step_codes); });
+}
+
+int feast_gpu_set_pencil_hermitian(feast_gpu_ctx* c, const feast_operator_t* a, const feast_operator_t* b) {
+  return guarded(c, [&] {
+    validate_hermitian(a);
+    validate_hermitian(b);
+    if (a->n != b->n) fail(FEAST_EINPUT, "feast_solve: operator dimensions differ");
+    EmbeddedOp ea, eb;
+    embed_hermitian(a, ea);
+    embed_hermitian(b, eb);
+    set_pencil(c, &ea.op, &eb.op);
+    c->hermitian = true;
+    c->nz = a->n;
+    c->norm_a1 = norm_one_hermitian(a);
+  });
+}
+
+int feast_gpu_solve_hermitian(feast_gpu_ctx* c, double emin, double emax, const feast_config_t* config,
+                              const double* initial_y, int y_cols, feast_result_t* result) {
+  return guarded(c, [&] {
+    if (!c->hermitian) fail(FEAST_EINPUT, "feast_gpu_solve_hermitian: set a Hermitian pencil first");
+    feast_solve(c, emin, emax, config, initial_y, y_cols, result);
+  });
 }
 
 int feast_gpu_set_inner_solver(feast_gpu_ctx* c, int kind, double tol, int max_iter) {

@@ -189,8 +189,11 @@ cudaError_t scale_columns(const double* v, int m, const int* keep, const double*
 
 // ---------------- residuals ---------------------------------------------------
 // per column j: num = sum|AX - lam_j BX|, den = sum|AX|, xn = sum|X|  -> out[3*j + {0,1,2}]
+// pairs: rows are interleaved complex entries, summed as complex moduli (Hermitian pencils)
 cudaError_t residual_sums(int n, int m, const double* ax, const double* bx, const double* x,
-                          int ld, const double* lam, double* out, cudaStream_t st);
+                          int ld, const double* lam, double* out, cudaStream_t st, bool pairs = false);
+// out(:, j) = J in(:, j), J (re, im) = (-im, re) on interleaved pairs; n rows, ld, m columns
+cudaError_t rotate_pairs(const double* in, int n, int64_t ld, int m, double* out, cudaStream_t st);
 
 // random_block<double> (core.hpp:84-106) on the device: out(i, j) for i < n, j < m (ld), the
 // mt19937_64(seed) stream mapped to [-1, 1) column by column, bit-identical to the host

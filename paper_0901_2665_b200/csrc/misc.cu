@@ -8,21 +8,30 @@
 namespace feastgpu {
 
 // One CTA per eigenpair column; fixed-order block reductions (run-to-run deterministic).
+// pairs: the rows are interleaved complex entries (Hermitian pencils), summed as complex moduli
 __global__ void __launch_bounds__(256) residual_sums_kernel(int n, const double* __restrict__ ax,
                                                             const double* __restrict__ bx,
                                                             const double* __restrict__ x, int ld,
                                                             const double* __restrict__ lam,
-                                                            double* __restrict__ out) {
+                                                            double* __restrict__ out, int pairs) {
   const int j = blockIdx.x;
   const double l = lam[j];
   const double* a = ax + (int64_t)j * ld;
   const double* b = bx + (int64_t)j * ld;
   const double* xc = x + (int64_t)j * ld;
   double num = 0.0, den = 0.0, xn = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    num += fabs(a[i] - l * b[i]);
-    den += fabs(a[i]);
-    xn += fabs(xc[i]);
+  if (pairs) {
+    for (int i = threadIdx.x; 2 * i + 1 < n; i += blockDim.x) {
+      num += hypot(a[2 * i] - l * b[2 * i], a[2 * i + 1] - l * b[2 * i + 1]);
+      den += hypot(a[2 * i], a[2 * i + 1]);
+      xn += hypot(xc[2 * i], xc[2 * i + 1]);
+    }
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      num += fabs(a[i] - l * b[i]);
+      den += fabs(a[i]);
+      xn += fabs(xc[i]);
+    }
   }
   __shared__ double red[3][8];
   num = warp_sum(num);
@@ -39,9 +48,9 @@ __global__ void __launch_bounds__(256) residual_sums_kernel(int n, const double*
 }
 
 cudaError_t residual_sums(int n, int m, const double* ax, const double* bx, const double* x, int ld,
-                          const double* lam, double* out, cudaStream_t st) {
+                          const double* lam, double* out, cudaStream_t st, bool pairs) {
   if (m <= 0) return cudaSuccess;
-  residual_sums_kernel<<<m, 256, 0, st>>>(n, ax, bx, x, ld, lam, out);
+  residual_sums_kernel<<<m, 256, 0, st>>>(n, ax, bx, x, ld, lam, out, pairs ? 1 : 0);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -136,6 +145,25 @@ cudaError_t operator_norm1(int L, int b, const double* a, double* out, cudaStrea
   const int64_t rows = L > 0 ? (int64_t)L * b : b;
   operator_norm1_kernel<<<(unsigned)std::min<int64_t>((rows + 255) / 256, 4096), 256, 0, st>>>(
       L, b, a, reinterpret_cast<unsigned long long*>(out));
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// out(:, j) = J in(:, j): (re, im) -> (-im, re) per interleaved pair (multiplication by i of a
+// complex column carried as a real one); rows [n, ld) zero
+__global__ void rotate_pairs_kernel(const double* __restrict__ in, int n, int64_t ld, int m, double* __restrict__ out) {
+  const int64_t total = ld * m;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % ld, j = e / ld;
+    const double* c = in + j * ld;
+    out[i + j * ld] = i >= n ? 0.0 : ((i & 1) ? c[i - 1] : -c[i + 1]);
+  }
+}
+
+cudaError_t rotate_pairs(const double* in, int n, int64_t ld, int m, double* out, cudaStream_t st) {
+  const int64_t total = ld * m;
+  if (!total) return cudaSuccess;
+  rotate_pairs_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, st>>>(in, n, ld, m, out);
   ++g_launches;
   return cudaGetLastError();
 }

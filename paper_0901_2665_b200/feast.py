@@ -102,6 +102,9 @@ def load_library(path: str = LIB_PATH):
     L.feast_gpu_set_row_distribution.argtypes = [C.c_void_p, C.c_int]
     L.feast_gpu_set_inner_solver.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_int]
     L.feast_gpu_set_factor_policy.argtypes = [C.c_void_p, C.c_int]
+    L.feast_gpu_set_pencil_hermitian.argtypes = [C.c_void_p, _op, _op]
+    L.feast_gpu_solve_hermitian.argtypes = [C.c_void_p, C.c_double, C.c_double, C.POINTER(abi.FeastConfigT), _dp,
+                                            C.c_int, C.POINTER(abi.FeastResultT)]
     L.feast_gpu_sweep.argtypes = [C.c_void_p, _op, _op, _op, _dp, C.c_int, C.c_double, C.c_double,
                                   C.POINTER(abi.FeastConfigT), C.c_void_p, _ip]
     L.feast_gpu_group_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
@@ -134,7 +137,8 @@ EXPORTED_SYMBOLS = [
     "feast_gpu_contour_pass_hermitian", "feast_gpu_set_twist", "feast_gpu_set_lookahead",
     "feast_gpu_lookahead_count", "feast_gpu_set_row_distribution", "feast_gpu_group_create",
     "feast_gpu_group_destroy", "feast_gpu_set_group", "feast_gpu_set_inner_solver",
-    "feast_gpu_set_factor_policy", "feast_gpu_sweep",
+    "feast_gpu_set_factor_policy", "feast_gpu_sweep", "feast_gpu_set_pencil_hermitian",
+    "feast_gpu_solve_hermitian",
 ]
 
 
@@ -421,6 +425,30 @@ class GpuContext:
         self._check(self.L.feast_gpu_solve(self.h, interval.lo, interval.hi, C.byref(cfg), abi.dptr(y0),
                                            0 if y0 is None else y0.shape[1], C.byref(r)))
         return _result_of(out, r, n)
+
+    def set_pencil_hermitian(self, a, b):
+        """Complex Hermitian pencil (SymmetricOperator<cplx>): operators of kind DENSE_Z / CSR_Z."""
+        self._ca, self._cb = a.to_c(), b.to_c()
+        self._check(self.L.feast_gpu_set_pencil_hermitian(self.h, C.byref(self._ca), C.byref(self._cb)))
+        self.n = a.n
+
+    def solve_hermitian(self, interval: SearchInterval, config: FeastConfig, initial_y=None) -> FeastResult:
+        """feast_solve<cplx> (core.hpp:264-391) on the Hermitian pencil: complex eigenvectors and
+        subspace, real eigenvalues."""
+        n = self.n
+        self.n_e = config.n_e
+        out, r = _result_buffers(2 * n, config)  # complex n x m0 as interleaved real 2n x m0
+        y0 = None if initial_y is None else np.asfortranarray(initial_y, dtype=np.complex128)
+        if y0 is not None and y0.shape[0] != n:
+            raise InputError("feast_solve: initial block shape mismatch")
+        cfg = config.to_c()
+        self._check(self.L.feast_gpu_solve_hermitian(self.h, interval.lo, interval.hi, C.byref(cfg), abi.zptr(y0),
+                                                     0 if y0 is None else y0.shape[1], C.byref(r)))
+        res = _result_of(out, r, 2 * n)
+        to_c = lambda a: np.asfortranarray(a).reshape(-1, order="F").view(np.complex128).reshape((n, a.shape[1]), order="F")
+        res.eigenvectors = to_c(res.eigenvectors)
+        res.subspace = to_c(res.subspace)
+        return res
 
     def sweep(self, a0, b, s, steps, interval: SearchInterval, config: FeastConfig):
         """run_sweep (run.cpp:63-125) on the device: one FeastResult per step, or the

@@ -65,6 +65,25 @@ class Operator:
         return Operator(abi.STORAGE_BLOCKTRI, L * b, nblocks=L, bsize=b, diag=d, lower=lo)
 
     @staticmethod
+    def from_dense_hermitian(m: np.ndarray) -> "Operator":
+        """Complex Hermitian dense operator (SymmetricOperator<cplx>::from_dense)."""
+        m = np.asfortranarray(m, dtype=np.complex128)
+        assert m.shape[0] == m.shape[1]
+        return Operator(abi.STORAGE_DENSE_Z, m.shape[0], dense=m)
+
+    @staticmethod
+    def from_csr_hermitian(n, row_ptr, col_idx, values) -> "Operator":
+        """Complex Hermitian-complete CSR operator (SymmetricOperator<cplx>, Full layout)."""
+        return Operator(abi.STORAGE_CSR_Z, n,
+                        row_ptr=np.ascontiguousarray(row_ptr, dtype=np.int32),
+                        col_idx=np.ascontiguousarray(col_idx, dtype=np.int32),
+                        values=np.ascontiguousarray(values, dtype=np.complex128))
+
+    @property
+    def is_complex(self) -> bool:
+        return self.kind in (abi.STORAGE_DENSE_Z, abi.STORAGE_CSR_Z)
+
+    @staticmethod
     def identity_csr(n: int) -> "Operator":
         return Operator.from_csr(n, np.arange(n + 1), np.arange(n), np.ones(n))
 
@@ -78,10 +97,10 @@ class Operator:
     def to_c(self) -> abi.FeastOperatorT:
         s = abi.FeastOperatorT()
         s.kind, s.n = self.kind, self.n
-        s.dense = abi.dptr(self.dense)
+        s.dense = abi.zptr(self.dense) if self.is_complex else abi.dptr(self.dense)
         s.row_ptr = abi.iptr(self.row_ptr)
         s.col_idx = abi.iptr(self.col_idx)
-        s.values = abi.dptr(self.values)
+        s.values = abi.zptr(self.values) if self.is_complex else abi.dptr(self.values)
         s.nblocks, s.bsize = self.nblocks, self.bsize
         s.diag = abi.dptr(self.diag)
         s.lower = abi.dptr(self.lower)
@@ -89,10 +108,10 @@ class Operator:
 
     def to_dense(self) -> np.ndarray:
         n = self.n
-        if self.kind == abi.STORAGE_DENSE:
+        if self.kind in (abi.STORAGE_DENSE, abi.STORAGE_DENSE_Z):
             return np.array(self.dense)
-        m = np.zeros((n, n))
-        if self.kind == abi.STORAGE_CSR:
+        m = np.zeros((n, n), dtype=np.complex128 if self.is_complex else np.float64)
+        if self.kind in (abi.STORAGE_CSR, abi.STORAGE_CSR_Z):
             rows = np.repeat(np.arange(n), np.diff(self.row_ptr))
             m[rows, self.col_idx] = self.values
             return m
@@ -107,9 +126,9 @@ class Operator:
 
     def to_scipy(self):
         import scipy.sparse as sp
-        if self.kind == abi.STORAGE_DENSE:
+        if self.kind in (abi.STORAGE_DENSE, abi.STORAGE_DENSE_Z):
             return sp.csr_matrix(self.dense)
-        if self.kind == abi.STORAGE_CSR:
+        if self.kind in (abi.STORAGE_CSR, abi.STORAGE_CSR_Z):
             return sp.csr_matrix((self.values, self.col_idx, self.row_ptr), shape=(self.n, self.n))
         L, b = self.nblocks, self.bsize
         blocks = [[None] * L for _ in range(L)]
@@ -122,7 +141,7 @@ class Operator:
         return sp.bmat(blocks, format="csr")
 
     def matmul(self, x: np.ndarray) -> np.ndarray:
-        if self.kind == abi.STORAGE_DENSE:
+        if self.kind in (abi.STORAGE_DENSE, abi.STORAGE_DENSE_Z):
             return self.dense @ x
         return self.to_scipy() @ x
 
