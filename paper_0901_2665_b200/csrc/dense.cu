@@ -260,30 +260,50 @@ __global__ void term_kernel(int n, int m, int ldv, const double2* coeff, const d
 }
 
 // blocked forward/backward substitution on the factors of zgetrf_batched, in place on the
-// (already row-permuted) right-hand sides W (n x m per node, ld ldv, batch stride sv)
+// (already row-permuted) right-hand sides W (n x m per node, ld ldv, batch stride sv).
+// Two levels: inside an outer block of kSolveNbo rows the 64-row blocks are solved with their
+// diagonal-block inverses and update only the rest of the outer block; the rows below (above, for
+// U) get ONE update per outer block with K = kSolveNbo. With K = 64 every trailing update was a
+// short-K GEMM that spent most of each CTA in pipeline fill and the C read-modify-write
+// (ncu: DMMA pipe 58 %, long-scoreboard stalls on the epilogue loads); K = 256 amortises both.
+constexpr int kSolveNbo = 256;
 static void zgetrs_core(int n, int nodes, int m, const double2* lu, int64_t stride, const double2* dinv,
                         double2* w, int ldv, int64_t sv, cudaStream_t st) {
   const int nb = kDenseNb, nblk = (n + nb - 1) / nb;
   const int64_t sd = (int64_t)nblk * 2 * nb * nb;
   const double2 one = make_double2(1.0, 0.0), mone = make_double2(-1.0, 0.0),
                 zero = make_double2(0.0, 0.0);
-  for (int blk = 0; blk < nblk; ++blk) {
-    const int k0 = blk * nb, kb = std::min(nb, n - k0);
-    double2* rk = w + k0;
-    zgemm_batched(kb, m, kb, one, dinv + (int64_t)blk * 2 * nb * nb, nb, sd, rk, ldv, sv, zero, rk, ldv, sv,
-                  nodes, st);
-    const int rest = n - k0 - kb;
-    if (rest > 0)
-      zgemm_batched(rest, m, kb, mone, lu + (k0 + kb) + (int64_t)k0 * n, n, stride, rk, ldv, sv, one,
-                    w + k0 + kb, ldv, sv, nodes, st);
+  for (int K0 = 0; K0 < n; K0 += kSolveNbo) {  // L: forward
+    const int K1 = std::min(K0 + kSolveNbo, n);
+    for (int blk = K0 / nb; blk * nb < K1; ++blk) {
+      const int k0 = blk * nb, kb = std::min(nb, n - k0);
+      double2* rk = w + k0;
+      zgemm_batched(kb, m, kb, one, dinv + (int64_t)blk * 2 * nb * nb, nb, sd, rk, ldv, sv, zero, rk, ldv, sv,
+                    nodes, st);
+      const int rest = K1 - k0 - kb;
+      if (rest > 0)
+        zgemm_batched(rest, m, kb, mone, lu + (k0 + kb) + (int64_t)k0 * n, n, stride, rk, ldv, sv, one,
+                      w + k0 + kb, ldv, sv, nodes, st);
+    }
+    if (n - K1 > 0)
+      zgemm_batched(n - K1, m, K1 - K0, mone, lu + K1 + (int64_t)K0 * n, n, stride, w + K0, ldv, sv, one, w + K1,
+                    ldv, sv, nodes, st);
   }
-  for (int blk = nblk - 1; blk >= 0; --blk) {
-    const int k0 = blk * nb, kb = std::min(nb, n - k0);
-    double2* rk = w + k0;
-    zgemm_batched(kb, m, kb, one, dinv + (int64_t)blk * 2 * nb * nb + nb * nb, nb, sd, rk, ldv, sv, zero, rk,
-                  ldv, sv, nodes, st);
-    if (k0 > 0)
-      zgemm_batched(k0, m, kb, mone, lu + (int64_t)k0 * n, n, stride, rk, ldv, sv, one, w, ldv, sv, nodes, st);
+  for (int K1 = n; K1 > 0;) {  // U: backward
+    const int K0 = ((K1 - 1) / kSolveNbo) * kSolveNbo;
+    for (int blk = (K1 - 1) / nb; blk * nb >= K0 && blk >= 0; --blk) {
+      const int k0 = blk * nb, kb = std::min(nb, n - k0);
+      double2* rk = w + k0;
+      zgemm_batched(kb, m, kb, one, dinv + (int64_t)blk * 2 * nb * nb + nb * nb, nb, sd, rk, ldv, sv, zero, rk,
+                    ldv, sv, nodes, st);
+      if (k0 > K0)
+        zgemm_batched(k0 - K0, m, kb, mone, lu + K0 + (int64_t)k0 * n, n, stride, rk, ldv, sv, one, w + K0, ldv, sv,
+                      nodes, st);
+    }
+    if (K0 > 0)
+      zgemm_batched(K0, m, K1 - K0, mone, lu + (int64_t)K0 * n, n, stride, w + K0, ldv, sv, one, w, ldv, sv, nodes,
+                    st);
+    K1 = K0;
   }
 }
 
