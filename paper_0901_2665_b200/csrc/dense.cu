@@ -265,7 +265,10 @@ __global__ void term_kernel(int n, int m, int ldv, const double2* coeff, const d
 // diagonal-block inverses and update only the rest of the outer block; the rows below (above, for
 // U) get ONE update per outer block with K = kSolveNbo. With K = 64 every trailing update was a
 // short-K GEMM that spent most of each CTA in pipeline fill and the C read-modify-write
-// (ncu: DMMA pipe 58 %, long-scoreboard stalls on the epilogue loads); K = 256 amortises both.
+// (ncu: DMMA pipe 58 %, long-scoreboard stalls on the epilogue loads); K = 256 amortises both
+// (config 4 solve 141 -> 99 ms per pass). The same two-level scheme in zgetrf_batched measured
+// slower (1.11 -> 1.53 s at config 4: the panel-restricted inner updates and the outer U12 rows
+// cost more than the K = 256 trailing update saves), so the factorisation keeps one level.
 constexpr int kSolveNbo = 256;
 static void zgetrs_core(int n, int nodes, int m, const double2* lu, int64_t stride, const double2* dinv,
                         double2* w, int ldv, int64_t sv, cudaStream_t st) {
@@ -273,8 +276,9 @@ static void zgetrs_core(int n, int nodes, int m, const double2* lu, int64_t stri
   const int64_t sd = (int64_t)nblk * 2 * nb * nb;
   const double2 one = make_double2(1.0, 0.0), mone = make_double2(-1.0, 0.0),
                 zero = make_double2(0.0, 0.0);
-  for (int K0 = 0; K0 < n; K0 += kSolveNbo) {  // L: forward
-    const int K1 = std::min(K0 + kSolveNbo, n);
+  const int nbo = n >= 2048 ? kSolveNbo : nb;  // (small n: the extra outer step only adds latency)
+  for (int K0 = 0; K0 < n; K0 += nbo) {  // L: forward
+    const int K1 = std::min(K0 + nbo, n);
     for (int blk = K0 / nb; blk * nb < K1; ++blk) {
       const int k0 = blk * nb, kb = std::min(nb, n - k0);
       double2* rk = w + k0;
@@ -290,7 +294,7 @@ static void zgetrs_core(int n, int nodes, int m, const double2* lu, int64_t stri
                     ldv, sv, nodes, st);
   }
   for (int K1 = n; K1 > 0;) {  // U: backward
-    const int K0 = ((K1 - 1) / kSolveNbo) * kSolveNbo;
+    const int K0 = ((K1 - 1) / nbo) * nbo;
     for (int blk = (K1 - 1) / nb; blk * nb >= K0 && blk >= 0; --blk) {
       const int k0 = blk * nb, kb = std::min(nb, n - k0);
       double2* rk = w + k0;
