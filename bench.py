@@ -296,6 +296,23 @@ def secondary_config(F, name, args, local, world, rank, dist, flush):
         out["note"] = (f"config-5 sample: L = {L} of {full_L} layers; contour solves, projections and "
                        f"X = Q Phi scale linearly in L (x{full_L // L} at full size), the reduced "
                        f"eigensolve (M0 = 768) does not")
+        # the full config on ONE GPU cannot keep 16 nodes' factors (25.7 GB each) resident: its memory
+        # plan streams node batches of one and refactors every pass; the same plan on the sample
+        if world == 1:
+            ctx = comm_context(F, local, world, rank, dist)
+            ctx.set_node_batch(1)
+            ctx.set_pencil(prob.a, prob.b)
+            ctx.prepare(prob.emin, prob.emax, prob.n_e)
+            ctx.bench_init(prob.m0, prob.seed)
+            ctx.bench_passes(1, 0)
+            ms1, ph1 = ctx.bench_passes(2, 0)
+            ctx.close()
+            out["streamed_node_batches"] = {
+                "ms_per_pass_sample": ms1 / 2, "contour_ms_per_pass_sample": ph1[0] / 2,
+                "ms_per_pass_full_size_estimate": ms1 / 2 * full_L / L,
+                "method": f"set_node_batch(1): every pass refactors each node and sweeps it (2 passes timed); "
+                          f"the full-size estimate scales the sample's pass by {full_L // L} (factor and "
+                          f"sweep are linear in the layer count; the reduced eigensolve is a small part)"}
     return out
 
 

@@ -53,6 +53,8 @@ struct ZgemmArgs {
   double2* c;
   int ldc;
   int64_t sc;
+  int splits = 1;  // split-K: blockIdx.z = batch * splits + slice; slice s covers K [s ksplit, ..)
+  int ksplit = 0;
 };
 
 __global__ void __launch_bounds__(256, 2) zgemm_kernel(ZgemmArgs p) {
@@ -61,10 +63,13 @@ __global__ void __launch_bounds__(256, 2) zgemm_kernel(ZgemmArgs p) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
   const int wm = warp & 1, wn = warp >> 1;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const double2* A = p.a + blockIdx.z * p.sa;
-  const double2* B = p.b + blockIdx.z * p.sb;
-  double2* C = p.c + blockIdx.z * p.sc;
-  const int nk = (p.k + BK - 1) / BK;
+  const int bz = blockIdx.z / p.splits, ks = blockIdx.z % p.splits;
+  const int kbeg = ks * p.ksplit;
+  const double2* A = p.a + bz * p.sa + (int64_t)kbeg * p.lda;
+  const double2* B = p.b + bz * p.sb + kbeg;
+  double2* C = p.c + blockIdx.z * p.sc;  // (split-K: slot of this batch entry and slice)
+  const int kloc = p.splits > 1 ? min(p.ksplit, p.k - kbeg) : p.k;
+  const int nk = (kloc + BK - 1) / BK;
 
   auto load = [&](int kt) {
     if (kt < nk) {
@@ -76,7 +81,7 @@ __global__ void __launch_bounds__(256, 2) zgemm_kernel(ZgemmArgs p) {
       for (int r = 0; r < 4; ++r) {
         const int e = tid + r * 256;
         const int mm = e & (BM - 1), kk = e >> 6;
-        const bool v = (m0 + mm < p.m) && (k0 + kk < p.k);
+        const bool v = (m0 + mm < p.m) && (k0 + kk < kloc);
         const double2* src = v ? A + (m0 + mm) + (int64_t)(k0 + kk) * p.lda : A;
         cp_async16_zfill(As + kk * SA + mm, src, v);
       }
@@ -85,7 +90,7 @@ __global__ void __launch_bounds__(256, 2) zgemm_kernel(ZgemmArgs p) {
       for (int r = 0; r < 4; ++r) {
         const int e = tid + r * 256;
         const int kk = e & (BK - 1), nn = e >> 4;
-        const bool v = (n0 + nn < p.n) && (k0 + kk < p.k);
+        const bool v = (n0 + nn < p.n) && (k0 + kk < kloc);
         const double2* src = v ? B + (k0 + kk) + (int64_t)(n0 + nn) * p.ldb : B;
         cp_async16_zfill(Bs + nn * SB + kk, src, v);
       }
@@ -144,6 +149,44 @@ __global__ void __launch_bounds__(256, 2) zgemm_kernel(ZgemmArgs p) {
   }
 }
 
+// C = alpha sum_s P_s + beta C over the split-K slots P (m x n, ld m, slot (batch, slice)),
+// slices added in order (deterministic)
+__global__ void zsplitk_reduce_kernel(const double2* __restrict__ w, int splits, int m, int n, double2 alpha,
+                                      double2 beta, double2* c, int ldc, int64_t sc) {
+  const int bz = blockIdx.y;
+  const int64_t slot = (int64_t)m * n, total = slot;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % m, j = e / m;
+    const double2* src = w + (int64_t)bz * splits * slot + e;
+    double2 acc = src[0];
+    for (int s = 1; s < splits; ++s) acc = cadd(acc, src[s * slot]);
+    double2* cp = c + bz * sc + i + j * ldc;
+    double2 out = cmul(alpha, acc);
+    if (beta.x != 0.0 || beta.y != 0.0) out = cadd(out, cmul(beta, *cp));
+    *cp = out;
+  }
+}
+
+// split-K workspace, per device, grown on demand from the stream-ordered pool (never freed)
+static double2* zsplitk_ws(size_t count, cudaStream_t st) {
+  static double2* ws[16] = {};
+  static size_t cap[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 16) return nullptr;
+  if (cap[dev] < count) {
+    if (ws[dev]) cudaFreeAsync(ws[dev], st);
+    ws[dev] = nullptr;
+    cap[dev] = 0;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&ws[dev]), sizeof(double2) * count, st) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    cap[dev] = count;
+  }
+  return ws[dev];
+}
+
 cudaError_t zgemm_batched(int m, int n, int k, double2 alpha, const double2* a, int lda, int64_t sa,
                           const double2* b, int ldb, int64_t sb, double2 beta, double2* c, int ldc,
                           int64_t sc, int batch, cudaStream_t st) {
@@ -153,6 +196,30 @@ cudaError_t zgemm_batched(int m, int n, int k, double2 alpha, const double2* a, 
   if (!attr) {
     cudaFuncSetAttribute(zgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
+  }
+  // split-K when one batch entry's tile grid is small (the block factor's b x b products: 16 tiles
+  // at b = 256, 64 at b = 512) and K is long enough: with a few nodes (streamed node batches, one
+  // node per GPU) the plain grid leaves most SMs idle. The slice count depends on the per-entry
+  // shape only, never on the batch, so resident and streamed node plans stay bit-identical.
+  const int tiles = ((n + zg::BN - 1) / zg::BN) * ((m + zg::BM - 1) / zg::BM);
+  int splits = 1;
+  if (tiles < 74 && k >= 128) splits = std::min({(148 + tiles - 1) / tiles, k / 64, 8});
+  if (splits > 1) {
+    const int ksplit = ((k + splits - 1) / splits + zg::BK - 1) / zg::BK * zg::BK;
+    splits = (k + ksplit - 1) / ksplit;
+    const int64_t slot = (int64_t)m * n;
+    double2* w = zsplitk_ws((size_t)slot * splits * batch, st);
+    if (w) {
+      ZgemmArgs p{m, n, k, make_double2(1.0, 0.0), make_double2(0.0, 0.0), a, lda, sa, b, ldb, sb, w, m, slot,
+                  splits, ksplit};
+      dim3 grid((n + zg::BN - 1) / zg::BN, (m + zg::BM - 1) / zg::BM, batch * splits);
+      zgemm_kernel<<<grid, 256, smem, st>>>(p);
+      ++g_launches;
+      dim3 rg((unsigned)std::min<int64_t>((slot + 255) / 256, 1024), batch);
+      zsplitk_reduce_kernel<<<rg, 256, 0, st>>>(w, splits, m, n, alpha, beta, c, ldc, sc);
+      ++g_launches;
+      return cudaGetLastError();
+    }
   }
   ZgemmArgs p{m, n, k, alpha, beta, a, lda, sa, b, ldb, sb, c, ldc, sc};
   dim3 grid((n + zg::BN - 1) / zg::BN, (m + zg::BM - 1) / zg::BM, batch);
