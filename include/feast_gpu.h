@@ -209,6 +209,14 @@ int feast_gpu_set_factor_policy(feast_gpu_ctx* ctx, int policy);
  * next factorisation. */
 int feast_gpu_set_twist(feast_gpu_ctx* ctx, int enable);
 
+/* SPIKE partitioning of the block-Thomas chain (b <= 32): chunks = P cuts each node's L layers
+ * into P independently factored and swept chunks (P times more parallel chains, P times shorter),
+ * with the couplings restored through spikes, a reduced system of 2 (P - 1) b unknowns per node
+ * and a GEMM correction (spike.cu). 0 = automatic, 1 = off; P must be a power of two; it is
+ * reduced until it divides L with at least 8 layers per chunk. Takes effect at the next
+ * factorisation; the solves agree with the unpartitioned ones to rounding. */
+int feast_gpu_set_spike(feast_gpu_ctx* ctx, int chunks);
+
 /* random_block<double> (core.hpp:84-106) generated on the device: out (host, n*m column-major)
  * = 2 * ((w >> 11) * 2^-53) - 1 over the std::mt19937_64(seed) words w, bit-identical to the
  * reference's host generator. feast_gpu_solve draws its initial block this way. */

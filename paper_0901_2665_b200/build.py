@@ -15,7 +15,7 @@ OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libfeastgpu.so")
 SOURCES = ["blocktri.cu", "sweep.cu", "sweep_small.cu", "sweep_tma.cu", "gemm.cu", "band_apply.cu",
            "dense.cu", "chol.cu", "chol_tiles.cu", "eig.cu", "tridiag.cu", "tridiag_tiles.cu",
-           "tri_back.cu", "misc.cu", "csr_ingest.cu", "bicgstab.cu", "feast_gpu.cpp"]
+           "tri_back.cu", "misc.cu", "csr_ingest.cu", "bicgstab.cu", "spike.cu", "feast_gpu.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMPILE_FLAGS = [*ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC"]
 LINK_FLAGS = [*ARCH, "-shared", "-cudart", "static", "-Xlinker", "-soname=libfeastgpu.so"]

@@ -229,12 +229,16 @@ __global__ void __launch_bounds__(FacShape<B>::NT) bt_factor_small_kernel(BtFact
   constexpr bool RAW = Sh::RAW_SMEM;
   constexpr size_t BB = (size_t)B * B;
   const bool tw = a.kmid >= 0;
-  const int node = tw ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int node = tw ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;  // factor slot (node, chunk)
   const int half = tw ? (int)(blockIdx.x & 1) : 0;
   const int L = a.L, kmid = tw ? a.kmid : L - 1;
   const int nsteps = half == 0 ? kmid + 1 : L - 1 - kmid;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const double2 z = a.z[node];
+  const double2 z = a.z[node / a.chunks];
+  // this chunk's layers of the pencil (chunks == 1: the whole chain)
+  const size_t lay0 = (size_t)(node % a.chunks) * L;
+  const double2* abdiag = a.abdiag + lay0 * BB;
+  const double2* ablow = a.ablow + lay0 * BB;
   extern __shared__ __align__(16) double2 fsm[];
   double2* Sv = fsm;                  // B x LDS: S, then S^{-1}
   double2* Gp = Sv + B * LDS;         // B x LDS: G of the previous layer (B operand of the S update)
@@ -254,11 +258,11 @@ __global__ void __launch_bounds__(FacShape<B>::NT) bt_factor_small_kernel(BtFact
   auto prefetch = [&](int r) {
     if (RAW && r < nsteps) {
       const int l = layer_of(r);
-      const double2* d = a.abdiag + (size_t)l * BB;
+      const double2* d = abdiag + (size_t)l * BB;
       double2* dd = rawD + (r & 1) * BB;
       for (int e = tid; e < (int)BB; e += NT) cp_async16(dd + e, d + e);
       if (has_out(l)) {
-        const double2* c = a.ablow + (size_t)(half == 0 ? l : l - 1) * BB;
+        const double2* c = ablow + (size_t)(half == 0 ? l : l - 1) * BB;
         double2* cd = rawC + (r % 3) * BB;
         for (int e = tid; e < (int)BB; e += NT) cp_async16(cd + e, c + e);
       }
@@ -272,14 +276,14 @@ __global__ void __launch_bounds__(FacShape<B>::NT) bt_factor_small_kernel(BtFact
     prefetch(r + 1);
     cp_async_wait<1>();
     __syncthreads();
-    const double2* dsrc = RAW ? rawD + (r & 1) * BB : a.abdiag + (size_t)l * BB;
+    const double2* dsrc = RAW ? rawD + (r & 1) * BB : abdiag + (size_t)l * BB;
     // raw (A, B) pairs of the in / out couplings (as stored: C_c = M(c+1, c), col-major)
     const double2* cin = r == 0 ? nullptr
                          : RAW ? rawC + ((r + 2) % 3) * BB
-                               : a.ablow + (size_t)(half == 0 ? l - 1 : l) * BB;
+                               : ablow + (size_t)(half == 0 ? l - 1 : l) * BB;
     const double2* cout = !has_out(l) ? nullptr
                           : RAW ? rawC + (r % 3) * BB
-                                : a.ablow + (size_t)(half == 0 ? l : l - 1) * BB;
+                                : ablow + (size_t)(half == 0 ? l : l - 1) * BB;
     // top: Cin = C_{l-1}, Cout = C_l^T ; bottom: Cin = C_l^T, Cout = C_{l-1}
     auto Ci = [&](int i, int t) { return czb(half == 0 ? cin[i + t * B] : cin[t + i * B], z); };
     auto Co = [&](int i, int t) { return czb(half == 0 ? cout[t + i * B] : cout[i + t * B], z); };

@@ -353,6 +353,12 @@ struct feast_gpu_ctx {
   DevBuf<BicgCol> bcol;
   DevBuf<int> bflag;
   DevBuf<double2> bz;
+  // SPIKE partitioning of the block-Thomas chain (spike.cu, b <= 32): requested chunk count
+  // (feast_gpu_set_spike; 0 = automatic) and the one the current factors use
+  int spike_req = 0, spike = 1;
+  DevBuf<double2> spk, rlu, rdinv, rz, rzs;  // spikes [V | W], reduced LU, its block inverses, reduced RHS
+  DevBuf<double> sra, rzr;                  // correction operands [Re cV | -Im cV | Re cW | -Im cW], z parts
+  DevBuf<int> ripiv, rperm;
   bool hermitian = false;  // set_pencil_hermitian: the doubled real pencil of a complex one
   int nz = 0;              // its complex dimension
   bool twist = true;  // two-ended block-Thomas recursion where it applies (feast_gpu_set_twist)
@@ -1265,6 +1271,87 @@ void plan_batch(feast_gpu_ctx* c, int m) {
   c->batch = (size_t)own * per <= avail ? own : (int)std::max<size_t>(1, avail / per);
 }
 
+constexpr int kSpikeAuto = 1;  // automatic chunk count (measured)
+
+// SPIKE chunk count for the current pencil: requested (feast_gpu_set_spike) or automatic, a power
+// of two dividing L with at least 8 layers per chunk (b <= 32 only: the bulk-copy sweep)
+int spike_chunks(const feast_gpu_ctx* c) {
+  if (!c->blocktri || c->b > 32 || c->inner_kind != 0) return 1;
+  int P = c->spike_req > 0 ? c->spike_req : kSpikeAuto;
+  while (P > 1 && (c->L % P != 0 || c->L / P < 8)) P /= 2;
+  return std::max(P, 1);
+}
+
+// the SPIKE data of owned nodes [s0, s0 + cnt) (factor slots 0..cnt-1): spikes V, W by one complex
+// sweep of the chunks, the reduced matrix and its LU, the correction operand (spike.cu)
+void spike_factor(feast_gpu_ctx* c, int s0, int cnt) {
+  const int P = c->spike, Lc = c->L / P, b = c->b, slots = c->wnodes();
+  const int nr = 2 * (P - 1) * b, nblk = (nr + kDenseNb - 1) / kDenseNb;
+  const int64_t ld = c->npad;
+  c->spk.ensure((size_t)slots * ld * 2 * b);
+  CK(spike_rhs(c->L, b, P, cnt, c->ablow.p, c->dz.p + s0, c->spk.p, ld, c->stream));
+  BtSweepArgs sa{Lc, b, cnt * P, 2 * b, (int)ld, c->ablow.p, c->dz.p + s0, c->dcoeff.p + s0, c->sinv.p, c->gfac.p,
+                 c->hfac.p, nullptr, nullptr, c->spk.p, 1, c->kmid};
+  sa.chunks = P;
+  CK(bt_sweep(sa, c->stream));
+  c->rlu.ensure((size_t)slots * nr * nr);
+  c->rdinv.ensure((size_t)slots * nblk * 2 * kDenseNb * kDenseNb);
+  c->ripiv.ensure((size_t)slots * nr);
+  c->rperm.ensure((size_t)slots * nr);
+  CK(spike_reduced(c->L, b, P, cnt, c->spk.p, ld, c->rlu.p, c->stream));
+  CK(zgetrf_batched(nr, cnt, c->rlu.p, (int64_t)nr * nr, c->ripiv.p, c->rperm.p, c->rdinv.p, c->fstatus.p, c->stream));
+  c->sra.ensure((size_t)slots * ld * 4 * b);
+  CK(spike_coef(b, cnt, c->spk.p, ld, c->dcoeff.p + s0, c->sra.p, c->stream));
+}
+
+// block-Thomas solves (b <= 32) of owned nodes [sn, sn + cnt) held in factor slots [slot, slot + cnt)
+// for m right-hand sides: real mode (y -> T = Re(c x)) or complex mode (W in place), with the SPIKE
+// reduced system and correction when the factors are chunked. w / t are the first node's blocks
+// (ld npad, node stride npad m).
+void bt_solve(feast_gpu_ctx* c, int sn, int slot, int cnt, int m, const double* y, double* t, double2* w,
+              int complex_mode) {
+  const int P = c->spike, Lc = c->L / P, b = c->b;
+  const size_t bb = (size_t)b * b;
+  const size_t cs0 = (size_t)slot * P;  // first chunk slot
+  BtSweepArgs a{Lc, b, cnt * P, m, c->npad, c->ablow.p, c->dz.p + sn, c->dcoeff.p + sn, c->sinv.p + cs0 * Lc * bb,
+                c->gfac.p + cs0 * (Lc > 1 ? Lc - 1 : 0) * bb, c->hfac.p + cs0 * (Lc > 1 ? Lc - 1 : 0) * bb, y, t, w,
+                complex_mode, c->kmid};
+  a.chunks = P;
+  CK(bt_sweep(a, c->stream));
+  if (P == 1) return;
+  const int nr = 2 * (P - 1) * b, nblk = (nr + kDenseNb - 1) / kDenseNb;
+  const int64_t ld = c->npad;
+  const double2* rlu = c->rlu.p + (size_t)slot * nr * nr;
+  c->rz.ensure((size_t)cnt * nr * m);
+  c->rzs.ensure((size_t)cnt * nr * m);
+  CK(spike_gather(c->L, b, P, cnt, w, ld, m, c->rz.p, c->stream));
+  CK(zgetrs_batched(nr, cnt, m, rlu, (int64_t)nr * nr, c->rperm.p + (size_t)slot * nr,
+                    c->rdinv.p + (size_t)slot * nblk * 2 * kDenseNb * kDenseNb, c->rz.p, nr, c->rzs.p, c->stream));
+  if (!complex_mode) {  // T_c -= [Re cV | -Im cV | Re cW | -Im cW] [Re v; Im v; Re u; Im u]
+    c->rzr.ensure((size_t)cnt * 4 * b * m * P);
+    CK(spike_zops(b, P, cnt, c->rz.p, m, c->rzr.p, c->stream));
+    const double* ra = c->sra.p + (size_t)slot * ld * 4 * b;
+    for (int cc = 0; cc < P; ++cc)
+      CK(dgemm_batched(false, Lc * b, m, 4 * b, -1.0, ra + (size_t)cc * Lc * b, (int)ld, ld * 4 * b,
+                       c->rzr.p + (size_t)cc * 4 * b * m, 4 * b, (int64_t)P * 4 * b * m, 1.0, t + (size_t)cc * Lc * b,
+                       (int)ld, ld * m, cnt, c->stream));
+    return;
+  }
+  // complex: W_c -= V_c v_c + W_c u_{c-1}
+  const double2 one = make_double2(1.0, 0.0), mone = make_double2(-1.0, 0.0);
+  const double2* spk = c->spk.p + (size_t)slot * ld * 2 * b;
+  for (int cc = 0; cc < P; ++cc) {
+    double2* wc = w + (size_t)cc * Lc * b;
+    const double2* sv = spk + (size_t)cc * Lc * b;
+    if (cc <= P - 2)
+      CK(zgemm_batched(Lc * b, m, b, mone, sv, (int)ld, ld * 2 * b, c->rz.p + (size_t)(2 * cc + 1) * b, nr,
+                       (int64_t)nr * m, one, wc, (int)ld, ld * m, cnt, c->stream));
+    if (cc >= 1)
+      CK(zgemm_batched(Lc * b, m, b, mone, sv + ld * b, (int)ld, ld * 2 * b, c->rz.p + (size_t)(2 * cc - 2) * b, nr,
+                       (int64_t)nr * m, one, wc, (int)ld, ld * m, cnt, c->stream));
+  }
+}
+
 // factors of owned nodes [s0, s0 + cnt) into factor slots 0..cnt-1
 void factor_range(feast_gpu_ctx* c, int s0, int cnt) {
   c->fstatus.ensure(1);
@@ -1276,9 +1363,13 @@ void factor_range(feast_gpu_ctx* c, int s0, int cnt) {
     c->gfac.ensure(std::max<size_t>(slots * (c->L - 1) * bb, 1));
     c->hfac.ensure(std::max<size_t>(slots * (c->L - 1) * bb, 1));
     if (c->b >= 128) c->fwork.ensure(bt_factor_work_elems(c->b, cnt));
-    BtFactorArgs a{c->L, c->b, cnt, c->abdiag.p, c->ablow.p, c->dz.p + s0, c->sinv.p, c->gfac.p, c->hfac.p,
-                   c->scratch.p, c->fstatus.p, c->fwork.p, c->kmid = bt_twist_layer(c->L, c->b, c->twist)};
+    const int P = c->spike = spike_chunks(c);
+    const int Lc = c->L / P;
+    BtFactorArgs a{Lc, c->b, cnt * P, c->abdiag.p, c->ablow.p, c->dz.p + s0, c->sinv.p, c->gfac.p, c->hfac.p,
+                   c->scratch.p, c->fstatus.p, c->fwork.p, c->kmid = bt_twist_layer(Lc, c->b, c->twist)};
+    a.chunks = P;
     CK(bt_factor(a, c->stream));
+    if (P > 1) spike_factor(c, s0, cnt);
     if (!c->streamed()) c->fwork.release();  // transient unless it is reused every pass
   } else {
     const int n = c->n, nb = kDenseNb, nblk = (n + nb - 1) / nb, slots = c->wnodes();
@@ -1377,7 +1468,9 @@ void contour_pass(feast_gpu_ctx* c, int m, const double* y, double* q, cudaEvent
     for (int s0 = 0; s0 < own; s0 += nbt) {
       const int cnt = std::min(nbt, own - s0);
       if (c->res0 != s0 || c->rescnt != cnt) factor_range(c, s0, cnt);
-      if (c->blocktri) {
+      if (c->blocktri && c->b <= 32) {
+        bt_solve(c, s0, 0, cnt, m, y, c->T.p, c->W.p, 0);
+      } else if (c->blocktri) {
         BtSweepArgs a{c->L, c->b, cnt, m, c->npad, c->ablow.p, c->dz.p + s0, c->dcoeff.p + s0, c->sinv.p,
                       c->gfac.p, c->hfac.p, y, c->T.p, c->W.p, 0, c->kmid};
         CK(bt_sweep(a, c->stream));
@@ -1483,9 +1576,7 @@ void contour_pass_hermitian(feast_gpu_ctx* c, int m) {
       } else {
         CK(real_to_complex_slots(c->Y.p, c->npad, m2, cnt, c->W.p, c->stream));
         if (c->blocktri) {
-          BtSweepArgs a{c->L, c->b, cnt, m2, c->npad, c->ablow.p, c->dz.p + s0, c->dcoeff.p + s0, c->sinv.p,
-                        c->gfac.p, c->hfac.p, nullptr, nullptr, c->W.p, 1, c->kmid};
-          CK(bt_sweep(a, c->stream));
+          bt_solve(c, s0, 0, cnt, m2, nullptr, nullptr, c->W.p, 1);
         } else {
           DenseSolveArgs a{c->n, cnt, m2, c->npad, c->lu.p, c->perm.p, c->dinv.p, c->dcoeff.p + s0, nullptr, c->T.p,
                            c->W.p, 1};
@@ -2455,7 +2546,7 @@ void feast_gpu_destroy(feast_gpu_ctx* c) {
   cudaStreamSynchronize(c->stream);
   AllocStream as(c->stream);
   for (DevBuf<double>* d : {&c->A, &c->Bm, &c->Y, &c->Q, &c->X, &c->AQ, &c->BQ, &c->T, &c->gw, &c->Aq, &c->Bq,
-                            &c->Cm, &c->Lm, &c->Phi, &c->Ev, &c->Vm, &c->S, &c->Tm, &c->Dv, &c->Aband, &c->Bband, &c->csr, &c->G, &c->breal, &c->A0, &c->Sop})
+                            &c->Cm, &c->Lm, &c->Phi, &c->Ev, &c->Vm, &c->S, &c->Tm, &c->Dv, &c->Aband, &c->Bband, &c->csr, &c->G, &c->breal, &c->A0, &c->Sop, &c->sra, &c->rzr})
     d->release();
   c->csrstats.release();  // every buffer, before the stream goes (the destructor would free on a dead stream)
   c->kfac.release();
@@ -2466,6 +2557,9 @@ void feast_gpu_destroy(feast_gpu_ctx* c) {
   c->bvec.release();
   c->bz.release();
   c->bcol.release();
+  for (DevBuf<double2>* d : {&c->spk, &c->rlu, &c->rdinv, &c->rz, &c->rzs}) d->release();
+  c->ripiv.release();
+  c->rperm.release();
   cudaStreamSynchronize(c->stream);  // the frees above are stream-ordered
   if (c->eig) eig_destroy(c->eig);
   for (auto& e : c->ev)
@@ -2633,7 +2727,9 @@ int feast_gpu_solve_shift(feast_gpu_ctx* c, int e, double* rhs, int m, int mode)
                          cudaMemcpyHostToDevice, c->stream));
     // (zB - A)^H = conj(zB - A) for real symmetric A, B: solve at conj by conjugating in/out
     if (mode) CK(conj_inplace(w, nv, c->stream));
-    if (c->blocktri) {
+    if (c->blocktri && !split) {
+      bt_solve(c, sn, s, 1, m, nullptr, nullptr, w, 1);
+    } else if (c->blocktri) {
       const size_t bb = (size_t)c->b * c->b;
       if (split) CK(split_complex(w, c->AQ.p, c->npad, c->npad, m, c->stream));
       BtSweepArgs a{c->L, c->b, 1, split ? 2 * m : m, c->npad, c->ablow.p, c->dz.p + sn, c->dcoeff.p + sn,
@@ -2871,6 +2967,14 @@ int feast_gpu_set_factor_policy(feast_gpu_ctx* c, int policy) {
   return guarded(c, [&] {
     if (policy < 0 || policy > 2) fail(FEAST_EINPUT, "set_factor_policy: policy must be 0 (Auto), 1 (Dense) or 2 (Banded)");
     c->factor_policy = policy;
+  });
+}
+
+int feast_gpu_set_spike(feast_gpu_ctx* c, int chunks) {
+  return guarded(c, [&] {
+    if (chunks < 0 || chunks > 64 || (chunks & (chunks - 1))) fail(FEAST_EINPUT, "set_spike: chunks must be 0 or a power of two <= 64");
+    c->spike_req = chunks;
+    c->factored = false;
   });
 }
 

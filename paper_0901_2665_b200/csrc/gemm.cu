@@ -197,13 +197,14 @@ cudaError_t zgemm_batched(int m, int n, int k, double2 alpha, const double2* a, 
     cudaFuncSetAttribute(zgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  // split-K when one batch entry's tile grid is small (the block factor's b x b products: 16 tiles
-  // at b = 256, 64 at b = 512) and K is long enough: with a few nodes (streamed node batches, one
-  // node per GPU) the plain grid leaves most SMs idle. The slice count depends on the per-entry
-  // shape only, never on the batch, so resident and streamed node plans stay bit-identical.
+  // split-K when the whole grid cannot fill the GPU (the block factor's b x b products with a few
+  // nodes: streamed node batches, one node per GPU) and K is long enough. The slice count is a
+  // function of the per-entry shape only, so two batch sizes that both split use the same slices.
+  // (Splitting a full grid only adds partial-sum traffic: the 16-node b = 512 factor ran 0.78 s
+  // unsplit against 1.33 s split three ways.)
   const int tiles = ((n + zg::BN - 1) / zg::BN) * ((m + zg::BM - 1) / zg::BM);
   int splits = 1;
-  if (tiles < 74 && k >= 128) splits = std::min({(148 + tiles - 1) / tiles, k / 64, 8});
+  if (tiles * batch < 148 && k >= 128) splits = std::min({(148 + tiles - 1) / tiles, k / 64, 8});
   if (splits > 1) {
     const int ksplit = ((k + splits - 1) / splits + zg::BK - 1) / zg::BK * zg::BK;
     splits = (k + ksplit - 1) / ksplit;
@@ -489,9 +490,9 @@ static cudaError_t dgemm_impl(char ta, char tb, int m, int n, int k, double alph
   return cudaGetLastError();
 }
 
-static cudaError_t dgemm_batched(bool TA, int m, int n, int k, double alpha, const double* A, int lda,
-                                 int64_t sa, const double* B, int ldb, int64_t sb, double beta, double* C,
-                                 int ldc, int64_t sc, int batch, cudaStream_t st) {
+cudaError_t dgemm_batched(bool TA, int m, int n, int k, double alpha, const double* A, int lda,
+                          int64_t sa, const double* B, int ldb, int64_t sb, double beta, double* C,
+                          int ldc, int64_t sc, int batch, cudaStream_t st) {
   if (m <= 0 || n <= 0 || batch <= 0) return cudaSuccess;
   DgemmArgs p{m, n, k, k, A, lda, B, ldb, C, ldc, sc, alpha, beta, 1, sa, sb};
   const int smem = dg::NS * dg::STAGE * (int)sizeof(double);

@@ -30,6 +30,10 @@ struct BtFactorArgs {
   int* status;            // set to 1 on a singular block pivot
   double2* work;          // b >= 128: bt_factor_work_elems(b, nodes) double2
   int kmid = -1;          // >= 0: twisted recursion meeting at layer kmid (bt_twist_layer)
+  // SPIKE chunks (b <= 32): `nodes` counts (node, chunk) pairs, chunk c of node e at slot
+  // e * chunks + c holds layers [c L, (c + 1) L) of the pencil (L = layers per chunk), factored as
+  // its own block-tridiagonal system (the couplings between chunks are left to the spikes)
+  int chunks = 1;
 };
 cudaError_t bt_factor(const BtFactorArgs& a, cudaStream_t st);
 // Meeting layer of the twisted (two-ended) block-Thomas recursion for b <= 64 and L >= 4
@@ -60,8 +64,33 @@ struct BtSweepArgs {
   double2* w;             // workspace / complex in-out: nodes * ldv*m
   int complex_mode;
   int kmid = -1;          // the factors' twisted meeting layer (must match bt_factor's)
+  // SPIKE chunks (b <= 32, bt_factor's): slot s = node * chunks + c solves chunk c's rows
+  // [c L b, (c + 1) L b) of node s / chunks's blocks (y, t, w at that row offset of the node's
+  // slot); in real mode the complex x of each chunk's first and last layer also go to w
+  int chunks = 1;
 };
 cudaError_t bt_sweep(const BtSweepArgs& a, cudaStream_t st);
+
+// SPIKE partitioning of the chain (spike.cu): spike right-hand sides, the reduced matrix
+// (nr = 2 (P-1) b per node), the correction operand [Re cV | -Im cV | Re cW | -Im cW], the reduced
+// right-hand sides gathered from the sweep's boundary x, and the per-chunk correction B-operands
+cudaError_t spike_rhs(int L, int b, int P, int nodes, const double2* ablow, const double2* z, double2* spk, int64_t ld,
+                      cudaStream_t st);
+cudaError_t spike_reduced(int L, int b, int P, int nodes, const double2* spk, int64_t ld, double2* R, cudaStream_t st);
+cudaError_t spike_coef(int b, int nodes, const double2* spk, int64_t ld, const double2* coeff, double* ra,
+                       cudaStream_t st);
+cudaError_t spike_gather(int L, int b, int P, int nodes, const double2* w, int64_t ld, int m, double2* rz,
+                         cudaStream_t st);
+cudaError_t spike_zops(int b, int P, int nodes, const double2* rz, int m, double* zr, cudaStream_t st);
+// batched complex GEMM (gemm.cu): C_z = alpha A_z B_z + beta C_z
+cudaError_t zgemm_batched(int m, int n, int k, double2 alpha, const double2* a, int lda, int64_t sa,
+                          const double2* b, int ldb, int64_t sb, double2 beta, double2* c, int ldc,
+                          int64_t sc, int batch, cudaStream_t st);
+// batched dense complex LU / solves (dense.cu), the reduced systems' factorisation
+cudaError_t zgetrf_batched(int n, int nodes, double2* lu, int64_t stride, int* ipiv, int* perm, double2* dinv,
+                           int* status, cudaStream_t st);
+cudaError_t zgetrs_batched(int n, int nodes, int m, const double2* lu, int64_t stride, const int* perm,
+                           const double2* dinv, double2* w, int ldv, double2* scratch, cudaStream_t st);
 
 // Q = -sum_{s} T_s (ascending s), n rows (ld) x m; accumulate: Q -= sum (the next node batch)
 cudaError_t reduce_terms(const double* t, int nodes, int64_t slice, int n, int m, int ld,
@@ -132,6 +161,11 @@ cudaError_t bicg_terms(const double2* x, int nodes, int n, int m, int64_t ld, co
 cudaError_t dgemm(char ta, char tb, int m, int n, int k, double alpha, const double* A, int lda,
                   const double* B, int ldb, double beta, double* C, int ldc, double* work,
                   size_t work_elems, cudaStream_t st);
+
+// batched C_z = alpha op(A_z) B_z + beta C_z (op = T when TA), z < batch, strides sa, sb, sc
+cudaError_t dgemm_batched(bool TA, int m, int n, int k, double alpha, const double* A, int lda, int64_t sa,
+                          const double* B, int ldb, int64_t sb, double beta, double* C, int ldc, int64_t sc,
+                          int batch, cudaStream_t st);
 
 // [S1 | S2] = Q^T [AQ | BQ] (m x 2m, ld m) with S1, S2 symmetric and m a multiple of 64: only
 // the upper tiles of each half are computed; follow with symmetrize_tiles on each half

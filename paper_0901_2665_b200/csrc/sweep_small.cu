@@ -88,12 +88,17 @@ __global__ void __launch_bounds__((SmallShape<B, NC, TPW, TW, CPLX_IN>::NWARPS +
   uint64_t* stepbar = empty + NSTAGE;  // NWARPS arrivals per step
   uint64_t* xbar = stepbar + 1;        // TW: the partner's NWARPS arrivals after its Xb stores
   uint64_t* midbar = xbar + 1;         // TW && CPLX_IN: the bottom passed its middle step
-  const double2 coeff = a.coeff[s];
+  // slot s = node * chunks + chunk (chunks == 1: the node's whole chain)
+  const int node = s / a.chunks;
+  const size_t row0 = (size_t)(s % a.chunks) * L * B;  // the chunk's first row in the node's blocks
+  const bool spike = a.chunks > 1;
+  const double2 coeff = a.coeff[node];
   const double2* sinv = a.sinv + (size_t)s * L * BB;
   const double2* hm = a.h + (size_t)s * (L > 1 ? L - 1 : 0) * BB;
   const double2* gm = a.g + (size_t)s * (L > 1 ? L - 1 : 0) * BB;
-  double2* W = a.w + (size_t)s * ldv * m;
-  double* T = a.complex_mode ? nullptr : a.t + (size_t)s * ldv * m;
+  double2* W = a.w + (size_t)node * ldv * m + row0;
+  double* T = a.complex_mode ? nullptr : a.t + (size_t)node * ldv * m + row0;
+  const double* Yin = a.y ? a.y + row0 : nullptr;
   auto layer_of = [&](int r) { return half == 0 ? r : L - 1 - r; };
 
   for (int i = tid; i < 2 * NC * SV; i += blockDim.x) Vs0[i] = make_double2(0.0, 0.0);
@@ -173,7 +178,7 @@ __global__ void __launch_bounds__((SmallShape<B, NC, TPW, TW, CPLX_IN>::NWARPS +
               asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(W + base + 4 * q),
                            "r"(ok ? 16 : 0));
             else
-              asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(a.y + base + 4 * q),
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(Yin + base + 4 * q),
                            "r"(ok ? 8 : 0));
           }
         }
@@ -293,6 +298,10 @@ __global__ void __launch_bounds__((SmallShape<B, NC, TPW, TW, CPLX_IN>::NWARPS +
     } else {
       if (col < m) T[row + (size_t)col * ldv] = coeff.x * x0.x - coeff.y * x0.y;
       if (col + 1 < m) T[row + (size_t)(col + 1) * ldv] = coeff.x * x1.x - coeff.y * x1.y;
+      if (spike && (l == 0 || l == L - 1)) {  // the chunk's boundary layers: x for the reduced system
+        if (col < m) W[row + (size_t)col * ldv] = x0;
+        if (col + 1 < m) W[row + (size_t)(col + 1) * ldv] = x1;
+      }
     }
   };
 

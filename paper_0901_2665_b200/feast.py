@@ -98,6 +98,7 @@ def load_library(path: str = LIB_PATH):
     L.feast_gpu_random_block.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_uint64, _dp]
     L.feast_gpu_set_node_batch.argtypes = [C.c_void_p, C.c_int]
     L.feast_gpu_set_twist.argtypes = [C.c_void_p, C.c_int]
+    L.feast_gpu_set_spike.argtypes = [C.c_void_p, C.c_int]
     L.feast_gpu_set_lookahead.argtypes = [C.c_void_p, C.c_int, C.c_double]
     L.feast_gpu_set_row_distribution.argtypes = [C.c_void_p, C.c_int]
     L.feast_gpu_set_inner_solver.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_int]
@@ -138,7 +139,7 @@ EXPORTED_SYMBOLS = [
     "feast_gpu_lookahead_count", "feast_gpu_set_row_distribution", "feast_gpu_group_create",
     "feast_gpu_group_destroy", "feast_gpu_set_group", "feast_gpu_set_inner_solver",
     "feast_gpu_set_factor_policy", "feast_gpu_sweep", "feast_gpu_set_pencil_hermitian",
-    "feast_gpu_solve_hermitian",
+    "feast_gpu_solve_hermitian", "feast_gpu_set_spike",
 ]
 
 
@@ -324,6 +325,10 @@ class GpuContext:
 
     def lookahead_count(self) -> int:
         return int(self.L.feast_gpu_lookahead_count(self.h))
+
+    def set_spike(self, chunks: int):
+        """SPIKE partitioning of the block-Thomas chain into `chunks` (0 auto, 1 off; b <= 32)."""
+        self._check(self.L.feast_gpu_set_spike(self.h, int(chunks)))
 
     def set_twist(self, enable: bool):
         """Two-ended block-Thomas recursion (default on) or the plain top-down chain (b <= 64)."""

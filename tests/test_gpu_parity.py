@@ -580,3 +580,54 @@ def test_banded_policy_needs_sparse_operands(F):
             c.set_pencil(prob.a, prob.b)
     finally:
         c.close()
+
+
+# SPIKE partitioning of the chain (spike.cu): chunks factored and swept independently, the
+# couplings restored by spikes + the reduced system + a GEMM correction. Against the reference's
+# pivoted BandedLU solves and accumulate_subspace_real, both with and without the twist inside
+# the chunks.
+@pytest.mark.parametrize("twist", [True, False])
+@pytest.mark.parametrize("L,b,P", [(16, 16, 2), (32, 16, 4), (64, 16, 8), (32, 32, 2), (64, 32, 4)])
+def test_spike_partitioned_solves(F, twist, L, b, P):
+    from paper_0901_2665_b200 import problems as P_
+    a, bb = P_.blocktri_operators(L, b, seed=L * 10 + b + P)
+    emin, emax, ne, m0 = -0.3, 0.4, 8, 20
+    c = F.GpuContext(0)
+    try:
+        c.set_twist(twist)
+        c.set_spike(P)
+        c.set_pencil(a, bb)
+        c.prepare(emin, emax, ne)
+        y = O.random_block(a.n, m0, 5)
+        q = c.contour_pass(y)
+        qr = O.accumulate_real(a, bb, emin, emax, ne, y)
+        assert np.max(np.abs(q - qr)) <= 1e-11 * max(1.0, np.max(np.abs(qr)))
+        z, _ = c.contour()
+        rng = np.random.default_rng(2)
+        rhs = rng.standard_normal((a.n, 3)) + 1j * rng.standard_normal((a.n, 3))
+        for e in (0, ne - 1):
+            for mode in (0, 1):
+                x = c.solve_shift(e, rhs, bool(mode))
+                assert rel(x, O.shift_solve(a, bb, z[e], rhs, mode)) <= 1e-12, (e, mode)
+    finally:
+        c.close()
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_spike_feast_solve_matches_unpartitioned(F, P):
+    from tests.golden_problems import generate
+    prob = generate("cfg2_n2048")
+    out = []
+    for chunks in (1, P):
+        c = F.GpuContext(0)
+        try:
+            c.set_spike(chunks)
+            c.set_pencil(prob.a, prob.b)
+            out.append(c.solve(F.SearchInterval(prob.emin, prob.emax),
+                               F.FeastConfig(m0=prob.m0, n_e=prob.n_e, seed=prob.seed)))
+        finally:
+            c.close()
+    r1, rp = out
+    assert rp.status == r1.status and rp.loops_used == r1.loops_used
+    assert np.all(np.abs(rp.eigenvalues - r1.eigenvalues) <= 1e-10 * np.maximum(np.abs(r1.eigenvalues), 1e-3))
+    assert sin_max_angle(rp.eigenvectors, r1.eigenvectors, prob.b.to_dense()) <= 1e-8
