@@ -1271,13 +1271,24 @@ void plan_batch(feast_gpu_ctx* c, int m) {
   c->batch = (size_t)own * per <= avail ? own : (int)std::max<size_t>(1, avail / per);
 }
 
-constexpr int kSpikeAuto = 1;  // automatic chunk count (measured)
-
-// SPIKE chunk count for the current pencil: requested (feast_gpu_set_spike) or automatic, a power
-// of two dividing L with at least 8 layers per chunk (b <= 32 only: the bulk-copy sweep)
+// SPIKE chunk count for the current pencil: requested (feast_gpu_set_spike), or automatic: the
+// smallest power of two (<= 8) that gives the sweep at least two CTAs per SM. Measured on config 2
+// (tools/spike_sweep.py, profiles/r02_spike_sweep.log): with 8 nodes on one GPU the unpartitioned
+// sweep already has 384 CTAs and the register-heavy CTAs cap residency at ~3 per SM, so P = 4 only
+// shortened it 12 % and its correction cost more; with one node per GPU (8-GPU sharding) the sweep
+// has 48 CTAs and P = 8 is what fills the GPU. Always a power of two dividing L with at least 8
+// layers per chunk (b <= 32 only: the bulk-copy sweep).
 int spike_chunks(const feast_gpu_ctx* c) {
   if (!c->blocktri || c->b > 32 || c->inner_kind != 0) return 1;
-  int P = c->spike_req > 0 ? c->spike_req : kSpikeAuto;
+  int P = c->spike_req;
+  if (P == 0) {
+    const int nc = c->b == 16 ? 8 : 16;  // columns per sweep CTA (sweep_small.cu)
+    const int64_t ctas = (int64_t)std::max(c->owned(), 1) * ((std::max(c->mcap, 1) + nc - 1) / nc) * 2;  // (not the batch: plans agree)
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    P = 1;
+    while (P < 8 && ctas * P < 2 * sms) P *= 2;
+  }
   while (P > 1 && (c->L % P != 0 || c->L / P < 8)) P /= 2;
   return std::max(P, 1);
 }

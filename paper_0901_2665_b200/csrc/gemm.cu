@@ -503,8 +503,12 @@ cudaError_t dgemm_batched(bool TA, int m, int n, int k, double alpha, const doub
     q.b += z0 * sb;
     q.c += z0 * sc;
     dim3 grid((n + dg::BN - 1) / dg::BN, (m + dg::BM - 1) / dg::BM, nz);
-    if (TA) launch_dgemm<true, false>(false, grid, smem, st, q);
-    else launch_dgemm<false, false>(false, grid, smem, st, q);
+    // 16-byte copies when every operand pair stays 16-byte aligned (as in dgemm_impl)
+    const bool v16 = ((TA ? k : m) % 2 == 0) && (k % 2 == 0) && lda % 2 == 0 && ldb % 2 == 0 && sa % 2 == 0 &&
+                     sb % 2 == 0 && (reinterpret_cast<uintptr_t>(q.a) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(q.b) & 15) == 0;
+    if (TA) launch_dgemm<true, false>(v16, grid, smem, st, q);
+    else launch_dgemm<false, false>(v16, grid, smem, st, q);
     ++g_launches;
   }
   return cudaGetLastError();
