@@ -1272,22 +1272,20 @@ void plan_batch(feast_gpu_ctx* c, int m) {
 }
 
 // SPIKE chunk count for the current pencil: requested (feast_gpu_set_spike), or automatic: the
-// smallest power of two (<= 8) that gives the sweep at least two CTAs per SM. Measured on config 2
-// (tools/spike_sweep.py, profiles/r02_spike_sweep.log): with 8 nodes on one GPU the unpartitioned
-// sweep already has 384 CTAs and the register-heavy CTAs cap residency at ~3 per SM, so P = 4 only
-// shortened it 12 % and its correction cost more; with one node per GPU (8-GPU sharding) the sweep
-// has 48 CTAs and P = 8 is what fills the GPU. Always a power of two dividing L with at least 8
-// layers per chunk (b <= 32 only: the bulk-copy sweep).
+// smallest power of two P <= 8 with owned nodes x P >= 8, i.e. the chunking that gives a rank
+// with few nodes (8-GPU sharding: one node per GPU) as many independent chains as eight nodes.
+// Measured on config 2 (tools/spike_sweep.py, profiles/r02_spike_sweep.log): with 8 nodes on one
+// GPU the unpartitioned sweep already has 384 CTAs and its register-heavy CTAs cap residency at
+// ~3 per SM, so P = 4 shortened the sweep only 12 % while its correction cost more; with one node
+// per GPU the sweep has 48 CTAs and P = 8 is what fills the GPU. The rule depends on the node
+// count only (not on M0, unknown at feast_gpu_prepare, nor on the node batch, so every memory plan
+// factors alike). Always a power of two dividing L with at least 8 layers per chunk (b <= 32).
 int spike_chunks(const feast_gpu_ctx* c) {
   if (!c->blocktri || c->b > 32 || c->inner_kind != 0) return 1;
   int P = c->spike_req;
   if (P == 0) {
-    const int nc = c->b == 16 ? 8 : 16;  // columns per sweep CTA (sweep_small.cu)
-    const int64_t ctas = (int64_t)std::max(c->owned(), 1) * ((std::max(c->mcap, 1) + nc - 1) / nc) * 2;  // (not the batch: plans agree)
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     P = 1;
-    while (P < 8 && ctas * P < 2 * sms) P *= 2;
+    while (P < 8 && (int64_t)std::max(c->owned(), 1) * P < 8) P *= 2;
   }
   while (P > 1 && (c->L % P != 0 || c->L / P < 8)) P /= 2;
   return std::max(P, 1);
