@@ -1258,14 +1258,19 @@ void plan_batch(feast_gpu_ctx* c, int m) {
     c->batch = std::min(c->batch_req, std::max(own, 1));
     return;
   }
-  size_t fr = 0, tot = 0;
-  CK(cudaMemGetInfo(&fr, &tot));
-  fr += pool_spare(c->device);
   const size_t have = sizeof(double2) * (c->sinv.n + c->gfac.n + c->hfac.n + c->lu.n + c->W.n) +
                       sizeof(double) * (c->T.n + c->Y.n + c->Q.n + c->X.n + c->AQ.n + c->gw.n);  // already ours
   const size_t nv = (size_t)c->npad * m, mm = (size_t)m * m;
   const size_t fixed = m > 0 ? sizeof(double) * (5 * nv + std::max<size_t>(mm * 64, nv)) : 0;  // Y Q X AQ|BQ gw
   const size_t per = factor_bytes_per_node(c) + (m > 0 ? sizeof(double2) * nv + sizeof(double) * nv * (c->blocktri ? 1 : 2) : 0);
+  // memory freed by earlier contexts stays in the pool: when it (and what this context already
+  // holds) covers every node, skip cudaMemGetInfo (a driver query of ~1 ms on the end-to-end path)
+  size_t fr = pool_spare(c->device);
+  if (0.8 * (double)(fr + have) - (double)fixed < (double)own * (double)per) {
+    size_t dev_free = 0, tot = 0;
+    CK(cudaMemGetInfo(&dev_free, &tot));
+    fr += dev_free;
+  }
   const double budget = 0.8 * (double)(fr + have) - (double)fixed;
   const size_t avail = budget > 0.0 ? (size_t)budget : 0;
   c->batch = (size_t)own * per <= avail ? own : (int)std::max<size_t>(1, avail / per);
