@@ -450,11 +450,8 @@ bool bt_swizzled_factors(int b) { return b == 16 || b == 32; }
 // b = 16, 32 (factors in the swizzled layout, bt_swizzled_factors)
 cudaError_t bt_sweep_small(const BtSweepArgs& a, cudaStream_t st) {
   switch (a.b) {
-    case 16: {
-      // 8 columns per CTA, the 16 rows split over 2 compute warps (measured against 8 x 1 warp,
-      // 16 and 32 columns per CTA with 1-8 warps: DESIGN.md, the bulk-copy pipeline)
-      return launch_bulk_any<16, 8, 1>(a, st);               // 2 warps
-    }
+    case 16:  // 8 columns per CTA on 4 compute warps (re | im split, software-pipelined steps)
+      return bt_sweep_split16(a, st);
     case 32:  // (complex right-hand sides: narrower column blocks keep the ring within 227 KB)
       return a.complex_mode ? launch_bulk_any<32, 8, 1>(a, st) : launch_bulk_any<32, 16, 1>(a, st);
   }
