@@ -72,6 +72,7 @@ struct BtSweepArgs {
 };
 cudaError_t bt_sweep(const BtSweepArgs& a, cudaStream_t st);
 cudaError_t bt_sweep_split16(const BtSweepArgs& a, cudaStream_t st);  // sweep_split.cu (b = 16)
+cudaError_t bt_sweep_pipe16(const BtSweepArgs& a, cudaStream_t st);   // sweep_pipe.cu (b = 16)
 
 // SPIKE partitioning of the chain (spike.cu): spike right-hand sides, the reduced matrix
 // (nr = 2 (P-1) b per node), the correction operand [Re cV | -Im cV | Re cW | -Im cW], the reduced
