@@ -37,9 +37,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAK_FP64_TFLOPS = 37.1  # DMMA m8n8k4 f64, measured on this pool's B200 (profiles/fp64_peak.txt)
-# the contour-solve kernel bench.py's roofline reports (config 2: b = 16, twisted, bulk-copy
-# pipeline, 8-column CTAs; sweep_small.cu) and its DRAM traffic key in profiles/r01_traffic.json
-SWEEP_KERNEL = "bt_sweep_bulk_kernel<16,8,1,0,1>"
+# the contour-solve kernel bench.py's roofline reports (config 2: b = 16, twisted, software-pipelined
+# chain steps, 8-column CTAs; sweep_pipe.cu) and its DRAM traffic key in profiles/traffic.json
+SWEEP_KERNEL = "bt_sweep_pipe_kernel<16,8,0,1>"
 
 
 def peaks():

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libfeastgpu.so")
-SOURCES = ["blocktri.cu", "sweep.cu", "sweep_small.cu", "sweep_split.cu", "sweep_pipe.cu", "sweep_tma.cu", "gemm.cu", "band_apply.cu",
+SOURCES = ["blocktri.cu", "sweep.cu", "sweep_small.cu", "sweep_pipe.cu", "sweep_tma.cu", "gemm.cu", "band_apply.cu",
            "dense.cu", "chol.cu", "chol_tiles.cu", "eig.cu", "tridiag.cu", "tridiag_tiles.cu",
            "tri_back.cu", "misc.cu", "csr_ingest.cu", "bicgstab.cu", "spike.cu", "feast_gpu.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -68,10 +68,8 @@ struct BtSweepArgs {
   // [c L b, (c + 1) L b) of node s / chunks's blocks (y, t, w at that row offset of the node's
   // slot); in real mode the complex x of each chunk's first and last layer also go to w
   int chunks = 1;
-  int dbg = 0;  // TEMP experiment flags
 };
 cudaError_t bt_sweep(const BtSweepArgs& a, cudaStream_t st);
-cudaError_t bt_sweep_split16(const BtSweepArgs& a, cudaStream_t st);  // sweep_split.cu (b = 16)
 cudaError_t bt_sweep_pipe16(const BtSweepArgs& a, cudaStream_t st);   // sweep_pipe.cu (b = 16)
 
 // SPIKE partitioning of the chain (spike.cu): spike right-hand sides, the reduced matrix

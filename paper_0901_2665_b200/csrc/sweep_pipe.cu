@@ -47,8 +47,15 @@ namespace feastgpu {
 template <int B, int NC, bool CPLX_IN, bool TW>
 struct PipeShape {
   static constexpr int MT = B / 8, NT = NC / 8, KQ = B / 4;
-  static constexpr int NCW = MT * NT;        // compute warps: one 8 x 8 complex tile each
-  static constexpr int NTHR = (NCW + 1) * 32;
+  // row tiles per compute warp: all of them for b = 16 (one warp owns a column tile's whole chain:
+  // no block barrier per step, each B fragment feeds both row tiles)
+  static constexpr int TPW = 1;
+  static constexpr int NCW = MT * NT / TPW;  // compute warps
+  // warps of a CTA take consecutive hardware warp slots and slot % 4 picks the SM sub-partition:
+  // pad the CTA to 3 warps (compute, producer, idle) so the compute warps of the 3 CTAs of an SM
+  // land on different sub-partitions (slots 0, 3, 6)
+  static constexpr int NIDLE = NCW == 1 ? 1 : 0;
+  static constexpr int NTHR = (NCW + 1 + NIDLE) * 32;
   static constexpr int NSLOT = 10;           // factor-block ring (even: a forward step takes 2)
   static constexpr int NRHS = NSLOT / 2;     // right-hand-side tiles, one per forward step in flight
   static constexpr int RY = 8;               // lane-private y ring (backward), RY - 1 steps ahead
@@ -60,7 +67,7 @@ struct PipeShape {
   static constexpr size_t BLOCKS = (size_t)NSLOT * BB * 16;
   static constexpr size_t VEC = (size_t)(TW ? 3 : 2) * VBUF * 16;
   static constexpr size_t RHS = (size_t)NRHS * NC * RS * RELB;
-  static constexpr size_t YRING = (size_t)RY * 2 * NCW * 32 * 16;
+  static constexpr size_t YRING = (size_t)RY * 2 * TPW * NCW * 32 * 16;
   static constexpr size_t BARS = 8 * (2 * NSLOT + 2);
   static constexpr size_t smem_bytes() { return BLOCKS + VEC + RHS + YRING + BARS; }
 };
@@ -69,7 +76,7 @@ template <int B, int NC, bool CPLX_IN, bool TW>
 __global__ void __launch_bounds__(PipeShape<B, NC, CPLX_IN, TW>::NTHR, (B == 16 && !CPLX_IN) ? 3 : 1)
     bt_sweep_pipe_kernel(BtSweepArgs a) {
   using Sh = PipeShape<B, NC, CPLX_IN, TW>;
-  constexpr int MT = Sh::MT, KQ = Sh::KQ, NCW = Sh::NCW, NSLOT = Sh::NSLOT, NRHS = Sh::NRHS, RY = Sh::RY;
+  constexpr int MT = Sh::MT, KQ = Sh::KQ, NCW = Sh::NCW, TPW = Sh::TPW, NSLOT = Sh::NSLOT, NRHS = Sh::NRHS, RY = Sh::RY;
   constexpr int SV = Sh::SV, RS = Sh::RS, RELB = Sh::RELB, BB = Sh::BB, VBUF = Sh::VBUF;
   constexpr int NMID = TW ? 3 : 2;
   constexpr int CT = NCW * 32;
@@ -122,6 +129,7 @@ __global__ void __launch_bounds__(PipeShape<B, NC, CPLX_IN, TW>::NTHR, (B == 16 
   __syncthreads();
   if (TW) cg::this_cluster().sync();  // barriers initialised before any remote arrival
 
+  if (warp > NCW) return;  // idle padding warps
   if (warp == NCW) {  // ===================== producer warp =====================
     // One warp, kept to a few dozen instructions per step (its serial instruction latency must
     // stay well under a chain step): all pointers advance incrementally, every lane spins on the
@@ -220,31 +228,39 @@ __global__ void __launch_bounds__(PipeShape<B, NC, CPLX_IN, TW>::NTHR, (B == 16 
   }
 
   // ===================== compute warps =====================
+  // warp wt owns row tiles wt % (MT / TPW) * TPW + j (j < TPW) of column tile wt / (MT / TPW)
+  constexpr int WPC = MT / TPW;  // warps per column tile
   const int wt = warp;
-  const int arow = 8 * (wt % MT) + g;
-  const int aoff = t4 * B + (arow ^ (2 * t4));  // factor blocks: row r of column k at r ^ 2(k & 3)
-  const int bcol = 8 * (wt / MT) + g;
-  const int cl0 = 8 * (wt / MT) + 2 * t4;       // this lane's output columns cl0, cl0 + 1 (row arow)
+  const int ntile = wt / WPC;
+  int arow[TPW], aoff[TPW], vo[TPW];
+  const int bcol = 8 * ntile + g;
+  const int cl0 = 8 * ntile + 2 * t4;           // this lane's output columns cl0, cl0 + 1
+#pragma unroll
+  for (int j = 0; j < TPW; ++j) {
+    arow[j] = 8 * ((wt % WPC) * TPW + j) + g;
+    aoff[j] = t4 * B + (arow[j] ^ (2 * t4));    // factor blocks: row r of column k at r ^ 2(k & 3)
+    vo[j] = cl0 * SV + (arow[j] ^ (cl0 & 6));   // this lane's outputs (second column at + SV)
+  }
   // B fragment of k-step q: vector element (c = bcol, r = 4q + t4) at c SV + (r ^ (c & 6))
   //   = bcol SV + (t4 ^ (bcol & 2)) + 4 (q ^ sw), sw = (bcol >> 2) & 1
   const int sw4 = 4 * ((bcol >> 2) & 1);
   const int vb_e = bcol * SV + (t4 ^ (bcol & 2)) + sw4;  // even q: + 4q
   const int vb_o = bcol * SV + (t4 ^ (bcol & 2)) - sw4;  // odd q : + 4q
-  const int vo = cl0 * SV + (arow ^ (cl0 & 6));           // this lane's outputs (second column at + SV)
-  const bool ok0 = c0 + cl0 < m, ok1 = c0 + cl0 + 1 < m;
-  // W and T at (row arow of layer 0, column c0 + cl0); the next column at + wcol
-  double2* const wbase = W + arow + (size_t)(ok0 ? c0 + cl0 : 0) * ldv;
+  const uint32_t ok0 = c0 + cl0 < m, ok1 = c0 + cl0 + 1 < m;
+  // W and T at (row g of layer 0, column c0 + cl0); row tile j at + 8 j, the next column at + wcol
+  double2* const wbase = W + arow[0] + (size_t)(ok0 ? c0 + cl0 : 0) * ldv;
   const ptrdiff_t wcol = ok1 ? (ptrdiff_t)ldv : 0;
   const double2 coeff = a.coeff[node];
   double* const tbase =
-      CPLX_IN ? nullptr : a.t + (size_t)node * ldv * m + row0 + arow + (size_t)(ok0 ? c0 + cl0 : 0) * ldv;
+      CPLX_IN ? nullptr : a.t + (size_t)node * ldv * m + row0 + arow[0] + (size_t)(ok0 ? c0 + cl0 : 0) * ldv;
   const ptrdiff_t lstep = (ptrdiff_t)dl * B;  // elements per forward layer step
 
   auto bar_step = [&]() {
     if (NCW == 1) __syncwarp();
     else asm volatile("bar.sync 1, %0;\n" ::"n"(CT) : "memory");
   };
-  auto yslot = [&](int u) { return yring + (u & (RY - 1)) * 2 * CT + tid; };  // elements at [0], [CT]
+  // lane-private y ring: element (step u, row tile j, column e) at ((u % RY) (2 TPW) + 2 j + e) CT + tid
+  auto yslot = [&](int u) { return yring + (u & (RY - 1)) * 2 * TPW * CT + tid; };
   static_assert((RY & (RY - 1)) == 0, "RY must be a power of two");
   // y_l of backward step u comes from W (cp.async, issued RY - 1 steps ahead) unless the forward
   // step that produced it is too recent (rb <= (RY - 3) / 2), in which case that step wrote the slot
@@ -254,9 +270,13 @@ __global__ void __launch_bounds__(PipeShape<B, NC, CPLX_IN, TW>::NTHR, (B == 16 
   auto issue_y = [&](int u) {  // called with u = v + RY - 1 for v = 0, 1, ... (yp follows)
     if (u >= H + 1 + NDIRECT && u < nsteps) {
       double2* sl = yslot(u);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(sl)), "l"(yp), "r"(ok0 ? 16 : 0));
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(sl + CT)), "l"(yp + wcol),
-                   "r"(ok1 ? 16 : 0));
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(sl + (2 * j) * CT)),
+                     "l"(yp + 8 * j), "r"(ok0 ? 16 : 0));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(sl + (2 * j + 1) * CT)),
+                     "l"(yp + 8 * j + wcol), "r"(ok1 ? 16 : 0));
+      }
     }
     cp_async_commit();
     yp -= lstep;
@@ -273,8 +293,8 @@ __global__ void __launch_bounds__(PipeShape<B, NC, CPLX_IN, TW>::NTHR, (B == 16 
         for (int e = 0; e < 2; ++e) pr[p][e] = qr[p][e] = pi[p][e] = qi[p][e] = 0.0;
     }
   };
-  Acc acc, nxt;
-  double2 af[KQ];        // A fragments of the dependent product of the current step
+  Acc acc[TPW], nxt[TPW];
+  double2 af[TPW][KQ];   // A fragments of the dependent product of the current step
   int qs = 0, qpar = 0;  // ring slot (and its phase parity) of the next step to prepare
   int cs = 0;            // first ring slot of the current step
   int rt = 0;            // right-hand-side tile of the next step to prepare
@@ -303,32 +323,42 @@ __global__ void __launch_bounds__(PipeShape<B, NC, CPLX_IN, TW>::NTHR, (B == 16 
     if (!ok) mbar_spin(full + slot, qpar);
   };
   auto load_af = [&](int slot) {
-    const double2* Ab = Blk + (size_t)slot * BB + aoff;
 #pragma unroll
-    for (int q = 0; q < KQ; ++q) af[q] = Ab[4 * q * B];
+    for (int j = 0; j < TPW; ++j) {
+      const double2* Ab = Blk + (size_t)slot * BB + aoff[j];
+#pragma unroll
+      for (int q = 0; q < KQ; ++q) af[j][q] = Ab[4 * q * B];
+    }
   };
   // next accumulators = S^{-1} Y from block `slot` and right-hand-side tile rt
   auto rhs_mma = [&](int slot) {
-    const double2* Ab = Blk + (size_t)slot * BB + aoff;
-    nxt.zero();
+#pragma unroll
+    for (int j = 0; j < TPW; ++j) nxt[j].zero();
     if (CPLX_IN) {
       const double2* bp = reinterpret_cast<const double2*>(rhs) + (size_t)rt * NC * RS + bcol * RS + t4;
 #pragma unroll
       for (int q = 0; q < KQ; ++q) {
-        const double2 av = Ab[4 * q * B], bv = bp[4 * q];
-        dmma884(nxt.pr[q & 1][0], nxt.pr[q & 1][1], av.x, bv.x);
-        dmma884(nxt.qr[q & 1][0], nxt.qr[q & 1][1], av.y, bv.y);
-        dmma884(nxt.pi[q & 1][0], nxt.pi[q & 1][1], av.x, bv.y);
-        dmma884(nxt.qi[q & 1][0], nxt.qi[q & 1][1], av.y, bv.x);
+        const double2 bv = bp[4 * q];
+#pragma unroll
+        for (int j = 0; j < TPW; ++j) {
+          const double2 av = Blk[(size_t)slot * BB + aoff[j] + 4 * q * B];
+          dmma884(nxt[j].pr[q & 1][0], nxt[j].pr[q & 1][1], av.x, bv.x);
+          dmma884(nxt[j].qr[q & 1][0], nxt[j].qr[q & 1][1], av.y, bv.y);
+          dmma884(nxt[j].pi[q & 1][0], nxt[j].pi[q & 1][1], av.x, bv.y);
+          dmma884(nxt[j].qi[q & 1][0], nxt[j].qi[q & 1][1], av.y, bv.x);
+        }
       }
     } else {
       const double* bp = reinterpret_cast<const double*>(rhs) + (size_t)rt * NC * RS + bcol * RS + t4;
 #pragma unroll
       for (int q = 0; q < KQ; ++q) {
-        const double2 av = Ab[4 * q * B];
         const double yv = bp[4 * q];
-        dmma884(nxt.pr[q & 1][0], nxt.pr[q & 1][1], av.x, yv);
-        dmma884(nxt.qi[q & 1][0], nxt.qi[q & 1][1], av.y, yv);
+#pragma unroll
+        for (int j = 0; j < TPW; ++j) {
+          const double2 av = Blk[(size_t)slot * BB + aoff[j] + 4 * q * B];
+          dmma884(nxt[j].pr[q & 1][0], nxt[j].pr[q & 1][1], av.x, yv);
+          dmma884(nxt[j].qi[q & 1][0], nxt[j].qi[q & 1][1], av.y, yv);
+        }
       }
     }
     if (++rt == NRHS) rt = 0;
@@ -341,18 +371,21 @@ __global__ void __launch_bounds__(PipeShape<B, NC, CPLX_IN, TW>::NTHR, (B == 16 
   auto vec_mma = [&](const double2 (&bv)[KQ]) {
 #pragma unroll
     for (int q = 0; q < KQ; ++q) {
-      dmma884(acc.pr[q & 1][0], acc.pr[q & 1][1], af[q].x, bv[q].x);
-      dmma884(acc.qr[q & 1][0], acc.qr[q & 1][1], af[q].y, bv[q].y);
-      dmma884(acc.pi[q & 1][0], acc.pi[q & 1][1], af[q].x, bv[q].y);
-      dmma884(acc.qi[q & 1][0], acc.qi[q & 1][1], af[q].y, bv[q].x);
+#pragma unroll
+      for (int j = 0; j < TPW; ++j) {
+        dmma884(acc[j].pr[q & 1][0], acc[j].pr[q & 1][1], af[j][q].x, bv[q].x);
+        dmma884(acc[j].qr[q & 1][0], acc[j].qr[q & 1][1], af[j][q].y, bv[q].y);
+        dmma884(acc[j].pi[q & 1][0], acc[j].pi[q & 1][1], af[j][q].x, bv[q].y);
+        dmma884(acc[j].qi[q & 1][0], acc[j].qi[q & 1][1], af[j][q].y, bv[q].x);
+      }
     }
   };
   // the NEGATED result: -re = Q - P, -im = -(P' + Q')
-  auto fold_neg = [&](double2& n0, double2& n1) {
-    n0.x = (acc.qr[0][0] + acc.qr[1][0]) - (acc.pr[0][0] + acc.pr[1][0]);
-    n0.y = -(acc.pi[0][0] + acc.pi[1][0]) - (acc.qi[0][0] + acc.qi[1][0]);
-    n1.x = (acc.qr[0][1] + acc.qr[1][1]) - (acc.pr[0][1] + acc.pr[1][1]);
-    n1.y = -(acc.pi[0][1] + acc.pi[1][1]) - (acc.qi[0][1] + acc.qi[1][1]);
+  auto fold_neg = [&](const Acc& c, double2& n0, double2& n1) {
+    n0.x = (c.qr[0][0] + c.qr[1][0]) - (c.pr[0][0] + c.pr[1][0]);
+    n0.y = -(c.pi[0][0] + c.pi[1][0]) - (c.qi[0][0] + c.qi[1][0]);
+    n1.x = (c.qr[0][1] + c.qr[1][1]) - (c.pr[0][1] + c.pr[1][1]);
+    n1.y = -(c.pi[0][1] + c.pi[1][1]) - (c.qi[0][1] + c.qi[1][1]);
   };
   auto release = [&](int slot, int n) {
     __syncwarp();
@@ -365,17 +398,28 @@ __global__ void __launch_bounds__(PipeShape<B, NC, CPLX_IN, TW>::NTHR, (B == 16 
     Vcur = Vprv;
     Vprv = t;
   };
-  // epilogue from the negated x at element offset o (layer * B) of this lane's W / T columns
-  auto epilogue = [&](ptrdiff_t o, bool boundary, double2 n0, double2 n1) {
+  // predicated stores (no divergent branch around a two-instruction body)
+  auto st_c = [&](double2* p, double2 v, uint32_t ok) {
+    asm volatile("{\n.reg .pred P1;\nsetp.ne.u32 P1, %3, 0;\n@P1 st.global.v2.f64 [%0], {%1, %2};\n}\n" ::"l"(p),
+                 "d"(v.x), "d"(v.y), "r"(ok)
+                 : "memory");
+  };
+  auto st_r = [&](double* p, double v, uint32_t ok) {
+    asm volatile("{\n.reg .pred P1;\nsetp.ne.u32 P1, %2, 0;\n@P1 st.global.f64 [%0], %1;\n}\n" ::"l"(p), "d"(v),
+                 "r"(ok)
+                 : "memory");
+  };
+  // epilogue of row tile j from the negated x; wp / tp: this lane's W / T element of the layer (row tile 0)
+  auto epilogue = [&](double2* wp, double* tp, int j, bool boundary, double2 n0, double2 n1) {
     if (CPLX_IN) {
-      if (ok0) wbase[o] = make_double2(-n0.x, -n0.y);
-      if (ok1) wbase[o + wcol] = make_double2(-n1.x, -n1.y);
+      st_c(wp + 8 * j, make_double2(-n0.x, -n0.y), ok0);
+      st_c(wp + 8 * j + wcol, make_double2(-n1.x, -n1.y), ok1);
     } else {
-      if (ok0) tbase[o] = coeff.y * n0.y - coeff.x * n0.x;
-      if (ok1) tbase[o + wcol] = coeff.y * n1.y - coeff.x * n1.x;
+      st_r(tp + 8 * j, coeff.y * n0.y - coeff.x * n0.x, ok0);
+      st_r(tp + 8 * j + wcol, coeff.y * n1.y - coeff.x * n1.x, ok1);
       if (boundary) {  // SPIKE: the chunk's boundary layers keep x for the reduced system
-        if (ok0) wbase[o] = make_double2(-n0.x, -n0.y);
-        if (ok1) wbase[o + wcol] = make_double2(-n1.x, -n1.y);
+        st_c(wp + 8 * j, make_double2(-n0.x, -n0.y), ok0);
+        st_c(wp + 8 * j + wcol, make_double2(-n1.x, -n1.y), ok1);
       }
     }
   };
@@ -389,7 +433,8 @@ __global__ void __launch_bounds__(PipeShape<B, NC, CPLX_IN, TW>::NTHR, (B == 16 
   rhs_mma(qs);
   load_af(qs + 1);
   adv_q(2);
-  acc = nxt;
+#pragma unroll
+  for (int j = 0; j < TPW; ++j) acc[j] = nxt[j];
 
   // ---------------- forward steps ----------------
   // TAIL steps (the last NDIRECT, and the very last with the twisted exchange) hand y to the
@@ -417,30 +462,33 @@ __global__ void __launch_bounds__(PipeShape<B, NC, CPLX_IN, TW>::NTHR, (B == 16 
     rhs_mma(qs);          // step v + 1 (forward or middle): S^{-1} Y into nxt
     load_af(qs + 1);
     adv_q(2);
-    double2 n0, n1;
-    fold_neg(n0, n1);
-    acc = nxt;
-    Vcur[vo] = n0;
-    Vcur[vo + SV] = n1;
-    const double2 y0 = make_double2(-n0.x, -n0.y), y1 = make_double2(-n1.x, -n1.y);
-    if (TAIL) {
-      const bool last = v == H - 1;
-      if (TW && last) {  // the partner's middle step needs this vector
-        double2* px = cg::this_cluster().map_shared_rank(Xb, half ^ 1);
-        px[vo] = n0;
-        px[vo + SV] = n1;
+    const bool last = v == H - 1;
+#pragma unroll
+    for (int j = 0; j < TPW; ++j) {
+      double2 n0, n1;
+      fold_neg(acc[j], n0, n1);
+      acc[j] = nxt[j];
+      Vcur[vo[j]] = n0;
+      Vcur[vo[j] + SV] = n1;
+      const double2 y0 = make_double2(-n0.x, -n0.y), y1 = make_double2(-n1.x, -n1.y);
+      if (TAIL) {
+        if (TW && last) {  // the partner's middle step needs this vector
+          double2* px = cg::this_cluster().map_shared_rank(Xb, half ^ 1);
+          px[vo[j]] = n0;
+          px[vo[j] + SV] = n1;
+        }
+        double2* sl = yslot(2 * H - v);  // backward step H + 1 + rb, rb = H - 1 - v
+        sl[(2 * j) * CT] = y0;
+        sl[(2 * j + 1) * CT] = y1;
+      } else {
+        st_c(wp + 8 * j, y0, ok0);
+        st_c(wp + 8 * j + wcol, y1, ok1);
       }
-      double2* sl = yslot(2 * H - v);  // backward step H + 1 + rb, rb = H - 1 - v
-      sl[0] = y0;
-      sl[CT] = y1;
-      if (TW && last) {
-        asm volatile("fence.acq_rel.cluster;\n" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(xbar, half ^ 1);
-      }
-    } else {
-      if (ok0) wp[0] = y0;
-      if (ok1) wp[wcol] = y1;
+    }
+    if (TAIL && TW && last) {
+      asm volatile("fence.acq_rel.cluster;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(xbar, half ^ 1);
     }
     wp += lstep;
     swap_buffers();
@@ -476,8 +524,6 @@ __global__ void __launch_bounds__(PipeShape<B, NC, CPLX_IN, TW>::NTHR, (B == 16 
       load_af(qs);
       adv_q(1);
     }
-    double2 n0, n1;
-    fold_neg(n0, n1);
     if (TW && CPLX_IN) {  // W row k holds the RHS both CTAs read; the top overwrites it with x_k
       if (half == 1) {
         __syncwarp();
@@ -486,15 +532,23 @@ __global__ void __launch_bounds__(PipeShape<B, NC, CPLX_IN, TW>::NTHR, (B == 16 
         mbar_wait_cluster(midbar, 0);
       }
     }
-    Vcur[vo] = n0;
-    Vcur[vo + SV] = n1;
-    if (half == 0) epilogue((ptrdiff_t)kmid * B, spike && (kmid == 0 || kmid == L - 1), n0, n1);
+#pragma unroll
+    for (int j = 0; j < TPW; ++j) {
+      double2 n0, n1;
+      fold_neg(acc[j], n0, n1);
+      Vcur[vo[j]] = n0;
+      Vcur[vo[j] + SV] = n1;
+      if (half == 0)
+        epilogue(wbase + (ptrdiff_t)kmid * B, CPLX_IN ? nullptr : tbase + (ptrdiff_t)kmid * B, j,
+                 spike && (kmid == 0 || kmid == L - 1), n0, n1);
+    }
     swap_buffers();
   }
 
   // ---------------- backward steps ----------------
-  ptrdiff_t eo = (ptrdiff_t)(l0 + dl * (H - 1)) * B;  // layer offset of the backward step's rows
-  int lb = l0 + dl * (H - 1);
+  // (a chunk's boundary layers 0 and L - 1 are the last backward steps of the two halves)
+  double2* ewp = wbase + (ptrdiff_t)(l0 + dl * (H - 1)) * B;
+  double* etp = CPLX_IN ? nullptr : tbase + (ptrdiff_t)(l0 + dl * (H - 1)) * B;
 #pragma unroll 1
   for (int v = H + 1; v < nsteps; ++v) {
     double2 bv[KQ];
@@ -502,7 +556,8 @@ __global__ void __launch_bounds__(PipeShape<B, NC, CPLX_IN, TW>::NTHR, (B == 16 
     load_b(Vprv, bv);
     const bool more = v + 1 < nsteps;
     const uint32_t t0 = more ? test(qs) : 1u;
-    acc.zero();
+#pragma unroll
+    for (int j = 0; j < TPW; ++j) acc[j].zero();
     vec_mma(bv);
     release(cs, 1);
     issue_y(v + RY - 1);
@@ -514,18 +569,21 @@ __global__ void __launch_bounds__(PipeShape<B, NC, CPLX_IN, TW>::NTHR, (B == 16 
     }
     cp_async_wait<RY - 1>();
     const double2* sl = yslot(v);
-    const double2 y0 = sl[0], y1 = sl[CT];
-    double2 n0, n1;
-    fold_neg(n0, n1);
-    n0.x -= y0.x;   // -(y + r)
-    n0.y -= y0.y;
-    n1.x -= y1.x;
-    n1.y -= y1.y;
-    Vcur[vo] = n0;
-    Vcur[vo + SV] = n1;
-    epilogue(eo, spike && (lb == 0 || lb == L - 1), n0, n1);
-    eo -= lstep;
-    lb -= dl;
+#pragma unroll
+    for (int j = 0; j < TPW; ++j) {
+      const double2 y0 = sl[(2 * j) * CT], y1 = sl[(2 * j + 1) * CT];
+      double2 n0, n1;
+      fold_neg(acc[j], n0, n1);
+      n0.x -= y0.x;   // -(y + r)
+      n0.y -= y0.y;
+      n1.x -= y1.x;
+      n1.y -= y1.y;
+      Vcur[vo[j]] = n0;
+      Vcur[vo[j] + SV] = n1;
+      epilogue(ewp, etp, j, spike && !more, n0, n1);
+    }
+    ewp -= lstep;
+    if (!CPLX_IN) etp -= lstep;
     swap_buffers();
   }
   cp_async_wait<0>();
@@ -561,7 +619,7 @@ static cudaError_t launch_pipe(const BtSweepArgs& a, cudaStream_t st) {
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-// b = 16: 8 columns per CTA on 2 compute warps + the producer warp
+// b = 16: 8 columns per CTA, one compute warp + the producer warp
 cudaError_t bt_sweep_pipe16(const BtSweepArgs& a, cudaStream_t st) {
   return a.kmid >= 0 ? launch_pipe<16, 8, true>(a, st) : launch_pipe<16, 8, false>(a, st);
 }

@@ -450,8 +450,8 @@ bool bt_swizzled_factors(int b) { return b == 16 || b == 32; }
 // b = 16, 32 (factors in the swizzled layout, bt_swizzled_factors)
 cudaError_t bt_sweep_small(const BtSweepArgs& a, cudaStream_t st) {
   switch (a.b) {
-    case 16:  // 8 columns per CTA on 4 compute warps (re | im split, software-pipelined steps)
-      return getenv("FEAST_SWEEP_Z") ? bt_sweep_split16(a, st) : bt_sweep_pipe16(a, st);
+    case 16:  // sweep_pipe.cu: 8 columns per CTA, software-pipelined steps, lean producer warp
+      return bt_sweep_pipe16(a, st);
     case 32:  // (complex right-hand sides: narrower column blocks keep the ring within 227 KB)
       return a.complex_mode ? launch_bulk_any<32, 8, 1>(a, st) : launch_bulk_any<32, 16, 1>(a, st);
   }
