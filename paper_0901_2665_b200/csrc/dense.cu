@@ -13,10 +13,14 @@
 //   R = P Y; for k: Z_k = L_kk^{-1} R_k; R_{>k} -= L_{>k,k} Z_k;
 //            for k desc: X_k = U_kk^{-1} R_k; R_{<k} -= U_{<k,k} X_k;  T = Re(c_e X)
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 #include "common.cuh"
 #include "kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace feastgpu {
 
@@ -104,6 +108,109 @@ __global__ void __launch_bounds__(1024) panel_kernel(int n, int64_t stride, int 
   }
 }
 
+// The same unblocked panel on a cluster of kPanelCluster CTAs per node: the panel of a large
+// matrix (8192 x 64 complex = 8 MB) streams through L2 once per column step, which one SM's load
+// path sustains at ~100 GB/s (6 ms per panel at n = 8192, longer than the whole trailing update
+// beside it). Rows are dealt to the cluster in chunks of 1024 (row r belongs to CTA (r / 1024) % CL,
+// so a 128-byte line of a column has one owner); per column step
+//   (1) every CTA finds its pivot candidate and posts it to all CTAs of the cluster (DSMEM);
+//       cluster barrier; every CTA picks the same winner (largest modulus, lowest row on ties);
+//   (2) every CTA reads the old pivot row and the old row `col` of the panel (L2 loads: another
+//       SM may hold a stale L1 line of a neighbouring former pivot row); cluster barrier;
+//   (3) the owners of rows col and p write the exchanged rows, then every thread scales and
+//       updates its own rows.
+// Same pivots and the same arithmetic per element as panel_kernel: bit-identical factors.
+constexpr int kPanelCluster = 8;
+__global__ void __cluster_dims__(kPanelCluster, 1, 1) __launch_bounds__(1024)
+    panel_cluster_kernel(int n, int64_t stride, int k0, int kb, double2* lu, int* ipiv, int* status) {
+  constexpr int CL = kPanelCluster;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int s = blockIdx.x / CL;
+  double2* A = lu + (int64_t)s * stride;
+  int* piv = ipiv + (int64_t)s * n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ double rv[32];
+  __shared__ int ri[32];
+  __shared__ double cand_v[2][CL];   // candidates of all CTAs, double-buffered by column parity
+  __shared__ int cand_i[2][CL];
+  __shared__ double2 rowk[kDenseNb], rowc[kDenseNb];
+  auto owner = [&](int r) { return (r >> 10) % CL; };
+  for (int j = 0; j < kb; ++j) {
+    const int col = k0 + j;
+    double best = -1.0;
+    int bi = n;
+    // my rows: chunks rank, rank + CL, ... of 1024 rows; start at the first row >= col
+    for (int base = (rank << 10); base < n; base += CL << 10) {
+      const int i = base + tid;
+      if (i >= col && i < n) {
+        const double v = cabs_(A[i + (int64_t)col * n]);
+        if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    if (lane == 0) { rv[warp] = best; ri[warp] = bi; }
+    __syncthreads();
+    if (warp == 0) {
+      best = rv[lane];
+      bi = ri[lane];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+      }
+      if (lane < CL) {  // post to CTA `lane`
+        *cluster.map_shared_rank(&cand_v[j & 1][rank], lane) = best;
+        *cluster.map_shared_rank(&cand_i[j & 1][rank], lane) = bi;
+      }
+    }
+    cluster.sync();  // (1)
+    best = -1.0;
+    bi = n;
+#pragma unroll
+    for (int r = 0; r < CL; ++r) {
+      const double ov = cand_v[j & 1][r];
+      const int oi = cand_i[j & 1][r];
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    const int p = (best > 0.0) ? bi : -1;
+    if (p < 0) {  // singular: DenseLU throws NumericalError (lu.hpp:38); uniform over the cluster
+      if (rank == 0 && tid == 0) atomicExch(status, 1);
+      return;
+    }
+    if (rank == 0 && tid == 0) piv[col] = p;
+    if (tid < kb) {
+      rowk[tid] = __ldcg(A + p + (int64_t)(k0 + tid) * n);
+      rowc[tid] = __ldcg(A + col + (int64_t)(k0 + tid) * n);
+    }
+    cluster.sync();  // (2) every CTA holds the old rows before their owners overwrite them
+    if (p != col && tid < kb) {
+      if (owner(col) == rank) A[col + (int64_t)(k0 + tid) * n] = rowk[tid];
+      if (owner(p) == rank) A[p + (int64_t)(k0 + tid) * n] = rowc[tid];
+    }
+    __syncthreads();
+    const double2 pv = rowk[j];
+    for (int base = (rank << 10); base < n; base += CL << 10) {
+      const int i = base + tid;
+      if (i > col && i < n) {
+        const double2 l = cdiv(A[i + (int64_t)col * n], pv);
+        A[i + (int64_t)col * n] = l;
+        for (int c = j + 1; c < kb; ++c) {
+          double2* e = A + i + (int64_t)(k0 + c) * n;
+          *e = csub(*e, cmul(l, rowk[c]));
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // row interchanges of panel [k0, k0+kb) on the columns outside it
 __global__ void laswp_kernel(int n, int64_t stride, int k0, int kb, double2* lu, const int* ipiv) {
   const int s = blockIdx.y;
@@ -176,41 +283,74 @@ __global__ void perm_kernel(int n, int nodes, const int* ipiv, int* perm) {
 
 // Batched right-looking LU with partial pivoting of `nodes` complex n x n matrices stored
 // `stride` apart (in place), plus the row permutation and the diagonal-block inverses the
-// blocked solves use. Shared by the dense path and the large-block block-Thomas factor.
+// blocked solves use. Shared by the dense path and the SPIKE reduced systems.
+//
+// Look-ahead (la != nullptr): the unblocked panel runs on one CTA per node, so on the main
+// stream it left all but `nodes` SMs idle for about as long as the trailing updates take. The
+// trailing update of step k is therefore split: the columns of panel k+1 first, then panel k+1
+// (and its diagonal-block inverses) on the high-priority side stream beside the update of the
+// remaining columns. Only the row interchanges of panel k+1 on the other columns wait for both
+// (they move rows of L21, which the remaining update reads). Same arithmetic, same order within
+// every element's update: the factors are bit-identical to the serial order.
 cudaError_t zgetrf_batched(int n, int nodes, double2* lu, int64_t stride, int* ipiv, int* perm, double2* dinv,
-                           int* status, cudaStream_t st) {
+                           int* status, cudaStream_t st, const LuLookahead* la) {
   const int nb = kDenseNb;
   const int nblk = (n + nb - 1) / nb;
   const double2 one = make_double2(1.0, 0.0), mone = make_double2(-1.0, 0.0),
                 zero = make_double2(0.0, 0.0);
-  for (int blk = 0; blk < nblk; ++blk) {
+  const int64_t sd = (int64_t)nblk * 2 * nb * nb;
+  {
+    const int sm = (int)sizeof(double2) * nb * (nb + 1);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(diag_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+      attr = true;
+    }
+  }
+  auto panel = [&](int blk, cudaStream_t s) {
     const int k0 = blk * nb, kb = std::min(nb, n - k0);
-    panel_kernel<<<nodes, 1024, 0, st>>>(n, stride, k0, kb, lu, ipiv, status);
-    ++g_launches;
+    // tall panels: a cluster of CTAs per node (the rows of one CTA would stream through one SM)
+    if (n - k0 >= 4096) panel_cluster_kernel<<<nodes * kPanelCluster, 1024, 0, s>>>(n, stride, k0, kb, lu, ipiv, status);
+    else panel_kernel<<<nodes, 1024, 0, s>>>(n, stride, k0, kb, lu, ipiv, status);
+    diag_inv_kernel<<<nodes, 128, (int)sizeof(double2) * nb * (nb + 1), s>>>(n, stride, blk, nblk, lu, dinv);
+    g_launches += 2;
+  };
+  // columns [c0, c0 + nc) of the trailing matrix of step blk: U12 = L11^{-1} A12, A22 -= L21 U12
+  auto update = [&](int blk, int c0, int nc) {
+    const int k0 = blk * nb, kb = std::min(nb, n - k0), rest = n - k0 - kb;
+    if (nc <= 0) return;
+    double2* a12 = lu + k0 + (int64_t)c0 * n;
+    zgemm_batched(kb, nc, kb, one, dinv + (int64_t)blk * 2 * nb * nb, nb, sd, a12, n, stride, zero, a12, n, stride,
+                  nodes, st);
+    zgemm_batched(rest, nc, kb, mone, lu + (k0 + kb) + (int64_t)k0 * n, n, stride, a12, n, stride, one,
+                  lu + (k0 + kb) + (int64_t)c0 * n, n, stride, nodes, st);
+  };
+  auto laswp = [&](int blk) {
+    const int k0 = blk * nb, kb = std::min(nb, n - k0);
     if (n - kb > 0) {
       dim3 grid((n - kb + 255) / 256, nodes);
       laswp_kernel<<<grid, 256, 0, st>>>(n, stride, k0, kb, lu, ipiv);
       ++g_launches;
     }
-    {
-      const int sm = (int)sizeof(double2) * nb * (nb + 1);
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(diag_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-        attr = true;
-      }
-      diag_inv_kernel<<<nodes, 128, sm, st>>>(n, stride, blk, nblk, lu, dinv);
-    }
-    ++g_launches;
-    const int rest = n - k0 - kb;
-    if (rest > 0) {
-      double2* a12 = lu + k0 + (int64_t)(k0 + kb) * n;
-      const double2* linv = dinv + (int64_t)blk * 2 * nb * nb;
-      zgemm_batched(kb, rest, kb, one, linv, nb, (int64_t)nblk * 2 * nb * nb, a12, n, stride, zero,
-                    a12, n, stride, nodes, st);
-      const double2* l21 = lu + (k0 + kb) + (int64_t)k0 * n;
-      double2* a22 = lu + (k0 + kb) + (int64_t)(k0 + kb) * n;
-      zgemm_batched(rest, rest, kb, mone, l21, n, stride, a12, n, stride, one, a22, n, stride, nodes, st);
+  };
+  const bool ahead = la && la->side && nblk > 1;
+  panel(0, st);
+  for (int blk = 0; blk < nblk; ++blk) {
+    const int k0 = blk * nb, kb = std::min(nb, n - k0), k1 = k0 + kb, rest = n - k1;
+    laswp(blk);
+    if (rest <= 0) break;
+    const int kb1 = std::min(nb, rest);  // width of panel blk + 1
+    update(blk, k1, kb1);
+    if (ahead) {
+      cudaEventRecord(la->ev_cols, st);
+      cudaStreamWaitEvent(la->side, la->ev_cols, 0);
+      panel(blk + 1, la->side);
+      cudaEventRecord(la->ev_panel, la->side);
+      update(blk, k1 + kb1, rest - kb1);
+      cudaStreamWaitEvent(st, la->ev_panel, 0);
+    } else {
+      update(blk, k1 + kb1, rest - kb1);
+      panel(blk + 1, st);
     }
   }
   perm_kernel<<<(nodes + 31) / 32, 32, 0, st>>>(n, nodes, ipiv, perm);
@@ -224,7 +364,7 @@ cudaError_t dense_factor(const DenseFactorArgs& a, cudaStream_t st) {
   dim3 grid((unsigned)std::min<int64_t>((nn + 255) / 256, 1024), nodes);
   assemble_kernel<<<grid, 256, 0, st>>>(n, a.a, a.bm, a.z, a.lu);
   ++g_launches;
-  return zgetrf_batched(n, nodes, a.lu, nn, a.ipiv, a.perm, a.dinv, a.status, st);
+  return zgetrf_batched(n, nodes, a.lu, nn, a.ipiv, a.perm, a.dinv, a.status, st, a.la.side ? &a.la : nullptr);
 }
 
 // R_s = P_s Y (real -> complex), or P_s W_s (complex, via scratch copy in t-as-double2)

@@ -340,6 +340,7 @@ struct feast_gpu_ctx {
   double la_kmax = 1e3;  // admission bound of the look-ahead pass (kLookaheadMaxK)
   cudaStream_t eigs = nullptr;  // high-priority stream of the reduced eigensolve
   cudaEvent_t ev_proj = nullptr, ev_eig = nullptr, ev_pre_eig = nullptr;
+  cudaEvent_t ev_lu_cols = nullptr, ev_lu_panel = nullptr;  // LU look-ahead (dense factorisation)
   double* hpin = nullptr;       // pinned: status, cancellation factor, eigenvalues
   size_t hpin_n = 0;
   DevBuf<double> kfac;
@@ -1392,6 +1393,7 @@ void factor_range(feast_gpu_ctx* c, int s0, int cnt) {
     c->perm.ensure((size_t)slots * n);
     c->dinv.ensure((size_t)slots * nblk * 2 * nb * nb);
     DenseFactorArgs a{n, cnt, c->A.p, c->Bm.p, c->dz.p + s0, c->lu.p, c->ipiv.p, c->perm.p, c->dinv.p, c->fstatus.p};
+    a.la = LuLookahead{c->eigs, c->ev_lu_cols, c->ev_lu_panel};  // panels beside the trailing updates
     CK(dense_factor(a, c->stream));
   }
   int st = 0;
@@ -2540,6 +2542,8 @@ int feast_gpu_create(int device, void* stream, feast_gpu_ctx** out) {
     CK(cudaStreamCreateWithPriority(&c->eigs, cudaStreamNonBlocking, hi));
     CK(cudaEventCreateWithFlags(&c->ev_proj, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->ev_pre_eig, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_lu_cols, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_lu_panel, cudaEventDisableTiming));
     CK(cudaEventCreate(&c->ev_eig));
     for (auto& pe : c->pev)
       for (auto& e : pe) CK(cudaEventCreate(&e));
@@ -2588,6 +2592,8 @@ void feast_gpu_destroy(feast_gpu_ctx* c) {
   }
   if (c->ev_proj) cudaEventDestroy(c->ev_proj);
   if (c->ev_pre_eig) cudaEventDestroy(c->ev_pre_eig);
+  if (c->ev_lu_cols) cudaEventDestroy(c->ev_lu_cols);
+  if (c->ev_lu_panel) cudaEventDestroy(c->ev_lu_panel);
   if (c->ev_eig) cudaEventDestroy(c->ev_eig);
   pinned_small_release(c->hpin, c->hpin_n);
   if (c->own_stream) cudaStreamDestroy(c->stream);

@@ -88,8 +88,9 @@ cudaError_t zgemm_batched(int m, int n, int k, double2 alpha, const double2* a, 
                           const double2* b, int ldb, int64_t sb, double2 beta, double2* c, int ldc,
                           int64_t sc, int batch, cudaStream_t st);
 // batched dense complex LU / solves (dense.cu), the reduced systems' factorisation
+struct LuLookahead;
 cudaError_t zgetrf_batched(int n, int nodes, double2* lu, int64_t stride, int* ipiv, int* perm, double2* dinv,
-                           int* status, cudaStream_t st);
+                           int* status, cudaStream_t st, const LuLookahead* la = nullptr);
 cudaError_t zgetrs_batched(int n, int nodes, int m, const double2* lu, int64_t stride, const int* perm,
                            const double2* dinv, double2* w, int ldv, double2* scratch, cudaStream_t st);
 
@@ -103,6 +104,11 @@ cudaError_t bt_apply(int L, int b, const double* diag, const double* low, const 
                      double* y, int ldy, int m, cudaStream_t st, int l0 = 0, int l1 = -1);
 
 // ---------------- dense shifted solves (batched complex LU) -------------------
+// look-ahead resources of zgetrf_batched: a (high-priority) side stream and two events
+struct LuLookahead {
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_cols = nullptr, ev_panel = nullptr;
+};
 struct DenseFactorArgs {
   int n, nodes;
   const double* a;        // n*n real
@@ -113,6 +119,7 @@ struct DenseFactorArgs {
   int* perm;              // nodes * n (row permutation applied to the RHS)
   double2* dinv;          // nodes * (n/nb) * 2 * nb*nb : inverses of unit-L and U diagonal blocks
   int* status;
+  LuLookahead la;         // side == nullptr: panels on the main stream
 };
 cudaError_t dense_factor(const DenseFactorArgs& a, cudaStream_t st);
 constexpr int kDenseNb = 64;
