@@ -211,20 +211,19 @@ __global__ void __cluster_dims__(kPanelCluster, 1, 1) __launch_bounds__(1024)
   }
 }
 
-// row interchanges of panel [k0, k0+kb) on the columns outside it
-__global__ void laswp_kernel(int n, int64_t stride, int k0, int kb, double2* lu, const int* ipiv) {
+// row interchanges ipiv[r0 .. r0+nr) applied to columns [c0, c0+nc)
+__global__ void laswp_kernel(int n, int64_t stride, int r0, int nr, int c0, int nc, double2* lu, const int* ipiv) {
   const int s = blockIdx.y;
   double2* A = lu + (int64_t)s * stride;
   const int* piv = ipiv + (int64_t)s * n;
-  const int others = n - kb;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < others; c += gridDim.x * blockDim.x) {
-    const int col = c < k0 ? c : c + kb;
-    for (int r = k0; r < k0 + kb; ++r) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
+    double2* col = A + (int64_t)(c0 + c) * n;
+    for (int r = r0; r < r0 + nr; ++r) {
       const int p = piv[r];
       if (p != r) {
-        const double2 t0 = A[r + (int64_t)col * n];
-        A[r + (int64_t)col * n] = A[p + (int64_t)col * n];
-        A[p + (int64_t)col * n] = t0;
+        const double2 t0 = col[r];
+        col[r] = col[p];
+        col[p] = t0;
       }
     }
   }
@@ -285,17 +284,22 @@ __global__ void perm_kernel(int n, int nodes, const int* ipiv, int* perm) {
 // `stride` apart (in place), plus the row permutation and the diagonal-block inverses the
 // blocked solves use. Shared by the dense path and the SPIKE reduced systems.
 //
-// Look-ahead (la != nullptr): the unblocked panel runs on one CTA per node, so on the main
-// stream it left all but `nodes` SMs idle for about as long as the trailing updates take. The
-// trailing update of step k is therefore split: the columns of panel k+1 first, then panel k+1
-// (and its diagonal-block inverses) on the high-priority side stream beside the update of the
-// remaining columns. Only the row interchanges of panel k+1 on the other columns wait for both
-// (they move rows of L21, which the remaining update reads). Same arithmetic, same order within
-// every element's update: the factors are bit-identical to the serial order.
+// Two levels for n >= 2048: super-panels of W = 256 columns are factored with 64-column panels
+// whose updates stay inside the super-panel; the columns to its right get the super-panel's row
+// interchanges, U12 = L_SS^{-1} A12 block by block, and ONE trailing update with K = 256. (A K = 64
+// trailing update moves 32 bytes of C per 512 flops, 16 flop/B against the 5.7 flop/B ridge with
+// nothing left for A and B; ncu had it at 0.58 of the DMMA peak, the K = 256 GEMM runs at 0.70.)
+//
+// Look-ahead (la != nullptr): the unblocked panels run on one CTA (or one cluster) per node, so on
+// the main stream they left most SMs idle for about as long as the trailing updates take. The
+// columns of the next super-panel are therefore updated first, and the next super-panel is
+// factored on the high-priority side stream beside the update of the remaining columns; only its
+// row interchanges on the other columns wait for both.
 cudaError_t zgetrf_batched(int n, int nodes, double2* lu, int64_t stride, int* ipiv, int* perm, double2* dinv,
                            int* status, cudaStream_t st, const LuLookahead* la) {
   const int nb = kDenseNb;
   const int nblk = (n + nb - 1) / nb;
+  const int W = n >= 2048 ? 256 : nb;
   const double2 one = make_double2(1.0, 0.0), mone = make_double2(-1.0, 0.0),
                 zero = make_double2(0.0, 0.0);
   const int64_t sd = (int64_t)nblk * 2 * nb * nb;
@@ -307,50 +311,66 @@ cudaError_t zgetrf_batched(int n, int nodes, double2* lu, int64_t stride, int* i
       attr = true;
     }
   }
-  auto panel = [&](int blk, cudaStream_t s) {
-    const int k0 = blk * nb, kb = std::min(nb, n - k0);
-    // tall panels: a cluster of CTAs per node (the rows of one CTA would stream through one SM)
-    if (n - k0 >= 4096) panel_cluster_kernel<<<nodes * kPanelCluster, 1024, 0, s>>>(n, stride, k0, kb, lu, ipiv, status);
-    else panel_kernel<<<nodes, 1024, 0, s>>>(n, stride, k0, kb, lu, ipiv, status);
-    diag_inv_kernel<<<nodes, 128, (int)sizeof(double2) * nb * (nb + 1), s>>>(n, stride, blk, nblk, lu, dinv);
-    g_launches += 2;
+  auto gemm = [&](int m_, int n_, int k_, double2 alpha, const double2* a_, const double2* b_, double2 beta,
+                  double2* c_, cudaStream_t s) {
+    if (m_ > 0 && n_ > 0 && k_ > 0) zgemm_batched(m_, n_, k_, alpha, a_, n, stride, b_, n, stride, beta, c_, n, stride, nodes, s);
   };
-  // columns [c0, c0 + nc) of the trailing matrix of step blk: U12 = L11^{-1} A12, A22 -= L21 U12
-  auto update = [&](int blk, int c0, int nc) {
-    const int k0 = blk * nb, kb = std::min(nb, n - k0), rest = n - k0 - kb;
-    if (nc <= 0) return;
-    double2* a12 = lu + k0 + (int64_t)c0 * n;
-    zgemm_batched(kb, nc, kb, one, dinv + (int64_t)blk * 2 * nb * nb, nb, sd, a12, n, stride, zero, a12, n, stride,
-                  nodes, st);
-    zgemm_batched(rest, nc, kb, mone, lu + (k0 + kb) + (int64_t)k0 * n, n, stride, a12, n, stride, one,
-                  lu + (k0 + kb) + (int64_t)c0 * n, n, stride, nodes, st);
+  auto at = [&](int r, int c) { return lu + r + (int64_t)c * n; };
+  auto linv = [&](int k0) { return dinv + (int64_t)(k0 / nb) * 2 * nb * nb; };
+  auto laswp = [&](int r0, int r1, int c0, int c1, cudaStream_t s) {
+    if (c1 - c0 <= 0 || r1 - r0 <= 0) return;
+    dim3 grid((c1 - c0 + 255) / 256, nodes);
+    laswp_kernel<<<grid, 256, 0, s>>>(n, stride, r0, r1 - r0, c0, c1 - c0, lu, ipiv);
+    ++g_launches;
   };
-  auto laswp = [&](int blk) {
-    const int k0 = blk * nb, kb = std::min(nb, n - k0);
-    if (n - kb > 0) {
-      dim3 grid((n - kb + 255) / 256, nodes);
-      laswp_kernel<<<grid, 256, 0, st>>>(n, stride, k0, kb, lu, ipiv);
-      ++g_launches;
+  // columns [K0, K1) from row K0 down: panels of nb columns, interchanges and updates inside [K0, K1)
+  auto factor_super = [&](int K0, int K1, cudaStream_t s) {
+    for (int k0 = K0; k0 < K1; k0 += nb) {
+      const int kb = std::min(nb, K1 - k0), k1 = k0 + kb;
+      // tall panels: a cluster of CTAs per node (the rows of one CTA would stream through one SM)
+      if (n - k0 >= 4096) panel_cluster_kernel<<<nodes * kPanelCluster, 1024, 0, s>>>(n, stride, k0, kb, lu, ipiv, status);
+      else panel_kernel<<<nodes, 1024, 0, s>>>(n, stride, k0, kb, lu, ipiv, status);
+      diag_inv_kernel<<<nodes, 128, (int)sizeof(double2) * nb * (nb + 1), s>>>(n, stride, k0 / nb, nblk, lu, dinv);
+      g_launches += 2;
+      laswp(k0, k1, K0, k0, s);
+      laswp(k0, k1, k1, K1, s);
+      // U12 = L11^{-1} A12 (in place), A22 -= L21 U12 on the super-panel's remaining columns
+      if (K1 - k1 > 0)
+        zgemm_batched(kb, K1 - k1, kb, one, linv(k0), nb, sd, at(k0, k1), n, stride, zero, at(k0, k1), n, stride,
+                      nodes, s);
+      gemm(n - k1, K1 - k1, kb, mone, at(k1, k0), at(k0, k1), one, at(k1, k1), s);
     }
   };
-  const bool ahead = la && la->side && nblk > 1;
-  panel(0, st);
-  for (int blk = 0; blk < nblk; ++blk) {
-    const int k0 = blk * nb, kb = std::min(nb, n - k0), k1 = k0 + kb, rest = n - k1;
-    laswp(blk);
-    if (rest <= 0) break;
-    const int kb1 = std::min(nb, rest);  // width of panel blk + 1
-    update(blk, k1, kb1);
+  // columns [c0, c0 + nc) right of the factored super-panel [K0, K1): U12 block by block, then the
+  // trailing rows with K = K1 - K0
+  auto outer = [&](int K0, int K1, int c0, int nc, cudaStream_t s) {
+    if (nc <= 0) return;
+    for (int k0 = K0; k0 < K1; k0 += nb) {
+      const int kb = std::min(nb, K1 - k0), k1 = k0 + kb;
+      zgemm_batched(kb, nc, kb, one, linv(k0), nb, sd, at(k0, c0), n, stride, zero, at(k0, c0), n, stride, nodes, s);
+      gemm(K1 - k1, nc, kb, mone, at(k1, k0), at(k0, c0), one, at(k1, c0), s);
+    }
+    gemm(n - K1, nc, K1 - K0, mone, at(K1, K0), at(K0, c0), one, at(K1, c0), s);
+  };
+  const bool ahead = la && la->side && n > W;
+  factor_super(0, std::min(W, n), st);
+  for (int K0 = 0; K0 < n; K0 += W) {
+    const int K1 = std::min(K0 + W, n);
+    laswp(K0, K1, 0, K0, st);
+    laswp(K0, K1, K1, n, st);
+    if (K1 >= n) break;
+    const int K2 = std::min(K1 + W, n);
+    outer(K0, K1, K1, K2 - K1, st);
     if (ahead) {
       cudaEventRecord(la->ev_cols, st);
       cudaStreamWaitEvent(la->side, la->ev_cols, 0);
-      panel(blk + 1, la->side);
+      factor_super(K1, K2, la->side);
       cudaEventRecord(la->ev_panel, la->side);
-      update(blk, k1 + kb1, rest - kb1);
+      outer(K0, K1, K2, n - K2, st);
       cudaStreamWaitEvent(st, la->ev_panel, 0);
     } else {
-      update(blk, k1 + kb1, rest - kb1);
-      panel(blk + 1, st);
+      outer(K0, K1, K2, n - K2, st);
+      factor_super(K1, K2, st);
     }
   }
   perm_kernel<<<(nodes + 31) / 32, 32, 0, st>>>(n, nodes, ipiv, perm);
