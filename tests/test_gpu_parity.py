@@ -233,6 +233,63 @@ def test_residuals_match_reference(ctx):
     assert np.allclose(res, rr, rtol=1e-3, atol=1e-16)
 
 
+@pytest.mark.parametrize("path", FIX)
+def test_operator_applies_match_reference(ctx, path):
+    """SymmetricOperator::apply (operator.hpp:132-158) on every storage route, through
+    residual_norms with RANDOM vectors and shifts: ||A x - lambda B x||_1 is then an O(1) quantity
+    (not a rounding-level one as for converged pairs), so both applies are compared with the
+    reference's to 1e-12."""
+    prob, g = load_fixture(path)
+    ctx.set_pencil(prob.a, prob.b)
+    rng = np.random.default_rng(77)
+    m = 12
+    x = np.asfortranarray(rng.standard_normal((prob.n, m)))
+    lam = rng.uniform(prob.emin - 1.0, prob.emax + 1.0, m)
+    res, ab, mx = ctx.residual_norms(lam, x)
+    rr, rab, rmx = O.residual_norms(prob.a, prob.b, lam, x)
+    assert np.array_equal(ab, rab)
+    assert np.max(np.abs(res - rr) / rr) <= 1e-12
+    assert abs(mx - rmx) <= 1e-12 * rmx
+
+
+@pytest.mark.parametrize("path", FIX)
+def test_rayleigh_ritz_matches_reference(ctx, path):
+    """rayleigh_ritz (core.hpp:228-240: applies, adjoint_matmul + hermitian_part, reduced_gevp,
+    X = Q Phi) on a filtered subspace that holds the wanted eigenvectors (B times the fixture's
+    eigenvectors, topped up with random columns: the Ritz values of a first pass from a random block
+    are too ill-conditioned to compare at 1e-10): same Ritz values as the reference's, a
+    B-orthonormal Ritz basis that diagonalises A on span(Q), spanning span(Q)."""
+    prob, g = load_fixture(path)
+    ctx.set_pencil(prob.a, prob.b)
+    ctx.prepare(prob.emin, prob.emax, prob.n_e)
+    xf = g["eigenvectors"]
+    y = np.asfortranarray(O.random_block(prob.n, prob.m0, prob.seed))
+    y[:, : xf.shape[1]] = prob.b.to_dense() @ xf
+    q = O.accumulate_real(prob.a, prob.b, prob.emin, prob.emax, prob.n_e, y)
+    ev, x, tr = ctx.rayleigh_ritz(q)
+    rev, rx, rtr = O.rayleigh_ritz(prob.a, prob.b, q)
+    assert tr == rtr and len(ev) == len(rev)
+    scale = max(1.0, float(np.max(np.abs(rev))))
+    # the Ritz values next to the pencil's eigenvalues (well-conditioned) to 1e-10; the others
+    # (random top-up directions, some of them spurious inside the interval) are ill-conditioned
+    wanted = [int(np.argmin(np.abs(rev - lam))) for lam in g["eigenvalues"]]
+    assert np.max(np.abs(rev[wanted] - g["eigenvalues"])) <= 1e-9 * scale
+    assert np.max(np.abs(ev - rev)[wanted]) <= 1e-10 * scale
+    assert np.max(np.abs(ev - rev)) <= 1e-4 * scale
+    a, b = prob.a.to_dense(), prob.b.to_dense()
+    k = x.shape[1]
+
+    def defects(xx, lam):  # B-orthonormality and A-diagonality of a Ritz basis
+        return (np.max(np.abs(xx.T @ (b @ xx) - np.eye(k))),
+                np.max(np.abs(xx.T @ (a @ xx) - np.diag(lam))) / scale)
+    # the filtered block mixes columns of scale 1 and ~1e-5 (cond(B_Q) ~ 1e10), so the defects are
+    # far above rounding for the reference as well: the GPU's must not exceed its by much
+    (ob, oa), (rb, ra) = defects(x, ev), defects(rx, rev)
+    assert ob <= max(1e-9, 10 * rb) and oa <= max(1e-9, 10 * ra), (ob, rb, oa, ra)
+    coef, *_ = np.linalg.lstsq(q, x, rcond=None)
+    assert np.max(np.abs(q @ coef - x)) <= 1e-9 * np.max(np.abs(x))
+
+
 def test_input_errors(ctx, F):
     prob, _ = load_fixture(FIX[0])
     ctx.set_pencil(prob.a, prob.b)
