@@ -87,7 +87,9 @@ def main(names):
             out["eigenvectors"] = x
         if x.shape[1]:
             out["sketch"] = sketch_matrix(prob.n) @ x
-        path = os.path.join(GOLDEN, f"full_{name}.npz")
+        # GOLDEN_OUT: another output directory (gpurun_out/ when the reference runs on the GPU box's
+        # host cores, from where only that directory travels back)
+        path = os.path.join(os.environ.get("GOLDEN_OUT", GOLDEN), f"full_{name}.npz")
         np.savez_compressed(path, **out)
         print(f"{name}: {r['status']} m={r['m']} loops={r['loops_used']} max_res={r['max_residual']:.2e} "
               f"wall={wall:.0f}s -> {path}", flush=True)

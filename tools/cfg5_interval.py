@@ -12,7 +12,9 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_0901_2665_b200 import problems as P  # noqa: E402
 
-L, b, seed, want = 2048, 512, 5, 512
+# usage: cfg5_interval.py [L [tol]]   (the scaled config 5 of SURVEY 8(c): L = 64, tol ~ a third of the spacing)
+L, b, seed, want = (int(sys.argv[1]) if len(sys.argv) > 1 else 2048), 512, 5, 512
+TOL = float(sys.argv[2]) if len(sys.argv) > 2 else 3e-6
 t0 = time.time()
 a, bb = P.blocktri_operators(L, b, seed)
 print(f"generated in {time.time() - t0:.0f} s", flush=True)
@@ -35,7 +37,7 @@ while cy <= target:
     cy = count(y)
 cx = c0 if x == lo else count(x)
 # bisection: keep count(x) <= target < count(y)
-while y - x > 3e-6:
+while y - x > TOL:
     mid = 0.5 * (x + y)
     cm = count(mid)
     if cm <= target:
@@ -57,4 +59,8 @@ data[f"blocktri_L{L}_b{b}_s{seed}_k{want}"] = {"lo": lo, "hi": hi, "count_lo": c
                                                "first_above_bracket": [x, y],
                                                "method": "tools/cfg5_interval.py (lo = 0, bisection)"}
 json.dump(data, open(path, "w"), indent=1, sort_keys=True)
+out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+if os.path.isdir(out):  # (run on the GPU box: only gpurun_out/ travels back)
+    json.dump({f"blocktri_L{L}_b{b}_s{seed}_k{want}": data[f"blocktri_L{L}_b{b}_s{seed}_k{want}"]},
+              open(os.path.join(out, f"interval_L{L}.json"), "w"), indent=1, sort_keys=True)
 print(f"interval [{lo}, {hi}] holds {want}; total {time.time() - t0:.0f} s", flush=True)
