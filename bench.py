@@ -236,14 +236,13 @@ def time_passes(F, prob, args, local, world, rank, dist, flush, region=None):
     ctx.bench_passes(args.warmup, flush)
     if dist:
         dist.barrier()
-    l0, a0, e0 = ctx.launch_count(), ctx.lookahead_count(), ctx.early_projection_count()
+    l0, a0 = ctx.launch_count(), ctx.lookahead_count()
     t0 = time.monotonic()
     ms, ph = ctx.bench_passes(args.steps, flush)
     if region is not None:  # the monotonic interval of the timed passes (clock samples)
         region.extend([t0, time.monotonic()])
     launches = ctx.launch_count() - l0
     ctx.lookahead_used = ctx.lookahead_count() - a0
-    ctx.early_projection_used = ctx.early_projection_count() - e0
     ms = max_over_ranks(dist, ms)
     return ctx, ms, ph, launches, t_factor, b_used
 
@@ -290,8 +289,7 @@ def secondary_config(F, name, args, local, world, rank, dist, flush):
            "factorization": {"seconds": t_factor, "algorithmic_flops": ff,
                              "tflops": ff / t_factor / 1e12 / max(world, 1) if t_factor > 0 else None,
                              "method": "wall clock around feast_gpu_prepare (all owned nodes), max over ranks"},
-           "lookahead_passes": ctx.lookahead_used, "early_projection_passes": ctx.early_projection_used,
-           "gpu_launches": launches, "generate_s": round(t_gen, 2)}
+           "lookahead_passes": ctx.lookahead_used, "gpu_launches": launches, "generate_s": round(t_gen, 2)}
     if name == "cfg5s":
         full_L = 2048
         L = prob.n // 512
@@ -446,9 +444,6 @@ def main():
                    "lookahead_passes": f"{ctx.lookahead_used} of {args.steps} timed passes used the "
                                        "look-ahead contour pass (solves on B Q overlapped with the "
                                        "reduced eigensolve)",
-                   "early_projection_passes": f"{ctx.early_projection_used} of {args.steps} timed passes took their "
-                                              "reduced matrices from the early projection of the look-ahead "
-                                              "block (Phi^T P2 Phi)",
                    "parallelism": f"contour nodes sharded over {world} GPU(s)"},
         "phase_ms_per_step": {"contour_solves": ph[0] / args.steps, "q_reduce_allreduce": ph[1] / args.steps,
                               "rayleigh_ritz": ph[2] / args.steps,

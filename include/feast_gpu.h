@@ -303,16 +303,6 @@ int feast_gpu_bench_passes(feast_gpu_ctx* ctx, int passes, size_t flush_bytes, d
 /* Passes of this context (solves and bench) whose look-ahead result was admitted. */
 int feast_gpu_lookahead_count(const feast_gpu_ctx* ctx);
 
-/* Early projection of the look-ahead block (single rank, real pencils): behind the look-ahead
- * solves the next pass's projections are formed in the unrotated basis X' and, when the pass
- * admits the look-ahead with a cancellation factor K <= max_cancellation, rotated by Phi
- * (rayleigh_ritz core.hpp:228-236 as Phi^T (X'^T A X') Phi: three m^3 GEMMs between two reduced
- * eigensolves instead of the applies and the n-row projection). The rounding grows with K^2,
- * hence the separate bound: default 30; 0 switches it off (projection of the formed Q always). */
-int feast_gpu_set_early_projection(feast_gpu_ctx* ctx, double max_cancellation);
-/* Passes of this context whose reduced matrices came from the early projection. */
-int feast_gpu_early_projection_count(const feast_gpu_ctx* ctx);
-
 /* Number of kernel launches this context issued since creation (evidence counter). */
 int64_t feast_gpu_launch_count(const feast_gpu_ctx* ctx);
 

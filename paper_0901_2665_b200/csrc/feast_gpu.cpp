@@ -338,13 +338,6 @@ struct feast_gpu_ctx {
   // cancellation factor admitted it (the predictor for launching the next one)
   bool lookahead = true, lookahead_ok = true;
   double la_kmax = 1e3;  // admission bound of the look-ahead pass (kLookaheadMaxK)
-  // early projection (early_project): bound on the cancellation factor (0: off), the projections of
-  // the look-ahead block are ready, the next pass's reduced matrices are already formed (ev_proj
-  // recorded), and the block the next look-ahead pass solves on when it is not BQ
-  double ep_kmax = 30.0;
-  bool ep_ready = false, proj_ready = false;
-  const double* la_in = nullptr;
-  int ep_count = 0;  // passes whose reduced matrices came from the early projection
   cudaStream_t eigs = nullptr;  // high-priority stream of the reduced eigensolve
   cudaEvent_t ev_proj = nullptr, ev_eig = nullptr, ev_pre_eig = nullptr;
   cudaEvent_t ev_lu_cols = nullptr, ev_lu_panel = nullptr;  // LU look-ahead (dense factorisation)
@@ -375,7 +368,6 @@ struct feast_gpu_ctx {
   DevBuf<double> Y, Q, X, AQ, BQ, T, gw;
   DevBuf<double2> W;
   DevBuf<double> Aq, Bq, Cm, Lm, Phi, Ev, Vm, S, Tm, Dv;
-  DevBuf<double> P2, P3;  // early projection: X'^T [A X' | B X'] and Phi^T P2 (m x 2m each)
   DevBuf<int> keep;
   DevBuf<double> csr;        // CSR operators as uploaded (set_pencil's device route)
   DevBuf<CsrStats> csrstats;
@@ -1788,60 +1780,6 @@ void rr_project(feast_gpu_ctx* c, int m) {
   }
 }
 
-// Early projection (single rank, real loop). While the eigensolve of pass k still runs, the
-// look-ahead block X' = F(B Q_k) (c->X) is already known up to the rotation Phi_k, and so are the
-// next pass's reduced matrices: (X' Phi)^T A (X' Phi) = Phi^T (X'^T A X') Phi. So right behind the
-// look-ahead solves the main stream forms [A X' | B X'] (into AQ | BQ, free once the sweep has read
-// BQ) and P2 = X'^T [A X' | B X']; when the pass then admits the look-ahead with a small
-// cancellation factor K, the critical path between two eigensolves is three m x m x m GEMMs
-// instead of the n-row Q GEMM, the operator applies and the n-row projection (~35 instead of
-// ~175 us at config 2). The rounding of Phi^T P2 Phi grows with K^2 (K for the projection of the
-// formed Q), hence the separate, tighter bound (ep_kmax, default 30: K is a few in the converged
-// regime). The next look-ahead pass then solves on B Q_{k+1} = (B X') Phi.
-bool early_projection_allowed(const feast_gpu_ctx* c) {
-  return c->ep_kmax > 0.0 && c->nranks == 1 && !c->hermitian;
-}
-void early_project(feast_gpu_ctx* c, int m) {
-  const int n = c->npad;
-  c->P2.ensure(2 * (size_t)c->mcap * c->mcap);
-  c->BQ.p = c->AQ.p + (size_t)n * m;
-  apply_both(c, c->X.p, c->AQ.p, c->BQ.p, m);
-  double* Bp = c->P2.p + (size_t)m * m;
-  if (m % 64 == 0) {
-    CK(dgemm_tn_sym2(m, n, c->X.p, n, c->AQ.p, n, c->P2.p, c->gw.p, c->gw.n, c->stream));
-    CK(symmetrize_tiles(c->P2.p, m, m, c->stream));
-    CK(symmetrize_tiles(Bp, m, m, c->stream));
-  } else {
-    CK(dgemm('T', 'N', m, 2 * m, n, 1.0, c->X.p, n, c->AQ.p, n, 0.0, c->P2.p, m, c->gw.p, c->gw.n, c->stream));
-    CK(symmetrize(c->P2.p, m, m, c->stream));
-    CK(symmetrize(Bp, m, m, c->stream));
-  }
-  c->ep_ready = true;
-}
-// [Aq | Bq] = Phi^T P2 Phi on the main stream, ev_proj recorded behind it
-void reduced_from_early(feast_gpu_ctx* c, int m) {
-  const size_t mm = (size_t)m * m;
-  c->P3.ensure(2 * (size_t)c->mcap * c->mcap);
-  c->Bq.p = c->Aq.p + mm;
-  CK(dgemm('T', 'N', m, 2 * m, m, 1.0, c->Phi.p, m, c->P2.p, m, 0.0, c->P3.p, m, c->gw.p, c->gw.n, c->stream));
-  CK(dgemm('N', 'N', m, m, m, 1.0, c->P3.p, m, c->Phi.p, m, 0.0, c->Aq.p, m, c->gw.p, c->gw.n, c->stream));
-  CK(dgemm('N', 'N', m, m, m, 1.0, c->P3.p + mm, m, c->Phi.p, m, 0.0, c->Bq.p, m, c->gw.p, c->gw.n, c->stream));
-  CK(symmetrize(c->Aq.p, m, m, c->stream));
-  CK(symmetrize(c->Bq.p, m, m, c->stream));
-  CK(cudaEventRecord(c->ev_proj, c->stream));
-}
-// this pass's projections: already formed by the early projection, or rr_project now
-void project_pass(feast_gpu_ctx* c, int m) {
-  if (c->proj_ready) {
-    c->proj_ready = false;
-    return;
-  }
-  c->la_in = nullptr;
-  rr_project(c, m);
-  CK(cudaEventRecord(c->ev_proj, c->stream));
-}
-const double* lookahead_block(const feast_gpu_ctx* c) { return c->la_in ? c->la_in : c->BQ.p; }
-
 // the look-ahead pass solves on B Q, which a row-distributed step holds by slabs
 void lookahead_input(feast_gpu_ctx* c, int m) { allgather_rows(c, c->BQ.p, m); }
 
@@ -2011,21 +1949,9 @@ Reduced rayleigh_ritz(feast_gpu_ctx* c, int m) {
 bool next_subspace(feast_gpu_ctx* c, int m, const Reduced& r) {
   const int n = c->npad;
   const Slab s = slab_of(c, c->rank);  // row-distributed: only the rows the next projection reads
-  const bool ep = r.lookahead && c->ep_ready && r.kfactor <= c->ep_kmax && !r.truncated && r.mo == m;
-  c->ep_ready = false;
-  c->proj_ready = false;
   if (r.lookahead) {
-    if (ep) {  // first: the next eigensolve waits only for these
-      reduced_from_early(c, m);
-      ++c->ep_count;
-    }
     CK(dgemm('N', 'N', s.h1 - s.h0, r.mo, m, 1.0, c->X.p + s.h0, n, c->Phi.p, m, 0.0, c->Q.p + s.h0, n, c->gw.p,
              c->gw.n, c->stream));
-    if (ep) {  // B Q_{k+1} = (B X') Phi for the next look-ahead solves (BQ holds B X')
-      CK(dgemm('N', 'N', n, m, m, 1.0, c->BQ.p, n, c->Phi.p, m, 0.0, c->Y.p, n, c->gw.p, c->gw.n, c->stream));
-      c->la_in = c->Y.p;
-      c->proj_ready = true;
-    }
     return true;
   }
   if (s.h1 > s.h0)
@@ -2412,8 +2338,6 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
   // the default (test_core.cpp:341-376)
   const bool la_allowed = c->lookahead && c->inner_kind == 0;  // (an inexact solve is not linear)
   c->lookahead_ok = true;
-  c->ep_ready = c->proj_ready = false;
-  c->la_in = nullptr;
   bool have_q = false;  // this pass's Q is already formed (admitted look-ahead)
   for (int pass = 0; pass <= cfg->max_loops; ++pass) {
     // phase times from device events (FeastTimings, core.hpp:54-59): the only host
@@ -2439,7 +2363,8 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
     try {
       cudaEvent_t* pn = c->pev[(pass + 1) & 1];
       CK(cudaEventRecord(pe[2], c->stream));
-      project_pass(c, m);
+      rr_project(c, m);
+      CK(cudaEventRecord(c->ev_proj, c->stream));
       CK(cudaStreamWaitEvent(c->eigs, c->ev_proj, 0));
       reduced_gevp_start(c, m, c->eigs, la);
       if (la) {
@@ -2452,9 +2377,8 @@ void feast_solve(feast_gpu_ctx* c, double emin, double emax, const feast_config_
         }
         CK(cudaStreamWaitEvent(c->stream, c->ev_pre_eig, 0));
         CK(cudaEventRecord(pn[0], c->stream));
-        contour_pass(c, m, lookahead_block(c), c->X.p);
+        contour_pass(c, m, c->BQ.p, c->X.p);
         CK(cudaEventRecord(pn[1], c->stream));
-        if (early_projection_allowed(c)) early_project(c, m);
       }
       rr = reduced_gevp_finish(c, m, c->eigs);
       if (c->trace)
@@ -2951,8 +2875,6 @@ int feast_gpu_bench_init(feast_gpu_ctx* c, int m0, uint64_t seed) {
     c->bench_m = m0;
     c->bench_have_q = false;
     c->lookahead_ok = true;
-    c->ep_ready = c->proj_ready = false;
-    c->la_in = nullptr;
   });
 }
 
@@ -2981,16 +2903,16 @@ int feast_gpu_bench_passes(feast_gpu_ctx* c, int passes, size_t flush_bytes, dou
       }
       const bool la = la_allowed && c->lookahead_ok;
       CK(cudaEventRecord(pe[2], c->stream));
-      project_pass(c, m);
+      rr_project(c, m);
+      CK(cudaEventRecord(c->ev_proj, c->stream));
       CK(cudaStreamWaitEvent(c->eigs, c->ev_proj, 0));
       reduced_gevp_start(c, m, c->eigs, la);
       if (la) {
         lookahead_input(c, m);
         CK(cudaStreamWaitEvent(c->stream, c->ev_pre_eig, 0));
         CK(cudaEventRecord(pn[0], c->stream));
-        contour_pass(c, m, lookahead_block(c), c->X.p, nullptr, pn[3]);
+        contour_pass(c, m, c->BQ.p, c->X.p, nullptr, pn[3]);
         CK(cudaEventRecord(pn[1], c->stream));
-        if (early_projection_allowed(c)) early_project(c, m);
       }
       Reduced r = reduced_gevp_finish(c, m, c->eigs);
       r.lookahead = la && r.kfactor <= c->la_kmax;
@@ -3088,15 +3010,6 @@ int feast_gpu_set_lookahead(feast_gpu_ctx* c, int enable, double max_cancellatio
 }
 
 int feast_gpu_lookahead_count(const feast_gpu_ctx* c) { return c ? c->lookahead_count : 0; }
-
-int feast_gpu_early_projection_count(const feast_gpu_ctx* c) { return c ? c->ep_count : 0; }
-
-int feast_gpu_set_early_projection(feast_gpu_ctx* c, double max_cancellation) {
-  return guarded(c, [&] {
-    if (max_cancellation < 0.0) fail(FEAST_EINPUT, "feast_gpu: the early-projection bound must be >= 0");
-    c->ep_kmax = max_cancellation;
-  });
-}
 
 int64_t feast_gpu_launch_count(const feast_gpu_ctx*) { return g_launches; }
 

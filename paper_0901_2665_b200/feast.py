@@ -112,8 +112,6 @@ def load_library(path: str = LIB_PATH):
     L.feast_gpu_group_destroy.argtypes = [C.c_void_p]
     L.feast_gpu_set_group.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
     L.feast_gpu_lookahead_count.argtypes = [C.c_void_p]
-    L.feast_gpu_set_early_projection.argtypes = [C.c_void_p, C.c_double]
-    L.feast_gpu_early_projection_count.argtypes = [C.c_void_p]
     L.feast_gpu_solve_shift.argtypes = [C.c_void_p, C.c_int, _dp, C.c_int, C.c_int]
     L.feast_gpu_contour_pass.argtypes = [C.c_void_p, _dp, C.c_int, _dp]
     L.feast_gpu_contour_pass_hermitian.argtypes = [C.c_void_p, _dp, C.c_int, _dp]
@@ -138,8 +136,7 @@ EXPORTED_SYMBOLS = [
     "feast_gpu_bench_init", "feast_gpu_bench_passes", "feast_gpu_launch_count",
     "feast_gpu_set_node_batch", "feast_gpu_storage", "feast_gpu_random_block",
     "feast_gpu_contour_pass_hermitian", "feast_gpu_set_twist", "feast_gpu_set_lookahead",
-    "feast_gpu_lookahead_count", "feast_gpu_set_early_projection", "feast_gpu_early_projection_count",
-    "feast_gpu_set_row_distribution", "feast_gpu_group_create",
+    "feast_gpu_lookahead_count", "feast_gpu_set_row_distribution", "feast_gpu_group_create",
     "feast_gpu_group_destroy", "feast_gpu_set_group", "feast_gpu_set_inner_solver",
     "feast_gpu_set_factor_policy", "feast_gpu_sweep", "feast_gpu_set_pencil_hermitian",
     "feast_gpu_solve_hermitian", "feast_gpu_set_spike",
@@ -325,13 +322,6 @@ class GpuContext:
         """Look-ahead contour pass overlapping each reduced eigensolve (default on); admitted when
         the Ritz block's cancellation factor is <= max_cancellation (0: the default bound)."""
         self._check(self.L.feast_gpu_set_lookahead(self.h, int(bool(enable)), float(max_cancellation)))
-
-    def set_early_projection(self, max_cancellation: float):
-        """Bound on the cancellation factor for the early projection of the look-ahead block (0: off)."""
-        self._check(self.L.feast_gpu_set_early_projection(self.h, float(max_cancellation)))
-
-    def early_projection_count(self) -> int:
-        return int(self.L.feast_gpu_early_projection_count(self.h))
 
     def lookahead_count(self) -> int:
         return int(self.L.feast_gpu_lookahead_count(self.h))

@@ -13,7 +13,13 @@
 """
 import numpy as np
 
-VALIDATED = 1e-8   # spurious pairs have reference-metric residuals ~ 1e-1 .. 1
+# Validation threshold on the reference-metric residual (residual.hpp: relative to |lambda|).
+# Spurious Ritz pairs sit at ~1e-1 .. 1, converged ones at <= ~1e-8: on full-size config 3 the pair
+# at lambda = 6.2e-5 (|lambda| tiny, so the metric amplifies an absolute residual of ~1e-12 by
+# 1.6e4) has 9e-10 in the reference and 1.5e-8 on the GPU (b = 256 explicit block inverses; its
+# north-star residual, asserted below, is <= 1e-10). The threshold only has to separate the two
+# populations.
+VALIDATED = 1e-6
 
 
 def norm1(op):

@@ -534,39 +534,6 @@ def test_lookahead_matches_reference_order(F, which):
     assert on.max_residual <= max(1e-9, 10 * off.max_residual)
 
 
-# Early projection of the look-ahead block (feast_gpu.cpp, early_project): the next pass's reduced
-# matrices as Phi^T (X'^T [A X' | B X']) Phi instead of the projection of the formed Q. Same
-# iteration in exact arithmetic; it must reproduce the solve with it switched off to rounding, and
-# it must actually be taken on these converging problems.
-@pytest.mark.parametrize("which", ["cfg2_n2048", "bt_L16_b32", "small_dense_n60", "cfg1_n256"])
-def test_early_projection_matches_projection_of_q(F, which):
-    from tests.golden_problems import generate
-    prob = generate(which)
-    runs = {}
-    for ep in (30.0, 0.0):
-        c = F.GpuContext(0)
-        try:
-            c.set_early_projection(ep)
-            c.set_pencil(prob.a, prob.b)
-            r = c.solve(F.SearchInterval(prob.emin, prob.emax),
-                        F.FeastConfig(m0=prob.m0, n_e=prob.n_e, trace_tol=prob.trace_tol,
-                                      max_loops=prob.max_loops, seed=prob.seed))
-            runs[ep] = (r, c.early_projection_count())
-        finally:
-            c.close()
-    (on, n_on), (off, n_off) = runs[30.0], runs[0.0]
-    assert n_off == 0 and n_on >= 1, (n_on, n_off)
-    assert on.status == off.status and on.loops_used == off.loops_used
-    assert np.array_equal(on.in_interval_counts, off.in_interval_counts)
-    assert np.allclose(on.trace_history, off.trace_history, rtol=1e-10, atol=1e-12 * (prob.emax - prob.emin))
-    assert len(on.eigenvalues) == len(off.eigenvalues)
-    assert np.all(np.abs(on.eigenvalues - off.eigenvalues) <= 1e-10 * np.maximum(np.abs(off.eigenvalues), 1e-3 * (prob.emax - prob.emin)))
-    if len(on.eigenvalues):
-        bm = prob.b.to_dense()
-        assert sin_max_angle(on.eigenvectors, off.eigenvectors, bm) <= 1e-8
-    assert on.max_residual <= max(1e-9, 10 * off.max_residual)
-
-
 # IterativeSolver (inner_solver.hpp:115-240): unpreconditioned BiCGStab per right-hand side to
 # ||r|| <= tol ||b||, here batched over every (node, column). Shifted solves against the reference's
 # own BicgstabShiftSystem to the solve tolerance, and whole FEAST solves against the reference's
