@@ -450,6 +450,33 @@ def test_contour_pass_small_blocks(F, twist, L, b):
 
 # the initial block is drawn on the device (mt19937_64 in a single CTA, two-phase twist): the
 # stream must be bit-identical to random_block<double> (core.hpp:84-106, test_core.cpp:49-71)
+# The b = 16 sweep synchronises through mbarriers, a named barrier, DSMEM stores and cp.async rings
+# (sweep_pipe.cu). compute-sanitizer is not available on the GPU pool, so races are looked for the
+# blunt way: the same contour pass and shifted solve repeated on a chain long enough to wrap every
+# ring many times, with a ragged last column block, must give the same bits every time, twisted or
+# not, with and without SPIKE chunks.
+@pytest.mark.parametrize("twist,chunks", [(True, 1), (False, 1), (True, 4)])
+def test_sweep_pipe_repeatable(F, twist, chunks):
+    from paper_0901_2665_b200 import problems as P
+    a, bb = P.blocktri_operators(128, 16, seed=77)
+    c = F.GpuContext(0)
+    try:
+        c.set_twist(twist)
+        c.set_spike(chunks)
+        c.set_pencil(a, bb)
+        c.prepare(-0.3, 0.4, 8)
+        y = O.random_block(a.n, 45, 9)
+        rhs = np.random.default_rng(4).standard_normal((a.n, 11)) + 1j * np.random.default_rng(5).standard_normal((a.n, 11))
+        q0, x0 = c.contour_pass(y), c.solve_shift(3, rhs.copy(), False)
+        qr = O.accumulate_real(a, bb, -0.3, 0.4, 8, y)
+        assert np.max(np.abs(q0 - qr)) <= 1e-11 * max(1.0, np.max(np.abs(qr)))
+        for _ in range(8):
+            assert np.array_equal(c.contour_pass(y), q0)
+            assert np.array_equal(c.solve_shift(3, rhs.copy(), False), x0)
+    finally:
+        c.close()
+
+
 @pytest.mark.parametrize("n,m,seed", [(1, 1, 42), (5, 3, 7), (311, 2, 42), (312, 2, 1), (313, 3, 5),
                                       (16384, 192, 42)])
 def test_device_random_block_bit_identical(ctx, n, m, seed):
