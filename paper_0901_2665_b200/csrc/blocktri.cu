@@ -47,7 +47,7 @@ int64_t g_launches = 0;
 //
 // Per layer: S = M - Cin Gprev (DMMA tiles, operands converted from the (A, B) pairs on the
 // fly), S^{-1} by Gauss-Jordan with partial pivoting (largest |.|^2, first index on ties)
-// in place — in one warp's registers for b <= 32 (lane j owns column j), in shared memory for
+// in place — rows spread over the CTA's threads for b <= 32 (gj_cta), in shared memory for
 // b = 64 — then H = S^{-1} Cin and G = S^{-1} Cout (DMMA). For b <= 32 the next layer's raw
 // blocks are prefetched with cp.async while this one is processed.
 // ---------------------------------------------------------------------------
@@ -83,64 +83,70 @@ FEAST_DEV void cgemm_tiles(int warp, int nwarps, int lane, FA fa, FB fb, FO out)
   }
 }
 
-// In-place Gauss-Jordan inverse of Sv (B x B, column stride lds) by one warp, rows spread over
-// the lanes (32 / B lanes per row, each owning B / (32 / B)... columns of it) and IMPLICIT
-// partial pivoting: the pivot of column k is the unused row with the largest |.|^2 (first
-// index on ties, a warp arg-max), it is never moved; at the end the row that pivoted column k
-// holds row k of (P S)^{-1}, and S^{-1}[i, p_t] = that row's element t. No row swaps, no
-// dynamically indexed registers, and the k loop stays rolled (small code).
-template <int B>
-FEAST_DEV void gj_rows(double2* Sv, int lds, int* pivs, int lane, int* status) {
-  constexpr int CS = 32 / B;     // lanes per row
-  constexpr int NCOL = B / CS;   // columns per lane
-  const int r = lane % B, j0 = (lane / B) * NCOL;
+// In-place Gauss-Jordan inverse of Sv (B x B, column stride lds) by the whole CTA (NT = B x NG
+// threads: thread t owns row t % B and NCOL = B / NG columns of it) with IMPLICIT partial pivoting:
+// the pivot row of column k is never moved; at the end the row that pivoted column k holds row k of
+// (P S)^{-1}, and S^{-1}[i, p_t] = that row's element t. No row swaps, no dynamically indexed
+// registers, the k loop stays rolled.
+//   * Pivot search: ONE warp-wide integer max (REDUX) per step on a 32-bit key, the top 27 bits of
+//     |a_ik|^2 (its binary64 pattern orders like the value) over B - 1 - i in the low bits: the
+//     unused row with the largest modulus to within 2^-15 relative, lowest index among those
+//     (threshold partial pivoting with a threshold of 1 - 3e-5). Every warp repeats it on its own
+//     lanes (same result, no exchange). The shuffle arg-max it replaces (4 dependent levels of 64-bit
+//     shuffles and FP64 compares) was the longest dependent chain of a pivot step.
+//   * Two block barriers per pivot step separate the reads of the pivot row and column from their
+//     overwriting. (One warp doing the whole elimination, the first version, left the other three
+//     waiting for two thirds of the kernel: ncu, profiles/r02_summary.md.)
+template <int B, int NT>
+FEAST_DEV void gj_cta(double2* Sv, int lds, int* pivs, int* status) {
+  constexpr int NG = NT / B, NCOL = B / NG;
+  static_assert(NT % B == 0 && B % NG == 0 && B <= 32, "gj_cta: one row per lane group");
+  const int tid = threadIdx.x;
+  const int r = tid % B, j0 = (tid / B) * NCOL;
   bool used = false, bad = false;
   int mystep = 0;
 #pragma unroll 1
   for (int k = 0; k < B; ++k) {
     const double2 ak = Sv[r + k * lds];
-    double best = used ? -1.0 : ak.x * ak.x + ak.y * ak.y;
-    int p = r;
-#pragma unroll
-    for (int o = B / 2; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int op = __shfl_xor_sync(0xffffffffu, p, o);
-      if (ob > best || (ob == best && op < p)) {
-        best = ob;
-        p = op;
-      }
-    }
-    bad |= !(best > 0.0);
+    // (lanes r and r + B of a warp hold the same row when B = 16: the warp-wide max is the 16-row max)
+    const unsigned key =
+        used ? 0u : (((unsigned)__double2hiint(ak.x * ak.x + ak.y * ak.y) & ~(unsigned)(B - 1)) | (unsigned)(B - 1 - r));
+    const int p = B - 1 - (int)(__reduce_max_sync(0xffffffffu, key) & (unsigned)(B - 1));
     const bool isp = r == p;
     used |= isp;
     mystep = isp ? k : mystep;
-    if (lane == 0) pivs[k] = p;
-    // 1 / a_pk = conj(a_pk) / |a_pk|^2 (|a_pk|^2 = best, the pivot is O(1) here)
+    if (tid == 0) pivs[k] = p;
+    // 1 / a_pk = conj(a_pk) / |a_pk|^2
     const double2 apk = Sv[p + k * lds];
+    const double best = apk.x * apk.x + apk.y * apk.y;
+    bad |= !(best > 0.0);
     const double rn = 1.0 / best;
     const double2 inv = make_double2(apk.x * rn, -apk.y * rn);
-    double2 piv[NCOL];  // the pivot row (its owner lanes overwrite it below)
+    double2 piv[NCOL], a0[NCOL];
 #pragma unroll
-    for (int jj = 0; jj < NCOL; ++jj) piv[jj] = Sv[p + (j0 + jj) * lds];
-    __syncwarp();
+    for (int jj = 0; jj < NCOL; ++jj) {
+      piv[jj] = Sv[p + (j0 + jj) * lds];
+      a0[jj] = Sv[r + (j0 + jj) * lds];
+    }
+    __syncthreads();  // every thread holds the pivot row / column entries it needs
     const double2 mk = make_double2(-ak.x, -ak.y);
 #pragma unroll
     for (int jj = 0; jj < NCOL; ++jj) {
       const bool jk = j0 + jj == k;
       const double2 pv = jk ? inv : cmul(piv[jj], inv);   // scaled pivot row
-      const double2 a0 = jk ? make_double2(0.0, 0.0) : Sv[r + (j0 + jj) * lds];
-      const double2 upd = make_double2(a0.x + mk.x * pv.x - mk.y * pv.y, a0.y + mk.x * pv.y + mk.y * pv.x);
+      const double2 a = jk ? make_double2(0.0, 0.0) : a0[jj];
+      const double2 upd = make_double2(a.x + mk.x * pv.x - mk.y * pv.y, a.y + mk.x * pv.y + mk.y * pv.x);
       Sv[r + (j0 + jj) * lds] = isp ? pv : upd;
     }
-    __syncwarp();
+    __syncthreads();
   }
   double2 mine[NCOL];
 #pragma unroll
   for (int jj = 0; jj < NCOL; ++jj) mine[jj] = Sv[r + (j0 + jj) * lds];
-  __syncwarp();
+  __syncthreads();
 #pragma unroll
   for (int jj = 0; jj < NCOL; ++jj) Sv[mystep + pivs[j0 + jj] * lds] = mine[jj];
-  if (bad && lane == 0) atomicExch(status, 1);
+  if (bad && tid == 0) atomicExch(status, 1);
 }
 
 // the same elimination by the whole CTA in shared memory (b = 64)
@@ -312,7 +318,7 @@ __global__ void __launch_bounds__(FacShape<B>::NT) bt_factor_small_kernel(BtFact
 
     // (2) S^{-1} in place
     if constexpr (RAW) {
-      if (warp == 0) gj_rows<B>(Sv, LDS, pivs, lane, a.status);
+      gj_cta<B, NT>(Sv, LDS, pivs, a.status);
     } else {
       gj_smem<B, NT>(Sv, LDS, pivs, cpos, a.status);
     }
