@@ -708,57 +708,77 @@ __global__ void tri_eigvals_kernel(TriArgs p) {
 // ---------------------------------------------------------------------------
 // LU of T - lam I with partial pivoting (dgttrf): D (diag of U), DU, DU2 (supers of U),
 // DL (multipliers), ipiv[i] = 1 if rows i, i+1 were swapped
-__device__ void gttrf(int m, const double* d, const double* e, double lam, double* D, double* DL, double* DU,
-                      double* DU2, int* ipiv, double tiny) {
-  for (int i = 0; i < m; ++i) D[i] = d[i] - lam;
+// Pivoted LU of T - lam I (dgttf2) on one lane. The running row (its diagonal and super-diagonal
+// entries) is carried in registers, so the dependent chain of a step is compare -> reciprocal ->
+// FMA; through shared memory (the first version re-read D[i], DU[i] it had stored one step
+// earlier) every step paid two store-to-load round trips. D is left raw: the caller inverts it with
+// all lanes (gttrf_finish).
+__device__ void gttrf(int m, const double* __restrict__ d, const double* __restrict__ e, double lam,
+                      double* __restrict__ D, double* __restrict__ DL, double* __restrict__ DU,
+                      double* __restrict__ DU2, int* __restrict__ ipiv, double tiny) {
+  double di = d[0] - lam;          // row i after the eliminations so far: diagonal ...
+  double dui = m > 1 ? e[0] : 0.0;  // ... and super-diagonal
   for (int i = 0; i + 1 < m; ++i) {
-    DL[i] = e[i];
-    DU[i] = e[i];
-    DU2[i] = 0.0;
-    ipiv[i] = 0;
-  }
-  for (int i = 0; i + 1 < m; ++i) {
-    if (fabs(D[i]) >= fabs(DL[i])) {
-      if (D[i] == 0.0) D[i] = tiny;
-      const double f = DL[i] * fast_rcp(D[i]);
+    const double dli = e[i];                       // sub-diagonal entry (i + 1, i)
+    const double dn = d[i + 1] - lam;              // row i + 1 as given: diagonal ...
+    const double dun = i + 2 < m ? e[i + 1] : 0.0;  // ... and super-diagonal
+    if (fabs(di) >= fabs(dli)) {
+      if (di == 0.0) di = tiny;
+      const double f = dli * fast_rcp(di);
+      D[i] = di;
       DL[i] = f;
-      D[i + 1] -= f * DU[i];
-    } else {
-      const double f = D[i] * fast_rcp(DL[i]);
-      D[i] = DL[i];
+      DU[i] = dui;
+      DU2[i] = 0.0;
+      ipiv[i] = 0;
+      di = dn - f * dui;
+      dui = dun;
+    } else {  // rows i and i + 1 interchanged
+      const double f = di * fast_rcp(dli);
+      D[i] = dli;
       DL[i] = f;
-      const double t = DU[i];
-      DU[i] = D[i + 1];
-      D[i + 1] = t - f * D[i + 1];
-      if (i + 2 < m) {
-        DU2[i] = DU[i + 1];
-        DU[i + 1] = -f * DU[i + 1];
-      }
+      DU[i] = dn;
+      DU2[i] = dun;
       ipiv[i] = 1;
+      di = dui - f * dn;
+      dui = -f * dun;
     }
   }
-  for (int i = 0; i < m; ++i) {  // store reciprocals: the solves then chain FMAs only
+  D[m - 1] = di;
+}
+// D <- 1 / D (clamped away from zero) by the whole warp: the solves then chain FMAs only
+__device__ void gttrf_finish(int m, double* D, double tiny, int lane) {
+  for (int i = lane; i < m; i += 32) {
     double di = D[i];
     if (fabs(di) < tiny) di = di < 0.0 ? -tiny : tiny;
     D[i] = 1.0 / di;
   }
 }
 
-__device__ void gtts2(int m, const double* D, const double* DL, const double* DU, const double* DU2,
-                      const int* ipiv, double* b) {
+// the two substitutions (dgtts2) on one lane, the running entries in registers (one FMA per
+// forward step, two FMAs and a multiply per backward step on the dependent chain)
+__device__ void gtts2(int m, const double* __restrict__ D, const double* __restrict__ DL,
+                      const double* __restrict__ DU, const double* __restrict__ DU2,
+                      const int* __restrict__ ipiv, double* __restrict__ b) {
+  double bi = b[0];
   for (int i = 0; i + 1 < m; ++i) {
+    const double bn = b[i + 1], l = DL[i];
     if (!ipiv[i]) {
-      b[i + 1] -= DL[i] * b[i];
+      b[i] = bi;
+      bi = bn - l * bi;
     } else {
-      const double t = b[i];
-      b[i] = b[i + 1];
-      b[i + 1] = t - DL[i] * b[i];
+      b[i] = bn;
+      bi = bi - l * bn;
     }
   }
   // D holds 1 / diag(U)
-  b[m - 1] *= D[m - 1];
-  if (m >= 2) b[m - 2] = (b[m - 2] - DU[m - 2] * b[m - 1]) * D[m - 2];
-  for (int i = m - 3; i >= 0; --i) b[i] = (b[i] - DU[i] * b[i + 1] - DU2[i] * b[i + 2]) * D[i];
+  double x1 = bi * D[m - 1], x2 = 0.0;  // x_{i+1}, x_{i+2}
+  b[m - 1] = x1;
+  for (int i = m - 2; i >= 0; --i) {
+    const double xi = (b[i] - DU[i] * x1 - DU2[i] * x2) * D[i];
+    b[i] = xi;
+    x2 = x1;
+    x1 = xi;
+  }
 }
 
 // inverse-iteration steps per vector: the Sturm eigenvalue is accurate to O(eps ||T||), so
@@ -821,6 +841,8 @@ __global__ void tri_eigvecs_kernel(TriArgs p) {
     if (j > cl && lam - prev < sep) lam = prev + sep;  // separate coincident shifts (dstein)
     prev = lam;
     if (lane == 0) gttrf(m, sd, se, lam, D, DL, DU, DU2, ipiv, eps * tnorm);
+    __syncwarp();
+    gttrf_finish(m, D, eps * tnorm, lane);
     double* zj = zs;
     for (int i = lane; i < m; i += 32) {  // deterministic pseudo-random start
       uint32_t h = (uint32_t)i * 2654435761u ^ ((uint32_t)j * 40503u + 12345u);
