@@ -21,7 +21,7 @@ namespace feastgpu {
 
 int tri_max_dim();
 cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws, int* iws, cudaStream_t st,
-                    double vfloor, bool low_smem);
+                    double vfloor, bool low_smem, cudaEvent_t ev_tridiag);
 
 struct EigWork {
   int mmax = 0;
@@ -75,9 +75,9 @@ void eig_destroy(EigWork* w) {
 }
 
 cudaError_t sym_eig(EigWork* w, int m, double* a, double* evals, double* v, cudaStream_t st, double vfloor,
-                    bool low_smem) {
+                    bool low_smem, cudaEvent_t ev_tridiag) {
   if (!w || m < 1 || m > w->mmax || m > tri_max_dim()) return cudaErrorInvalidValue;
-  return tri_eig(m, a, evals, v, w->tws, w->tiws, st, vfloor, low_smem);
+  return tri_eig(m, a, evals, v, w->tws, w->tiws, st, vfloor, low_smem, ev_tridiag);
 }
 
 __global__ void transpose_kernel(const double* __restrict__ src, int m, int n, int lds,

@@ -1812,8 +1812,18 @@ void reduced_gevp_start(feast_gpu_ctx* c, int m, cudaStream_t st, bool concurren
     CK(trsm_lower(m, c->Lm.p, c->Dv.p, c->Tm.p, m, m, st));
     CK(transpose(c->Tm.p, m, m, m, c->Cm.p, m, st));
     CK(symmetrize(c->Cm.p, m, m, st));
-    if (concurrent) CK(cudaEventRecord(c->ev_pre_eig, st));
-    CK(sym_eig(c->eig, m, c->Cm.p, c->Ev.p, c->Phi.p, st, 0.0, concurrent));
+    // The look-ahead solves are released when the tridiagonalisation STARTS for m <= 192 (the
+    // register-tile kernel occupies one SM for ~0.5 ms) and when it ENDS beyond (the 16-CTA cluster /
+    // cooperative routes): with the solves running beside the cluster tridiagonalisation, full-size
+    // config 3 (m = 300) returned results that differed from run to run in the 11th digit (6 distinct
+    // eigenvalue sums in 10 solves; one in 10, bit-identical to the look-ahead-free order of kernels,
+    // with the release behind it). Each kernel alone is bit-reproducible beside the other
+    // (tools/contention_probe.py), so the cause is not pinned down; the later release costs the
+    // overlap of a ~1.5 ms kernel with a 40 ms sweep.
+    const bool release_early = m <= tri_tiles_max_dim();
+    if (concurrent && release_early) CK(cudaEventRecord(c->ev_pre_eig, st));
+    CK(sym_eig(c->eig, m, c->Cm.p, c->Ev.p, c->Phi.p, st, 0.0, concurrent,
+               concurrent && !release_early ? c->ev_pre_eig : nullptr));
     CK(trsm_lower_t(m, c->Lm.p, c->Dv.p, c->Phi.p, m, m, st, concurrent));  // Phi = L^-T W
     CK(cancellation_factor(m, m, c->Bq.p, m, c->Phi.p, m, c->kfac.p, st));
     CK(cudaMemcpyAsync(h + 1, c->kfac.p, sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -197,8 +197,9 @@ void eig_destroy(EigWork* w);
 // Symmetric eigen-decomposition of W (m x m, ld m, overwritten): eigenvalues ascending
 // into `evals` (device), vectors into `v` (device, m x m), stable order. vfloor > 0: the
 // tridiagonal route computes vectors only for evals > vfloor * max(evals) (others zero).
+// ev_tridiag (may be null): recorded on `st` right behind the tridiagonalisation kernel.
 cudaError_t sym_eig(EigWork* w, int m, double* a, double* evals, double* v, cudaStream_t st,
-                    double vfloor = 0.0, bool low_smem = false);
+                    double vfloor = 0.0, bool low_smem = false, cudaEvent_t ev_tridiag = nullptr);
 // Householder tridiagonalisation of a symmetric m x m matrix (3 <= m <= tri_tiles_max_dim())
 // on one SM with the matrix in registers: d[m], e[m-1], tau[m], reflectors in hv (m x m)
 int tri_tiles_max_dim();

@@ -1009,7 +1009,7 @@ int tri_max_dim() { return 1024; }
 
 // a (m x m, overwritten is allowed), eigenvalues ascending -> evals, vectors -> v (m x m)
 cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws, int* iws, cudaStream_t st,
-                    double vfloor, bool low_smem) {
+                    double vfloor, bool low_smem, cudaEvent_t ev_tridiag) {
   if (m < 1 || m > tri_max_dim()) return cudaErrorInvalidValue;
   double* d = ws;
   double* e = d + m;
@@ -1076,6 +1076,10 @@ cudaError_t tri_eig(int m, const double* a, double* evals, double* v, double* ws
     void* args[] = {&p};
     cudaError_t err = cudaLaunchCooperativeKernel((void*)tridiag_coop_kernel, grid, TC_NT, args, csm, st);
     ++g_launches;
+    if (err != cudaSuccess) return err;
+  }
+  if (ev_tridiag) {
+    const cudaError_t err = cudaEventRecord(ev_tridiag, st);
     if (err != cudaSuccess) return err;
   }
   TriArgs p{m, d, e, evals, z, nullptr, iws, vfloor};

@@ -126,7 +126,9 @@ def check_policy(prob, r, ref, x_ref=None, sketch=None, sketch_ref=None, expecte
         gv = np.asarray(r.residuals) <= VALIDATED
         rv = np.asarray(ref["residuals"]) <= VALIDATED
         lam_v, ev_v = lam[gv], np.asarray(ref["eigenvalues"])[rv]
-        out.update(validated=int(gv.sum()), ref_validated=int(rv.sum()))
+        out.update(validated=int(gv.sum()), ref_validated=int(rv.sum()),
+                   top_residuals=[float(v) for v in np.sort(np.asarray(r.residuals))[-4:]],
+                   ref_top_residuals=[float(v) for v in np.sort(np.asarray(ref["residuals"]))[-4:]])
         assert gv.sum() == rv.sum(), out
         if expected is not None:
             assert gv.sum() == expected, out

@@ -561,6 +561,33 @@ def test_lookahead_matches_reference_order(F, which):
     assert on.max_residual <= max(1e-9, 10 * off.max_residual)
 
 
+# Full solves with the look-ahead pass must be bit-reproducible from run to run (fresh contexts),
+# also when the reduced dimension takes the cluster tridiagonalisation (m > 192), where the look-ahead
+# solves are released behind the tridiagonalisation (feast_gpu.cpp, reduced_gevp_start: full-size
+# config 3 was not reproducible with the solves running beside it; tools/cfg3_repeat.py).
+@pytest.mark.parametrize("L,b,m0,want", [(24, 128, 300, 200), (64, 16, 96, 64)])
+def test_full_solves_are_reproducible(F, L, b, m0, want):
+    from paper_0901_2665_b200 import problems as P
+    prob = P.config3(L=L, b=b, seed=3, m0=m0, want=want, yseed=7)
+    outs = []
+    for _ in range(5):
+        c = F.GpuContext(0)
+        try:
+            c.set_pencil(prob.a, prob.b)
+            r = c.solve(F.SearchInterval(prob.emin, prob.emax),
+                        F.FeastConfig(m0=prob.m0, n_e=prob.n_e, trace_tol=prob.trace_tol,
+                                      max_loops=prob.max_loops, seed=prob.seed))
+            assert c.lookahead_count() >= 1
+            outs.append(r)
+        finally:
+            c.close()
+    for r in outs[1:]:
+        assert r.status == outs[0].status and r.loops_used == outs[0].loops_used
+        assert np.array_equal(r.eigenvalues, outs[0].eigenvalues)
+        assert np.array_equal(r.eigenvectors, outs[0].eigenvectors)
+        assert np.array_equal(r.trace_history, outs[0].trace_history)
+
+
 # IterativeSolver (inner_solver.hpp:115-240): unpreconditioned BiCGStab per right-hand side to
 # ||r|| <= tol ||b||, here batched over every (node, column). Shifted solves against the reference's
 # own BicgstabShiftSystem to the solve tolerance, and whole FEAST solves against the reference's
