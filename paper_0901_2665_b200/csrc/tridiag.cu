@@ -470,6 +470,9 @@ __global__ void __launch_bounds__(TCL_NT) tridiag_cluster_kernel(int m, const do
       tau[k] = tt;
     }
   };
+  // every CTA of the cluster must be running before its shared memory is written remotely (the
+  // first reflector below is pushed into all 16 CTAs)
+  cl.sync();
   if (m > 2 && q == 0) build(0, 0, true);
   cl.sync();
 

@@ -19,4 +19,6 @@ for i in range(int(sys.argv[1]) if len(sys.argv) > 1 else 12):
 ref = hist[0]
 for i, h in enumerate(hist[1:], 1):
     d = np.nonzero(h != ref)[0]
+    if len(d):
+        print("   rel dev per pass:", " ".join("%.0e" % (abs(a - b) / abs(b)) for a, b in zip(h, ref)))
     print(i, "identical" if len(d) == 0 else ("first differs at pass %d (rel %.1e), %d passes differ" % (d[0], abs(h[d[0]] - ref[d[0]]) / abs(ref[d[0]]), len(d))))
